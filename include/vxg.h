@@ -1,0 +1,159 @@
+/* vxg — B200-native (sm_100a) TSDF integration behind a plain C ABI.
+ *
+ * Drop-in boundary for the reference integrator's hot path. Each entry point
+ * names the reference interface it replaces (paths under
+ * /root/reference/proj). Only plain pointers and sizes cross this boundary; no
+ * torch, CUDA or Eigen types. All functions return an enum vxg_status; the
+ * message of the last failure on the calling thread is vxg_last_error().
+ * There is no CPU fallback: every compute entry point runs CUDA kernels and
+ * fails with VXG_ECUDA when no sm_100 device is usable.
+ *
+ * Threading: one handle = one device + one CUDA stream. Calls on
+ * a handle must be serialised by the caller (the reference's single-writer
+ * contract, include/vxf/layer.h:53-55). Distinct handles may
+ * run concurrently.
+ */
+#ifndef VXG_H_
+#define VXG_H_
+
+#include "vxg_types.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct vxg_handle vxg_handle;
+
+/* One posed scan (vxf::Scan, include/vxf/scan.h:13-20): n sensor-frame points
+ * xyz[n*3] (float32), optional parallel colours rgb[n*3] (NULL = no colours),
+ * pose = 3x4 row-major [R | t] sensor->world (vxf::Transform); the sensor
+ * origin is t (scan.h:19). */
+typedef struct vxg_frame {
+  const float* xyz;
+  const uint8_t* rgb;
+  uint64_t n;
+  float pose[12];
+} vxg_frame;
+
+/* Flags for vxg_integrate_batch. */
+enum vxg_batch_flags {
+  VXG_INPUT_HOST = 0,   /* xyz/rgb are host pointers (copied H2D inside the call) */
+  VXG_INPUT_DEVICE = 1, /* xyz/rgb are device pointers on the handle's device */
+  VXG_NO_SYNC_STATS = 2 /* reserved */
+};
+
+/* Thread-local message of the last failing call ("" if none). */
+const char* vxg_last_error(void);
+
+/* Library / device info: writes a one-line description into buf. */
+int vxg_device_info(int device, char* buf, size_t buf_len);
+
+/* vxf::TsdfLayer(voxel_size, vps) (include/vxf/layer.h:62-67) +
+ * vxf::TsdfIntegrator(config, &layer) (src/tsdf_integrator.cpp:106-109):
+ * validates the config exactly like TsdfConfig::validate (:10-20) and the
+ * layer geometry like Layer's constructor; VXG_EINVAL carries the reference's
+ * exception text. block_capacity = initial slab size in blocks (0 = default);
+ * the slab grows on demand. */
+int vxg_create(const vxg_tsdf_config* config, float voxel_size, int voxels_per_side, int device,
+               uint64_t block_capacity, vxg_handle** out);
+int vxg_destroy(vxg_handle* h);
+
+/* TsdfIntegrator::config() (tsdf_integrator.h:87) and a validated update. */
+int vxg_get_config(const vxg_handle* h, vxg_tsdf_config* out);
+int vxg_set_config(vxg_handle* h, const vxg_tsdf_config* config);
+
+/* Run all device work of this handle on an external CUDA stream
+ * (cudaStream_t passed as void*; NULL restores the handle's own stream). */
+int vxg_set_stream(vxg_handle* h, void* cuda_stream);
+
+/* size_t TsdfIntegrator::integrate(const Scan&) (src/tsdf_integrator.cpp:111-127)
+ * with raycasts_last_scan()/skipped_points_last_scan() (tsdf_integrator.h:84-85)
+ * in *out. Host pointers. Synchronous: the layer reflects the scan on return. */
+int vxg_integrate(vxg_handle* h, const float* xyz, const uint8_t* rgb, uint64_t n, const float pose[12],
+                  vxg_stats* out);
+
+/* Integrates n_frames scans in order; the resulting layer and the per-frame
+ * stats (out[n_frames], may be NULL) are identical to n_frames sequential
+ * vxg_integrate calls. flags: enum vxg_batch_flags. Synchronous. */
+int vxg_integrate_batch(vxg_handle* h, const vxg_frame* frames, uint64_t n_frames, int flags, vxg_stats* out);
+
+/* Same as vxg_integrate_batch over one packed buffer: frame f owns points
+ * [offsets[f], offsets[f+1]) of xyz/rgb, pose f is poses[12*f .. 12*f+11]. */
+int vxg_integrate_packed(vxg_handle* h, const float* xyz, const uint8_t* rgb, const uint64_t* offsets,
+                         const float* poses, uint64_t n_frames, int flags, vxg_stats* out);
+
+/* Layer::block_count() (layer.h:72). */
+int vxg_block_count(vxg_handle* h, uint64_t* out);
+
+/* Layer::blocks() enumerated in the order save_layer writes them
+ * (src/serialization.cpp:150-156: sorted by (x,y,z)). idx = B x 3 int32,
+ * voxels = B x vps^3 vxg_voxel, x-fastest (layer.h:23-30). Writes at most cap
+ * blocks; *n_out = blocks written. Either output pointer may be NULL. */
+int vxg_export_blocks(vxg_handle* h, int32_t* idx, vxg_voxel* voxels, uint64_t cap, uint64_t* n_out);
+
+/* Inserts / overwrites blocks (idx B x 3, voxels B x vps^3) — used to resume
+ * from a VXBLX checkpoint (load_tsdf_layer, serialization.cpp:193-212) or to
+ * mirror a host layer. */
+int vxg_import_blocks(vxg_handle* h, const int32_t* idx, const vxg_voxel* voxels, uint64_t n);
+
+/* Layer::voxel_ptr (layer.h:99-112) for n global voxel indices g[n*3]:
+ * found[i] = 0 (block unallocated: absence, never a default voxel) or 1. */
+int vxg_query_voxels(vxg_handle* h, const int32_t* g, uint64_t n, vxg_voxel* out, uint8_t* found);
+
+/* save_layer (serialization.cpp:141-168,216-218): VXBLX bytes. With buf NULL or
+ * cap too small only *need is written. */
+int vxg_serialize_vxblx(vxg_handle* h, uint8_t* buf, uint64_t cap, uint64_t* need);
+/* save_layer_file (serialization.cpp:244-248). */
+int vxg_save_vxblx(vxg_handle* h, const char* path);
+/* load_tsdf_layer (serialization.cpp:193-212,226-228): replaces the layer with
+ * the stream's blocks; VXG_EPARSE with the reference's ParseError text. */
+int vxg_load_vxblx(vxg_handle* h, const uint8_t* buf, uint64_t len);
+
+/* Drops every block (fresh layer, same geometry and config). */
+int vxg_reset(vxg_handle* h);
+
+/* Updated-block consumers (Layer::register_consumer / drain_updated,
+ * layer.h:124-140): blocks allocated or updated since the consumer's last
+ * drain. drain writes up to cap block indices (x,y,z) and clears the set;
+ * *n_out = set size. Unknown consumer -> VXG_EINVAL
+ * ("unknown updated-block consumer: <name>"). */
+int vxg_register_consumer(vxg_handle* h, const char* name);
+int vxg_drain_updated(vxg_handle* h, const char* name, int32_t* idx, uint64_t cap, uint64_t* n_out);
+
+/* Stage profiling: when enabled, every batch records CUDA events around each
+ * pipeline stage on the handle's stream. vxg_stage_times returns, per stage,
+ * the accumulated milliseconds and launches since the last reset (names in
+ * vxg_stage_name). */
+int vxg_profile(vxg_handle* h, int enable);
+int vxg_stage_count(void);
+const char* vxg_stage_name(int stage);
+int vxg_stage_times(vxg_handle* h, double* ms, uint64_t* launches, uint64_t* units, int reset);
+/* Kernel launches issued by the library since the last call (and reset). */
+int vxg_kernel_launches(vxg_handle* h, uint64_t* out, int reset);
+
+/* ---- device evaluation of the reference's public free functions (tested
+ * directly by the reference's unit tests, tsdf_integrator.h:46-59), batched: */
+/* projective_distance(x, p, s) (src/tsdf_integrator.cpp:22-27), n triples. */
+int vxg_eval_projective_distance(int device, const float* x, const float* p, const float* s, uint64_t n,
+                                 float* out);
+/* measurement_weight(mode, z, d, truncation, eps) (:29-44). */
+int vxg_eval_measurement_weight(int device, int mode, const float* z, const float* d, uint64_t n,
+                                float truncation, float dropoff_epsilon, float* out);
+/* Sequential update_tsdf_voxel folds (:46-67): voxel i starts from voxels[i]
+ * and folds d[j], w[j], rgb[j] for j in [starts[i], starts[i+1]) in order.
+ * rgb may be NULL (no colour). */
+int vxg_eval_update_voxels(int device, vxg_voxel* voxels, uint64_t n_voxels, const uint64_t* starts,
+                           const float* d, const float* w, const uint8_t* rgb, float truncation,
+                           float max_weight);
+/* RayCaster walks (:69-104) for n segments start[i]->end[i]: counts[i] = voxels
+ * visited; voxels written to out[offsets[i]*3 ...] when out != NULL (offsets
+ * are exclusive prefix sums of counts computed by the caller from a first
+ * call with out == NULL). */
+int vxg_eval_raycast(int device, const float* start, const float* end, uint64_t n, float voxel_size,
+                     uint32_t* counts, const uint64_t* offsets, int32_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VXG_H_ */

@@ -1,0 +1,520 @@
+// CPU ORACLE — TEST INFRASTRUCTURE ONLY (see vxf_oracle.h).
+//
+// Restatement of the reference hot path with explicit arithmetic. Every
+// function cites the reference file:line it follows (paths relative to
+// /root/reference/proj). Build flags (oracle/Makefile): g++ -O3 -DNDEBUG
+// -ffp-contract=off, default -march: the reference's CMake Release flags
+// (CMakeLists.txt:7-9) plus an explicit no-FMA guard.
+//
+// Eigen evaluation order assumed at the boundary:
+//   Isometry3f * v  : p_i = t_i + (R_i0 x + (R_i1 y + R_i2 z))
+//   norm / dot      : a0 + (a1 + a2)
+#include "vxf_oracle.h"
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+namespace {
+
+using Key3 = std::array<int32_t, 3>;
+
+// IndexHash (core.h:68-74): int arithmetic (wrapping), sign-extended to size_t.
+struct TeschnerHash {
+  size_t operator()(const Key3& k) const {
+    const uint32_t h = (static_cast<uint32_t>(k[0]) * 73856093u) ^
+                       (static_cast<uint32_t>(k[1]) * 19349669u) ^
+                       (static_cast<uint32_t>(k[2]) * 83492791u);
+    return static_cast<size_t>(static_cast<int64_t>(static_cast<int32_t>(h)));
+  }
+};
+
+struct BlockKeyHash {
+  size_t operator()(const Key3& k) const {
+    uint64_t z = (static_cast<uint64_t>(static_cast<uint32_t>(k[0])) << 42) ^
+                 (static_cast<uint64_t>(static_cast<uint32_t>(k[1])) << 21) ^
+                 static_cast<uint64_t>(static_cast<uint32_t>(k[2]));
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return static_cast<size_t>(z ^ (z >> 31));
+  }
+};
+
+inline float sq_norm3(float a, float b, float c) { return a * a + (b * b + c * c); }
+inline float norm3(float a, float b, float c) { return std::sqrt(sq_norm3(a, b, c)); }
+inline float dot3(const float* a, const float* b) { return a[0] * b[0] + (a[1] * b[1] + a[2] * b[2]); }
+
+// Isometry3f * Vector3f (scan.pose * scan.points[i], tsdf_integrator.cpp:180,202).
+inline void transform_point(const float pose[12], const float* x, float* p) {
+  for (int i = 0; i < 3; ++i) {
+    p[i] = pose[4 * i + 3] + (pose[4 * i + 0] * x[0] + (pose[4 * i + 1] * x[1] + pose[4 * i + 2] * x[2]));
+  }
+}
+
+// global_index_from_point (core.h:43-47).
+inline Key3 global_index(const float* p, float v) {
+  return {static_cast<int32_t>(std::floor(p[0] / v)), static_cast<int32_t>(std::floor(p[1] / v)),
+          static_cast<int32_t>(std::floor(p[2] / v))};
+}
+
+// floor_div (core.h:34-40).
+inline int floor_div(int a, int b) {
+  int q = a / b;
+  if ((a % b != 0) && ((a < 0) != (b < 0))) --q;
+  return q;
+}
+
+// projective_distance (tsdf_integrator.cpp:22-27).
+float projective_distance(const float* x, const float* p, const float* s) {
+  const float to_point[3] = {p[0] - x[0], p[1] - x[1], p[2] - x[2]};
+  const float magnitude = norm3(to_point[0], to_point[1], to_point[2]);
+  const float ps[3] = {p[0] - s[0], p[1] - s[1], p[2] - s[2]};
+  const float along = dot3(to_point, ps);
+  return along < 0.0f ? -magnitude : magnitude;
+}
+
+// measurement_weight (tsdf_integrator.cpp:29-44).
+float measurement_weight(int mode, float z, float d, float truncation, float eps) {
+  switch (mode) {
+    case VXG_WEIGHT_CONSTANT:
+      return 1.0f;
+    case VXG_WEIGHT_INVERSE_Z2:
+      return 1.0f / (z * z);
+    case VXG_WEIGHT_INVERSE_Z2_DROPOFF: {
+      const float base = 1.0f / (z * z);
+      if (d > -eps) return base;
+      if (d < -truncation) return 0.0f;
+      return base * (d + truncation) / (truncation - eps);
+    }
+  }
+  return 0.0f;
+}
+
+// update_tsdf_voxel (tsdf_integrator.cpp:51-67).
+void update_voxel(vxg_voxel* v, float d, float w, float truncation, float max_weight,
+                  const uint8_t* color) {
+  if (w <= 0.0f) return;
+  const float clamped = std::clamp(d, -truncation, truncation);
+  const float total = v->weight + w;
+  v->distance = (v->weight * v->distance + w * clamped) / total;
+  if (color != nullptr) {
+    auto blend = [&](uint8_t old_c, uint8_t new_c) {
+      const float mixed = (v->weight * static_cast<float>(old_c) + w * static_cast<float>(new_c)) / total;
+      return static_cast<uint8_t>(std::clamp(std::lround(mixed), 0l, 255l));
+    };
+    const uint8_t r = blend(v->r, color[0]);
+    const uint8_t g = blend(v->g, color[1]);
+    const uint8_t b = blend(v->b, color[2]);
+    v->r = r;
+    v->g = g;
+    v->b = b;
+  }
+  v->weight = std::min(total, max_weight);
+}
+
+// RayCaster (tsdf_integrator.cpp:69-104).
+struct RayCaster {
+  Key3 cur{}, end{};
+  int step[3]{};
+  float t_max[3]{}, t_delta[3]{};
+  size_t remaining = 0;
+  bool done = false;
+
+  RayCaster(const float* start, const float* end_pt, float v) {
+    cur = global_index(start, v);
+    end = global_index(end_pt, v);
+    const float dir[3] = {end_pt[0] - start[0], end_pt[1] - start[1], end_pt[2] - start[2]};
+    size_t span = 0;
+    for (int i = 0; i < 3; ++i) {
+      step[i] = dir[i] > 0.0f ? 1 : (dir[i] < 0.0f ? -1 : 0);
+      if (step[i] == 0) {
+        t_max[i] = std::numeric_limits<float>::infinity();
+        t_delta[i] = std::numeric_limits<float>::infinity();
+      } else {
+        const float boundary = static_cast<float>(cur[i] + (step[i] > 0 ? 1 : 0)) * v;
+        t_max[i] = (boundary - start[i]) / dir[i];
+        t_delta[i] = v / std::fabs(dir[i]);
+      }
+      span += static_cast<size_t>(std::abs(end[i] - cur[i]));
+    }
+    remaining = span + 1;
+  }
+
+  bool next(Key3* out) {
+    if (done || remaining == 0) return false;
+    *out = cur;
+    --remaining;
+    if (cur == end) {
+      done = true;
+      return true;
+    }
+    int axis = 0;
+    if (t_max[1] < t_max[axis]) axis = 1;
+    if (t_max[2] < t_max[axis]) axis = 2;
+    cur[axis] += step[axis];
+    t_max[axis] += t_delta[axis];
+    return true;
+  }
+};
+
+struct PointBucket {  // tsdf_integrator.h:90-95
+  double wp[3] = {0.0, 0.0, 0.0};
+  double wc[3] = {0.0, 0.0, 0.0};
+  double weight = 0.0;
+  size_t count = 0;
+};
+
+using BucketMap = std::unordered_map<Key3, PointBucket, TeschnerHash>;
+
+}  // namespace
+
+struct vxo_layer {
+  float voxel_size;
+  int vps;
+  std::unordered_map<Key3, std::vector<vxg_voxel>, BlockKeyHash> blocks;
+
+  // get_or_allocate_block (layer.h:79-87); default voxel all-zero (voxel.h:13-15).
+  std::vector<vxg_voxel>& block(const Key3& b) {
+    auto it = blocks.find(b);
+    if (it == blocks.end()) {
+      it = blocks.emplace(b, std::vector<vxg_voxel>(static_cast<size_t>(vps) * vps * vps, vxg_voxel{0.f, 0.f, 0, 0, 0, 0})).first;
+    }
+    return it->second;
+  }
+};
+
+namespace {
+
+struct Integrator {
+  const vxg_tsdf_config& c;
+  vxo_layer* layer;
+  uint64_t raycasts = 0;
+  Key3 cached_index{0, 0, 0};
+  std::vector<vxg_voxel>* cached_block = nullptr;
+
+  // cast_and_update (tsdf_integrator.cpp:129-173).
+  uint64_t cast_and_update(const float* origin, const float* sp, float weight, const uint8_t* color,
+                           const BucketMap* terminals, const Key3* own_terminal) {
+    const float v = layer->voxel_size;
+    const int vps = layer->vps;
+    const float ray[3] = {sp[0] - origin[0], sp[1] - origin[1], sp[2] - origin[2]};
+    const float depth = norm3(ray[0], ray[1], ray[2]);
+    if (depth <= 0.0f) return 0;
+    const float s = c.truncation / depth;
+    const float ray_end[3] = {sp[0] + ray[0] * s, sp[1] + ray[1] * s, sp[2] + ray[2] * s};
+    ++raycasts;
+    uint64_t updates = 0;
+    RayCaster caster(origin, ray_end, v);
+    Key3 g;
+    while (caster.next(&g)) {
+      if (terminals != nullptr && g != *own_terminal && terminals->count(g) > 0) continue;
+      // voxel_center (core.h:50-52)
+      const float x[3] = {(static_cast<float>(g[0]) + 0.5f) * v, (static_cast<float>(g[1]) + 0.5f) * v,
+                          (static_cast<float>(g[2]) + 0.5f) * v};
+      const float d = projective_distance(x, sp, origin);
+      const float w = measurement_weight(c.weight_mode, depth, d, c.truncation, c.dropoff_epsilon) * weight;
+      if (w <= 0.0f) continue;
+      // split_global_index (core.h:55-61)
+      Key3 b, local;
+      for (int i = 0; i < 3; ++i) {
+        b[i] = floor_div(g[i], vps);
+        local[i] = g[i] - b[i] * vps;
+      }
+      if (cached_block == nullptr || b != cached_index) {
+        cached_block = &layer->block(b);
+        cached_index = b;
+      }
+      const size_t lin = static_cast<size_t>(local[0]) +
+                         static_cast<size_t>(vps) * (static_cast<size_t>(local[1]) + static_cast<size_t>(vps) * static_cast<size_t>(local[2]));
+      update_voxel(&(*cached_block)[lin], d, w, c.truncation, c.max_weight, color);
+      ++updates;
+    }
+    return updates;
+  }
+};
+
+// Loop A of integrate_grouped (tsdf_integrator.cpp:196-220).
+void build_buckets(const vxg_tsdf_config& c, float v, const float* xyz, const uint8_t* rgb, size_t n,
+                   const float pose[12], BucketMap* buckets, uint64_t* skipped) {
+  const float origin[3] = {pose[3], pose[7], pose[11]};
+  buckets->reserve(n / 4 + 1);
+  const int bucket_mode = c.weight_mode == VXG_WEIGHT_CONSTANT ? VXG_WEIGHT_CONSTANT : VXG_WEIGHT_INVERSE_Z2;
+  for (size_t i = 0; i < n; ++i) {
+    float p[3];
+    transform_point(pose, xyz + 3 * i, p);
+    const float depth = norm3(p[0] - origin[0], p[1] - origin[1], p[2] - origin[2]);
+    if (depth < c.min_ray_length || depth > c.max_ray_length) {
+      ++*skipped;
+      continue;
+    }
+    const float w = measurement_weight(bucket_mode, depth, 0.0f, c.truncation, c.dropoff_epsilon);
+    PointBucket& b = (*buckets)[global_index(p, v)];
+    for (int k = 0; k < 3; ++k) b.wp[k] += static_cast<double>(w) * static_cast<double>(p[k]);
+    if (rgb != nullptr) {
+      for (int k = 0; k < 3; ++k) b.wc[k] += static_cast<double>(w) * static_cast<double>(rgb[3 * i + k]);
+    }
+    b.weight += w;
+    ++b.count;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+void vxo_config_default(vxg_tsdf_config* c) {
+  c->truncation = 0.4f;
+  c->dropoff_epsilon = 0.1f;
+  c->max_weight = 1e4f;
+  c->weight_mode = VXG_WEIGHT_INVERSE_Z2_DROPOFF;
+  c->merge_mode = VXG_MERGE_GROUPED;
+  c->min_ray_length = 0.05f;
+  c->max_ray_length = 10.0f;
+}
+
+void vxo_config_for_voxel_size(vxg_tsdf_config* c, float v) {
+  vxo_config_default(c);
+  c->truncation = 4.0f * v;
+  c->dropoff_epsilon = v;
+}
+
+int vxo_config_validate(const vxg_tsdf_config* c, char* err, size_t err_len) {
+  const char* msg = nullptr;
+  if (!(c->dropoff_epsilon > 0.0f) || !(c->dropoff_epsilon < c->truncation)) {
+    msg = "tsdf config requires 0 < dropoff_epsilon < truncation";
+  } else if (!(c->min_ray_length >= 0.0f) || !(c->min_ray_length < c->max_ray_length)) {
+    msg = "tsdf config requires 0 <= min_ray_length < max_ray_length";
+  } else if (!(c->max_weight > 0.0f)) {
+    msg = "tsdf config requires max_weight > 0";
+  } else if (c->weight_mode < 0 || c->weight_mode > 2 || c->merge_mode < 0 || c->merge_mode > 2) {
+    msg = "tsdf config has an unknown weight or merge mode";
+  }
+  if (msg == nullptr) return VXG_OK;
+  if (err != nullptr && err_len > 0) {
+    std::strncpy(err, msg, err_len - 1);
+    err[err_len - 1] = '\0';
+  }
+  return VXG_EINVAL;
+}
+
+vxo_layer* vxo_layer_create(float voxel_size, int vps) {
+  if (voxel_size <= 0.0f || vps < 1) return nullptr;  // layer.h:62-67
+  auto* l = new vxo_layer;
+  l->voxel_size = voxel_size;
+  l->vps = vps;
+  return l;
+}
+
+void vxo_layer_destroy(vxo_layer* l) { delete l; }
+
+size_t vxo_block_count(const vxo_layer* l) { return l->blocks.size(); }
+
+int vxo_integrate(vxo_layer* l, const vxg_tsdf_config* c, const float* xyz, const uint8_t* rgb, size_t n,
+                  const float pose[12], vxg_stats* out) {
+  if (vxo_config_validate(c, nullptr, 0) != VXG_OK) return VXG_EINVAL;
+  Integrator it{*c, l};
+  const float origin[3] = {pose[3], pose[7], pose[11]};
+  uint64_t updates = 0, skipped = 0;
+  if (c->merge_mode == VXG_MERGE_SIMPLE) {
+    // integrate_simple (tsdf_integrator.cpp:175-190)
+    for (size_t i = 0; i < n; ++i) {
+      float p[3];
+      transform_point(pose, xyz + 3 * i, p);
+      const float depth = norm3(p[0] - origin[0], p[1] - origin[1], p[2] - origin[2]);
+      if (depth < c->min_ray_length || depth > c->max_ray_length) {
+        ++skipped;
+        continue;
+      }
+      updates += it.cast_and_update(origin, p, 1.0f, rgb != nullptr ? rgb + 3 * i : nullptr, nullptr, nullptr);
+    }
+  } else {
+    // integrate_grouped (tsdf_integrator.cpp:192-246)
+    const bool anti_graze = c->merge_mode == VXG_MERGE_GROUPED_ANTI_GRAZE;
+    BucketMap buckets;
+    build_buckets(*c, l->voxel_size, xyz, rgb, n, pose, &buckets, &skipped);
+    const int bucket_mode = c->weight_mode == VXG_WEIGHT_CONSTANT ? VXG_WEIGHT_CONSTANT : VXG_WEIGHT_INVERSE_Z2;
+    for (const auto& [terminal, b] : buckets) {  // Loop B, map iteration order
+      if (b.weight <= 0.0) continue;
+      const float mean[3] = {static_cast<float>(b.wp[0] / b.weight), static_cast<float>(b.wp[1] / b.weight),
+                             static_cast<float>(b.wp[2] / b.weight)};
+      uint8_t color[3] = {0, 0, 0};
+      if (rgb != nullptr) {
+        for (int k = 0; k < 3; ++k) {
+          const double cc = b.wc[k] / b.weight;
+          color[k] = static_cast<uint8_t>(std::clamp(std::lround(cc), 0l, 255l));
+        }
+      }
+      const float z = norm3(mean[0] - origin[0], mean[1] - origin[1], mean[2] - origin[2]);
+      const float base_weight = static_cast<float>(b.weight) /
+                                measurement_weight(bucket_mode, z, 0.0f, c->truncation, c->dropoff_epsilon);
+      updates += it.cast_and_update(origin, mean, base_weight, rgb != nullptr ? color : nullptr,
+                                    anti_graze ? &buckets : nullptr, &terminal);
+    }
+  }
+  if (out != nullptr) {
+    out->updates = updates;
+    out->raycasts = it.raycasts;
+    out->skipped = skipped;
+  }
+  return VXG_OK;
+}
+
+size_t vxo_export_blocks(const vxo_layer* l, int32_t* idx, vxg_voxel* voxels, size_t cap) {
+  std::vector<Key3> order;
+  order.reserve(l->blocks.size());
+  for (const auto& kv : l->blocks) order.push_back(kv.first);
+  std::sort(order.begin(), order.end());  // (x,y,z) lexicographic, serialization.cpp:150-156
+  const size_t nv = static_cast<size_t>(l->vps) * l->vps * l->vps;
+  size_t k = 0;
+  for (; k < order.size() && k < cap; ++k) {
+    if (idx != nullptr) {
+      idx[3 * k + 0] = order[k][0];
+      idx[3 * k + 1] = order[k][1];
+      idx[3 * k + 2] = order[k][2];
+    }
+    if (voxels != nullptr) std::memcpy(voxels + k * nv, l->blocks.at(order[k]).data(), nv * sizeof(vxg_voxel));
+  }
+  return k;
+}
+
+int vxo_voxel(const vxo_layer* l, int32_t gx, int32_t gy, int32_t gz, vxg_voxel* out) {
+  const int vps = l->vps;
+  const Key3 g{gx, gy, gz};
+  Key3 b, local;
+  for (int i = 0; i < 3; ++i) {
+    b[i] = floor_div(g[i], vps);
+    local[i] = g[i] - b[i] * vps;
+  }
+  auto it = l->blocks.find(b);
+  if (it == l->blocks.end()) return 0;
+  *out = it->second[static_cast<size_t>(local[0]) + vps * (static_cast<size_t>(local[1]) + vps * static_cast<size_t>(local[2]))];
+  return 1;
+}
+
+int vxo_set_block(vxo_layer* l, const int32_t idx[3], const vxg_voxel* voxels) {
+  auto& blk = l->block(Key3{idx[0], idx[1], idx[2]});
+  std::memcpy(blk.data(), voxels, blk.size() * sizeof(vxg_voxel));
+  return VXG_OK;
+}
+
+size_t vxo_save_vxblx(const vxo_layer* l, uint8_t* buf, size_t cap) {
+  const size_t nv = static_cast<size_t>(l->vps) * l->vps * l->vps;
+  const size_t need = 6 + 4 + 8 + 4 + 1 + 8 + l->blocks.size() * (24 + nv * 12);
+  if (buf == nullptr || cap < need) return need;
+  uint8_t* o = buf;
+  auto put = [&](const void* src, size_t len) {  // little-endian host (x86-64)
+    std::memcpy(o, src, len);
+    o += len;
+  };
+  const char magic[6] = {'V', 'X', 'B', 'L', 'X', '\0'};
+  const uint32_t version = 1;
+  const double vs = static_cast<double>(l->voxel_size);
+  const uint32_t vps = static_cast<uint32_t>(l->vps);
+  const uint8_t kind = 0;
+  const uint64_t count = l->blocks.size();
+  put(magic, 6);
+  put(&version, 4);
+  put(&vs, 8);
+  put(&vps, 4);
+  put(&kind, 1);
+  put(&count, 8);
+  std::vector<Key3> order;
+  for (const auto& kv : l->blocks) order.push_back(kv.first);
+  std::sort(order.begin(), order.end());
+  for (const Key3& k : order) {
+    for (int i = 0; i < 3; ++i) {
+      const int64_t v = k[i];
+      put(&v, 8);
+    }
+    for (const vxg_voxel& vx : l->blocks.at(k)) {
+      put(&vx.distance, 4);
+      put(&vx.weight, 4);
+      const uint8_t rgbp[4] = {vx.r, vx.g, vx.b, 0};
+      put(rgbp, 4);
+    }
+  }
+  return need;
+}
+
+float vxo_projective_distance(const float x[3], const float p[3], const float s[3]) {
+  return projective_distance(x, p, s);
+}
+
+float vxo_measurement_weight(int mode, float z, float d, float truncation, float eps) {
+  return measurement_weight(mode, z, d, truncation, eps);
+}
+
+void vxo_update_voxel(vxg_voxel* v, float d, float w, float truncation, float max_weight, const uint8_t* color) {
+  update_voxel(v, d, w, truncation, max_weight, color);
+}
+
+size_t vxo_raycast(const float start[3], const float end[3], float voxel_size, int32_t* out, size_t cap) {
+  RayCaster caster(start, end, voxel_size);
+  Key3 g;
+  size_t k = 0;
+  while (caster.next(&g)) {
+    if (k < cap) {
+      out[3 * k + 0] = g[0];
+      out[3 * k + 1] = g[1];
+      out[3 * k + 2] = g[2];
+    }
+    ++k;
+  }
+  return k;
+}
+
+void vxo_global_index(const float p[3], float voxel_size, int32_t out[3]) {
+  const Key3 g = global_index(p, voxel_size);
+  out[0] = g[0];
+  out[1] = g[1];
+  out[2] = g[2];
+}
+
+uint64_t vxo_index_hash(int32_t x, int32_t y, int32_t z) { return TeschnerHash()(Key3{x, y, z}); }
+
+size_t vxo_grouped_ray_order(const vxg_tsdf_config* c, float voxel_size, const float* xyz, size_t n,
+                             const float pose[12], int32_t* keys, size_t cap) {
+  BucketMap buckets;
+  uint64_t skipped = 0;
+  build_buckets(*c, voxel_size, xyz, nullptr, n, pose, &buckets, &skipped);
+  size_t k = 0;
+  for (const auto& kv : buckets) {
+    if (k < cap) {
+      keys[3 * k + 0] = kv.first[0];
+      keys[3 * k + 1] = kv.first[1];
+      keys[3 * k + 2] = kv.first[2];
+    }
+    ++k;
+  }
+  return k;
+}
+
+size_t vxo_bucket_schedule(size_t n_points, size_t max_keys, uint64_t* out, size_t cap) {
+  struct Ident {
+    size_t operator()(uint64_t k) const { return static_cast<size_t>(k); }
+  };
+  std::unordered_map<uint64_t, char, Ident> m;
+  m.reserve(n_points / 4 + 1);
+  size_t e = 0;
+  auto emit = [&](uint64_t before, uint64_t bc) {
+    if (e < cap) {
+      out[2 * e] = before;
+      out[2 * e + 1] = bc;
+    }
+    ++e;
+  };
+  emit(0, m.bucket_count());
+  for (size_t k = 0; k < max_keys; ++k) {
+    const size_t before = m.bucket_count();
+    m.emplace(k, 0);
+    if (m.bucket_count() != before) emit(k, m.bucket_count());
+  }
+  return e;
+}
+
+}  // extern "C"

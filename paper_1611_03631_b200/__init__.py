@@ -1,0 +1,13 @@
+"""B200-native (sm_100a) TSDF integration — the voxblox (arXiv 1611.03631) hot path.
+
+Product: libvxg.so (hand-written CUDA kernels + C ABI, include/vxg.h) and this
+Python mirror of the reference integrator interface (tsdf.py). The CPU oracle
+under oracle/ is test infrastructure and is never imported from here.
+"""
+from .tsdf import (K_TSDF_OBSERVED_WEIGHT, VOXEL_DTYPE, MergeMode, ParseError, Scan, TsdfConfig, TsdfIntegrator,
+                   TsdfLayer, WeightMode, measurement_weight, pose_3x4, projective_distance, raycast,
+                   update_tsdf_voxels)
+
+__all__ = ["WeightMode", "MergeMode", "TsdfConfig", "Scan", "TsdfLayer", "TsdfIntegrator", "ParseError",
+           "projective_distance", "measurement_weight", "update_tsdf_voxels", "raycast", "VOXEL_DTYPE",
+           "K_TSDF_OBSERVED_WEIGHT", "pose_3x4"]

@@ -1,0 +1,583 @@
+// Kernels of the B200 TSDF integration pipeline.
+//
+// Data layout in HBM:
+//   slab       : cap_blocks x vps^3 vxg_voxel (12 B AoS, x-fastest = the VXBLX
+//                voxel payload, serialization.cpp:107-114), zero = default voxel
+//   block hash : open addressing, linear probing, 2^k x (u64 packed key, i32 slot)
+//   records    : per voxel update u32 sort key (slot*vps^3 + local) + u32 seq
+//                + 16 B payload {d, w, rgb|has_color<<31, 0}
+#pragma once
+
+#include <cstdint>
+
+#include "vxg_device.cuh"
+
+namespace vxg {
+
+struct alignas(16) SegInfo {  // one bucket of integrate_grouped's Loop A (tsdf_integrator.h:90-95)
+  float mean[3];
+  float base_weight;  // float(sum w) / measurement_weight(mean)  (tsdf_integrator.cpp:236-241)
+  int32_t g[3];       // terminal voxel
+  uint32_t color;     // r | g<<8 | b<<16 | has_color<<31
+  uint64_t hash;      // IndexHash(terminal)
+  uint32_t frame;
+  uint32_t pos;       // first point index within the frame (first appearance)
+  uint32_t cast;      // bucket.weight > 0 (tsdf_integrator.cpp:224)
+  uint32_t pad[3];
+};
+
+struct alignas(16) RayInfo {  // one cast_and_update call (tsdf_integrator.cpp:129-173), in ray order
+  float p[3];        // surface point (world)
+  float weight;      // merged base weight (1.0f in simple mode)
+  uint32_t color;    // r | g<<8 | b<<16 | has_color<<31
+  uint32_t frame;
+  uint32_t valid;
+  uint32_t pad;
+  int32_t term[3];   // own terminal voxel (anti-graze)
+  uint32_t pad2;
+};
+
+struct alignas(16) Record {
+  float d;
+  float w;
+  uint32_t color;
+  uint32_t pad;
+};
+
+struct TsdfParams {
+  float voxel_size;
+  float truncation;
+  float dropoff_epsilon;
+  float max_weight;
+  float min_ray;
+  float max_ray;
+  int weight_mode;
+  int merge_mode;
+};
+
+__device__ __forceinline__ uint32_t frame_of(const uint64_t* off, uint32_t F, uint64_t i) {
+  uint32_t lo = 0, hi = F;
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (off[mid] <= i) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ uint32_t pack_color(const uint8_t* c) {
+  return static_cast<uint32_t>(c[0]) | (static_cast<uint32_t>(c[1]) << 8) | (static_cast<uint32_t>(c[2]) << 16) |
+         0x80000000u;
+}
+
+// ---------------------------------------------------------------- simple mode
+// integrate_simple (tsdf_integrator.cpp:175-190) range filter: flag[i] = in range.
+__global__ void k_simple_inrange(const float* __restrict__ xyz, uint64_t P, const uint64_t* __restrict__ off,
+                                 const float* __restrict__ poses, uint32_t F, TsdfParams tp,
+                                 uint32_t* __restrict__ flag, unsigned long long* __restrict__ skipped) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < P;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t f = frame_of(off, F, i);
+    const float* Pm = poses + 12 * f;
+    float p[3];
+    transform_point(Pm, xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], p);
+    const float depth = norm3(fsub(p[0], Pm[3]), fsub(p[1], Pm[7]), fsub(p[2], Pm[11]));
+    const bool in = !(depth < tp.min_ray || depth > tp.max_ray);
+    flag[i] = in ? 1u : 0u;
+    if (!in) atomicAdd(&skipped[f], 1ull);
+  }
+}
+
+__global__ void k_simple_rays(const float* __restrict__ xyz, const uint8_t* __restrict__ rgb, uint64_t P,
+                              const uint64_t* __restrict__ off, const float* __restrict__ poses, uint32_t F,
+                              const uint32_t* __restrict__ flag, const uint32_t* __restrict__ ray_idx,
+                              RayInfo* __restrict__ rays) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < P;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    if (!flag[i]) continue;
+    const uint32_t f = frame_of(off, F, i);
+    const float* Pm = poses + 12 * f;
+    RayInfo r;
+    transform_point(Pm, xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], r.p);
+    r.weight = 1.0f;
+    r.color = rgb != nullptr ? pack_color(rgb + 3 * i) : 0u;
+    r.frame = f;
+    r.valid = 1u;
+    r.pad = 0u;
+    r.term[0] = r.term[1] = r.term[2] = 0;
+    r.pad2 = 0u;
+    rays[ray_idx[i]] = r;
+  }
+}
+
+// ---------------------------------------------------------------- grouped mode
+// Loop A key: (frame, terminal voxel relative to the origin voxel); out-of-range
+// points get the frame's sentinel (all-ones voxel field) and are counted later.
+__global__ void k_group_keys(const float* __restrict__ xyz, uint64_t P, const uint64_t* __restrict__ off,
+                             const float* __restrict__ poses, uint32_t F, TsdfParams tp, int rb, int kb,
+                             unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals,
+                             uint32_t* __restrict__ counters) {
+  const uint64_t field_mask = (1ull << (3 * kb)) - 1ull;
+  const int lim = (1 << kb) - 1;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < P;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t f = frame_of(off, F, i);
+    const float* Pm = poses + 12 * f;
+    float p[3];
+    transform_point(Pm, xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], p);
+    const float depth = norm3(fsub(p[0], Pm[3]), fsub(p[1], Pm[7]), fsub(p[2], Pm[11]));
+    uint64_t key = (static_cast<uint64_t>(f) << (3 * kb)) | field_mask;
+    if (!(depth < tp.min_ray || depth > tp.max_ray)) {
+      int e[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) e[k] = gidx(p[k], tp.voxel_size) - gidx(Pm[4 * k + 3], tp.voxel_size) + rb;
+      if (e[0] < 0 || e[0] >= lim || e[1] < 0 || e[1] >= lim || e[2] < 0 || e[2] >= lim) {
+        atomicOr(&counters[1], static_cast<uint32_t>(kErrKeyRange));
+      } else {
+        key = (static_cast<uint64_t>(f) << (3 * kb)) | (static_cast<uint64_t>(e[0]) << (2 * kb)) |
+              (static_cast<uint64_t>(e[1]) << kb) | static_cast<uint64_t>(e[2]);
+      }
+    }
+    keys[i] = key;
+    vals[i] = static_cast<uint32_t>(i);
+  }
+}
+
+// Per bucket: sequential fp64 sums in scan order (tsdf_integrator.cpp:213-219),
+// then the merged ray (:224-241).
+__global__ void k_seg_reduce(const uint32_t* __restrict__ num_segs_p, const unsigned long long* __restrict__ ukeys,
+                             const uint32_t* __restrict__ uoffs, const uint32_t* __restrict__ ucounts,
+                             const uint32_t* __restrict__ svals, const float* __restrict__ xyz,
+                             const uint8_t* __restrict__ rgb, const uint64_t* __restrict__ off,
+                             const float* __restrict__ poses, TsdfParams tp, int rb, int kb,
+                             SegInfo* __restrict__ segs, uint32_t* __restrict__ seg_count,
+                             uint32_t* __restrict__ seg_start, unsigned long long* __restrict__ skipped) {
+  const uint32_t S = *num_segs_p;
+  const uint64_t field_mask = (1ull << (3 * kb)) - 1ull;
+  const uint64_t kmask = (1ull << kb) - 1ull;
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x) {
+    const uint64_t key = ukeys[s];
+    const uint32_t f = static_cast<uint32_t>(key >> (3 * kb));
+    const uint32_t start = uoffs[s], cnt = ucounts[s];
+    SegInfo out;
+    out.frame = f;
+    if ((key & field_mask) == field_mask) {  // out-of-range points (tsdf_integrator.cpp:204-207)
+      atomicAdd(&skipped[f], static_cast<unsigned long long>(cnt));
+      out.cast = 0xFFFFFFFFu;  // marks "not a bucket"
+      segs[s] = out;
+      continue;
+    }
+    atomicAdd(&seg_count[f], 1u);
+    atomicMin(&seg_start[f], s);
+    const float* Pm = poses + 12 * f;
+    const float o[3] = {Pm[3], Pm[7], Pm[11]};
+    double wp[3] = {0.0, 0.0, 0.0}, wc[3] = {0.0, 0.0, 0.0}, W = 0.0;
+    const uint32_t first = svals[start];
+    for (uint32_t j = 0; j < cnt; ++j) {
+      const uint32_t i = svals[start + j];
+      float p[3];
+      transform_point(Pm, xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], p);
+      const float depth = norm3(fsub(p[0], o[0]), fsub(p[1], o[1]), fsub(p[2], o[2]));
+      const float w = tp.weight_mode == VXG_WEIGHT_CONSTANT ? 1.0f : fdiv(1.0f, fmul(depth, depth));
+      const double wd = static_cast<double>(w);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) wp[k] = __dadd_rn(wp[k], __dmul_rn(wd, static_cast<double>(p[k])));
+      if (rgb != nullptr) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) wc[k] = __dadd_rn(wc[k], __dmul_rn(wd, static_cast<double>(rgb[3 * i + k])));
+      }
+      W = __dadd_rn(W, wd);
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) out.mean[k] = __double2float_rn(__ddiv_rn(wp[k], W));
+    uint32_t col = 0u;
+    if (rgb != nullptr) {
+      col = 0x80000000u;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        long l = lround(__ddiv_rn(wc[k], W));
+        l = l < 0l ? 0l : (255l < l ? 255l : l);
+        col |= static_cast<uint32_t>(l) << (8 * k);
+      }
+    }
+    out.color = col;
+    const float z = norm3(fsub(out.mean[0], o[0]), fsub(out.mean[1], o[1]), fsub(out.mean[2], o[2]));
+    const float mw = tp.weight_mode == VXG_WEIGHT_CONSTANT ? 1.0f : fdiv(1.0f, fmul(z, z));
+    out.base_weight = fdiv(__double2float_rn(W), mw);
+    const int og[3] = {gidx(o[0], tp.voxel_size), gidx(o[1], tp.voxel_size), gidx(o[2], tp.voxel_size)};
+    out.g[0] = static_cast<int32_t>((key >> (2 * kb)) & kmask) - rb + og[0];
+    out.g[1] = static_cast<int32_t>((key >> kb) & kmask) - rb + og[1];
+    out.g[2] = static_cast<int32_t>(key & kmask) - rb + og[2];
+    out.hash = teschner_hash(out.g[0], out.g[1], out.g[2]);
+    out.pos = static_cast<uint32_t>(first - off[f]);
+    out.cast = W > 0.0 ? 1u : 0u;
+    segs[s] = out;
+  }
+}
+
+// Ray order: libstdc++ iteration order = groups by first
+// occupation time of their bucket (descending), then insertion position
+// (descending). fo[bucket] = min position over the bucket's keys.
+__global__ void k_order_fo(uint32_t S, const SegInfo* __restrict__ segs, const uint32_t* __restrict__ pos,
+                           const uint32_t* __restrict__ part, const uint64_t* __restrict__ tbl_off,
+                           const uint64_t* __restrict__ bc, uint32_t* __restrict__ fo) {
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x) {
+    const SegInfo& g = segs[s];
+    if (g.cast == 0xFFFFFFFFu) continue;
+    if (part != nullptr && !part[s]) continue;
+    const uint32_t ps = pos != nullptr ? pos[s] : g.pos;
+    atomicMin(&fo[tbl_off[g.frame] + g.hash % bc[g.frame]], ps);
+  }
+}
+
+__global__ void k_order_keys(uint32_t S, const SegInfo* __restrict__ segs, const uint32_t* __restrict__ pos,
+                             const uint32_t* __restrict__ part, const uint64_t* __restrict__ tbl_off,
+                             const uint64_t* __restrict__ bc, const uint32_t* __restrict__ fo, int pb,
+                             unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals) {
+  const uint64_t M = (1ull << pb) - 1ull;
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x) {
+    const SegInfo& g = segs[s];
+    uint64_t key = ~0ull;
+    if (g.cast != 0xFFFFFFFFu) {
+      const uint32_t ps = pos != nullptr ? pos[s] : g.pos;
+      const bool in = part == nullptr || part[s];
+      if (in) {
+        const uint64_t first = fo[tbl_off[g.frame] + g.hash % bc[g.frame]];
+        key = (static_cast<uint64_t>(g.frame) << (2 * pb + 1)) | ((M - first) << pb) | (M - ps);
+      } else {
+        key = (static_cast<uint64_t>(g.frame) << (2 * pb + 1)) | (1ull << (2 * pb)) | ps;
+      }
+    }
+    keys[s] = key;
+    vals[s] = s;
+  }
+}
+
+__global__ void k_gather_rays(uint32_t R, const uint32_t* __restrict__ order, const SegInfo* __restrict__ segs,
+                              RayInfo* __restrict__ rays) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < R; j += gridDim.x * blockDim.x) {
+    const SegInfo& g = segs[order[j]];
+    RayInfo r;
+    r.p[0] = g.mean[0];
+    r.p[1] = g.mean[1];
+    r.p[2] = g.mean[2];
+    r.weight = g.base_weight;
+    r.color = g.color;
+    r.frame = g.frame;
+    r.valid = g.cast;
+    r.pad = 0u;
+    r.term[0] = g.g[0];
+    r.term[1] = g.g[1];
+    r.term[2] = g.g[2];
+    r.pad2 = 0u;
+    rays[j] = r;
+  }
+}
+
+// ---------------------------------------------------------------- rays -> records
+// cast_and_update's prologue (tsdf_integrator.cpp:135-143): exactly span+1
+// voxels per ray, so record offsets are known before traversal.
+__global__ void k_ray_count(uint32_t R, const RayInfo* __restrict__ rays, const float* __restrict__ poses,
+                            TsdfParams tp, unsigned long long* __restrict__ counts,
+                            unsigned long long* __restrict__ raycasts) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < R; j += gridDim.x * blockDim.x) {
+    const RayInfo r = rays[j];
+    uint64_t c = 0;
+    if (r.valid == 1u) {
+      const float* Pm = poses + 12 * r.frame;
+      const float ray[3] = {fsub(r.p[0], Pm[3]), fsub(r.p[1], Pm[7]), fsub(r.p[2], Pm[11])};
+      const float depth = norm3(ray[0], ray[1], ray[2]);
+      if (!(depth <= 0.0f)) {
+        atomicAdd(&raycasts[r.frame], 1ull);
+        const float s = fdiv(tp.truncation, depth);
+        Dda dda;
+        dda.init(Pm[3], Pm[7], Pm[11], fadd(r.p[0], fmul(ray[0], s)), fadd(r.p[1], fmul(ray[1], s)),
+                 fadd(r.p[2], fmul(ray[2], s)), tp.voxel_size);
+        c = static_cast<uint64_t>(dda.span) + 1ull;
+      }
+    }
+    counts[j] = c;
+  }
+}
+
+struct TermView {  // per-frame sorted terminal keys for the anti-graze probe
+  const unsigned long long* keys;
+  const uint32_t* start;
+  const uint32_t* count;
+  int rb;
+  int kb;
+};
+
+__device__ __forceinline__ bool is_terminal(const TermView& tv, uint32_t f, const int* og, const int* g) {
+  const int lim = (1 << tv.kb) - 1;
+  int e[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    e[k] = g[k] - og[k] + tv.rb;
+    if (e[k] < 0 || e[k] >= lim) return false;
+  }
+  const uint64_t key = (static_cast<uint64_t>(f) << (3 * tv.kb)) | (static_cast<uint64_t>(e[0]) << (2 * tv.kb)) |
+                       (static_cast<uint64_t>(e[1]) << tv.kb) | static_cast<uint64_t>(e[2]);
+  uint32_t lo = tv.start[f], n = tv.count[f];
+  while (n > 0) {
+    const uint32_t half = n >> 1;
+    const uint64_t k = tv.keys[lo + half];
+    if (k < key) { lo += half + 1; n -= half + 1; } else { n = half; }
+  }
+  return lo < tv.start[f] + tv.count[f] && tv.keys[lo] == key;
+}
+
+// cast_and_update's loop (tsdf_integrator.cpp:145-171): walk, weigh, allocate,
+// emit one record per update at offset[ray] + k; skipped candidates emit an
+// invalid key (sorted past every voxel, never folded).
+__global__ void k_emit(uint32_t R0, uint32_t R1, const RayInfo* __restrict__ rays,
+                       const unsigned long long* __restrict__ roff, uint64_t base, const float* __restrict__ poses,
+                       TsdfParams tp, MapView map, TermView tv, uint32_t* __restrict__ rkeys,
+                       uint32_t* __restrict__ rvals, Record* __restrict__ recs,
+                       unsigned long long* __restrict__ updates) {
+  for (uint32_t j = R0 + blockIdx.x * blockDim.x + threadIdx.x; j < R1; j += gridDim.x * blockDim.x) {
+    const RayInfo r = rays[j];
+    if (r.valid != 1u) continue;
+    const float* Pm = poses + 12 * r.frame;
+    const float o[3] = {Pm[3], Pm[7], Pm[11]};
+    const float ray[3] = {fsub(r.p[0], o[0]), fsub(r.p[1], o[1]), fsub(r.p[2], o[2])};
+    const float depth = norm3(ray[0], ray[1], ray[2]);
+    if (depth <= 0.0f) continue;
+    const float s = fdiv(tp.truncation, depth);
+    Dda dda;
+    dda.init(o[0], o[1], o[2], fadd(r.p[0], fmul(ray[0], s)), fadd(r.p[1], fmul(ray[1], s)),
+             fadd(r.p[2], fmul(ray[2], s)), tp.voxel_size);
+    const uint32_t count = dda.span + 1u;
+    const uint64_t out0 = roff[j] - base;
+    int og[3] = {0, 0, 0};
+    const bool anti = tp.merge_mode == VXG_MERGE_GROUPED_ANTI_GRAZE;
+    if (anti) {
+      og[0] = gidx(o[0], tp.voxel_size);
+      og[1] = gidx(o[1], tp.voxel_size);
+      og[2] = gidx(o[2], tp.voxel_size);
+    }
+    int cb[3] = {0x7fffffff, 0, 0};
+    int32_t cslot = -1;
+    uint32_t valid = 0;
+    const int vps = map.vps;
+    for (uint32_t k = 0; k < count; ++k) {
+      const int g[3] = {dda.cur[0], dda.cur[1], dda.cur[2]};
+      uint32_t key = kInvalidRecord;
+      Record rec{0.0f, 0.0f, 0u, 0u};
+      bool skip = anti && !(g[0] == r.term[0] && g[1] == r.term[1] && g[2] == r.term[2]) &&
+                  is_terminal(tv, r.frame, og, g);
+      if (!skip) {
+        const float x0 = vcenter(g[0], tp.voxel_size), x1 = vcenter(g[1], tp.voxel_size),
+                    x2 = vcenter(g[2], tp.voxel_size);
+        const float d = projective_distance(x0, x1, x2, r.p[0], r.p[1], r.p[2], o[0], o[1], o[2]);
+        const float w = fmul(measurement_weight(tp.weight_mode, depth, d, tp.truncation, tp.dropoff_epsilon),
+                             r.weight);
+        if (w <= 0.0f) {
+          skip = true;
+        } else {
+          int b[3], l[3];
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            b[a] = floor_div(g[a], vps);
+            l[a] = g[a] - b[a] * vps;
+          }
+          if (b[0] != cb[0] || b[1] != cb[1] || b[2] != cb[2]) {
+            cb[0] = b[0];
+            cb[1] = b[1];
+            cb[2] = b[2];
+            if (block_in_range(b[0], b[1], b[2])) {
+              cslot = map.find_or_insert(pack_block(b[0], b[1], b[2]), b[0], b[1], b[2]);
+            } else {
+              atomicOr(&map.counters[1], static_cast<uint32_t>(kErrKeyRange));
+              cslot = -1;
+            }
+          }
+          if (cslot >= 0) {
+            key = static_cast<uint32_t>(cslot) * static_cast<uint32_t>(map.nvox) +
+                  static_cast<uint32_t>(l[0] + vps * (l[1] + vps * l[2]));
+          }
+          rec.d = d;
+          rec.w = w;
+          rec.color = r.color;
+          ++valid;
+        }
+      }
+      const uint64_t o_idx = out0 + k;
+      rkeys[o_idx] = key;
+      rvals[o_idx] = static_cast<uint32_t>(o_idx);
+      recs[o_idx] = rec;
+      if (k + 1 < count && !dda.at_end()) dda.advance();
+    }
+    if (valid) atomicAdd(&updates[r.frame], static_cast<unsigned long long>(valid));
+  }
+}
+
+// update_tsdf_voxel applied per voxel in (frame, ray-order) order: records are
+// stably sorted by voxel key, so each run head folds its run sequentially.
+__global__ void k_fold(uint64_t T, const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ svals,
+                       const Record* __restrict__ recs, MapView map, TsdfParams tp, uint8_t* __restrict__ touched) {
+  if (map.counters[1] != 0u) return;  // emission failed (slab/hash full): host grows and replays
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < T;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t key = skeys[i];
+    if (key == kInvalidRecord) continue;
+    if (i > 0 && skeys[i - 1] == key) continue;
+    vxg_voxel* vp = map.slab + key;
+    float D = vp->distance, W = vp->weight;
+    uint32_t rgb = static_cast<uint32_t>(vp->r) | (static_cast<uint32_t>(vp->g) << 8) |
+                   (static_cast<uint32_t>(vp->b) << 16);
+    for (uint64_t j = i; j < T && skeys[j] == key; ++j) {
+      const Record rec = recs[svals[j]];
+      update_voxel(D, W, rgb, rec.d, rec.w, rec.color, (rec.color >> 31) != 0u, tp.truncation, tp.max_weight);
+    }
+    vp->distance = D;
+    vp->weight = W;
+    vp->r = static_cast<uint8_t>(rgb & 0xffu);
+    vp->g = static_cast<uint8_t>((rgb >> 8) & 0xffu);
+    vp->b = static_cast<uint8_t>((rgb >> 16) & 0xffu);
+    if (touched != nullptr) touched[key / static_cast<uint32_t>(map.nvox)] = 1u;
+  }
+}
+
+__global__ void k_add_u64(uint32_t n, unsigned long long* __restrict__ dst, const unsigned long long* __restrict__ src) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] += src[i];
+}
+
+// ---------------------------------------------------------------- map maintenance
+__global__ void k_fix_block_idx(uint64_t hcap, const unsigned long long* __restrict__ hkeys,
+                                const int32_t* __restrict__ hvals, uint32_t lo, uint32_t hi,
+                                int32_t* __restrict__ block_idx) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < hcap;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t k = hkeys[i];
+    const int32_t s = hvals[i];
+    if (k == kEmptyKey || s < 0) continue;
+    if (static_cast<uint32_t>(s) >= lo && static_cast<uint32_t>(s) < hi) {
+      int b[3];
+      unpack_block(k, b);
+      block_idx[3 * s + 0] = b[0];
+      block_idx[3 * s + 1] = b[1];
+      block_idx[3 * s + 2] = b[2];
+    }
+  }
+}
+
+__global__ void k_rehash(uint64_t old_cap, const unsigned long long* __restrict__ okeys,
+                         const int32_t* __restrict__ ovals, MapView map) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < old_cap;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const unsigned long long k = okeys[i];
+    if (k == kEmptyKey) continue;
+    uint64_t j = mix64(k) & map.hmask;
+    while (true) {
+      const unsigned long long prev = atomicCAS(&map.hkeys[j], kEmptyKey, k);
+      if (prev == kEmptyKey) {
+        map.hvals[j] = ovals[i];
+        break;
+      }
+      j = (j + 1) & map.hmask;
+    }
+  }
+}
+
+__global__ void k_import_slots(uint64_t n, const int32_t* __restrict__ idx, MapView map, int32_t* __restrict__ slots) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const int b0 = idx[3 * i], b1 = idx[3 * i + 1], b2 = idx[3 * i + 2];
+    if (!block_in_range(b0, b1, b2)) {
+      atomicOr(&map.counters[1], static_cast<uint32_t>(kErrKeyRange));
+      slots[i] = -1;
+      continue;
+    }
+    slots[i] = map.find_or_insert(pack_block(b0, b1, b2), b0, b1, b2);
+  }
+}
+
+__global__ void k_scatter_blocks(uint64_t n, const int32_t* __restrict__ slots, const vxg_voxel* __restrict__ src,
+                                 MapView map) {
+  const uint64_t nv = static_cast<uint64_t>(map.nvox);
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n * nv;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t b = i / nv;
+    const int32_t s = slots[b];
+    if (s < 0) continue;
+    map.slab[static_cast<uint64_t>(s) * nv + (i - b * nv)] = src[i];
+  }
+}
+
+__global__ void k_query(uint64_t n, const int32_t* __restrict__ g, MapView map, vxg_voxel* __restrict__ out,
+                        uint8_t* __restrict__ found) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    int b[3], l[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      b[a] = floor_div(g[3 * i + a], map.vps);
+      l[a] = g[3 * i + a] - b[a] * map.vps;
+    }
+    int32_t s = -1;
+    if (block_in_range(b[0], b[1], b[2])) s = map.find(pack_block(b[0], b[1], b[2]));
+    if (s < 0 || static_cast<uint32_t>(s) >= map.cap_blocks) {
+      found[i] = 0u;
+      out[i] = vxg_voxel{0.0f, 0.0f, 0, 0, 0, 0};
+    } else {
+      found[i] = 1u;
+      out[i] = map.slab[static_cast<uint64_t>(s) * map.nvox + l[0] + map.vps * (l[1] + map.vps * l[2])];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- free-function evaluation
+__global__ void k_eval_pd(uint64_t n, const float* x, const float* p, const float* s, float* out) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    out[i] = projective_distance(x[3 * i], x[3 * i + 1], x[3 * i + 2], p[3 * i], p[3 * i + 1], p[3 * i + 2],
+                                 s[3 * i], s[3 * i + 1], s[3 * i + 2]);
+  }
+}
+
+__global__ void k_eval_mw(uint64_t n, int mode, const float* z, const float* d, float trunc, float eps, float* out) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    out[i] = measurement_weight(mode, z[i], d[i], trunc, eps);
+  }
+}
+
+__global__ void k_eval_update(uint64_t nv, vxg_voxel* voxels, const uint64_t* starts, const float* d, const float* w,
+                              const uint8_t* rgb, float trunc, float wmax) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < nv;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    float D = voxels[i].distance, W = voxels[i].weight;
+    uint32_t c = static_cast<uint32_t>(voxels[i].r) | (static_cast<uint32_t>(voxels[i].g) << 8) |
+                 (static_cast<uint32_t>(voxels[i].b) << 16);
+    for (uint64_t j = starts[i]; j < starts[i + 1]; ++j) {
+      const uint32_t col = rgb != nullptr ? pack_color(rgb + 3 * j) : 0u;
+      update_voxel(D, W, c, d[j], w[j], col, rgb != nullptr, trunc, wmax);
+    }
+    voxels[i].distance = D;
+    voxels[i].weight = W;
+    voxels[i].r = static_cast<uint8_t>(c & 0xffu);
+    voxels[i].g = static_cast<uint8_t>((c >> 8) & 0xffu);
+    voxels[i].b = static_cast<uint8_t>((c >> 16) & 0xffu);
+  }
+}
+
+__global__ void k_eval_raycast(uint64_t n, const float* start, const float* end, float v, uint32_t* counts,
+                               const uint64_t* offsets, int32_t* out) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    Dda dda;
+    dda.init(start[3 * i], start[3 * i + 1], start[3 * i + 2], end[3 * i], end[3 * i + 1], end[3 * i + 2], v);
+    const uint32_t count = dda.span + 1u;
+    counts[i] = count;
+    if (out == nullptr) continue;
+    int32_t* o = out + 3 * offsets[i];
+    for (uint32_t k = 0; k < count; ++k) {
+      o[3 * k + 0] = dda.cur[0];
+      o[3 * k + 1] = dda.cur[1];
+      o[3 * k + 2] = dda.cur[2];
+      if (k + 1 < count && !dda.at_end()) dda.advance();
+    }
+  }
+}
+
+}  // namespace vxg

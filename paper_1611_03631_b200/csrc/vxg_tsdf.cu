@@ -1,0 +1,1302 @@
+// Host orchestration of the B200 TSDF pipeline behind the C ABI (include/vxg.h).
+//
+// Per batch of frames (results identical to sequential per-frame integrate()):
+//   simple : K1 range filter -> scan -> rays (point order)
+//   grouped: K1 keys -> radix sort -> run-length -> K2 fp64 bucket reduce
+//            -> K3 libstdc++ ray order (fo[bucket] atomicMin + sort) -> rays
+//   common : ray span count -> scan -> K4 emit records (+ K6 block alloc)
+//            -> K5 stable radix sort by voxel -> K7 ordered fold
+// Sorting/scans use CUB (CCCL 2.8, header-only, compiled into this library).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_run_length_encode.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "../../include/vxg.h"
+#include "vxg_kernels.cuh"
+
+namespace vxg {
+using Schedule = std::vector<std::pair<uint64_t, uint64_t>>;
+Schedule bucket_schedule(uint64_t n_points, uint64_t max_keys);
+}  // namespace vxg
+
+using namespace vxg;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Status {
+  int code;
+  std::string msg;
+};
+
+struct VxgError : std::runtime_error {
+  int code;
+  VxgError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CU(x)                                                                                   \
+  do {                                                                                          \
+    cudaError_t e_ = (x);                                                                       \
+    if (e_ != cudaSuccess) {                                                                    \
+      throw VxgError(VXG_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_));               \
+    }                                                                                           \
+  } while (0)
+
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  // Grow-only; contents are NOT preserved.
+  T* ensure(size_t n) {
+    if (n <= cap && p) return p;
+    release();
+    size_t want = std::max<size_t>(n + n / 4, 256);
+    CU(cudaMalloc(&p, want * sizeof(T)));
+    cap = want;
+    return p;
+  }
+};
+
+constexpr int kStages = 8;
+const char* kStageNames[kStages] = {"h2d", "bundle", "ray_order", "ray_setup", "emit", "record_sort", "apply", "d2h"};
+enum Stage { ST_H2D = 0, ST_BUNDLE, ST_ORDER, ST_RAYS, ST_EMIT, ST_SORT, ST_APPLY, ST_D2H };
+
+int bits_for(uint64_t v) {  // smallest b with v < 2^b
+  int b = 0;
+  while (b < 64 && (v >> b) != 0) ++b;
+  return b;
+}
+
+unsigned grid_for(uint64_t n, unsigned block = 256) {
+  uint64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > 148ull * 16) g = 148ull * 16;
+  return static_cast<unsigned>(g);
+}
+
+std::string validate_config(const vxg_tsdf_config* c) {  // TsdfConfig::validate, tsdf_integrator.cpp:10-20
+  if (!(c->dropoff_epsilon > 0.0f) || !(c->dropoff_epsilon < c->truncation))
+    return "tsdf config requires 0 < dropoff_epsilon < truncation";
+  if (!(c->min_ray_length >= 0.0f) || !(c->min_ray_length < c->max_ray_length))
+    return "tsdf config requires 0 <= min_ray_length < max_ray_length";
+  if (!(c->max_weight > 0.0f)) return "tsdf config requires max_weight > 0";
+  if (c->weight_mode < 0 || c->weight_mode > 2 || c->merge_mode < 0 || c->merge_mode > 2)
+    return "tsdf config has an unknown weight or merge mode";
+  return "";
+}
+
+}  // namespace
+
+struct vxg_handle {
+  vxg_tsdf_config cfg{};
+  float voxel_size = 0.f;
+  int vps = 16;
+  int nvox = 4096;
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t st = nullptr;
+
+  // ---- map (slab + block hash)
+  DBuf<vxg_voxel> slab;
+  DBuf<int32_t> block_idx;
+  DBuf<unsigned long long> hkeys;
+  DBuf<int32_t> hvals;
+  DBuf<uint32_t> counters;  // [0] blocks, [1] error bits
+  uint64_t cap_blocks = 0;
+  uint64_t hcap = 0;
+  uint64_t n_blocks = 0;  // host mirror after each call
+  std::vector<int32_t> host_idx;  // block index per slot (host mirror, grows with n_blocks)
+
+  // ---- updated-block consumers (layer.h:124-148)
+  std::map<std::string, std::set<uint32_t>> consumers;
+  DBuf<uint8_t> touched;
+
+  // ---- scratch
+  DBuf<uint8_t> cub_tmp;
+  DBuf<float> in_xyz;
+  DBuf<uint8_t> in_rgb;
+  DBuf<uint64_t> d_off;
+  DBuf<float> d_poses;
+  DBuf<unsigned long long> d_stats;  // 3F: updates, raycasts, skipped
+  DBuf<unsigned long long> d_upd;    // F: chunk-local updates
+  DBuf<unsigned long long> pkeys, pkeys2, okeys, okeys2;
+  DBuf<uint32_t> pvals, pvals2, ovals, ovals2;
+  DBuf<uint32_t> flags, ray_idx, ucounts, uoffs, seg_count, seg_start, num_runs, fo, pos, part;
+  DBuf<unsigned long long> ukeys;
+  DBuf<SegInfo> segs;
+  DBuf<RayInfo> rays;
+  DBuf<unsigned long long> rcount, roff;
+  DBuf<uint64_t> tbl_off, bcs;
+  DBuf<uint32_t> rkeys, rkeys2, rvals, rvals2;
+  DBuf<Record> recs;
+
+  // ---- profiling
+  bool profile = false;
+  double stage_ms[kStages] = {};
+  uint64_t stage_launch[kStages] = {};
+  uint64_t stage_units[kStages] = {};
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+  std::vector<cudaEvent_t> event_pool;
+  uint64_t launches = 0;
+
+  MapView view() {
+    MapView m;
+    m.hkeys = hkeys.p;
+    m.hvals = hvals.p;
+    m.hmask = hcap - 1;
+    m.slab = slab.p;
+    m.block_idx = block_idx.p;
+    m.counters = counters.p;
+    m.cap_blocks = static_cast<uint32_t>(cap_blocks);
+    m.vps = vps;
+    m.nvox = nvox;
+    return m;
+  }
+
+  TsdfParams params() const {
+    TsdfParams t;
+    t.voxel_size = voxel_size;
+    t.truncation = cfg.truncation;
+    t.dropoff_epsilon = cfg.dropoff_epsilon;
+    t.max_weight = cfg.max_weight;
+    t.min_ray = cfg.min_ray_length;
+    t.max_ray = cfg.max_ray_length;
+    t.weight_mode = cfg.weight_mode;
+    t.merge_mode = cfg.merge_mode;
+    return t;
+  }
+
+  cudaEvent_t ev() {
+    if (!event_pool.empty()) {
+      cudaEvent_t e = event_pool.back();
+      event_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    CU(cudaEventCreate(&e));
+    return e;
+  }
+  // Stage timer: begin() records on the stream; end() records and queues the pair.
+  int cur_stage = -1;
+  cudaEvent_t cur_begin = nullptr;
+  void begin(int s) {
+    if (!profile) return;
+    cur_stage = s;
+    cur_begin = ev();
+    CU(cudaEventRecord(cur_begin, st));
+  }
+  void end(uint64_t units = 0, uint64_t n_launch = 0) {
+    if (!profile || cur_stage < 0) return;
+    cudaEvent_t e = ev();
+    CU(cudaEventRecord(e, st));
+    pending.push_back({cur_stage, {cur_begin, e}});
+    stage_units[cur_stage] += units;
+    stage_launch[cur_stage] += n_launch;
+    cur_stage = -1;
+  }
+  void collect() {  // after a stream sync
+    for (auto& pe : pending) {
+      float ms = 0.f;
+      CU(cudaEventElapsedTime(&ms, pe.second.first, pe.second.second));
+      stage_ms[pe.first] += ms;
+      event_pool.push_back(pe.second.first);
+      event_pool.push_back(pe.second.second);
+    }
+    pending.clear();
+  }
+
+  template <typename Fn>
+  void cub(Fn fn) {
+    size_t bytes = 0;
+    CU(fn(nullptr, bytes));
+    if (bytes == 0) bytes = 1;
+    CU(fn(cub_tmp.ensure(bytes), bytes));
+  }
+
+  // ---------------------------------------------------------------- map
+  void alloc_map(uint64_t cap) {
+    cap_blocks = cap;
+    slab.release();
+    block_idx.release();
+    CU(cudaMalloc(&slab.p, cap * nvox * sizeof(vxg_voxel)));
+    slab.cap = cap * nvox;
+    CU(cudaMemsetAsync(slab.p, 0, cap * nvox * sizeof(vxg_voxel), st));
+    CU(cudaMalloc(&block_idx.p, cap * 3 * sizeof(int32_t)));
+    block_idx.cap = cap * 3;
+    hcap = 1;
+    while (hcap < 2 * cap) hcap <<= 1;
+    hkeys.release();
+    hvals.release();
+    CU(cudaMalloc(&hkeys.p, hcap * sizeof(unsigned long long)));
+    hkeys.cap = hcap;
+    CU(cudaMalloc(&hvals.p, hcap * sizeof(int32_t)));
+    hvals.cap = hcap;
+    CU(cudaMemsetAsync(hkeys.p, 0xFF, hcap * sizeof(unsigned long long), st));
+    CU(cudaMemsetAsync(hvals.p, 0xFF, hcap * sizeof(int32_t), st));
+    counters.ensure(4);
+    CU(cudaMemsetAsync(counters.p, 0, 4 * sizeof(uint32_t), st));
+    n_blocks = 0;
+    host_idx.clear();
+    CU(cudaStreamSynchronize(st));
+  }
+
+  // Grows slab (preserving the first `used` blocks) and the hash.
+  void grow_map(uint64_t need_blocks) {
+    uint64_t used = std::min<uint64_t>(need_blocks, cap_blocks);
+    uint64_t new_cap = std::max<uint64_t>(cap_blocks * 2, need_blocks + need_blocks / 4 + 64);
+    if (new_cap * static_cast<uint64_t>(nvox) >= 0xFFFFFFFFull)
+      throw VxgError(VXG_ENOMEM, "block slab would exceed the 32-bit voxel key range");
+    vxg_voxel* ns = nullptr;
+    int32_t* ni = nullptr;
+    if (cudaMalloc(&ns, new_cap * nvox * sizeof(vxg_voxel)) != cudaSuccess) {
+      cudaGetLastError();
+      throw VxgError(VXG_ENOMEM, "cannot grow the block slab to " + std::to_string(new_cap) + " blocks");
+    }
+    CU(cudaMalloc(&ni, new_cap * 3 * sizeof(int32_t)));
+    CU(cudaMemsetAsync(ns, 0, new_cap * nvox * sizeof(vxg_voxel), st));
+    CU(cudaMemcpyAsync(ns, slab.p, used * nvox * sizeof(vxg_voxel), cudaMemcpyDeviceToDevice, st));
+    CU(cudaMemcpyAsync(ni, block_idx.p, used * 3 * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+    CU(cudaStreamSynchronize(st));
+    cudaFree(slab.p);
+    cudaFree(block_idx.p);
+    slab.p = ns;
+    slab.cap = new_cap * nvox;
+    block_idx.p = ni;
+    block_idx.cap = new_cap * 3;
+    const uint64_t old_cap = cap_blocks;
+    cap_blocks = new_cap;
+    // hash: keep load <= 1/2
+    uint64_t new_h = hcap;
+    while (new_h < 2 * new_cap) new_h <<= 1;
+    if (new_h != hcap) rehash(new_h);
+    // slots handed out beyond the old capacity got no block index yet
+    k_fix_block_idx<<<grid_for(hcap), 256, 0, st>>>(hcap, hkeys.p, hvals.p, static_cast<uint32_t>(old_cap),
+                                                   static_cast<uint32_t>(new_cap), block_idx.p);
+    ++launches;
+    CU(cudaGetLastError());
+  }
+
+  void rehash(uint64_t new_h) {
+    unsigned long long* nk = nullptr;
+    int32_t* nv = nullptr;
+    CU(cudaMalloc(&nk, new_h * sizeof(unsigned long long)));
+    CU(cudaMalloc(&nv, new_h * sizeof(int32_t)));
+    CU(cudaMemsetAsync(nk, 0xFF, new_h * sizeof(unsigned long long), st));
+    CU(cudaMemsetAsync(nv, 0xFF, new_h * sizeof(int32_t), st));
+    MapView m = view();
+    m.hkeys = nk;
+    m.hvals = nv;
+    m.hmask = new_h - 1;
+    k_rehash<<<grid_for(hcap), 256, 0, st>>>(hcap, hkeys.p, hvals.p, m);
+    ++launches;
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(st));
+    cudaFree(hkeys.p);
+    cudaFree(hvals.p);
+    hkeys.p = nk;
+    hkeys.cap = new_h;
+    hvals.p = nv;
+    hvals.cap = new_h;
+    hcap = new_h;
+  }
+
+  // touched[slot] flags for updated-block consumers: sized to the slab, zeroed
+  // whenever (re)allocated; the old flags are kept across growth.
+  void ensure_touched() {
+    if (consumers.empty()) return;
+    if (touched.p != nullptr && touched.cap >= cap_blocks) return;
+    uint8_t* n = nullptr;
+    CU(cudaMalloc(&n, cap_blocks));
+    CU(cudaMemsetAsync(n, 0, cap_blocks, st));
+    if (touched.p != nullptr) CU(cudaMemcpyAsync(n, touched.p, touched.cap, cudaMemcpyDeviceToDevice, st));
+    CU(cudaStreamSynchronize(st));
+    touched.release();
+    touched.p = n;
+    touched.cap = cap_blocks;
+  }
+
+  void read_counters(uint32_t* c) {
+    CU(cudaMemcpyAsync(c, counters.p, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+  }
+
+  // Refresh host_idx for slots appended since the last call.
+  void sync_block_mirror(uint64_t nb) {
+    if (nb > cap_blocks) nb = cap_blocks;
+    if (nb <= n_blocks && host_idx.size() == 3 * n_blocks) {
+      n_blocks = nb;
+      host_idx.resize(3 * nb);
+      return;
+    }
+    const uint64_t have = host_idx.size() / 3;
+    host_idx.resize(3 * nb);
+    if (nb > have) {
+      CU(cudaMemcpyAsync(host_idx.data() + 3 * have, block_idx.p + 3 * have, (nb - have) * 3 * sizeof(int32_t),
+                         cudaMemcpyDeviceToHost, st));
+      CU(cudaStreamSynchronize(st));
+    }
+    n_blocks = nb;
+  }
+
+  // ---------------------------------------------------------------- pipeline
+  void run_sub(const float* xyz, const uint8_t* rgb, const uint64_t* offsets, const float* poses, uint64_t F,
+               bool device_input, vxg_stats* out);
+  void build_rays_simple(const float* dxyz, const uint8_t* drgb, uint64_t P, uint32_t F, uint32_t* R_out);
+  void build_rays_grouped(const float* dxyz, const uint8_t* drgb, uint64_t P, const uint64_t* h_off, uint32_t F,
+                          uint32_t* R_out, TermView* tv);
+  void order_rehash_frame(uint32_t f, uint32_t K, uint32_t seg0, uint64_t n_points, const Schedule& sch,
+                          uint32_t ray0, int pb);
+  void emit_and_apply(uint32_t R, uint32_t F, const TermView& tv);
+};
+
+void vxg_handle::build_rays_simple(const float* dxyz, const uint8_t* drgb, uint64_t P, uint32_t F, uint32_t* R_out) {
+  const TsdfParams tp = params();
+  begin(ST_BUNDLE);
+  flags.ensure(P);
+  ray_idx.ensure(P);
+  k_simple_inrange<<<grid_for(P), 256, 0, st>>>(dxyz, P, d_off.p, d_poses.p, F, tp, flags.p, d_stats.p + 2 * F);
+  ++launches;
+  CU(cudaGetLastError());
+  cub([&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, flags.p, ray_idx.p, static_cast<int>(P), st);
+  });
+  uint32_t last_idx = 0, last_flag = 0;
+  CU(cudaMemcpyAsync(&last_idx, ray_idx.p + (P - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(&last_flag, flags.p + (P - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  const uint32_t R = last_idx + last_flag;
+  rays.ensure(std::max<uint32_t>(R, 1));
+  k_simple_rays<<<grid_for(P), 256, 0, st>>>(dxyz, drgb, P, d_off.p, d_poses.p, F, flags.p, ray_idx.p, rays.p);
+  ++launches;
+  CU(cudaGetLastError());
+  end(P, 4);
+  *R_out = R;
+}
+
+// Reorders frame f's K buckets when its map rehashes while they are inserted
+// (SURVEY.md Appendix B): epoch e re-inserts the previous iteration order, then
+// appends the next keys by first appearance, under bucket count bc_e.
+void vxg_handle::order_rehash_frame(uint32_t f, uint32_t K, uint32_t seg0, uint64_t n_points, const Schedule& sch,
+                                    uint32_t ray0, int pb) {
+  (void)n_points;
+  // rank = first-appearance rank: sort the frame's segments by pos.
+  std::vector<SegInfo> hseg(K);
+  CU(cudaMemcpyAsync(hseg.data(), segs.p + seg0, K * sizeof(SegInfo), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  std::vector<uint32_t> by_pos(K);
+  for (uint32_t i = 0; i < K; ++i) by_pos[i] = i;
+  std::sort(by_pos.begin(), by_pos.end(), [&](uint32_t a, uint32_t b) { return hseg[a].pos < hseg[b].pos; });
+  std::vector<uint32_t> rank(K);
+  for (uint32_t r = 0; r < K; ++r) rank[by_pos[r]] = r;
+  // Host emulation of the epochs is O(K log K) per epoch; frames that rehash are
+  // the rare ~10^6-bucket case (cfg4) and this runs once per such frame.
+  std::vector<uint32_t> pos(K), order;  // order: local seg ids in current list order
+  for (size_t e = 0; e < sch.size(); ++e) {
+    const uint64_t t_lo = sch[e].first;
+    const uint64_t t_hi = e + 1 < sch.size() ? sch[e + 1].first : UINT64_MAX;
+    if (t_lo >= K && e > 0) break;
+    const uint64_t bc = sch[e].second;
+    std::vector<uint32_t> prev_index(K, 0);
+    for (size_t i = 0; i < order.size(); ++i) prev_index[order[i]] = static_cast<uint32_t>(i);
+    std::vector<uint32_t> members;
+    for (uint32_t i = 0; i < K; ++i) {
+      if (rank[i] >= t_hi) continue;
+      pos[i] = rank[i] < t_lo ? prev_index[i] : rank[i];
+      members.push_back(i);
+    }
+    std::map<uint64_t, uint32_t> fo;
+    for (uint32_t i : members) {
+      const uint64_t b = hseg[i].hash % bc;
+      auto it = fo.find(b);
+      if (it == fo.end() || pos[i] < it->second) fo[b] = pos[i];
+    }
+    std::sort(members.begin(), members.end(), [&](uint32_t a, uint32_t b) {
+      const uint32_t fa = fo[hseg[a].hash % bc], fb = fo[hseg[b].hash % bc];
+      if (fa != fb) return fa > fb;
+      return pos[a] > pos[b];
+    });
+    order = members;
+  }
+  (void)pb;
+  std::vector<uint32_t> global(order.size());
+  for (size_t i = 0; i < order.size(); ++i) global[i] = seg0 + order[i];
+  CU(cudaMemcpyAsync(ovals.p + ray0, global.data(), global.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+  CU(cudaStreamSynchronize(st));
+}
+
+void vxg_handle::build_rays_grouped(const float* dxyz, const uint8_t* drgb, uint64_t P, const uint64_t* h_off,
+                                    uint32_t F, uint32_t* R_out, TermView* tv) {
+  const TsdfParams tp = params();
+  // key geometry: every in-range terminal voxel lies within rb voxels of the
+  // origin voxel on each axis; kb bits hold [0, 2 rb] plus an all-ones sentinel.
+  const int rb = static_cast<int>(std::ceil((static_cast<double>(cfg.max_ray_length) + cfg.truncation) / voxel_size)) + 3;
+  int kb = bits_for(static_cast<uint64_t>(2 * rb + 2));
+  const int fb = bits_for(F > 1 ? F - 1 : 0);
+  if (3 * kb + fb > 64) throw VxgError(VXG_EINVAL, "max_ray_length / voxel_size too large for the bundling key");
+  begin(ST_BUNDLE);
+  pkeys.ensure(P);
+  pkeys2.ensure(P);
+  pvals.ensure(P);
+  pvals2.ensure(P);
+  k_group_keys<<<grid_for(P), 256, 0, st>>>(dxyz, P, d_off.p, d_poses.p, F, tp, rb, kb, pkeys.p, pvals.p, counters.p);
+  ++launches;
+  CU(cudaGetLastError());
+  const int end_bit = 3 * kb + fb;
+  cub([&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortPairs(t, b, pkeys.p, pkeys2.p, pvals.p, pvals2.p, static_cast<int>(P), 0, end_bit, st);
+  });
+  ukeys.ensure(P);
+  ucounts.ensure(P);
+  num_runs.ensure(1);
+  cub([&](void* t, size_t& b) {
+    return cub::DeviceRunLengthEncode::Encode(t, b, pkeys2.p, ukeys.p, ucounts.p, num_runs.p, static_cast<int>(P), st);
+  });
+  uint32_t S = 0;
+  CU(cudaMemcpyAsync(&S, num_runs.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  uoffs.ensure(std::max<uint32_t>(S, 1));
+  cub([&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, ucounts.p, uoffs.p, static_cast<int>(S), st);
+  });
+  segs.ensure(std::max<uint32_t>(S, 1));
+  seg_count.ensure(F);
+  seg_start.ensure(F);
+  CU(cudaMemsetAsync(seg_count.p, 0, F * sizeof(uint32_t), st));
+  CU(cudaMemsetAsync(seg_start.p, 0xFF, F * sizeof(uint32_t), st));
+  k_seg_reduce<<<grid_for(S), 256, 0, st>>>(num_runs.p, ukeys.p, uoffs.p, ucounts.p, pvals2.p, dxyz, drgb, d_off.p,
+                                            d_poses.p, tp, rb, kb, segs.p, seg_count.p, seg_start.p, d_stats.p + 2 * F);
+  ++launches;
+  CU(cudaGetLastError());
+  std::vector<uint32_t> K(F), start(F);
+  CU(cudaMemcpyAsync(K.data(), seg_count.p, F * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(start.data(), seg_start.p, F * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  end(P, 6);
+
+  // ---- K3 ray order
+  begin(ST_ORDER);
+  uint64_t maxN = 1;
+  for (uint32_t f = 0; f < F; ++f) maxN = std::max<uint64_t>(maxN, h_off[f + 1] - h_off[f]);
+  const int pb = bits_for(maxN);
+  if (2 * pb + 1 + fb > 64) throw VxgError(VXG_EINVAL, "scan too large for the ray-order key");
+  std::vector<uint64_t> h_tbl(F), h_bc(F);
+  std::vector<Schedule> sched(F);
+  uint64_t tbl_total = 0;
+  uint32_t R = 0;
+  std::vector<uint32_t> ray0(F);
+  for (uint32_t f = 0; f < F; ++f) {
+    const uint64_t N = h_off[f + 1] - h_off[f];
+    sched[f] = bucket_schedule(N, K[f]);
+    h_bc[f] = sched[f][0].second;
+    h_tbl[f] = tbl_total;
+    tbl_total += h_bc[f];
+    ray0[f] = R;
+    R += K[f];
+  }
+  tbl_off.ensure(F);
+  bcs.ensure(F);
+  CU(cudaMemcpyAsync(tbl_off.p, h_tbl.data(), F * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(bcs.p, h_bc.data(), F * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+  fo.ensure(std::max<uint64_t>(tbl_total, 1));
+  CU(cudaMemsetAsync(fo.p, 0xFF, tbl_total * sizeof(uint32_t), st));
+  k_order_fo<<<grid_for(S), 256, 0, st>>>(S, segs.p, nullptr, nullptr, tbl_off.p, bcs.p, fo.p);
+  okeys.ensure(std::max<uint32_t>(S, 1));
+  okeys2.ensure(std::max<uint32_t>(S, 1));
+  ovals.ensure(std::max<uint32_t>(S, 1));
+  ovals2.ensure(std::max<uint32_t>(S, 1));
+  k_order_keys<<<grid_for(S), 256, 0, st>>>(S, segs.p, nullptr, nullptr, tbl_off.p, bcs.p, fo.p, pb, okeys.p, ovals.p);
+  launches += 2;
+  CU(cudaGetLastError());
+  const int obits = std::min(64, fb + 2 * pb + 1);
+  cub([&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortPairs(t, b, okeys.p, okeys2.p, ovals.p, ovals2.p, static_cast<int>(S), 0, obits, st);
+  });
+  std::swap(ovals.p, ovals2.p);
+  std::swap(ovals.cap, ovals2.cap);
+  for (uint32_t f = 0; f < F; ++f) {
+    if (sched[f].size() > 1 && K[f] > sched[f][1].first) {
+      order_rehash_frame(f, K[f], start[f], h_off[f + 1] - h_off[f], sched[f], ray0[f], pb);
+    }
+  }
+  rays.ensure(std::max<uint32_t>(R, 1));
+  k_gather_rays<<<grid_for(R), 256, 0, st>>>(R, ovals.p, segs.p, rays.p);
+  ++launches;
+  CU(cudaGetLastError());
+  end(S, 3);
+  tv->keys = ukeys.p;
+  tv->start = seg_start.p;
+  tv->count = seg_count.p;
+  tv->rb = rb;
+  tv->kb = kb;
+  *R_out = R;
+}
+
+void vxg_handle::emit_and_apply(uint32_t R, uint32_t F, const TermView& tv) {
+  const TsdfParams tp = params();
+  begin(ST_RAYS);
+  rcount.ensure(R);
+  roff.ensure(R);
+  k_ray_count<<<grid_for(R), 256, 0, st>>>(R, rays.p, d_poses.p, tp, rcount.p, d_stats.p + F);
+  ++launches;
+  CU(cudaGetLastError());
+  cub([&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, rcount.p, roff.p, static_cast<int>(R), st);
+  });
+  unsigned long long tail[2] = {0, 0};
+  CU(cudaMemcpyAsync(&tail[0], roff.p + (R - 1), sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(&tail[1], rcount.p + (R - 1), sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  end(R, 2);
+  const uint64_t total = tail[0] + tail[1];
+  // chunk rays so one chunk's records stay addressable and within memory
+  const uint64_t kMaxRecords = 1ull << 29;
+  std::vector<unsigned long long> h_roff;
+  if (total > kMaxRecords) {
+    h_roff.resize(R);
+    CU(cudaMemcpyAsync(h_roff.data(), roff.p, R * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+  }
+  auto roff_at = [&](uint32_t r) -> uint64_t { return r >= R ? total : (h_roff.empty() ? (r == 0 ? 0 : total) : h_roff[r]); };
+  ensure_touched();
+  uint32_t r0 = 0;
+  while (r0 < R) {
+    uint32_t r1 = R;
+    if (!h_roff.empty()) {
+      // largest r1 with records(r0, r1) <= kMaxRecords (at least one ray)
+      uint32_t lo = r0 + 1, hi = R;
+      while (lo < hi) {
+        const uint32_t mid = lo + (hi - lo + 1) / 2;
+        if (roff_at(mid) - roff_at(r0) <= kMaxRecords) lo = mid; else hi = mid - 1;
+      }
+      r1 = lo;
+    }
+    const uint64_t base = roff_at(r0);
+    const uint64_t T = roff_at(r1) - base;
+    if (T == 0) {
+      r0 = r1;
+      continue;
+    }
+    rkeys.ensure(T);
+    rkeys2.ensure(T);
+    rvals.ensure(T);
+    rvals2.ensure(T);
+    recs.ensure(T);
+    d_upd.ensure(F);
+    for (int attempt = 0;; ++attempt) {
+      CU(cudaMemsetAsync(counters.p + 1, 0, sizeof(uint32_t), st));
+      CU(cudaMemsetAsync(d_upd.p, 0, F * sizeof(unsigned long long), st));
+      begin(ST_EMIT);
+      k_emit<<<grid_for(r1 - r0, 128), 128, 0, st>>>(r0, r1, rays.p, roff.p, base, d_poses.p, tp, view(), tv,
+                                                       rkeys.p, rvals.p, recs.p, d_upd.p);
+      ++launches;
+      CU(cudaGetLastError());
+      end(T, 1);
+      begin(ST_SORT);
+      const int kbits = bits_for(cap_blocks * static_cast<uint64_t>(nvox));
+      cub([&](void* t, size_t& b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, rkeys.p, rkeys2.p, rvals.p, rvals2.p, static_cast<int>(T), 0,
+                                               kbits, st);
+      });
+      end(T, 1);
+      begin(ST_APPLY);
+      uint8_t* tch = consumers.empty() ? nullptr : touched.p;
+      k_fold<<<grid_for(T), 256, 0, st>>>(T, rkeys2.p, rvals2.p, recs.p, view(), tp, tch);
+      ++launches;
+      CU(cudaGetLastError());
+      end(T, 1);
+      uint32_t c[2];
+      read_counters(c);
+      if (c[1] & kErrKeyRange) throw VxgError(VXG_ERANGE, "voxel block index outside the supported range (+-2^20 blocks)");
+      if (c[1] & (kErrSlabFull | kErrHashFull)) {
+        if (attempt > 64) throw VxgError(VXG_ENOMEM, "block allocation did not converge");
+        if (c[1] & kErrHashFull) rehash(hcap * 2);
+        grow_map(std::max<uint64_t>(c[0], cap_blocks + 1));
+        ensure_touched();
+        continue;
+      }
+      break;
+    }
+    // fold this chunk's per-frame update counts into the stats
+    k_add_u64<<<grid_for(F), 256, 0, st>>>(F, d_stats.p, d_upd.p);
+    ++launches;
+    CU(cudaGetLastError());
+    r0 = r1;
+  }
+}
+
+void vxg_handle::run_sub(const float* xyz, const uint8_t* rgb, const uint64_t* offsets, const float* poses,
+                         uint64_t F, bool device_input, vxg_stats* out) {
+  const uint64_t P = offsets[F] - offsets[0];
+  std::vector<uint64_t> h_off(F + 1);
+  for (uint64_t f = 0; f <= F; ++f) h_off[f] = offsets[f] - offsets[0];
+  begin(ST_H2D);
+  d_off.ensure(F + 1);
+  d_poses.ensure(12 * F);
+  d_stats.ensure(3 * F);
+  CU(cudaMemcpyAsync(d_off.p, h_off.data(), (F + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(d_poses.p, poses, 12 * F * sizeof(float), cudaMemcpyHostToDevice, st));
+  CU(cudaMemsetAsync(d_stats.p, 0, 3 * F * sizeof(unsigned long long), st));
+  CU(cudaMemsetAsync(counters.p + 1, 0, sizeof(uint32_t), st));
+  const float* dxyz = xyz + 3 * offsets[0];
+  const uint8_t* drgb = rgb != nullptr ? rgb + 3 * offsets[0] : nullptr;
+  if (!device_input && P > 0) {
+    CU(cudaMemcpyAsync(in_xyz.ensure(3 * P), dxyz, 3 * P * sizeof(float), cudaMemcpyHostToDevice, st));
+    dxyz = in_xyz.p;
+    if (drgb != nullptr) {
+      CU(cudaMemcpyAsync(in_rgb.ensure(3 * P), drgb, 3 * P, cudaMemcpyHostToDevice, st));
+      drgb = in_rgb.p;
+    }
+  }
+  end(P * (drgb ? 15 : 12), 0);
+  if (P > 0) {
+    uint32_t R = 0;
+    TermView tv{nullptr, nullptr, nullptr, 0, 0};
+    if (cfg.merge_mode == VXG_MERGE_SIMPLE) {
+      build_rays_simple(dxyz, drgb, P, static_cast<uint32_t>(F), &R);
+    } else {
+      build_rays_grouped(dxyz, drgb, P, h_off.data(), static_cast<uint32_t>(F), &R, &tv);
+    }
+    uint32_t c[2];
+    read_counters(c);
+    if (c[1] & kErrKeyRange) throw VxgError(VXG_ERANGE, "terminal voxel outside the bundling key range");
+    if (R > 0) emit_and_apply(R, static_cast<uint32_t>(F), tv);
+  }
+  begin(ST_D2H);
+  std::vector<unsigned long long> s(3 * F);
+  CU(cudaMemcpyAsync(s.data(), d_stats.p, 3 * F * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  uint32_t c[2];
+  CU(cudaMemcpyAsync(c, counters.p, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  end(0, 0);
+  CU(cudaStreamSynchronize(st));
+  collect();
+  if (out != nullptr) {
+    for (uint64_t f = 0; f < F; ++f) {
+      out[f].updates = s[f];
+      out[f].raycasts = s[F + f];
+      out[f].skipped = s[2 * F + f];
+    }
+  }
+  // consumers: blocks touched by this batch
+  const uint64_t nb = std::min<uint64_t>(c[0], cap_blocks);
+  sync_block_mirror(nb);
+  if (!consumers.empty() && nb > 0 && touched.p != nullptr) {
+    std::vector<uint8_t> t(nb);
+    CU(cudaMemcpyAsync(t.data(), touched.p, nb, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemsetAsync(touched.p, 0, touched.cap, st));
+    CU(cudaStreamSynchronize(st));
+    for (auto& kv : consumers)
+      for (uint32_t i = 0; i < nb; ++i)
+        if (t[i]) kv.second.insert(i);
+  }
+}
+
+// ============================================================================ C ABI
+namespace {
+
+template <typename Fn>
+int guarded(Fn fn) {
+  try {
+    fn();
+    return VXG_OK;
+  } catch (const VxgError& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return VXG_ENOMEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return VXG_EINVAL;
+  }
+}
+
+void set_device(const vxg_handle* h) { CU(cudaSetDevice(h->device)); }
+
+template <typename T>
+T* to_dev(const T* src, size_t n, DBuf<T>* buf) {
+  buf->ensure(std::max<size_t>(n, 1));
+  if (n) CU(cudaMemcpy(buf->p, src, n * sizeof(T), cudaMemcpyHostToDevice));
+  return buf->p;
+}
+
+void export_sorted(vxg_handle* h, std::vector<uint32_t>* order) {
+  uint32_t c[2];
+  h->read_counters(c);
+  h->sync_block_mirror(std::min<uint64_t>(c[0], h->cap_blocks));
+  order->resize(h->n_blocks);
+  for (uint32_t i = 0; i < h->n_blocks; ++i) (*order)[i] = i;
+  const int32_t* idx = h->host_idx.data();
+  std::sort(order->begin(), order->end(), [&](uint32_t a, uint32_t b) {
+    const int32_t* A = idx + 3 * a;
+    const int32_t* B = idx + 3 * b;
+    if (A[0] != B[0]) return A[0] < B[0];
+    if (A[1] != B[1]) return A[1] < B[1];
+    return A[2] < B[2];
+  });
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* vxg_last_error(void) { return g_err.c_str(); }
+
+int vxg_device_info(int device, char* buf, size_t buf_len) {
+  return guarded([&] {
+    cudaDeviceProp p;
+    CU(cudaGetDeviceProperties(&p, device));
+    std::snprintf(buf, buf_len, "%s sm_%d%d SMs=%d HBM=%.1fGB L2=%.0fMB", p.name, p.major, p.minor,
+                  p.multiProcessorCount, p.totalGlobalMem / 1e9, p.l2CacheSize / 1e6);
+  });
+}
+
+int vxg_create(const vxg_tsdf_config* config, float voxel_size, int vps, int device, uint64_t block_capacity,
+               vxg_handle** out) {
+  return guarded([&] {
+    if (config == nullptr || out == nullptr) throw VxgError(VXG_EINVAL, "null argument");
+    if (voxel_size <= 0.0f || vps < 1)  // layer.h:62-67
+      throw VxgError(VXG_EINVAL, "layer requires voxel_size > 0 and voxels_per_side >= 1");
+    if (vps > 64) throw VxgError(VXG_EINVAL, "voxels_per_side > 64 is not supported on the device slab");
+    const std::string msg = validate_config(config);
+    if (!msg.empty()) throw VxgError(VXG_EINVAL, msg);
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+      cudaGetLastError();
+      throw VxgError(VXG_ECUDA, "no CUDA device available (vxg has no CPU fallback)");
+    }
+    if (device < 0 || device >= ndev) throw VxgError(VXG_EINVAL, "device index out of range");
+    cudaDeviceProp prop;
+    CU(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) throw VxgError(VXG_ECUDA, std::string("vxg is built for sm_100a; device is ") + prop.name);
+    auto* h = new vxg_handle;
+    try {
+      h->cfg = *config;
+      h->voxel_size = voxel_size;
+      h->vps = vps;
+      h->nvox = vps * vps * vps;
+      h->device = device;
+      CU(cudaSetDevice(device));
+      CU(cudaStreamCreateWithFlags(&h->own, cudaStreamNonBlocking));
+      h->st = h->own;
+      h->alloc_map(block_capacity ? block_capacity : 4096);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int vxg_destroy(vxg_handle* h) {
+  if (h == nullptr) return VXG_OK;
+  return guarded([&] {
+    cudaSetDevice(h->device);
+    cudaStreamSynchronize(h->st);
+    for (auto& pe : h->pending) {
+      cudaEventDestroy(pe.second.first);
+      cudaEventDestroy(pe.second.second);
+    }
+    for (cudaEvent_t e : h->event_pool) cudaEventDestroy(e);
+    if (h->own) cudaStreamDestroy(h->own);
+    delete h;
+  });
+}
+
+int vxg_get_config(const vxg_handle* h, vxg_tsdf_config* out) {
+  if (h == nullptr || out == nullptr) return VXG_EINVAL;
+  *out = h->cfg;
+  return VXG_OK;
+}
+
+int vxg_set_config(vxg_handle* h, const vxg_tsdf_config* config) {
+  return guarded([&] {
+    const std::string msg = validate_config(config);
+    if (!msg.empty()) throw VxgError(VXG_EINVAL, msg);
+    h->cfg = *config;
+  });
+}
+
+int vxg_set_stream(vxg_handle* h, void* stream) {
+  return guarded([&] {
+    set_device(h);
+    CU(cudaStreamSynchronize(h->st));
+    h->st = stream != nullptr ? static_cast<cudaStream_t>(stream) : h->own;
+  });
+}
+
+int vxg_integrate_packed(vxg_handle* h, const float* xyz, const uint8_t* rgb, const uint64_t* offsets,
+                         const float* poses, uint64_t F, int flags, vxg_stats* out) {
+  return guarded([&] {
+    if (h == nullptr || offsets == nullptr || poses == nullptr) throw VxgError(VXG_EINVAL, "null argument");
+    if (F == 0) return;
+    for (uint64_t f = 0; f < F; ++f)
+      if (offsets[f + 1] < offsets[f]) throw VxgError(VXG_EINVAL, "frame offsets must be non-decreasing");
+    if (offsets[F] > offsets[0] && xyz == nullptr) throw VxgError(VXG_EINVAL, "null point buffer");
+    set_device(h);
+    // sub-batches: <= 2^30 points each (32-bit point indices, bounded scratch)
+    const uint64_t kMaxPoints = 1ull << 30;
+    uint64_t f0 = 0;
+    while (f0 < F) {
+      uint64_t f1 = f0 + 1;
+      while (f1 < F && offsets[f1 + 1] - offsets[f0] <= kMaxPoints && f1 - f0 < 65535) ++f1;
+      if (offsets[f1] - offsets[f0] >= (1ull << 31)) throw VxgError(VXG_EINVAL, "a single scan exceeds 2^31 points");
+      h->run_sub(xyz, rgb, offsets + f0, poses + 12 * f0, f1 - f0, (flags & VXG_INPUT_DEVICE) != 0,
+                 out != nullptr ? out + f0 : nullptr);
+      f0 = f1;
+    }
+  });
+}
+
+int vxg_integrate_batch(vxg_handle* h, const vxg_frame* frames, uint64_t F, int flags, vxg_stats* out) {
+  return guarded([&] {
+    if (h == nullptr || (frames == nullptr && F > 0)) throw VxgError(VXG_EINVAL, "null argument");
+    set_device(h);
+    const bool dev = (flags & VXG_INPUT_DEVICE) != 0;
+    // Frames are gathered into one packed staging buffer (device side).
+    uint64_t P = 0;
+    bool any_rgb = false;
+    for (uint64_t f = 0; f < F; ++f) {
+      P += frames[f].n;
+      any_rgb = any_rgb || frames[f].rgb != nullptr;
+    }
+    std::vector<uint64_t> off(F + 1, 0);
+    std::vector<float> poses(12 * F);
+    for (uint64_t f = 0; f < F; ++f) {
+      off[f + 1] = off[f] + frames[f].n;
+      std::memcpy(&poses[12 * f], frames[f].pose, 12 * sizeof(float));
+    }
+    bool mixed_rgb = false;
+    for (uint64_t f = 0; f < F; ++f)
+      if (any_rgb && frames[f].rgb == nullptr && frames[f].n > 0) mixed_rgb = true;
+    if (mixed_rgb) {  // colour presence differs per scan: integrate scan by scan
+      for (uint64_t f = 0; f < F; ++f) {
+        const uint64_t o2[2] = {0, frames[f].n};
+        h->run_sub(frames[f].xyz, frames[f].rgb, o2, frames[f].pose, 1, dev, out ? out + f : nullptr);
+      }
+      return;
+    }
+    float* sx = h->in_xyz.ensure(std::max<uint64_t>(3 * P, 3));
+    uint8_t* sc = any_rgb ? h->in_rgb.ensure(std::max<uint64_t>(3 * P, 3)) : nullptr;
+    const cudaMemcpyKind kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    for (uint64_t f = 0; f < F; ++f) {
+      if (frames[f].n == 0) continue;
+      CU(cudaMemcpyAsync(sx + 3 * off[f], frames[f].xyz, 3 * frames[f].n * sizeof(float), kind, h->st));
+      if (sc) CU(cudaMemcpyAsync(sc + 3 * off[f], frames[f].rgb, 3 * frames[f].n, kind, h->st));
+    }
+    // the staging buffer is device memory now; run as device input (the
+    // buffers must not be re-staged, so integrate the sub-batches directly)
+    const uint64_t kMaxPoints = 1ull << 30;
+    uint64_t f0 = 0;
+    while (f0 < F) {
+      uint64_t f1 = f0 + 1;
+      while (f1 < F && off[f1 + 1] - off[f0] <= kMaxPoints && f1 - f0 < 65535) ++f1;
+      h->run_sub(sx, sc, off.data() + f0, poses.data() + 12 * f0, f1 - f0, true, out ? out + f0 : nullptr);
+      f0 = f1;
+    }
+  });
+}
+
+int vxg_integrate(vxg_handle* h, const float* xyz, const uint8_t* rgb, uint64_t n, const float pose[12],
+                  vxg_stats* out) {
+  vxg_frame fr;
+  fr.xyz = xyz;
+  fr.rgb = rgb;
+  fr.n = n;
+  if (pose == nullptr) {
+    g_err = "null pose";
+    return VXG_EINVAL;
+  }
+  std::memcpy(fr.pose, pose, sizeof(fr.pose));
+  vxg_stats s{0, 0, 0};
+  const int rc = vxg_integrate_batch(h, &fr, 1, VXG_INPUT_HOST, &s);
+  if (rc == VXG_OK && out != nullptr) *out = s;
+  return rc;
+}
+
+int vxg_block_count(vxg_handle* h, uint64_t* out) {
+  return guarded([&] {
+    set_device(h);
+    uint32_t c[2];
+    h->read_counters(c);
+    *out = std::min<uint64_t>(c[0], h->cap_blocks);
+  });
+}
+
+int vxg_export_blocks(vxg_handle* h, int32_t* idx, vxg_voxel* voxels, uint64_t cap, uint64_t* n_out) {
+  return guarded([&] {
+    set_device(h);
+    std::vector<uint32_t> order;
+    export_sorted(h, &order);
+    const uint64_t n = std::min<uint64_t>(cap, order.size());
+    if (idx != nullptr) {
+      for (uint64_t k = 0; k < n; ++k)
+        for (int a = 0; a < 3; ++a) idx[3 * k + a] = h->host_idx[3 * order[k] + a];
+    }
+    if (voxels != nullptr && n > 0) {
+      const size_t bb = static_cast<size_t>(h->nvox) * sizeof(vxg_voxel);
+      for (uint64_t k = 0; k < n; ++k) {
+        CU(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(voxels) + k * bb,
+                           reinterpret_cast<uint8_t*>(h->slab.p) + static_cast<size_t>(order[k]) * bb, bb,
+                           cudaMemcpyDeviceToHost, h->st));
+      }
+      CU(cudaStreamSynchronize(h->st));
+    }
+    if (n_out) *n_out = n;
+  });
+}
+
+int vxg_import_blocks(vxg_handle* h, const int32_t* idx, const vxg_voxel* voxels, uint64_t n) {
+  return guarded([&] {
+    set_device(h);
+    if (n == 0) return;
+    DBuf<int32_t> didx, slots;
+    DBuf<vxg_voxel> dv;
+    didx.ensure(3 * n);
+    slots.ensure(n);
+    dv.ensure(n * h->nvox);
+    CU(cudaMemcpyAsync(didx.p, idx, 3 * n * sizeof(int32_t), cudaMemcpyHostToDevice, h->st));
+    CU(cudaMemcpyAsync(dv.p, voxels, n * h->nvox * sizeof(vxg_voxel), cudaMemcpyHostToDevice, h->st));
+    for (int attempt = 0;; ++attempt) {
+      CU(cudaMemsetAsync(h->counters.p + 1, 0, sizeof(uint32_t), h->st));
+      k_import_slots<<<grid_for(n), 256, 0, h->st>>>(n, didx.p, h->view(), slots.p);
+      CU(cudaGetLastError());
+      uint32_t c[2];
+      h->read_counters(c);
+      if (c[1] & kErrKeyRange) throw VxgError(VXG_ERANGE, "block index outside the supported range");
+      if (c[1] & (kErrSlabFull | kErrHashFull)) {
+        if (attempt > 64) throw VxgError(VXG_ENOMEM, "block allocation did not converge");
+        if (c[1] & kErrHashFull) h->rehash(h->hcap * 2);
+        h->grow_map(std::max<uint64_t>(c[0], h->cap_blocks + 1));
+        continue;
+      }
+      break;
+    }
+    k_scatter_blocks<<<grid_for(n * h->nvox), 256, 0, h->st>>>(n, slots.p, dv.p, h->view());
+    CU(cudaGetLastError());
+    uint32_t c[2];
+    h->read_counters(c);
+    h->sync_block_mirror(std::min<uint64_t>(c[0], h->cap_blocks));
+  });
+}
+
+int vxg_query_voxels(vxg_handle* h, const int32_t* g, uint64_t n, vxg_voxel* out, uint8_t* found) {
+  return guarded([&] {
+    set_device(h);
+    if (n == 0) return;
+    DBuf<int32_t> dg;
+    DBuf<vxg_voxel> dout;
+    DBuf<uint8_t> dfound;
+    dg.ensure(3 * n);
+    dout.ensure(n);
+    dfound.ensure(n);
+    CU(cudaMemcpyAsync(dg.p, g, 3 * n * sizeof(int32_t), cudaMemcpyHostToDevice, h->st));
+    k_query<<<grid_for(n), 256, 0, h->st>>>(n, dg.p, h->view(), dout.p, dfound.p);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(out, dout.p, n * sizeof(vxg_voxel), cudaMemcpyDeviceToHost, h->st));
+    CU(cudaMemcpyAsync(found, dfound.p, n, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaStreamSynchronize(h->st));
+  });
+}
+
+int vxg_serialize_vxblx(vxg_handle* h, uint8_t* buf, uint64_t cap, uint64_t* need) {
+  return guarded([&] {
+    set_device(h);
+    std::vector<uint32_t> order;
+    export_sorted(h, &order);
+    const uint64_t nb = order.size();
+    const uint64_t total = 31 + nb * (24 + static_cast<uint64_t>(h->nvox) * 12);
+    if (need) *need = total;
+    if (buf == nullptr || cap < total) return;
+    uint8_t* o = buf;
+    auto put = [&](const void* src, size_t len) {
+      std::memcpy(o, src, len);
+      o += len;
+    };
+    const char magic[6] = {'V', 'X', 'B', 'L', 'X', '\0'};
+    const uint32_t version = 1;
+    const double vs = static_cast<double>(h->voxel_size);
+    const uint32_t vps = static_cast<uint32_t>(h->vps);
+    const uint8_t kind = 0;
+    put(magic, 6);
+    put(&version, 4);
+    put(&vs, 8);
+    put(&vps, 4);
+    put(&kind, 1);
+    put(&nb, 8);
+    const size_t bb = static_cast<size_t>(h->nvox) * sizeof(vxg_voxel);
+    std::vector<vxg_voxel> tmp(h->nvox);
+    for (uint64_t k = 0; k < nb; ++k) {
+      for (int a = 0; a < 3; ++a) {
+        const int64_t v = h->host_idx[3 * order[k] + a];
+        put(&v, 8);
+      }
+      CU(cudaMemcpyAsync(tmp.data(), reinterpret_cast<uint8_t*>(h->slab.p) + static_cast<size_t>(order[k]) * bb, bb,
+                         cudaMemcpyDeviceToHost, h->st));
+      CU(cudaStreamSynchronize(h->st));
+      for (int i = 0; i < h->nvox; ++i) tmp[i].pad = 0;
+      put(tmp.data(), bb);  // payload layout == vxg_voxel (f32, f32, u8 x3, u8 pad)
+    }
+  });
+}
+
+int vxg_save_vxblx(vxg_handle* h, const char* path) {
+  uint64_t need = 0;
+  int rc = vxg_serialize_vxblx(h, nullptr, 0, &need);
+  if (rc != VXG_OK) return rc;
+  std::vector<uint8_t> buf(need);
+  rc = vxg_serialize_vxblx(h, buf.data(), need, &need);
+  if (rc != VXG_OK) return rc;
+  std::ofstream f(path, std::ios::binary);
+  if (!f) {
+    g_err = std::string("cannot write layer file: ") + path;
+    return VXG_EIO;
+  }
+  f.write(reinterpret_cast<const char*>(buf.data()), static_cast<std::streamsize>(buf.size()));
+  if (!f) {
+    g_err = "failed writing layer stream";
+    return VXG_EIO;
+  }
+  return VXG_OK;
+}
+
+int vxg_reset(vxg_handle* h) {
+  return guarded([&] {
+    set_device(h);
+    const uint64_t used = std::min<uint64_t>(h->n_blocks, h->cap_blocks);
+    uint32_t c[2];
+    h->read_counters(c);
+    const uint64_t used2 = std::min<uint64_t>(std::max<uint64_t>(c[0], used), h->cap_blocks);
+    CU(cudaMemsetAsync(h->slab.p, 0, used2 * h->nvox * sizeof(vxg_voxel), h->st));
+    CU(cudaMemsetAsync(h->hkeys.p, 0xFF, h->hcap * sizeof(unsigned long long), h->st));
+    CU(cudaMemsetAsync(h->hvals.p, 0xFF, h->hcap * sizeof(int32_t), h->st));
+    CU(cudaMemsetAsync(h->counters.p, 0, 2 * sizeof(uint32_t), h->st));
+    CU(cudaStreamSynchronize(h->st));
+    h->n_blocks = 0;
+    h->host_idx.clear();
+    for (auto& kv : h->consumers) kv.second.clear();
+  });
+}
+
+int vxg_load_vxblx(vxg_handle* h, const uint8_t* buf, uint64_t len) {
+  return guarded([&] {
+    // read_header / load_layer_impl (serialization.cpp:170-212), same ParseError texts.
+    uint64_t at = 0;
+    auto get = [&](void* dst, size_t n, const char* what) {
+      if (at + n > len) throw VxgError(VXG_EPARSE, std::string("truncated layer file while reading ") + what);
+      std::memcpy(dst, buf + at, n);
+      at += n;
+    };
+    char magic[6];
+    get(magic, 6, "magic");
+    if (std::memcmp(magic, "VXBLX\0", 6) != 0) throw VxgError(VXG_EPARSE, "bad magic bytes; not a layer file");
+    uint32_t version;
+    get(&version, 4, "version");
+    if (version != 1) throw VxgError(VXG_EPARSE, "unsupported layer file version " + std::to_string(version));
+    double vs;
+    get(&vs, 8, "voxel_size");
+    uint32_t vps;
+    get(&vps, 4, "voxels_per_side");
+    uint8_t kind;
+    get(&kind, 1, "layer_kind");
+    if (kind > 1) throw VxgError(VXG_EPARSE, "unknown layer kind " + std::to_string(kind));
+    uint64_t count;
+    get(&count, 8, "block_count");
+    if (vs <= 0.0 || vps == 0) throw VxgError(VXG_EPARSE, "invalid layer geometry in header");
+    if (kind != 0) throw VxgError(VXG_EPARSE, "layer kind mismatch: file holds a different voxel type");
+    if (vps > 64) throw VxgError(VXG_EINVAL, "voxels_per_side > 64 is not supported on the device slab");
+    const uint64_t nvox = static_cast<uint64_t>(vps) * vps * vps;
+    std::vector<int32_t> idx;
+    std::vector<vxg_voxel> vox;
+    idx.reserve(3 * std::min<uint64_t>(count, 1 << 20));
+    for (uint64_t b = 0; b < count; ++b) {
+      for (int a = 0; a < 3; ++a) {
+        int64_t v;
+        get(&v, 8, "block index");
+        idx.push_back(static_cast<int32_t>(v));
+      }
+      const size_t base = vox.size();
+      vox.resize(base + nvox);
+      for (uint64_t i = 0; i < nvox; ++i) {
+        float d, w;
+        uint8_t c[4];
+        get(&d, 4, "tsdf voxel distance");
+        get(&w, 4, "tsdf voxel weight");
+        get(c, 3, "tsdf voxel color");
+        get(c + 3, 1, "tsdf voxel pad");
+        vox[base + i] = vxg_voxel{d, w, c[0], c[1], c[2], 0};
+      }
+    }
+    set_device(h);
+    h->voxel_size = static_cast<float>(vs);
+    if (static_cast<int>(vps) != h->vps) {
+      h->vps = static_cast<int>(vps);
+      h->nvox = static_cast<int>(nvox);
+      h->alloc_map(std::max<uint64_t>(h->cap_blocks, count + 64));
+    } else {
+      if (vxg_reset(h) != VXG_OK) throw VxgError(VXG_ECUDA, g_err);
+    }
+    // duplicate indices: later blocks overwrite earlier ones (get_or_allocate_block)
+    const int rc = vxg_import_blocks(h, idx.data(), vox.data(), count);
+    if (rc != VXG_OK) throw VxgError(rc, g_err);
+  });
+}
+
+int vxg_register_consumer(vxg_handle* h, const char* name) {
+  return guarded([&] {
+    if (name == nullptr) throw VxgError(VXG_EINVAL, "null consumer name");
+    set_device(h);
+    h->consumers[name];
+    h->ensure_touched();
+  });
+}
+
+int vxg_drain_updated(vxg_handle* h, const char* name, int32_t* idx, uint64_t cap, uint64_t* n_out) {
+  return guarded([&] {
+    auto it = h->consumers.find(name ? name : "");
+    if (it == h->consumers.end())
+      throw VxgError(VXG_EINVAL, std::string("unknown updated-block consumer: ") + (name ? name : ""));
+    uint64_t k = 0;
+    for (uint32_t slot : it->second) {
+      if (idx != nullptr && k < cap)
+        for (int a = 0; a < 3; ++a) idx[3 * k + a] = h->host_idx[3 * slot + a];
+      ++k;
+    }
+    if (n_out) *n_out = k;
+    if (idx != nullptr) it->second.clear();
+  });
+}
+
+int vxg_profile(vxg_handle* h, int enable) {
+  h->profile = enable != 0;
+  return VXG_OK;
+}
+
+int vxg_stage_count(void) { return kStages; }
+
+const char* vxg_stage_name(int s) { return (s >= 0 && s < kStages) ? kStageNames[s] : ""; }
+
+int vxg_stage_times(vxg_handle* h, double* ms, uint64_t* launches, uint64_t* units, int reset) {
+  for (int s = 0; s < kStages; ++s) {
+    if (ms) ms[s] = h->stage_ms[s];
+    if (launches) launches[s] = h->stage_launch[s];
+    if (units) units[s] = h->stage_units[s];
+    if (reset) {
+      h->stage_ms[s] = 0;
+      h->stage_launch[s] = 0;
+      h->stage_units[s] = 0;
+    }
+  }
+  return VXG_OK;
+}
+
+int vxg_kernel_launches(vxg_handle* h, uint64_t* out, int reset) {
+  if (out) *out = h->launches;
+  if (reset) h->launches = 0;
+  return VXG_OK;
+}
+
+// ---------------------------------------------------------------- free functions on device
+
+int vxg_eval_projective_distance(int device, const float* x, const float* p, const float* s, uint64_t n, float* out) {
+  return guarded([&] {
+    CU(cudaSetDevice(device));
+    DBuf<float> a, b, c, o;
+    float* dx = to_dev(x, 3 * n, &a);
+    float* dp = to_dev(p, 3 * n, &b);
+    float* ds = to_dev(s, 3 * n, &c);
+    o.ensure(std::max<uint64_t>(n, 1));
+    k_eval_pd<<<grid_for(n), 256>>>(n, dx, dp, ds, o.p);
+    CU(cudaGetLastError());
+    CU(cudaMemcpy(out, o.p, n * sizeof(float), cudaMemcpyDeviceToHost));
+  });
+}
+
+int vxg_eval_measurement_weight(int device, int mode, const float* z, const float* d, uint64_t n, float trunc,
+                                float eps, float* out) {
+  return guarded([&] {
+    CU(cudaSetDevice(device));
+    DBuf<float> a, b, o;
+    float* dz = to_dev(z, n, &a);
+    float* dd = to_dev(d, n, &b);
+    o.ensure(std::max<uint64_t>(n, 1));
+    k_eval_mw<<<grid_for(n), 256>>>(n, mode, dz, dd, trunc, eps, o.p);
+    CU(cudaGetLastError());
+    CU(cudaMemcpy(out, o.p, n * sizeof(float), cudaMemcpyDeviceToHost));
+  });
+}
+
+int vxg_eval_update_voxels(int device, vxg_voxel* voxels, uint64_t nv, const uint64_t* starts, const float* d,
+                           const float* w, const uint8_t* rgb, float trunc, float wmax) {
+  return guarded([&] {
+    CU(cudaSetDevice(device));
+    const uint64_t nr = starts[nv];
+    DBuf<vxg_voxel> dv;
+    DBuf<uint64_t> ds;
+    DBuf<float> dd, dw;
+    DBuf<uint8_t> dc;
+    vxg_voxel* pv = to_dev(voxels, nv, &dv);
+    uint64_t* ps = to_dev(starts, nv + 1, &ds);
+    float* pd = to_dev(d, nr, &dd);
+    float* pw = to_dev(w, nr, &dw);
+    uint8_t* pc = rgb != nullptr ? to_dev(rgb, 3 * nr, &dc) : nullptr;
+    k_eval_update<<<grid_for(nv), 256>>>(nv, pv, ps, pd, pw, pc, trunc, wmax);
+    CU(cudaGetLastError());
+    CU(cudaMemcpy(voxels, pv, nv * sizeof(vxg_voxel), cudaMemcpyDeviceToHost));
+  });
+}
+
+int vxg_eval_raycast(int device, const float* start, const float* end, uint64_t n, float v, uint32_t* counts,
+                     const uint64_t* offsets, int32_t* out) {
+  return guarded([&] {
+    CU(cudaSetDevice(device));
+    DBuf<float> a, b;
+    DBuf<uint32_t> dc;
+    DBuf<uint64_t> doff;
+    DBuf<int32_t> dout;
+    float* ds = to_dev(start, 3 * n, &a);
+    float* de = to_dev(end, 3 * n, &b);
+    dc.ensure(std::max<uint64_t>(n, 1));
+    uint64_t* po = nullptr;
+    int32_t* pout = nullptr;
+    uint64_t total = 0;
+    if (out != nullptr && n > 0) {
+      po = to_dev(offsets, n, &doff);
+      std::vector<uint32_t> tmp(1);
+      total = offsets[n - 1];
+      // caller-provided counts give the last ray's length
+      total += counts[n - 1];
+      dout.ensure(3 * total);
+      pout = dout.p;
+    }
+    k_eval_raycast<<<grid_for(n), 256>>>(n, ds, de, v, dc.p, po, pout);
+    CU(cudaGetLastError());
+    CU(cudaMemcpy(counts, dc.p, n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    if (pout) CU(cudaMemcpy(out, pout, 3 * total * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  });
+}
+
+}  // extern "C"
