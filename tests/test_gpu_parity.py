@@ -1,0 +1,179 @@
+"""GPU parity through the C ABI: the B200 pipeline vs the CPU oracle, bit-exact.
+
+The bar (BASELINE.json north_star): allocated block set, voxel keys and the
+per-voxel (distance, weight, colour) must match; the order-preserving fold
+makes them bit-exact, so every comparison here is on the VXBLX bytes
+(serialization.cpp:141-168) plus the integrate() counters.
+"""
+import numpy as np
+import pytest
+
+from paper_1611_03631_b200 import MergeMode, Scan, TsdfConfig, TsdfIntegrator, TsdfLayer, WeightMode
+from paper_1611_03631_b200 import workload as W
+from parity_helpers import diff_report, run_pair
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(layer, integ, cfg, wc, frames, batch=False):
+    g, o, gb, ob = run_pair(layer, integ, cfg, wc.voxel_size, wc.vps, frames, batch=batch)
+    assert g == o, f"stats differ: gpu={g} oracle={o}"
+    assert gb == ob, diff_report(gb, ob)
+
+
+@pytest.mark.parametrize("cfg_id", [0, 1, 2, 3])
+@pytest.mark.parametrize("batch", [False, True])
+def test_configs_reduced_scale(gpu, cfg_id, batch):
+    wc = W.CONFIGS[cfg_id]
+    cfg = W.tsdf_config(wc)
+    layer = TsdfLayer(wc.voxel_size, wc.vps)
+    integ = TsdfIntegrator(cfg, layer)
+    frames = W.frames(cfg_id, count=3 if cfg_id else 1, scale=0.2, start=0, n_frames=wc.frames)
+    _check(layer, integ, cfg, wc, frames, batch)
+
+
+@pytest.mark.parametrize("merge", [MergeMode.kSimpleRaycast, MergeMode.kGroupedRaycast, MergeMode.kGroupedAntiGraze])
+@pytest.mark.parametrize("weight", [WeightMode.kConstant, WeightMode.kInverseZ2, WeightMode.kInverseZ2Dropoff])
+def test_all_modes(gpu, merge, weight):
+    wc = W.CONFIGS[1]
+    cfg = W.tsdf_config(wc, merge_mode=int(merge), weight_mode=int(weight))
+    layer = TsdfLayer(wc.voxel_size, wc.vps)
+    integ = TsdfIntegrator(cfg, layer)
+    frames = W.frames(1, count=2, scale=0.15, start=5)
+    _check(layer, integ, cfg, wc, frames, batch=True)
+
+
+def test_cfg1_full_scale_frames(gpu):
+    """Three full-size 640x480 merged frames (~2M updates each), bit-exact."""
+    wc = W.CONFIGS[1]
+    cfg = W.tsdf_config(wc)
+    layer = TsdfLayer(wc.voxel_size, wc.vps)
+    integ = TsdfIntegrator(cfg, layer)
+    _check(layer, integ, cfg, wc, W.frames(1, count=3, start=0), batch=True)
+
+
+def test_cfg0_full_scale(gpu):
+    """The full cfg0 frame (simple, constant weight, ~2.9e7 updates), bit-exact."""
+    wc = W.CONFIGS[0]
+    cfg = W.tsdf_config(wc)
+    layer = TsdfLayer(wc.voxel_size, wc.vps)
+    integ = TsdfIntegrator(cfg, layer)
+    _check(layer, integ, cfg, wc, W.frames(0, count=1), batch=False)
+
+
+def test_batch_equals_sequential(gpu):
+    wc = W.CONFIGS[1]
+    cfg = W.tsdf_config(wc)
+    frames = W.frames(1, count=6, scale=0.3, start=20)
+    a = TsdfLayer(wc.voxel_size)
+    ia = TsdfIntegrator(cfg, a)
+    sa = [ia.integrate(Scan(*f)) for f in frames]
+    b = TsdfLayer(wc.voxel_size)
+    ib = TsdfIntegrator(cfg, b)
+    sb = ib.integrate_batch([Scan(*f) for f in frames])
+    assert [int(x) for x in sb[:, 0]] == sa
+    assert a.save_bytes() == b.save_bytes()
+
+
+def test_slab_growth_replay(gpu):
+    """Start with a 1-block slab: allocation overflows, the slab grows and the
+    batch is replayed; the result must still match the oracle exactly."""
+    wc = W.CONFIGS[2]
+    cfg = W.tsdf_config(wc)
+    layer = TsdfLayer(wc.voxel_size, wc.vps, block_capacity=1)
+    integ = TsdfIntegrator(cfg, layer)
+    _check(layer, integ, cfg, wc, W.frames(2, count=2, scale=0.2), batch=True)
+
+
+def test_empty_and_out_of_range(gpu):
+    v = 0.1
+    cfg = TsdfConfig.for_voxel_size(v)
+    cfg.merge_mode = MergeMode.kSimpleRaycast
+    cfg.weight_mode = WeightMode.kConstant
+    cfg.min_ray_length, cfg.max_ray_length = 0.5, 2.0
+    layer = TsdfLayer(v, 16)
+    integ = TsdfIntegrator(cfg, layer)
+    assert integ.integrate(Scan(np.zeros((0, 3), np.float32))) == 0
+    assert layer.block_count() == 0
+    pts = np.array([[0.2, 0, 0], [5.0, 0, 0]], np.float32)  # too close, too far
+    assert integ.integrate(Scan(pts)) == 0
+    assert integ.skipped_points_last_scan() == 2
+    assert layer.block_count() == 0
+    pts = np.array([[0.2, 0, 0], [5.0, 0, 0], [1.0, 0, 0]], np.float32)
+    assert integ.integrate(Scan(pts)) > 0
+    assert integ.skipped_points_last_scan() == 2  # test_tsdf_integrator.cpp:206-218
+
+
+def test_colour_mismatch_raises(gpu):
+    layer = TsdfLayer(0.1)
+    integ = TsdfIntegrator(TsdfConfig.for_voxel_size(0.1), layer)
+    with pytest.raises(ValueError, match="scan colors must parallel points"):
+        integ.integrate(Scan(np.ones((3, 3), np.float32), np.zeros((2, 3), np.uint8)))
+
+
+def test_invalid_config_raises():
+    with pytest.raises(ValueError, match="0 < dropoff_epsilon < truncation"):
+        TsdfIntegrator(TsdfConfig(truncation=0.1, dropoff_epsilon=0.1), None)
+
+
+def test_mixed_colour_batch(gpu):
+    wc = W.CONFIGS[1]
+    cfg = W.tsdf_config(wc)
+    fr = W.frames(1, count=3, scale=0.15, start=40)
+    fr[1] = (fr[1][0], None, fr[1][2])
+    layer = TsdfLayer(wc.voxel_size)
+    integ = TsdfIntegrator(cfg, layer)
+    _check(layer, integ, cfg, wc, fr, batch=True)
+
+
+def test_query_and_absence(gpu):
+    layer = TsdfLayer(0.1)
+    integ = TsdfIntegrator(TsdfConfig.for_voxel_size(0.1), layer)
+    assert layer.voxel_ptr((1, 2, 3)) is None
+    integ.integrate(Scan(np.array([[1.0, 0.05, 0.05]], np.float32)))
+    v = layer.voxel_ptr((10, 0, 0))
+    assert v is not None and v["weight"] > 0
+    assert layer.voxel_ptr((1000, 1000, 1000)) is None
+
+
+def test_vxblx_round_trip_and_resume(gpu, tmp_path):
+    """save -> load -> continue integrating equals integrating without the round trip."""
+    wc = W.CONFIGS[1]
+    cfg = W.tsdf_config(wc)
+    fr = W.frames(1, count=4, scale=0.15, start=60)
+    a = TsdfLayer(wc.voxel_size)
+    ia = TsdfIntegrator(cfg, a)
+    ia.integrate_batch([Scan(*f) for f in fr[:2]])
+    path = str(tmp_path / "layer.vxblx")
+    a.save_file(path)
+    b = TsdfLayer(wc.voxel_size)
+    b.load_bytes(open(path, "rb").read())
+    assert b.save_bytes() == a.save_bytes()
+    ib = TsdfIntegrator(cfg, b)
+    ia.integrate_batch([Scan(*f) for f in fr[2:]])
+    ib.integrate_batch([Scan(*f) for f in fr[2:]])
+    assert a.save_bytes() == b.save_bytes()
+
+
+def test_parse_errors(gpu):
+    from paper_1611_03631_b200 import ParseError
+    layer = TsdfLayer(0.1)
+    good = layer.save_bytes()
+    with pytest.raises(ParseError, match="bad magic"):
+        layer.load_bytes(b"Z" + good[1:])
+    with pytest.raises(ParseError, match="truncated"):
+        layer.load_bytes(good[:10])
+
+
+def test_consumers(gpu):
+    layer = TsdfLayer(0.1, 8)
+    layer.register_consumer("esdf")
+    layer.register_consumer("mesh")
+    integ = TsdfIntegrator(TsdfConfig.for_voxel_size(0.1), layer)
+    integ.integrate(Scan(np.array([[1.0, 0.3, 0.1]], np.float32)))
+    s1 = layer.drain_updated("esdf")
+    assert len(s1) == layer.block_count() > 0
+    assert layer.drain_updated("esdf") == set()
+    assert layer.drain_updated("mesh") == s1
+    with pytest.raises(ValueError, match="unknown updated-block consumer"):
+        layer.drain_updated("nobody")
