@@ -220,6 +220,7 @@ def main():
 
     # ---- timed: device-resident inputs
     layer.profile(True)
+    layer.batch_info(reset=True)
     layer.stage_times(reset=True)
     layer.kernel_launches(reset=True)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -233,6 +234,7 @@ def main():
     dev_ms = t0.elapsed_time(t1)
     stages = layer.stage_times(reset=True)
     launches = layer.kernel_launches(reset=True)
+    info = layer.batch_info(reset=True)
     layer.profile(False)
     ms = torch.tensor([dev_ms], device="cuda")
     if dist is not None:
@@ -264,18 +266,15 @@ def main():
     dom = max(("emit", "record_sort", "apply", "bundle", "ray_order", "ray_setup"), key=lambda k: stages[k][0])
     apply_ms = stages["apply"][0] / max(stages["apply"][1], 1)
     n_upd = updates_per_step
-    n_vox_est = None
+    n_vox = info["n_vox"] / args.steps
     prof_path = os.path.join(ROOT, "profiles", "roofline_inputs.json")
     traffic = None
     try:
         with open(prof_path) as f:
-            pj = json.load(f)
-        n_vox_est = pj.get("n_vox_per_step")
-        traffic = pj.get("apply_dram_bytes_per_launch")
+            traffic = json.load(f).get("apply_dram_bytes_per_launch")
     except Exception:
         pass
-    rho_vox = n_vox_est if n_vox_est else n_upd * 0.1
-    apply_bytes = 16.0 * n_upd + 24.0 * rho_vox
+    apply_bytes = 16.0 * n_upd + 24.0 * n_vox
     achieved = apply_bytes / (apply_ms / 1e3) / 1e9 if apply_ms > 0 else 0.0
 
     # ---- CPU baseline (the reference, rank 0, N=1 only, bounded sample)
@@ -306,6 +305,8 @@ def main():
                          "model": "16 B/update + 24 B/distinct voxel (SURVEY.md 8d)",
                          "apply_ms_per_launch": apply_ms},
             "stages_ms_per_step": {k: v[0] / args.steps for k, v in stages.items()},
+            "work": {"records_per_step": info["records"] / args.steps, "n_vox_per_step": n_vox,
+                     "longest_fold_chain": info["max_chain"], "blocks": info["blocks"]},
             "dominant_stage": dom,
             "gpu_launches": launches,
             "clocks": clocks.summary(),

@@ -128,8 +128,21 @@ int vxg_profile(vxg_handle* h, int enable);
 int vxg_stage_count(void);
 const char* vxg_stage_name(int stage);
 int vxg_stage_times(vxg_handle* h, double* ms, uint64_t* launches, uint64_t* units, int reset);
+/* Work counters since the last reset: out[0] = candidate records emitted,
+ * out[1] = distinct voxels folded (N_vox), out[2] = longest per-voxel fold
+ * chain (records), out[3] = allocated blocks. */
+int vxg_batch_info(vxg_handle* h, uint64_t* out, int reset);
 /* Kernel launches issued by the library since the last call (and reset). */
 int vxg_kernel_launches(vxg_handle* h, uint64_t* out, int reset);
+
+/* Self-test of the fast exact fold arithmetic used by the apply kernel:
+ * n random divisions (shared-reciprocal fast path vs __fdiv_rn) and n_seq
+ * random update sequences of length len (fast fold vs the reference-order
+ * update_tsdf_voxel restatement), all on the device. out[0], out[1] =
+ * mismatch counts (both must be 0). */
+int vxg_selftest_fold(int device, uint64_t n, uint64_t n_seq, uint32_t len, uint64_t seed, uint64_t* out);
+/* Debug: lengths and voxel keys of the n longest fold chains of the last batch. */
+int vxg_debug_top_runs(vxg_handle* h, uint32_t* len, uint32_t* keys, uint32_t n);
 
 /* ---- device evaluation of the reference's public free functions (tested
  * directly by the reference's unit tests, tsdf_integrator.h:46-59), batched: */

@@ -70,7 +70,10 @@ SIGNATURES = [
     ("vxg_stage_count", c_int, []),
     ("vxg_stage_name", c_char_p, [c_int]),
     ("vxg_stage_times", c_int, [c_void_p, POINTER(c_double), POINTER(c_uint64), POINTER(c_uint64), c_int]),
+    ("vxg_batch_info", c_int, [c_void_p, POINTER(c_uint64), c_int]),
     ("vxg_kernel_launches", c_int, [c_void_p, POINTER(c_uint64), c_int]),
+    ("vxg_selftest_fold", c_int, [c_int, c_uint64, c_uint64, c_uint32, c_uint64, POINTER(c_uint64)]),
+    ("vxg_debug_top_runs", c_int, [c_void_p, POINTER(c_uint32), POINTER(c_uint32), c_uint32]),
     ("vxg_eval_projective_distance", c_int, [c_int, c_void_p, c_void_p, c_void_p, c_uint64, c_void_p]),
     ("vxg_eval_measurement_weight", c_int, [c_int, c_int, c_void_p, c_void_p, c_uint64, c_float, c_float, c_void_p]),
     ("vxg_eval_update_voxels", c_int,

@@ -32,7 +32,7 @@ struct alignas(16) RayInfo {  // one cast_and_update call (tsdf_integrator.cpp:1
   uint32_t color;    // r | g<<8 | b<<16 | has_color<<31
   uint32_t frame;
   uint32_t valid;
-  uint32_t pad;
+  float depth;       // ||p - origin|| (cast_and_update :136), set by k_ray_count
   int32_t term[3];   // own terminal voxel (anti-graze)
   uint32_t pad2;
 };
@@ -102,7 +102,7 @@ __global__ void k_simple_rays(const float* __restrict__ xyz, const uint8_t* __re
     r.color = rgb != nullptr ? pack_color(rgb + 3 * i) : 0u;
     r.frame = f;
     r.valid = 1u;
-    r.pad = 0u;
+    r.depth = 0.0f;
     r.term[0] = r.term[1] = r.term[2] = 0;
     r.pad2 = 0u;
     rays[ray_idx[i]] = r;
@@ -264,7 +264,7 @@ __global__ void k_gather_rays(uint32_t R, const uint32_t* __restrict__ order, co
     r.color = g.color;
     r.frame = g.frame;
     r.valid = g.cast;
-    r.pad = 0u;
+    r.depth = 0.0f;
     r.term[0] = g.g[0];
     r.term[1] = g.g[1];
     r.term[2] = g.g[2];
@@ -276,7 +276,7 @@ __global__ void k_gather_rays(uint32_t R, const uint32_t* __restrict__ order, co
 // ---------------------------------------------------------------- rays -> records
 // cast_and_update's prologue (tsdf_integrator.cpp:135-143): exactly span+1
 // voxels per ray, so record offsets are known before traversal.
-__global__ void k_ray_count(uint32_t R, const RayInfo* __restrict__ rays, const float* __restrict__ poses,
+__global__ void k_ray_count(uint32_t R, RayInfo* __restrict__ rays, const float* __restrict__ poses,
                             TsdfParams tp, unsigned long long* __restrict__ counts,
                             unsigned long long* __restrict__ raycasts) {
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < R; j += gridDim.x * blockDim.x) {
@@ -286,6 +286,7 @@ __global__ void k_ray_count(uint32_t R, const RayInfo* __restrict__ rays, const 
       const float* Pm = poses + 12 * r.frame;
       const float ray[3] = {fsub(r.p[0], Pm[3]), fsub(r.p[1], Pm[7]), fsub(r.p[2], Pm[11])};
       const float depth = norm3(ray[0], ray[1], ray[2]);
+      rays[j].depth = depth;
       if (!(depth <= 0.0f)) {
         atomicAdd(&raycasts[r.frame], 1ull);
         const float s = fdiv(tp.truncation, depth);
@@ -327,20 +328,21 @@ __device__ __forceinline__ bool is_terminal(const TermView& tv, uint32_t f, cons
 }
 
 // cast_and_update's loop (tsdf_integrator.cpp:145-171): walk, weigh, allocate,
-// emit one record per update at offset[ray] + k; skipped candidates emit an
-// invalid key (sorted past every voxel, never folded).
+// emit one record per update at offset[ray] + k: (voxel key, ray index). The
+// fold recomputes (d, w) from the ray with the same arithmetic, so records stay
+// 8 bytes. Skipped candidates (anti-graze, w <= 0) emit an invalid key (sorted
+// past every voxel, never folded).
 __global__ void k_emit(uint32_t R0, uint32_t R1, const RayInfo* __restrict__ rays,
                        const unsigned long long* __restrict__ roff, uint64_t base, const float* __restrict__ poses,
                        TsdfParams tp, MapView map, TermView tv, uint32_t* __restrict__ rkeys,
-                       uint32_t* __restrict__ rvals, Record* __restrict__ recs,
-                       unsigned long long* __restrict__ updates) {
+                       uint32_t* __restrict__ rvals, unsigned long long* __restrict__ updates) {
   for (uint32_t j = R0 + blockIdx.x * blockDim.x + threadIdx.x; j < R1; j += gridDim.x * blockDim.x) {
     const RayInfo r = rays[j];
     if (r.valid != 1u) continue;
     const float* Pm = poses + 12 * r.frame;
     const float o[3] = {Pm[3], Pm[7], Pm[11]};
     const float ray[3] = {fsub(r.p[0], o[0]), fsub(r.p[1], o[1]), fsub(r.p[2], o[2])};
-    const float depth = norm3(ray[0], ray[1], ray[2]);
+    const float depth = r.depth;
     if (depth <= 0.0f) continue;
     const float s = fdiv(tp.truncation, depth);
     Dda dda;
@@ -362,7 +364,6 @@ __global__ void k_emit(uint32_t R0, uint32_t R1, const RayInfo* __restrict__ ray
     for (uint32_t k = 0; k < count; ++k) {
       const int g[3] = {dda.cur[0], dda.cur[1], dda.cur[2]};
       uint32_t key = kInvalidRecord;
-      Record rec{0.0f, 0.0f, 0u, 0u};
       bool skip = anti && !(g[0] == r.term[0] && g[1] == r.term[1] && g[2] == r.term[2]) &&
                   is_terminal(tv, r.frame, og, g);
       if (!skip) {
@@ -371,9 +372,7 @@ __global__ void k_emit(uint32_t R0, uint32_t R1, const RayInfo* __restrict__ ray
         const float d = projective_distance(x0, x1, x2, r.p[0], r.p[1], r.p[2], o[0], o[1], o[2]);
         const float w = fmul(measurement_weight(tp.weight_mode, depth, d, tp.truncation, tp.dropoff_epsilon),
                              r.weight);
-        if (w <= 0.0f) {
-          skip = true;
-        } else {
+        if (!(w <= 0.0f)) {
           int b[3], l[3];
 #pragma unroll
           for (int a = 0; a < 3; ++a) {
@@ -395,51 +394,257 @@ __global__ void k_emit(uint32_t R0, uint32_t R1, const RayInfo* __restrict__ ray
             key = static_cast<uint32_t>(cslot) * static_cast<uint32_t>(map.nvox) +
                   static_cast<uint32_t>(l[0] + vps * (l[1] + vps * l[2]));
           }
-          rec.d = d;
-          rec.w = w;
-          rec.color = r.color;
           ++valid;
         }
       }
       const uint64_t o_idx = out0 + k;
       rkeys[o_idx] = key;
-      rvals[o_idx] = static_cast<uint32_t>(o_idx);
-      recs[o_idx] = rec;
+      rvals[o_idx] = j;
       if (k + 1 < count && !dda.at_end()) dda.advance();
     }
     if (valid) atomicAdd(&updates[r.frame], static_cast<unsigned long long>(valid));
   }
 }
 
-// update_tsdf_voxel applied per voxel in (frame, ray-order) order: records are
-// stably sorted by voxel key, so each run head folds its run sequentially.
-__global__ void k_fold(uint64_t T, const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ svals,
-                       const Record* __restrict__ recs, MapView map, TsdfParams tp, uint8_t* __restrict__ touched) {
+// update_tsdf_voxel applied per voxel in (frame, ray-order) order. Records are
+// stably sorted by voxel key into runs (one per voxel), handed out longest
+// first. A run's fold is an inherently serial chain, so the kernel keeps
+// everything that does not depend on the voxel state OFF that chain:
+//  * runs >= kLongRun (the critical path, a few thousand runs): one warp per run. The 32 lanes gather 32 records
+//    (coalesced ray ids, parallel ray reads) and evaluate (d, w) in parallel,
+//    two chunks ahead of the fold; every lane then folds the chunk from shared
+//    memory (redundantly, so no lane idles on a branch).
+//  * shorter runs: one thread per run, 32 runs per warp, (d, w) for
+//    kFoldChunk records evaluated ahead of each folded chunk.
+// The fold step itself is update_voxel_fast (shared reciprocal, stationary
+// colour skip), bit-identical to update_tsdf_voxel.
+constexpr uint32_t kLongRun = 4096;
+constexpr int kFoldChunk = 8;
+
+struct alignas(16) Upd {
+  float d;
+  float w;
+  uint32_t c;
+  uint32_t pad;
+};
+
+__device__ __forceinline__ Upd weigh(const RayInfo& ry, const float* __restrict__ poses, float x0, float x1, float x2,
+                                     const TsdfParams& tp) {
+  const float* Pm = poses + 12 * ry.frame;
+  Upd u;
+  u.d = projective_distance(x0, x1, x2, ry.p[0], ry.p[1], ry.p[2], Pm[3], Pm[7], Pm[11]);
+  u.w = fmul(measurement_weight(tp.weight_mode, ry.depth, u.d, tp.truncation, tp.dropoff_epsilon), ry.weight);
+  u.c = ry.color;
+  u.pad = 0u;
+  return u;
+}
+
+struct RunCtx {
+  uint32_t key, start, len;
+  float x0, x1, x2;
+};
+
+__device__ __forceinline__ RunCtx run_ctx(const MapView& map, const TsdfParams& tp, const uint32_t* ukeys,
+                                          const uint32_t* ustart, const uint32_t* ulen, uint32_t run) {
+  RunCtx c;
+  c.key = ukeys[run];
+  c.start = ustart[run];
+  c.len = ulen[run];
+  c.x0 = c.x1 = c.x2 = 0.0f;
+  if (c.key == kInvalidRecord) return c;  // run of skipped candidates: never folded
+  const int vps = map.vps;
+  const uint32_t slot = c.key / static_cast<uint32_t>(map.nvox);
+  const uint32_t lin = c.key - slot * static_cast<uint32_t>(map.nvox);
+  const int l0 = static_cast<int>(lin % vps), l1 = static_cast<int>((lin / vps) % vps),
+            l2 = static_cast<int>(lin / (vps * vps));
+  c.x0 = vcenter(map.block_idx[3 * slot + 0] * vps + l0, tp.voxel_size);
+  c.x1 = vcenter(map.block_idx[3 * slot + 1] * vps + l1, tp.voxel_size);
+  c.x2 = vcenter(map.block_idx[3 * slot + 2] * vps + l2, tp.voxel_size);
+  return c;
+}
+
+struct VoxState {
+  float D, W, cr, cg, cb;
+};
+
+__device__ __forceinline__ VoxState load_vox(const vxg_voxel* vp) {
+  VoxState s;
+  s.D = vp->distance;
+  s.W = vp->weight;
+  s.cr = static_cast<float>(vp->r);
+  s.cg = static_cast<float>(vp->g);
+  s.cb = static_cast<float>(vp->b);
+  return s;
+}
+
+__device__ __forceinline__ void store_vox(vxg_voxel* vp, const VoxState& s) {
+  vp->distance = s.D;
+  vp->weight = s.W;
+  vp->r = static_cast<uint8_t>(s.cr);
+  vp->g = static_cast<uint8_t>(s.cg);
+  vp->b = static_cast<uint8_t>(s.cb);
+}
+
+__device__ __forceinline__ uint32_t count_long_runs(const uint32_t* __restrict__ sorted_len, uint32_t nruns) {
+  uint32_t lo = 0, hi = nruns;  // first index with len < kLongRun (lengths sorted descending)
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (sorted_len[mid] >= kLongRun) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(256) k_fold_runs(
+    const uint32_t* __restrict__ num_runs_p, const uint32_t* __restrict__ order,
+    const uint32_t* __restrict__ sorted_len, const uint32_t* __restrict__ ukeys, const uint32_t* __restrict__ ustart,
+    const uint32_t* __restrict__ ulen, const uint32_t* __restrict__ svals, const RayInfo* __restrict__ rays,
+    const float* __restrict__ poses, MapView map, TsdfParams tp, uint8_t* __restrict__ touched,
+    uint32_t* __restrict__ work) {
+  __shared__ Upd sbuf[8][2][32];
   if (map.counters[1] != 0u) return;  // emission failed (slab/hash full): host grows and replays
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < T;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint32_t key = skeys[i];
-    if (key == kInvalidRecord) continue;
-    if (i > 0 && skeys[i - 1] == key) continue;
-    vxg_voxel* vp = map.slab + key;
-    float D = vp->distance, W = vp->weight;
-    uint32_t rgb = static_cast<uint32_t>(vp->r) | (static_cast<uint32_t>(vp->g) << 8) |
-                   (static_cast<uint32_t>(vp->b) << 16);
-    for (uint64_t j = i; j < T && skeys[j] == key; ++j) {
-      const Record rec = recs[svals[j]];
-      update_voxel(D, W, rgb, rec.d, rec.w, rec.color, (rec.color >> 31) != 0u, tp.truncation, tp.max_weight);
+  const uint32_t nruns = *num_runs_p;
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  uint32_t n_long = 0;
+  if (lane == 0) n_long = count_long_runs(sorted_len, nruns);
+  n_long = __shfl_sync(0xffffffffu, n_long, 0);
+
+  // ---- phase 1: long runs, one warp per run
+  while (true) {
+    uint32_t r = 0;
+    if (lane == 0) r = atomicAdd(&work[0], 1u);
+    r = __shfl_sync(0xffffffffu, r, 0);
+    if (r >= n_long) break;
+    const uint32_t run = order[r];
+    const RunCtx c = run_ctx(map, tp, ukeys, ustart, ulen, run);
+    if (c.key == kInvalidRecord) continue;
+    vxg_voxel* vp = map.slab + c.key;
+    VoxState st = load_vox(vp);
+    const uint32_t nchunks = (c.len + 31) >> 5;
+    // prologue: weigh chunk 0, fetch ids of chunk 1
+    {
+      const uint32_t j = lane;
+      if (j < c.len) sbuf[wid][0][lane] = weigh(rays[svals[c.start + j]], poses, c.x0, c.x1, c.x2, tp);
     }
-    vp->distance = D;
-    vp->weight = W;
-    vp->r = static_cast<uint8_t>(rgb & 0xffu);
-    vp->g = static_cast<uint8_t>((rgb >> 8) & 0xffu);
-    vp->b = static_cast<uint8_t>((rgb >> 16) & 0xffu);
-    if (touched != nullptr) touched[key / static_cast<uint32_t>(map.nvox)] = 1u;
+    uint32_t id_next = 0;
+    {
+      const uint32_t j = 32 + lane;
+      if (j < c.len) id_next = svals[c.start + j];
+    }
+    __syncwarp();
+    for (uint32_t k = 0; k < nchunks; ++k) {
+      // issue the loads for chunk k+1 (rays) and k+2 (ids) before folding chunk k
+      const uint32_t j1 = (k + 1) * 32 + lane, j2 = (k + 2) * 32 + lane;
+      RayInfo ry1;
+      const bool has1 = j1 < c.len;
+      if (has1) ry1 = rays[id_next];
+      uint32_t id2 = 0;
+      if (j2 < c.len) id2 = svals[c.start + j2];
+      const uint32_t cnt = min(32u, c.len - k * 32);
+      const Upd* ub = sbuf[wid][k & 1];
+      if (cnt == 32) {
+#pragma unroll 8
+        for (int u = 0; u < 32; ++u) {
+          const Upd x = ub[u];
+          update_voxel_fast(st.D, st.W, st.cr, st.cg, st.cb, x.d, x.w, x.c, tp.truncation, tp.max_weight);
+        }
+      } else {
+        for (uint32_t u = 0; u < cnt; ++u) {
+          const Upd x = ub[u];
+          update_voxel_fast(st.D, st.W, st.cr, st.cg, st.cb, x.d, x.w, x.c, tp.truncation, tp.max_weight);
+        }
+      }
+      if (has1) sbuf[wid][(k + 1) & 1][lane] = weigh(ry1, poses, c.x0, c.x1, c.x2, tp);
+      id_next = id2;
+      __syncwarp();
+    }
+    if (lane == 0) {
+      store_vox(vp, st);
+      if (touched != nullptr) touched[c.key / static_cast<uint32_t>(map.nvox)] = 1u;
+    }
+  }
+
+  // ---- phase 2: short runs, one thread per run
+  while (true) {
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(&work[1], 32u);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (n_long + base >= nruns) break;
+    const uint32_t r = n_long + base + lane;
+    if (r >= nruns) continue;
+    const RunCtx c = run_ctx(map, tp, ukeys, ustart, ulen, order[r]);
+    if (c.key == kInvalidRecord) continue;
+    vxg_voxel* vp = map.slab + c.key;
+    VoxState st = load_vox(vp);
+    for (uint32_t j = 0; j < c.len; j += kFoldChunk) {
+      Upd xs[kFoldChunk];
+#pragma unroll
+      for (int u = 0; u < kFoldChunk; ++u) {
+        if (j + u < c.len) xs[u] = weigh(rays[svals[c.start + j + u]], poses, c.x0, c.x1, c.x2, tp);
+      }
+#pragma unroll
+      for (int u = 0; u < kFoldChunk; ++u) {
+        if (j + u < c.len)
+          update_voxel_fast(st.D, st.W, st.cr, st.cg, st.cb, xs[u].d, xs[u].w, xs[u].c, tp.truncation, tp.max_weight);
+      }
+    }
+    store_vox(vp, st);
+    if (touched != nullptr) touched[c.key / static_cast<uint32_t>(map.nvox)] = 1u;
+  }
+}
+
+// Self-tests of the fast fold arithmetic against the reference-order path.
+__global__ void k_selftest_div(uint64_t n, uint64_t seed, unsigned long long* __restrict__ mismatches,
+                               float* __restrict__ example) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t h1 = mix64(seed ^ (i * 0x9e3779b97f4a7c15ULL)), h2 = mix64(h1 + 0x632be59bd9b4e019ULL);
+    // random sign/mantissa, exponents spanning [-70, 70] (includes out-of-range -> fallback)
+    const uint32_t ea = 127 + static_cast<int>((h1 >> 32) % 141) - 70, eb = 127 + static_cast<int>((h2 >> 32) % 141) - 70;
+    const float a = __uint_as_float((static_cast<uint32_t>(h1 >> 63) << 31) | (ea << 23) | (static_cast<uint32_t>(h1) & 0x7fffff));
+    const float b = __uint_as_float((eb << 23) | (static_cast<uint32_t>(h2) & 0x7fffff));
+    const Recip r = make_recip(b);
+    const float q = div_by(a, r);
+    const float ref = __fdiv_rn(a, b);
+    if (__float_as_uint(q) != __float_as_uint(ref)) {
+      if (atomicAdd(mismatches, 1ull) == 0ull) {
+        example[0] = a;
+        example[1] = b;
+      }
+    }
+  }
+}
+
+__global__ void k_selftest_fold(uint64_t n_seq, uint32_t len, uint64_t seed, float trunc, float wmax,
+                                unsigned long long* __restrict__ mismatches) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n_seq;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    float D0 = 0.f, W0 = 0.f, D1 = 0.f, W1 = 0.f, cr = 0.f, cg = 0.f, cb = 0.f;
+    uint32_t rgb = 0u;
+    uint64_t h = mix64(seed + i);
+    const float wscale = (h & 1) ? 0.01f : 50.0f;
+    for (uint32_t k = 0; k < len; ++k) {
+      h = mix64(h + k + 1);
+      const float d = (static_cast<float>(h & 0xffffff) / 16777216.0f - 0.5f) * 4.0f * trunc;
+      const float w = (static_cast<float>((h >> 24) & 0xffffff) / 16777216.0f) * wscale + 1e-6f;
+      const uint32_t col = static_cast<uint32_t>((h >> 40) & 0xffffffu) | (((h >> 12) & 3u) ? 0x80000000u : 0u);
+      update_voxel(D0, W0, rgb, d, w, col, (col >> 31) != 0u, trunc, wmax);
+      update_voxel_fast(D1, W1, cr, cg, cb, d, w, col, trunc, wmax);
+      const uint32_t rgb1 = static_cast<uint32_t>(cr) | (static_cast<uint32_t>(cg) << 8) | (static_cast<uint32_t>(cb) << 16);
+      if (__float_as_uint(D0) != __float_as_uint(D1) || __float_as_uint(W0) != __float_as_uint(W1) || rgb != rgb1) {
+        atomicAdd(mismatches, 1ull);
+        break;
+      }
+    }
   }
 }
 
 __global__ void k_add_u64(uint32_t n, unsigned long long* __restrict__ dst, const unsigned long long* __restrict__ src) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] += src[i];
+}
+
+__global__ void k_iota(uint32_t n, uint32_t* __restrict__ out) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = i;
 }
 
 // ---------------------------------------------------------------- map maintenance

@@ -152,7 +152,8 @@ struct vxg_handle {
   DBuf<unsigned long long> rcount, roff;
   DBuf<uint64_t> tbl_off, bcs;
   DBuf<uint32_t> rkeys, rkeys2, rvals, rvals2;
-  DBuf<Record> recs;
+  DBuf<uint32_t> run_keys, run_len, run_start, run_len2, run_order, run_iota, work;
+  uint64_t info_records = 0, info_runs = 0, info_max_run = 0;  // since the last vxg_batch_info reset
 
   // ---- profiling
   bool profile = false;
@@ -604,14 +605,13 @@ void vxg_handle::emit_and_apply(uint32_t R, uint32_t F, const TermView& tv) {
     rkeys2.ensure(T);
     rvals.ensure(T);
     rvals2.ensure(T);
-    recs.ensure(T);
     d_upd.ensure(F);
     for (int attempt = 0;; ++attempt) {
       CU(cudaMemsetAsync(counters.p + 1, 0, sizeof(uint32_t), st));
       CU(cudaMemsetAsync(d_upd.p, 0, F * sizeof(unsigned long long), st));
       begin(ST_EMIT);
       k_emit<<<grid_for(r1 - r0, 128), 128, 0, st>>>(r0, r1, rays.p, roff.p, base, d_poses.p, tp, view(), tv,
-                                                       rkeys.p, rvals.p, recs.p, d_upd.p);
+                                                       rkeys.p, rvals.p, d_upd.p);
       ++launches;
       CU(cudaGetLastError());
       end(T, 1);
@@ -621,13 +621,65 @@ void vxg_handle::emit_and_apply(uint32_t R, uint32_t F, const TermView& tv) {
         return cub::DeviceRadixSort::SortPairs(t, b, rkeys.p, rkeys2.p, rvals.p, rvals2.p, static_cast<int>(T), 0,
                                                kbits, st);
       });
-      end(T, 1);
+      // runs = one per voxel (plus at most one run of invalid keys)
+      const uint64_t max_runs = std::min<uint64_t>(T, cap_blocks * static_cast<uint64_t>(nvox) + 1);
+      run_keys.ensure(max_runs);
+      run_len.ensure(max_runs);
+      num_runs.ensure(1);
+      cub([&](void* t, size_t& b) {
+        return cub::DeviceRunLengthEncode::Encode(t, b, rkeys2.p, run_keys.p, run_len.p, num_runs.p,
+                                                  static_cast<int>(T), st);
+      });
+      uint32_t nruns = 0;
+      CU(cudaMemcpyAsync(&nruns, num_runs.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+      CU(cudaStreamSynchronize(st));
+      run_start.ensure(nruns);
+      run_len2.ensure(nruns);
+      run_order.ensure(nruns);
+      run_iota.ensure(nruns);
+      cub([&](void* t, size_t& b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, run_len.p, run_start.p, static_cast<int>(nruns), st);
+      });
+      k_iota<<<grid_for(nruns), 256, 0, st>>>(nruns, run_iota.p);
+      ++launches;
+      const int lbits = bits_for(T);
+      cub([&](void* t, size_t& b) {  // longest runs first: they bound the fold's critical path
+        return cub::DeviceRadixSort::SortPairsDescending(t, b, run_len.p, run_len2.p, run_iota.p, run_order.p,
+                                                         static_cast<int>(nruns), 0, lbits, st);
+      });
+      end(T, 6);
       begin(ST_APPLY);
       uint8_t* tch = consumers.empty() ? nullptr : touched.p;
-      k_fold<<<grid_for(T), 256, 0, st>>>(T, rkeys2.p, rvals2.p, recs.p, view(), tp, tch);
+      work.ensure(2);
+      CU(cudaMemsetAsync(work.p, 0, 2 * sizeof(uint32_t), st));
+      int dev_sms = 148;
+      cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
+      int per_sm = 0;
+      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fold_runs, 256, 0));
+      const unsigned fold_grid = static_cast<unsigned>(
+          std::max<uint64_t>(1, std::min<uint64_t>(static_cast<uint64_t>(dev_sms) * std::max(per_sm, 1),
+                                                   (nruns + 255) / 256)));
+      k_fold_runs<<<fold_grid, 256, 0, st>>>(num_runs.p, run_order.p, run_len2.p, run_keys.p, run_start.p,
+                                              run_len.p, rvals2.p, rays.p, d_poses.p, view(), tp, tch, work.p);
       ++launches;
       CU(cudaGetLastError());
       end(T, 1);
+      {
+        // longest valid chain: the invalid-key run (if any) is the last run by key
+        uint32_t top[2] = {0, 0}, ord0 = 0, lastkey = 0;
+        const uint32_t ntop = std::min<uint32_t>(nruns, 2);
+        if (nruns) {
+          CU(cudaMemcpyAsync(top, run_len2.p, ntop * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+          CU(cudaMemcpyAsync(&ord0, run_order.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+          CU(cudaMemcpyAsync(&lastkey, run_keys.p + (nruns - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        }
+        CU(cudaStreamSynchronize(st));
+        const bool has_invalid = nruns && lastkey == kInvalidRecord;
+        const uint32_t mr = (has_invalid && ord0 == nruns - 1) ? top[1] : top[0];
+        info_records += T;
+        info_runs += nruns - (has_invalid ? 1 : 0);
+        info_max_run = std::max<uint64_t>(info_max_run, mr);
+      }
       uint32_t c[2];
       read_counters(c);
       if (c[1] & kErrKeyRange) throw VxgError(VXG_ERANGE, "voxel block index outside the supported range (+-2^20 blocks)");
@@ -1211,6 +1263,49 @@ int vxg_stage_times(vxg_handle* h, double* ms, uint64_t* launches, uint64_t* uni
     }
   }
   return VXG_OK;
+}
+
+int vxg_batch_info(vxg_handle* h, uint64_t* out, int reset) {
+  if (h == nullptr || out == nullptr) return VXG_EINVAL;
+  out[0] = h->info_records;
+  out[1] = h->info_runs;
+  out[2] = h->info_max_run;
+  out[3] = h->n_blocks;
+  if (reset) h->info_records = h->info_runs = h->info_max_run = 0;
+  return VXG_OK;
+}
+
+// Self-test of the fast exact fold arithmetic: n random divisions and n_seq
+// random update sequences of length len, compared bit-for-bit with the
+// reference-order path (__fdiv_rn / update_voxel). out[0] = division
+// mismatches, out[1] = sequence mismatches.
+extern "C" int vxg_selftest_fold(int device, uint64_t n, uint64_t n_seq, uint32_t len, uint64_t seed, uint64_t* out) {
+  return guarded([&] {
+    CU(cudaSetDevice(device));
+    DBuf<unsigned long long> mm;
+    DBuf<float> ex;
+    mm.ensure(2);
+    ex.ensure(2);
+    CU(cudaMemset(mm.p, 0, 2 * sizeof(unsigned long long)));
+    k_selftest_div<<<148 * 16, 256>>>(n, seed, mm.p, ex.p);
+    k_selftest_fold<<<148 * 4, 128>>>(n_seq, len, seed, 0.1f, 1e4f, mm.p + 1);
+    CU(cudaGetLastError());
+    unsigned long long h[2];
+    CU(cudaMemcpy(h, mm.p, sizeof(h), cudaMemcpyDeviceToHost));
+    out[0] = h[0];
+    out[1] = h[1];
+  });
+}
+
+// Debug: the n longest fold chains of the last chunk (length, voxel key).
+extern "C" int vxg_debug_top_runs(vxg_handle* h, uint32_t* len, uint32_t* keys, uint32_t n) {
+  return guarded([&] {
+    set_device(h);
+    std::vector<uint32_t> ord(n);
+    CU(cudaMemcpy(len, h->run_len2.p, n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(ord.data(), h->run_order.p, n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    for (uint32_t i = 0; i < n; ++i) CU(cudaMemcpy(&keys[i], h->run_keys.p + ord[i], 4, cudaMemcpyDeviceToHost));
+  });
 }
 
 int vxg_kernel_launches(vxg_handle* h, uint64_t* out, int reset) {

@@ -235,6 +235,12 @@ class TsdfLayer:
         check(lib().vxg_kernel_launches(self._h, ctypes.byref(n), 1 if reset else 0))
         return int(n.value)
 
+    def batch_info(self, reset: bool = True) -> Dict[str, int]:
+        """records emitted, distinct voxels folded (N_vox), longest fold chain, blocks."""
+        out = (ctypes.c_uint64 * 4)()
+        check(lib().vxg_batch_info(self._h, out, 1 if reset else 0))
+        return {"records": int(out[0]), "n_vox": int(out[1]), "max_chain": int(out[2]), "blocks": int(out[3])}
+
     def set_stream(self, stream_ptr: Optional[int]) -> None:
         check(lib().vxg_set_stream(self._h, ctypes.c_void_p(stream_ptr) if stream_ptr else None))
 

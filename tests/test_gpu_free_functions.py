@@ -93,3 +93,15 @@ def test_raycast_random(gpu):
         assert np.array_equal(walks[i], buf[:k]), i
         gs, ge = np.floor(start[i] / np.float32(v)), np.floor(end[i] / np.float32(v))
         assert k == int(np.abs(ge - gs).sum()) + 1  # always span+1 voxels
+
+
+def test_fast_fold_selftest(gpu):
+    """The apply kernel's fast fold (shared reciprocal, colour-stationarity
+    skip) must equal the reference-order update_tsdf_voxel bit-for-bit:
+    2^28 random divisions over exponents [-70, 70] and 20k random fold
+    sequences of 2000 steps (incl. weight saturation)."""
+    from paper_1611_03631_b200._capi import check, lib
+    out = (ctypes.c_uint64 * 2)()
+    check(lib().vxg_selftest_fold(0, 1 << 28, 20000, 2000, 12345, out))
+    assert out[0] == 0, f"{out[0]} division mismatches"
+    assert out[1] == 0, f"{out[1]} fold-sequence mismatches"
