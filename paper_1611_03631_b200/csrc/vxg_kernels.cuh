@@ -494,6 +494,40 @@ __device__ __forceinline__ uint32_t count_long_runs(const uint32_t* __restrict__
   return lo;
 }
 
+// Saturated, colour-stationary lane: when W == max_weight at the start of a
+// 32-record chunk, W stays max_weight (total = Wmax + w > Wmax) and, if every
+// record of the chunk leaves every colour channel unchanged
+// (colour_stationary), a step reduces to
+//   D <- RN(RN(RN(Wmax*D) + wc) / T),  wc = RN(w*clamp(d)), T = RN(Wmax + w)
+// whose wc, T and reciprocal are per-record constants the lanes precompute in
+// parallel. The serial chain is then FMUL, FADD and the 3-FMA quotient.
+struct alignas(16) SatRec {
+  float wc;
+  float T;
+  float r1;
+  float pad;
+};
+
+__device__ __forceinline__ bool sat_prepare(const Upd& x, float cr, float cg, float cb, const TsdfParams& tp,
+                                            SatRec* out) {
+  const float w = x.w;
+  const float clamped = x.d < -tp.truncation ? -tp.truncation : (tp.truncation < x.d ? tp.truncation : x.d);
+  const float T = __fadd_rn(tp.max_weight, w);
+  const Recip rt = make_recip(T);
+  out->wc = __fmul_rn(w, clamped);
+  out->T = T;
+  out->r1 = rt.r1;
+  out->pad = 0.0f;
+  bool ok = (w > 0.0f) & (w < 0x1p100f) & rt.ok;
+  if (x.c >> 31) {
+    const float thr = __fmul_rn(0.499f, T);
+    ok = ok & colour_stationary(thr, w, cr, __uint2float_rn(x.c & 0xffu)) &
+         colour_stationary(thr, w, cg, __uint2float_rn((x.c >> 8) & 0xffu)) &
+         colour_stationary(thr, w, cb, __uint2float_rn((x.c >> 16) & 0xffu));
+  }
+  return ok;
+}
+
 __global__ void __launch_bounds__(256) k_fold_runs(
     const uint32_t* __restrict__ num_runs_p, const uint32_t* __restrict__ order,
     const uint32_t* __restrict__ sorted_len, const uint32_t* __restrict__ ukeys, const uint32_t* __restrict__ ustart,
@@ -501,6 +535,7 @@ __global__ void __launch_bounds__(256) k_fold_runs(
     const float* __restrict__ poses, MapView map, TsdfParams tp, uint8_t* __restrict__ touched,
     uint32_t* __restrict__ work) {
   __shared__ Upd sbuf[8][2][32];
+  __shared__ SatRec ssat[8][32];
   if (map.counters[1] != 0u) return;  // emission failed (slab/hash full): host grows and replays
   const uint32_t nruns = *num_runs_p;
   const int lane = threadIdx.x & 31;
@@ -508,6 +543,7 @@ __global__ void __launch_bounds__(256) k_fold_runs(
   uint32_t n_long = 0;
   if (lane == 0) n_long = count_long_runs(sorted_len, nruns);
   n_long = __shfl_sync(0xffffffffu, n_long, 0);
+  const float Wmax = tp.max_weight;
 
   // ---- phase 1: long runs, one warp per run
   while (true) {
@@ -515,25 +551,25 @@ __global__ void __launch_bounds__(256) k_fold_runs(
     if (lane == 0) r = atomicAdd(&work[0], 1u);
     r = __shfl_sync(0xffffffffu, r, 0);
     if (r >= n_long) break;
-    const uint32_t run = order[r];
-    const RunCtx c = run_ctx(map, tp, ukeys, ustart, ulen, run);
+    const RunCtx c = run_ctx(map, tp, ukeys, ustart, ulen, order[r]);
     if (c.key == kInvalidRecord) continue;
     vxg_voxel* vp = map.slab + c.key;
     VoxState st = load_vox(vp);
     const uint32_t nchunks = (c.len + 31) >> 5;
-    // prologue: weigh chunk 0, fetch ids of chunk 1
-    {
-      const uint32_t j = lane;
-      if (j < c.len) sbuf[wid][0][lane] = weigh(rays[svals[c.start + j]], poses, c.x0, c.x1, c.x2, tp);
-    }
+    Upd x0{0.0f, 0.0f, 0u, 0u};
+    if (lane < c.len) x0 = weigh(rays[svals[c.start + lane]], poses, c.x0, c.x1, c.x2, tp);
+    sbuf[wid][0][lane] = x0;
     uint32_t id_next = 0;
+    if (32 + lane < c.len) id_next = svals[c.start + 32 + lane];
+    bool sat_ok;
     {
-      const uint32_t j = 32 + lane;
-      if (j < c.len) id_next = svals[c.start + j];
+      SatRec sr;
+      const bool ok = sat_prepare(x0, st.cr, st.cg, st.cb, tp, &sr) || lane >= c.len;
+      ssat[wid][lane] = sr;
+      sat_ok = __all_sync(0xffffffffu, ok) && st.W == Wmax;
     }
     __syncwarp();
     for (uint32_t k = 0; k < nchunks; ++k) {
-      // issue the loads for chunk k+1 (rays) and k+2 (ids) before folding chunk k
       const uint32_t j1 = (k + 1) * 32 + lane, j2 = (k + 2) * 32 + lane;
       RayInfo ry1;
       const bool has1 = j1 < c.len;
@@ -542,19 +578,48 @@ __global__ void __launch_bounds__(256) k_fold_runs(
       if (j2 < c.len) id2 = svals[c.start + j2];
       const uint32_t cnt = min(32u, c.len - k * 32);
       const Upd* ub = sbuf[wid][k & 1];
-      if (cnt == 32) {
-#pragma unroll 8
-        for (int u = 0; u < 32; ++u) {
-          const Upd x = ub[u];
-          update_voxel_fast(st.D, st.W, st.cr, st.cg, st.cb, x.d, x.w, x.c, tp.truncation, tp.max_weight);
+      bool done = false;
+      if (sat_ok) {
+        // D-only chain; verify the numerators' fast range afterwards
+        float D = st.D;
+        bool all = true;
+        if (cnt == 32) {
+#pragma unroll 16
+          for (int u = 0; u < 32; ++u) {
+            const SatRec sr = ssat[wid][u];
+            const float a = __fadd_rn(__fmul_rn(Wmax, D), sr.wc);
+            all = all & fast_range(a);
+            const float q0 = __fmul_rn(a, sr.r1);
+            D = __fmaf_rn(sr.r1, __fmaf_rn(-sr.T, q0, a), q0);
+          }
+        } else {
+          for (uint32_t u = 0; u < cnt; ++u) {
+            const SatRec sr = ssat[wid][u];
+            const float a = __fadd_rn(__fmul_rn(Wmax, D), sr.wc);
+            all = all & fast_range(a);
+            const float q0 = __fmul_rn(a, sr.r1);
+            D = __fmaf_rn(sr.r1, __fmaf_rn(-sr.T, q0, a), q0);
+          }
         }
-      } else {
+        if (all) {
+          st.D = D;
+          done = true;
+        }
+      }
+      if (!done) {  // general path (also the replay of a chunk whose fast lane bailed out)
         for (uint32_t u = 0; u < cnt; ++u) {
           const Upd x = ub[u];
           update_voxel_fast(st.D, st.W, st.cr, st.cg, st.cb, x.d, x.w, x.c, tp.truncation, tp.max_weight);
         }
       }
-      if (has1) sbuf[wid][(k + 1) & 1][lane] = weigh(ry1, poses, c.x0, c.x1, c.x2, tp);
+      __syncwarp();
+      Upd x1{0.0f, 0.0f, 0u, 0u};
+      if (has1) x1 = weigh(ry1, poses, c.x0, c.x1, c.x2, tp);
+      sbuf[wid][(k + 1) & 1][lane] = x1;
+      SatRec sr;
+      const bool ok = sat_prepare(x1, st.cr, st.cg, st.cb, tp, &sr) || !has1;
+      ssat[wid][lane] = sr;
+      sat_ok = __all_sync(0xffffffffu, ok) && st.W == Wmax;
       id_next = id2;
       __syncwarp();
     }

@@ -177,3 +177,26 @@ def test_consumers(gpu):
     assert layer.drain_updated("mesh") == s1
     with pytest.raises(ValueError, match="unknown updated-block consumer"):
         layer.drain_updated("nobody")
+
+
+@pytest.mark.parametrize("max_weight", [5.0, 60.0])
+def test_weight_saturation(gpu, max_weight):
+    """Low max_weight saturates most voxels: exercises the fold's saturated,
+    colour-stationary fast lane and its exact fallback, bit-exact vs the oracle."""
+    wc = W.CONFIGS[1]
+    cfg = W.tsdf_config(wc)
+    cfg.max_weight = max_weight
+    layer = TsdfLayer(wc.voxel_size, wc.vps)
+    integ = TsdfIntegrator(cfg, layer)
+    _check(layer, integ, cfg, wc, W.frames(1, count=4, scale=0.5, start=30), batch=True)
+
+
+def test_long_chains_full_trajectory_slice(gpu):
+    """20 full-size frames in one batch: fold chains of several 10^4 records
+    (warp-cooperative path), bit-exact vs the oracle."""
+    wc = W.CONFIGS[1]
+    cfg = W.tsdf_config(wc)
+    layer = TsdfLayer(wc.voxel_size, wc.vps)
+    integ = TsdfIntegrator(cfg, layer)
+    _check(layer, integ, cfg, wc, W.frames(1, count=20, start=0), batch=True)
+    assert layer.batch_info()["max_chain"] > 4096
