@@ -31,10 +31,10 @@ struct alignas(16) RayInfo {  // one cast_and_update call (tsdf_integrator.cpp:1
   float weight;      // merged base weight (1.0f in simple mode)
   uint32_t color;    // r | g<<8 | b<<16 | has_color<<31
   uint32_t frame;
-  uint32_t valid;
   float depth;       // ||p - origin|| (cast_and_update :136), set by k_ray_count
+  float base;        // measurement_weight base 1/depth^2 (1 in constant mode), set by k_ray_count
   int32_t term[3];   // own terminal voxel (anti-graze)
-  uint32_t pad2;
+  uint32_t valid;
 };
 
 struct alignas(16) Record {
@@ -104,7 +104,7 @@ __global__ void k_simple_rays(const float* __restrict__ xyz, const uint8_t* __re
     r.valid = 1u;
     r.depth = 0.0f;
     r.term[0] = r.term[1] = r.term[2] = 0;
-    r.pad2 = 0u;
+    r.base = 0.0f;
     rays[ray_idx[i]] = r;
   }
 }
@@ -143,7 +143,10 @@ __global__ void k_group_keys(const float* __restrict__ xyz, uint64_t P, const ui
 }
 
 // Per bucket: sequential fp64 sums in scan order (tsdf_integrator.cpp:213-219),
-// then the merged ray (:224-241).
+// then the merged ray (:224-241). Points are fetched kSegChunk at a time
+// (independent loads and weights ahead of the dependent fp64 sums).
+constexpr int kSegChunk = 8;
+
 __global__ void k_seg_reduce(const uint32_t* __restrict__ num_segs_p, const unsigned long long* __restrict__ ukeys,
                              const uint32_t* __restrict__ uoffs, const uint32_t* __restrict__ ucounts,
                              const uint32_t* __restrict__ svals, const float* __restrict__ xyz,
@@ -158,34 +161,61 @@ __global__ void k_seg_reduce(const uint32_t* __restrict__ num_segs_p, const unsi
     const uint64_t key = ukeys[s];
     const uint32_t f = static_cast<uint32_t>(key >> (3 * kb));
     const uint32_t start = uoffs[s], cnt = ucounts[s];
+    const bool sentinel = (key & field_mask) == field_mask;  // out-of-range points (:204-207)
+    {
+      const unsigned active = __activemask();
+      const unsigned peers = __match_any_sync(active, f);
+      const uint32_t nb = __reduce_add_sync(peers, sentinel ? 0u : 1u);
+      const uint32_t mn = __reduce_min_sync(peers, sentinel ? 0xFFFFFFFFu : s);
+      if ((threadIdx.x & 31) == static_cast<unsigned>(__ffs(peers) - 1) && nb) {
+        atomicAdd(&seg_count[f], nb);
+        atomicMin(&seg_start[f], mn);
+      }
+    }
     SegInfo out;
     out.frame = f;
-    if ((key & field_mask) == field_mask) {  // out-of-range points (tsdf_integrator.cpp:204-207)
+    if (sentinel) {
       atomicAdd(&skipped[f], static_cast<unsigned long long>(cnt));
       out.cast = 0xFFFFFFFFu;  // marks "not a bucket"
       segs[s] = out;
       continue;
     }
-    atomicAdd(&seg_count[f], 1u);
-    atomicMin(&seg_start[f], s);
     const float* Pm = poses + 12 * f;
     const float o[3] = {Pm[3], Pm[7], Pm[11]};
     double wp[3] = {0.0, 0.0, 0.0}, wc[3] = {0.0, 0.0, 0.0}, W = 0.0;
     const uint32_t first = svals[start];
-    for (uint32_t j = 0; j < cnt; ++j) {
-      const uint32_t i = svals[start + j];
-      float p[3];
-      transform_point(Pm, xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], p);
-      const float depth = norm3(fsub(p[0], o[0]), fsub(p[1], o[1]), fsub(p[2], o[2]));
-      const float w = tp.weight_mode == VXG_WEIGHT_CONSTANT ? 1.0f : fdiv(1.0f, fmul(depth, depth));
-      const double wd = static_cast<double>(w);
+    for (uint32_t j0 = 0; j0 < cnt; j0 += kSegChunk) {
+      float pp[kSegChunk][3];
+      float ww[kSegChunk];
+      uint32_t cc[kSegChunk];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) wp[k] = __dadd_rn(wp[k], __dmul_rn(wd, static_cast<double>(p[k])));
-      if (rgb != nullptr) {
-#pragma unroll
-        for (int k = 0; k < 3; ++k) wc[k] = __dadd_rn(wc[k], __dmul_rn(wd, static_cast<double>(rgb[3 * i + k])));
+      for (int u = 0; u < kSegChunk; ++u) {
+        ww[u] = 0.0f;
+        cc[u] = 0u;
+        if (j0 + u < cnt) {
+          const uint32_t i = svals[start + j0 + u];
+          transform_point(Pm, xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], pp[u]);
+          const float depth = norm3(fsub(pp[u][0], o[0]), fsub(pp[u][1], o[1]), fsub(pp[u][2], o[2]));
+          ww[u] = tp.weight_mode == VXG_WEIGHT_CONSTANT ? 1.0f : fdiv(1.0f, fmul(depth, depth));
+          if (rgb != nullptr)
+            cc[u] = static_cast<uint32_t>(rgb[3 * i]) | (static_cast<uint32_t>(rgb[3 * i + 1]) << 8) |
+                    (static_cast<uint32_t>(rgb[3 * i + 2]) << 16);
+        }
       }
-      W = __dadd_rn(W, wd);
+#pragma unroll
+      for (int u = 0; u < kSegChunk; ++u) {
+        if (j0 + u < cnt) {
+          const double wd = static_cast<double>(ww[u]);
+#pragma unroll
+          for (int k = 0; k < 3; ++k) wp[k] = __dadd_rn(wp[k], __dmul_rn(wd, static_cast<double>(pp[u][k])));
+          if (rgb != nullptr) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+              wc[k] = __dadd_rn(wc[k], __dmul_rn(wd, static_cast<double>((cc[u] >> (8 * k)) & 0xffu)));
+          }
+          W = __dadd_rn(W, wd);
+        }
+      }
     }
 #pragma unroll
     for (int k = 0; k < 3; ++k) out.mean[k] = __double2float_rn(__ddiv_rn(wp[k], W));
@@ -268,27 +298,51 @@ __global__ void k_gather_rays(uint32_t R, const uint32_t* __restrict__ order, co
     r.term[0] = g.g[0];
     r.term[1] = g.g[1];
     r.term[2] = g.g[2];
-    r.pad2 = 0u;
+    r.base = 0.0f;
     rays[j] = r;
   }
 }
 
+// Warp-aggregated counter add: lanes with equal `key` (frames are contiguous in
+// ray order, so a warp usually spans one or two) combine into one atomic.
+__device__ __forceinline__ void warp_add_by_key(unsigned long long* __restrict__ arr, uint32_t key, uint32_t val) {
+  const unsigned active = __activemask();
+  const unsigned peers = __match_any_sync(active, key);
+  const uint32_t sum = __reduce_add_sync(peers, val);
+  if ((threadIdx.x & 31) == static_cast<unsigned>(__ffs(peers) - 1) && sum != 0u)
+    atomicAdd(&arr[key], static_cast<unsigned long long>(sum));
+}
+
+// measurement_weight (tsdf_integrator.cpp:29-44) with base = 1/(z*z) hoisted
+// per ray (same value: fdiv(1, fmul(z, z))).
+__device__ __forceinline__ float mweight_base(int mode, float base, float d, float truncation, float eps) {
+  if (mode == VXG_WEIGHT_CONSTANT) return 1.0f;
+  if (mode == VXG_WEIGHT_INVERSE_Z2) return base;
+  if (mode != VXG_WEIGHT_INVERSE_Z2_DROPOFF) return 0.0f;
+  if (d > -eps) return base;
+  if (d < -truncation) return 0.0f;
+  return fdiv(fmul(base, fadd(d, truncation)), fsub(truncation, eps));
+}
+
 // ---------------------------------------------------------------- rays -> records
 // cast_and_update's prologue (tsdf_integrator.cpp:135-143): exactly span+1
-// voxels per ray, so record offsets are known before traversal.
+// voxels per ray, so record offsets are known before traversal. Also stores
+// the ray's depth and hoisted 1/depth^2.
 __global__ void k_ray_count(uint32_t R, RayInfo* __restrict__ rays, const float* __restrict__ poses,
                             TsdfParams tp, unsigned long long* __restrict__ counts,
                             unsigned long long* __restrict__ raycasts) {
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < R; j += gridDim.x * blockDim.x) {
     const RayInfo r = rays[j];
     uint64_t c = 0;
+    uint32_t cast = 0;
     if (r.valid == 1u) {
       const float* Pm = poses + 12 * r.frame;
       const float ray[3] = {fsub(r.p[0], Pm[3]), fsub(r.p[1], Pm[7]), fsub(r.p[2], Pm[11])};
       const float depth = norm3(ray[0], ray[1], ray[2]);
       rays[j].depth = depth;
+      rays[j].base = tp.weight_mode == VXG_WEIGHT_CONSTANT ? 1.0f : fdiv(1.0f, fmul(depth, depth));
       if (!(depth <= 0.0f)) {
-        atomicAdd(&raycasts[r.frame], 1ull);
+        cast = 1u;
         const float s = fdiv(tp.truncation, depth);
         Dda dda;
         dda.init(Pm[3], Pm[7], Pm[11], fadd(r.p[0], fmul(ray[0], s)), fadd(r.p[1], fmul(ray[1], s)),
@@ -297,6 +351,7 @@ __global__ void k_ray_count(uint32_t R, RayInfo* __restrict__ rays, const float*
       }
     }
     counts[j] = c;
+    warp_add_by_key(raycasts, r.frame, cast);
   }
 }
 
@@ -327,82 +382,195 @@ __device__ __forceinline__ bool is_terminal(const TermView& tv, uint32_t f, cons
   return lo < tv.start[f] + tv.count[f] && tv.keys[lo] == key;
 }
 
+// Per-CTA direct-mapped cache of block slots in shared memory. An entry is one
+// 64-bit word (slot << 40 | 13-bit-per-axis block key), so concurrent
+// readers/writers never see a torn pair; blocks outside the 13-bit range
+// bypass the cache.
+constexpr int kBlockCacheSize = 1024;
+
+__device__ __forceinline__ bool cache_key13(int bx, int by, int bz, uint64_t* k) {
+  if (bx < -4096 || bx >= 4096 || by < -4096 || by >= 4096 || bz < -4096 || bz >= 4096) return false;
+  *k = (static_cast<uint64_t>(bx & 0x1FFF) << 26) | (static_cast<uint64_t>(by & 0x1FFF) << 13) |
+       static_cast<uint64_t>(bz & 0x1FFF);
+  return true;
+}
+
+__device__ __forceinline__ int32_t cached_find_or_insert(unsigned long long* cache, const MapView& map, int bx,
+                                                         int by, int bz) {
+  uint64_t k13;
+  const bool cacheable = cache_key13(bx, by, bz, &k13);
+  uint32_t idx = 0;
+  if (cacheable) {
+    idx = static_cast<uint32_t>(mix64(k13)) & (kBlockCacheSize - 1);
+    const unsigned long long e = cache[idx];
+    if (e != ~0ull && (e & ((1ull << 40) - 1)) == k13) return static_cast<int32_t>(e >> 40);
+  }
+  const int32_t slot = map.find_or_insert(pack_block(bx, by, bz), bx, by, bz);
+  if (cacheable && slot >= 0) cache[idx] = (static_cast<unsigned long long>(slot) << 40) | k13;
+  return slot;
+}
+
 // cast_and_update's loop (tsdf_integrator.cpp:145-171): walk, weigh, allocate,
-// emit one record per update at offset[ray] + k: (voxel key, ray index). The
-// fold recomputes (d, w) from the ray with the same arithmetic, so records stay
-// 8 bytes. Skipped candidates (anti-graze, w <= 0) emit an invalid key (sorted
-// past every voxel, never folded).
-__global__ void k_emit(uint32_t R0, uint32_t R1, const RayInfo* __restrict__ rays,
-                       const unsigned long long* __restrict__ roff, uint64_t base, const float* __restrict__ poses,
-                       TsdfParams tp, MapView map, TermView tv, uint32_t* __restrict__ rkeys,
-                       uint32_t* __restrict__ rvals, unsigned long long* __restrict__ updates) {
-  for (uint32_t j = R0 + blockIdx.x * blockDim.x + threadIdx.x; j < R1; j += gridDim.x * blockDim.x) {
+// emit one record per candidate voxel at offset[ray] + k: (voxel key, ray
+// index). The fold recomputes (d, w) from the ray with the same arithmetic, so
+// records stay 8 bytes. Skipped candidates (anti-graze, w <= 0) emit an
+// invalid key (sorted past every voxel, never folded).
+//  * rays are processed in order of decreasing length (perm) so a warp's lanes
+//    walk similar numbers of voxels; outputs still go to offset[ray].
+//  * the walk state is kept in named registers (no runtime-indexed arrays);
+//    per step only the stepped axis's centre and block/local split change
+//    (same integer -> same vcenter; floor-div carry), both equal to the
+//    reference's from-scratch values.
+struct Walk {
+  int c0, c1, c2;        // current voxel
+  int e0, e1, e2;        // end voxel
+  int s0, s1, s2;        // steps
+  float m0, m1, m2;      // t_max
+  float d0, d1, d2;      // t_delta
+};
+
+__device__ __forceinline__ void walk_axis_init(float st, float en, float v, int* cur, int* end, int* step,
+                                               float* tmax, float* tdelta, uint32_t* span) {
+  *cur = gidx(st, v);
+  *end = gidx(en, v);
+  const float dir = fsub(en, st);
+  *step = dir > 0.0f ? 1 : (dir < 0.0f ? -1 : 0);
+  if (*step == 0) {
+    *tmax = __int_as_float(0x7f800000);
+    *tdelta = __int_as_float(0x7f800000);
+  } else {
+    const float boundary = fmul(__int2float_rn(*cur + (*step > 0 ? 1 : 0)), v);
+    *tmax = fdiv(fsub(boundary, st), dir);
+    *tdelta = fdiv(v, fabsf(dir));
+  }
+  const int dd = *end - *cur;
+  *span += static_cast<uint32_t>(dd < 0 ? -dd : dd);
+}
+
+__global__ void __launch_bounds__(128) k_emit(uint32_t R0, uint32_t R1, const uint32_t* __restrict__ perm,
+                       const RayInfo* __restrict__ rays, const unsigned long long* __restrict__ roff, uint64_t base,
+                       const float* __restrict__ poses, TsdfParams tp, MapView map, TermView tv,
+                       uint32_t* __restrict__ rkeys, uint32_t* __restrict__ rvals,
+                       unsigned long long* __restrict__ updates) {
+  __shared__ unsigned long long bcache[kBlockCacheSize];
+  for (int i = threadIdx.x; i < kBlockCacheSize; i += blockDim.x) bcache[i] = ~0ull;
+  __syncthreads();
+  const int vps = map.vps;
+  const float v = tp.voxel_size;
+  const bool anti = tp.merge_mode == VXG_MERGE_GROUPED_ANTI_GRAZE;
+  for (uint32_t t = R0 + blockIdx.x * blockDim.x + threadIdx.x; t < R1; t += gridDim.x * blockDim.x) {
+    const uint32_t j = perm[t];
     const RayInfo r = rays[j];
-    if (r.valid != 1u) continue;
     const float* Pm = poses + 12 * r.frame;
-    const float o[3] = {Pm[3], Pm[7], Pm[11]};
-    const float ray[3] = {fsub(r.p[0], o[0]), fsub(r.p[1], o[1]), fsub(r.p[2], o[2])};
+    const float o0 = Pm[3], o1 = Pm[7], o2 = Pm[11];
     const float depth = r.depth;
-    if (depth <= 0.0f) continue;
-    const float s = fdiv(tp.truncation, depth);
-    Dda dda;
-    dda.init(o[0], o[1], o[2], fadd(r.p[0], fmul(ray[0], s)), fadd(r.p[1], fmul(ray[1], s)),
-             fadd(r.p[2], fmul(ray[2], s)), tp.voxel_size);
-    const uint32_t count = dda.span + 1u;
-    const uint64_t out0 = roff[j] - base;
-    int og[3] = {0, 0, 0};
-    const bool anti = tp.merge_mode == VXG_MERGE_GROUPED_ANTI_GRAZE;
-    if (anti) {
-      og[0] = gidx(o[0], tp.voxel_size);
-      og[1] = gidx(o[1], tp.voxel_size);
-      og[2] = gidx(o[2], tp.voxel_size);
-    }
-    int cb[3] = {0x7fffffff, 0, 0};
-    int32_t cslot = -1;
     uint32_t valid = 0;
-    const int vps = map.vps;
-    for (uint32_t k = 0; k < count; ++k) {
-      const int g[3] = {dda.cur[0], dda.cur[1], dda.cur[2]};
-      uint32_t key = kInvalidRecord;
-      bool skip = anti && !(g[0] == r.term[0] && g[1] == r.term[1] && g[2] == r.term[2]) &&
-                  is_terminal(tv, r.frame, og, g);
-      if (!skip) {
-        const float x0 = vcenter(g[0], tp.voxel_size), x1 = vcenter(g[1], tp.voxel_size),
-                    x2 = vcenter(g[2], tp.voxel_size);
-        const float d = projective_distance(x0, x1, x2, r.p[0], r.p[1], r.p[2], o[0], o[1], o[2]);
-        const float w = fmul(measurement_weight(tp.weight_mode, depth, d, tp.truncation, tp.dropoff_epsilon),
-                             r.weight);
-        if (!(w <= 0.0f)) {
-          int b[3], l[3];
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            b[a] = floor_div(g[a], vps);
-            l[a] = g[a] - b[a] * vps;
-          }
-          if (b[0] != cb[0] || b[1] != cb[1] || b[2] != cb[2]) {
-            cb[0] = b[0];
-            cb[1] = b[1];
-            cb[2] = b[2];
-            if (block_in_range(b[0], b[1], b[2])) {
-              cslot = map.find_or_insert(pack_block(b[0], b[1], b[2]), b[0], b[1], b[2]);
-            } else {
-              atomicOr(&map.counters[1], static_cast<uint32_t>(kErrKeyRange));
-              cslot = -1;
-            }
-          }
-          if (cslot >= 0) {
-            key = static_cast<uint32_t>(cslot) * static_cast<uint32_t>(map.nvox) +
-                  static_cast<uint32_t>(l[0] + vps * (l[1] + vps * l[2]));
-          }
-          ++valid;
+    if (r.valid == 1u && !(depth <= 0.0f)) {
+      const float ray0 = fsub(r.p[0], o0), ray1 = fsub(r.p[1], o1), ray2 = fsub(r.p[2], o2);
+      const float s = fdiv(tp.truncation, depth);
+      Walk wk;
+      uint32_t span = 0;
+      walk_axis_init(o0, fadd(r.p[0], fmul(ray0, s)), v, &wk.c0, &wk.e0, &wk.s0, &wk.m0, &wk.d0, &span);
+      walk_axis_init(o1, fadd(r.p[1], fmul(ray1, s)), v, &wk.c1, &wk.e1, &wk.s1, &wk.m1, &wk.d1, &span);
+      walk_axis_init(o2, fadd(r.p[2], fmul(ray2, s)), v, &wk.c2, &wk.e2, &wk.s2, &wk.m2, &wk.d2, &span);
+      const uint32_t count = span + 1u;
+      const uint64_t out0 = roff[j] - base;
+      int og0 = 0, og1 = 0, og2 = 0;
+      if (anti) {
+        og0 = gidx(o0, v);
+        og1 = gidx(o1, v);
+        og2 = gidx(o2, v);
+      }
+      float x0 = vcenter(wk.c0, v), x1 = vcenter(wk.c1, v), x2 = vcenter(wk.c2, v);
+      int b0 = floor_div(wk.c0, vps), b1 = floor_div(wk.c1, vps), b2 = floor_div(wk.c2, vps);
+      int l0 = wk.c0 - b0 * vps, l1 = wk.c1 - b1 * vps, l2 = wk.c2 - b2 * vps;
+      int cb0 = 0x7fffffff, cb1 = 0, cb2 = 0;
+      int32_t cslot = -1;
+      const uint64_t al_lo = (out0 + 3ull) & ~3ull, al_hi = (out0 + count) & ~3ull;
+      uint32_t q0 = 0, q1 = 0, q2 = 0, q3 = 0;
+      // the ray index is every record's sort value: vector fill
+      for (uint64_t o = out0; o < out0 + count;) {
+        if ((o & 3ull) == 0 && o + 4 <= out0 + count) {
+          *reinterpret_cast<uint4*>(rvals + o) = make_uint4(j, j, j, j);
+          o += 4;
+        } else {
+          rvals[o] = j;
+          ++o;
         }
       }
-      const uint64_t o_idx = out0 + k;
-      rkeys[o_idx] = key;
-      rvals[o_idx] = j;
-      if (k + 1 < count && !dda.at_end()) dda.advance();
+      for (uint32_t k = 0; k < count; ++k) {
+        uint32_t key = kInvalidRecord;
+        bool skip = false;
+        if (anti) {
+          const int g[3] = {wk.c0, wk.c1, wk.c2};
+          const int og[3] = {og0, og1, og2};
+          skip = !(wk.c0 == r.term[0] && wk.c1 == r.term[1] && wk.c2 == r.term[2]) && is_terminal(tv, r.frame, og, g);
+        }
+        if (!skip) {
+          // projective_distance(x, p, s) (tsdf_integrator.cpp:22-27); p - s == ray
+          const float t0 = fsub(r.p[0], x0), t1 = fsub(r.p[1], x1), t2 = fsub(r.p[2], x2);
+          const float magnitude = norm3(t0, t1, t2);
+          const float along = dot3(t0, t1, t2, ray0, ray1, ray2);
+          const float d = along < 0.0f ? -magnitude : magnitude;
+          const float w = fmul(mweight_base(tp.weight_mode, r.base, d, tp.truncation, tp.dropoff_epsilon), r.weight);
+          if (!(w <= 0.0f)) {
+            if (b0 != cb0 || b1 != cb1 || b2 != cb2) {
+              cb0 = b0;
+              cb1 = b1;
+              cb2 = b2;
+              if (block_in_range(b0, b1, b2)) {
+                cslot = cached_find_or_insert(bcache, map, b0, b1, b2);
+              } else {
+                atomicOr(&map.counters[1], static_cast<uint32_t>(kErrKeyRange));
+                cslot = -1;
+              }
+            }
+            if (cslot >= 0) {
+              key = static_cast<uint32_t>(cslot) * static_cast<uint32_t>(map.nvox) +
+                    static_cast<uint32_t>(l0 + vps * (l1 + vps * l2));
+            }
+            ++valid;
+          }
+        }
+        // 16-byte vector stores on the 4-aligned interior of the ray's range
+        const uint64_t o_idx = out0 + k;
+        if (o_idx < al_lo || o_idx >= al_hi) {
+          rkeys[o_idx] = key;
+        } else {
+          q0 = q1;
+          q1 = q2;
+          q2 = q3;
+          q3 = key;
+          if ((o_idx & 3ull) == 3ull) *reinterpret_cast<uint4*>(rkeys + (o_idx - 3)) = make_uint4(q0, q1, q2, q3);
+        }
+        if (k + 1 < count && !(wk.c0 == wk.e0 && wk.c1 == wk.e1 && wk.c2 == wk.e2)) {
+          // RayCaster::next tail: axis = argmin t_max, ties to the lowest axis
+          const bool a1 = wk.m1 < wk.m0;
+          const float mlo = a1 ? wk.m1 : wk.m0;
+          const bool a2 = wk.m2 < mlo;
+          if (a2) {
+            wk.c2 += wk.s2;
+            wk.m2 = fadd(wk.m2, wk.d2);
+            x2 = vcenter(wk.c2, v);
+            l2 += wk.s2;
+            if (l2 == vps) { l2 = 0; ++b2; } else if (l2 < 0) { l2 = vps - 1; --b2; }
+          } else if (a1) {
+            wk.c1 += wk.s1;
+            wk.m1 = fadd(wk.m1, wk.d1);
+            x1 = vcenter(wk.c1, v);
+            l1 += wk.s1;
+            if (l1 == vps) { l1 = 0; ++b1; } else if (l1 < 0) { l1 = vps - 1; --b1; }
+          } else {
+            wk.c0 += wk.s0;
+            wk.m0 = fadd(wk.m0, wk.d0);
+            x0 = vcenter(wk.c0, v);
+            l0 += wk.s0;
+            if (l0 == vps) { l0 = 0; ++b0; } else if (l0 < 0) { l0 = vps - 1; --b0; }
+          }
+        }
+      }
     }
-    if (valid) atomicAdd(&updates[r.frame], static_cast<unsigned long long>(valid));
+    warp_add_by_key(updates, r.frame, valid);
   }
 }
 
@@ -433,7 +601,7 @@ __device__ __forceinline__ Upd weigh(const RayInfo& ry, const float* __restrict_
   const float* Pm = poses + 12 * ry.frame;
   Upd u;
   u.d = projective_distance(x0, x1, x2, ry.p[0], ry.p[1], ry.p[2], Pm[3], Pm[7], Pm[11]);
-  u.w = fmul(measurement_weight(tp.weight_mode, ry.depth, u.d, tp.truncation, tp.dropoff_epsilon), ry.weight);
+  u.w = fmul(mweight_base(tp.weight_mode, ry.base, u.d, tp.truncation, tp.dropoff_epsilon), ry.weight);
   u.c = ry.color;
   u.pad = 0u;
   return u;

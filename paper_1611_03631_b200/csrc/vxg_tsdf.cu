@@ -149,7 +149,8 @@ struct vxg_handle {
   DBuf<unsigned long long> ukeys;
   DBuf<SegInfo> segs;
   DBuf<RayInfo> rays;
-  DBuf<unsigned long long> rcount, roff;
+  DBuf<unsigned long long> rcount, roff, rcount2;
+  DBuf<uint32_t> ray_perm, ray_iota;
   DBuf<uint64_t> tbl_off, bcs;
   DBuf<uint32_t> rkeys, rkeys2, rvals, rvals2;
   DBuf<uint32_t> run_keys, run_len, run_start, run_len2, run_order, run_iota, work;
@@ -582,6 +583,17 @@ void vxg_handle::emit_and_apply(uint32_t R, uint32_t F, const TermView& tv) {
     CU(cudaStreamSynchronize(st));
   }
   auto roff_at = [&](uint32_t r) -> uint64_t { return r >= R ? total : (h_roff.empty() ? (r == 0 ? 0 : total) : h_roff[r]); };
+  // emission order: rays by decreasing record count (balanced warps); the
+  // records still land at their ray-order offsets.
+  ray_perm.ensure(R);
+  ray_iota.ensure(R);
+  rcount2.ensure(R);
+  k_iota<<<grid_for(R), 256, 0, st>>>(R, ray_iota.p);
+  ++launches;
+  cub([&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortPairsDescending(t, b, rcount.p, rcount2.p, ray_iota.p, ray_perm.p,
+                                                     static_cast<int>(R), 0, 16, st);
+  });
   ensure_touched();
   uint32_t r0 = 0;
   while (r0 < R) {
@@ -610,7 +622,9 @@ void vxg_handle::emit_and_apply(uint32_t R, uint32_t F, const TermView& tv) {
       CU(cudaMemsetAsync(counters.p + 1, 0, sizeof(uint32_t), st));
       CU(cudaMemsetAsync(d_upd.p, 0, F * sizeof(unsigned long long), st));
       begin(ST_EMIT);
-      k_emit<<<grid_for(r1 - r0, 128), 128, 0, st>>>(r0, r1, rays.p, roff.p, base, d_poses.p, tp, view(), tv,
+      // single chunk: all rays in length order; multi-chunk: ray order
+      const uint32_t* perm = h_roff.empty() ? ray_perm.p : ray_iota.p;
+      k_emit<<<grid_for(r1 - r0, 128), 128, 0, st>>>(r0, r1, perm, rays.p, roff.p, base, d_poses.p, tp, view(), tv,
                                                        rkeys.p, rvals.p, d_upd.p);
       ++launches;
       CU(cudaGetLastError());
