@@ -112,9 +112,10 @@ __global__ void k_simple_rays(const float* __restrict__ xyz, const uint8_t* __re
 // ---------------------------------------------------------------- grouped mode
 // Loop A key: (frame, terminal voxel relative to the origin voxel); out-of-range
 // points get the frame's sentinel (all-ones voxel field) and are counted later.
+template <typename KeyT>
 __global__ void k_group_keys(const float* __restrict__ xyz, uint64_t P, const uint64_t* __restrict__ off,
                              const float* __restrict__ poses, uint32_t F, TsdfParams tp, int rb, int kb,
-                             unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals,
+                             KeyT* __restrict__ keys, uint32_t* __restrict__ vals,
                              uint32_t* __restrict__ counters) {
   const uint64_t field_mask = (1ull << (3 * kb)) - 1ull;
   const int lim = (1 << kb) - 1;
@@ -137,9 +138,15 @@ __global__ void k_group_keys(const float* __restrict__ xyz, uint64_t P, const ui
               (static_cast<uint64_t>(e[1]) << kb) | static_cast<uint64_t>(e[2]);
       }
     }
-    keys[i] = key;
+    keys[i] = static_cast<KeyT>(key);
     vals[i] = static_cast<uint32_t>(i);
   }
+}
+
+__global__ void k_widen_keys(const uint32_t* __restrict__ num_p, const uint32_t* __restrict__ in,
+                             unsigned long long* __restrict__ out) {
+  const uint32_t n = *num_p;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = in[i];
 }
 
 // Per bucket: sequential fp64 sums in scan order (tsdf_integrator.cpp:213-219),

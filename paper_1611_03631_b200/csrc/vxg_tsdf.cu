@@ -119,6 +119,8 @@ struct vxg_handle {
   int device = 0;
   cudaStream_t own = nullptr;
   cudaStream_t st = nullptr;
+  cudaStream_t copy_st = nullptr;         // H2D staging of host inputs (overlaps compute)
+  std::vector<cudaEvent_t> copy_events;
 
   // ---- map (slab + block hash)
   DBuf<vxg_voxel> slab;
@@ -460,23 +462,45 @@ void vxg_handle::build_rays_grouped(const float* dxyz, const uint8_t* drgb, uint
   const int fb = bits_for(F > 1 ? F - 1 : 0);
   if (3 * kb + fb > 64) throw VxgError(VXG_EINVAL, "max_ray_length / voxel_size too large for the bundling key");
   begin(ST_BUNDLE);
-  pkeys.ensure(P);
-  pkeys2.ensure(P);
   pvals.ensure(P);
   pvals2.ensure(P);
-  k_group_keys<<<grid_for(P), 256, 0, st>>>(dxyz, P, d_off.p, d_poses.p, F, tp, rb, kb, pkeys.p, pvals.p, counters.p);
-  ++launches;
-  CU(cudaGetLastError());
   const int end_bit = 3 * kb + fb;
-  cub([&](void* t, size_t& b) {
-    return cub::DeviceRadixSort::SortPairs(t, b, pkeys.p, pkeys2.p, pvals.p, pvals2.p, static_cast<int>(P), 0, end_bit, st);
-  });
   ukeys.ensure(P);
   ucounts.ensure(P);
   num_runs.ensure(1);
-  cub([&](void* t, size_t& b) {
-    return cub::DeviceRunLengthEncode::Encode(t, b, pkeys2.p, ukeys.p, ucounts.p, num_runs.p, static_cast<int>(P), st);
-  });
+  if (end_bit <= 32) {  // 32-bit keys: half the sort traffic
+    uint32_t* k32 = reinterpret_cast<uint32_t*>(pkeys.ensure((P + 1) / 2));
+    uint32_t* k32b = reinterpret_cast<uint32_t*>(pkeys2.ensure((P + 1) / 2));
+    uint32_t* u32 = reinterpret_cast<uint32_t*>(okeys.ensure((P + 1) / 2));
+    k_group_keys<uint32_t><<<grid_for(P), 256, 0, st>>>(dxyz, P, d_off.p, d_poses.p, F, tp, rb, kb, k32, pvals.p,
+                                                        counters.p);
+    ++launches;
+    CU(cudaGetLastError());
+    cub([&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, k32, k32b, pvals.p, pvals2.p, static_cast<int>(P), 0, end_bit, st);
+    });
+    cub([&](void* t, size_t& b) {
+      return cub::DeviceRunLengthEncode::Encode(t, b, k32b, u32, ucounts.p, num_runs.p, static_cast<int>(P), st);
+    });
+    k_widen_keys<<<grid_for(P), 256, 0, st>>>(num_runs.p, u32, ukeys.p);
+    ++launches;
+    CU(cudaGetLastError());
+  } else {
+    pkeys.ensure(P);
+    pkeys2.ensure(P);
+    k_group_keys<unsigned long long><<<grid_for(P), 256, 0, st>>>(dxyz, P, d_off.p, d_poses.p, F, tp, rb, kb,
+                                                                  pkeys.p, pvals.p, counters.p);
+    ++launches;
+    CU(cudaGetLastError());
+    cub([&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, pkeys.p, pkeys2.p, pvals.p, pvals2.p, static_cast<int>(P), 0,
+                                             end_bit, st);
+    });
+    cub([&](void* t, size_t& b) {
+      return cub::DeviceRunLengthEncode::Encode(t, b, pkeys2.p, ukeys.p, ucounts.p, num_runs.p, static_cast<int>(P),
+                                                st);
+    });
+  }
   uint32_t S = 0;
   CU(cudaMemcpyAsync(&S, num_runs.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
@@ -729,14 +753,7 @@ void vxg_handle::run_sub(const float* xyz, const uint8_t* rgb, const uint64_t* o
   CU(cudaMemsetAsync(counters.p + 1, 0, sizeof(uint32_t), st));
   const float* dxyz = xyz + 3 * offsets[0];
   const uint8_t* drgb = rgb != nullptr ? rgb + 3 * offsets[0] : nullptr;
-  if (!device_input && P > 0) {
-    CU(cudaMemcpyAsync(in_xyz.ensure(3 * P), dxyz, 3 * P * sizeof(float), cudaMemcpyHostToDevice, st));
-    dxyz = in_xyz.p;
-    if (drgb != nullptr) {
-      CU(cudaMemcpyAsync(in_rgb.ensure(3 * P), drgb, 3 * P, cudaMemcpyHostToDevice, st));
-      drgb = in_rgb.p;
-    }
-  }
+  if (!device_input) throw VxgError(VXG_EINVAL, "internal: run_sub expects staged device inputs");
   end(P * (drgb ? 15 : 12), 0);
   if (P > 0) {
     uint32_t R = 0;
@@ -887,6 +904,11 @@ int vxg_destroy(vxg_handle* h) {
       cudaEventDestroy(pe.second.second);
     }
     for (cudaEvent_t e : h->event_pool) cudaEventDestroy(e);
+    if (h->copy_st) {
+      cudaStreamSynchronize(h->copy_st);
+      cudaStreamDestroy(h->copy_st);
+    }
+    for (cudaEvent_t e : h->copy_events) cudaEventDestroy(e);
     if (h->own) cudaStreamDestroy(h->own);
     delete h;
   });
@@ -914,6 +936,88 @@ int vxg_set_stream(vxg_handle* h, void* stream) {
   });
 }
 
+namespace {
+
+struct Copy {
+  uint64_t dst_pt;  // destination point offset in the staging buffer
+  const float* xyz;
+  const uint8_t* rgb;
+  uint64_t n;
+};
+
+// Frame-aligned sub-batches: <= 2^30 points each (32-bit point indices).
+std::vector<std::pair<uint64_t, uint64_t>> plan_subbatches(const uint64_t* off, uint64_t F, bool host_input) {
+  const uint64_t P = off[F] - off[0];
+  // One sub-batch whenever it fits: the fold's critical path is set by the
+  // hottest voxels' chains, which do not shrink with smaller batches, so
+  // splitting only to overlap the H2D copy costs more than it hides.
+  (void)P;
+  (void)host_input;
+  const uint64_t target = 1ull << 30;
+  std::vector<std::pair<uint64_t, uint64_t>> parts;
+  uint64_t f0 = 0;
+  while (f0 < F) {
+    uint64_t f1 = f0 + 1;
+    while (f1 < F && off[f1 + 1] - off[f0] <= target && f1 - f0 < 65535) ++f1;
+    if (off[f1] - off[f0] >= (1ull << 31)) throw VxgError(VXG_EINVAL, "a single scan exceeds 2^31 points");
+    parts.emplace_back(f0, f1);
+    f0 = f1;
+  }
+  return parts;
+}
+
+// Device-resident inputs: run the sub-batches directly. Host inputs: stage them
+// into device memory on the copy stream (one event per sub-batch) and let each
+// sub-batch's compute wait only for its own copy.
+void integrate_staged(vxg_handle* h, const std::vector<Copy>& copies, const float* dev_xyz, const uint8_t* dev_rgb,
+                      bool any_rgb, const uint64_t* off, const float* poses, uint64_t F, bool device_input,
+                      vxg_stats* out) {
+  const auto parts = plan_subbatches(off, F, !device_input);
+  const float* bx = dev_xyz;
+  const uint8_t* bc = dev_rgb;
+  if (!device_input) {
+    const uint64_t P = off[F] - off[0];
+    float* sx = h->in_xyz.ensure(std::max<uint64_t>(3 * P, 3));
+    uint8_t* sc = any_rgb ? h->in_rgb.ensure(std::max<uint64_t>(3 * P, 3)) : nullptr;
+    if (h->copy_st == nullptr) CU(cudaStreamCreateWithFlags(&h->copy_st, cudaStreamNonBlocking));
+    while (h->copy_events.size() < parts.size()) {
+      cudaEvent_t e;
+      CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      h->copy_events.push_back(e);
+    }
+    // the staging buffers may still be read by the previous call's kernels
+    cudaEvent_t prev_done = h->ev();
+    CU(cudaEventRecord(prev_done, h->st));
+    CU(cudaStreamWaitEvent(h->copy_st, prev_done, 0));
+    size_t ci = 0;
+    for (size_t p = 0; p < parts.size(); ++p) {
+      const uint64_t end_pt = off[parts[p].second] - off[0];
+      while (ci < copies.size() && copies[ci].dst_pt < end_pt) {
+        const Copy& c = copies[ci++];
+        if (c.n == 0) continue;
+        CU(cudaMemcpyAsync(sx + 3 * c.dst_pt, c.xyz, 3 * c.n * sizeof(float), cudaMemcpyHostToDevice, h->copy_st));
+        if (sc != nullptr && c.rgb != nullptr)
+          CU(cudaMemcpyAsync(sc + 3 * c.dst_pt, c.rgb, 3 * c.n, cudaMemcpyHostToDevice, h->copy_st));
+      }
+      CU(cudaEventRecord(h->copy_events[p], h->copy_st));
+    }
+    h->event_pool.push_back(prev_done);
+    bx = sx;
+    bc = sc;
+  }
+  // rebase: staging buffers start at point off[0]
+  std::vector<uint64_t> roff(F + 1);
+  for (uint64_t f = 0; f <= F; ++f) roff[f] = off[f] - off[0];
+  for (size_t p = 0; p < parts.size(); ++p) {
+    if (!device_input) CU(cudaStreamWaitEvent(h->st, h->copy_events[p], 0));
+    const uint64_t f0 = parts[p].first, f1 = parts[p].second;
+    h->run_sub(device_input ? dev_xyz : bx, device_input ? dev_rgb : bc, (device_input ? off : roff.data()) + f0,
+               poses + 12 * f0, f1 - f0, true, out ? out + f0 : nullptr);
+  }
+}
+
+}  // namespace
+
 int vxg_integrate_packed(vxg_handle* h, const float* xyz, const uint8_t* rgb, const uint64_t* offsets,
                          const float* poses, uint64_t F, int flags, vxg_stats* out) {
   return guarded([&] {
@@ -923,66 +1027,62 @@ int vxg_integrate_packed(vxg_handle* h, const float* xyz, const uint8_t* rgb, co
       if (offsets[f + 1] < offsets[f]) throw VxgError(VXG_EINVAL, "frame offsets must be non-decreasing");
     if (offsets[F] > offsets[0] && xyz == nullptr) throw VxgError(VXG_EINVAL, "null point buffer");
     set_device(h);
-    // sub-batches: <= 2^30 points each (32-bit point indices, bounded scratch)
-    const uint64_t kMaxPoints = 1ull << 30;
-    uint64_t f0 = 0;
-    while (f0 < F) {
-      uint64_t f1 = f0 + 1;
-      while (f1 < F && offsets[f1 + 1] - offsets[f0] <= kMaxPoints && f1 - f0 < 65535) ++f1;
-      if (offsets[f1] - offsets[f0] >= (1ull << 31)) throw VxgError(VXG_EINVAL, "a single scan exceeds 2^31 points");
-      h->run_sub(xyz, rgb, offsets + f0, poses + 12 * f0, f1 - f0, (flags & VXG_INPUT_DEVICE) != 0,
-                 out != nullptr ? out + f0 : nullptr);
-      f0 = f1;
+    const bool dev = (flags & VXG_INPUT_DEVICE) != 0;
+    std::vector<Copy> copies;
+    if (!dev) {
+      // one copy per frame keeps the sub-batch events frame-aligned
+      for (uint64_t f = 0; f < F; ++f)
+        copies.push_back({offsets[f] - offsets[0], xyz + 3 * offsets[f], rgb ? rgb + 3 * offsets[f] : nullptr,
+                          offsets[f + 1] - offsets[f]});
     }
+    integrate_staged(h, copies, xyz, rgb, rgb != nullptr, offsets, poses, F, dev, out);
   });
 }
 
 int vxg_integrate_batch(vxg_handle* h, const vxg_frame* frames, uint64_t F, int flags, vxg_stats* out) {
   return guarded([&] {
     if (h == nullptr || (frames == nullptr && F > 0)) throw VxgError(VXG_EINVAL, "null argument");
+    if (F == 0) return;
     set_device(h);
     const bool dev = (flags & VXG_INPUT_DEVICE) != 0;
-    // Frames are gathered into one packed staging buffer (device side).
     uint64_t P = 0;
-    bool any_rgb = false;
+    bool any_rgb = false, mixed_rgb = false;
     for (uint64_t f = 0; f < F; ++f) {
       P += frames[f].n;
       any_rgb = any_rgb || frames[f].rgb != nullptr;
     }
-    std::vector<uint64_t> off(F + 1, 0);
-    std::vector<float> poses(12 * F);
-    for (uint64_t f = 0; f < F; ++f) {
-      off[f + 1] = off[f] + frames[f].n;
-      std::memcpy(&poses[12 * f], frames[f].pose, 12 * sizeof(float));
-    }
-    bool mixed_rgb = false;
     for (uint64_t f = 0; f < F; ++f)
       if (any_rgb && frames[f].rgb == nullptr && frames[f].n > 0) mixed_rgb = true;
     if (mixed_rgb) {  // colour presence differs per scan: integrate scan by scan
       for (uint64_t f = 0; f < F; ++f) {
         const uint64_t o2[2] = {0, frames[f].n};
-        h->run_sub(frames[f].xyz, frames[f].rgb, o2, frames[f].pose, 1, dev, out ? out + f : nullptr);
+        std::vector<Copy> c{{0, frames[f].xyz, frames[f].rgb, frames[f].n}};
+        integrate_staged(h, dev ? std::vector<Copy>{} : c, frames[f].xyz, frames[f].rgb, frames[f].rgb != nullptr,
+                         o2, frames[f].pose, 1, dev, out ? out + f : nullptr);
       }
       return;
     }
+    std::vector<uint64_t> off(F + 1, 0);
+    std::vector<float> poses(12 * F);
+    std::vector<Copy> copies;
+    for (uint64_t f = 0; f < F; ++f) {
+      off[f + 1] = off[f] + frames[f].n;
+      std::memcpy(&poses[12 * f], frames[f].pose, 12 * sizeof(float));
+      copies.push_back({off[f], frames[f].xyz, frames[f].rgb, frames[f].n});
+    }
+    if (!dev) {
+      integrate_staged(h, copies, nullptr, nullptr, any_rgb, off.data(), poses.data(), F, false, out);
+      return;
+    }
+    // device frames in separate allocations: gather into the packed staging buffer
     float* sx = h->in_xyz.ensure(std::max<uint64_t>(3 * P, 3));
     uint8_t* sc = any_rgb ? h->in_rgb.ensure(std::max<uint64_t>(3 * P, 3)) : nullptr;
-    const cudaMemcpyKind kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    for (uint64_t f = 0; f < F; ++f) {
-      if (frames[f].n == 0) continue;
-      CU(cudaMemcpyAsync(sx + 3 * off[f], frames[f].xyz, 3 * frames[f].n * sizeof(float), kind, h->st));
-      if (sc) CU(cudaMemcpyAsync(sc + 3 * off[f], frames[f].rgb, 3 * frames[f].n, kind, h->st));
+    for (const Copy& c : copies) {
+      if (c.n == 0) continue;
+      CU(cudaMemcpyAsync(sx + 3 * c.dst_pt, c.xyz, 3 * c.n * sizeof(float), cudaMemcpyDeviceToDevice, h->st));
+      if (sc) CU(cudaMemcpyAsync(sc + 3 * c.dst_pt, c.rgb, 3 * c.n, cudaMemcpyDeviceToDevice, h->st));
     }
-    // the staging buffer is device memory now; run as device input (the
-    // buffers must not be re-staged, so integrate the sub-batches directly)
-    const uint64_t kMaxPoints = 1ull << 30;
-    uint64_t f0 = 0;
-    while (f0 < F) {
-      uint64_t f1 = f0 + 1;
-      while (f1 < F && off[f1 + 1] - off[f0] <= kMaxPoints && f1 - f0 < 65535) ++f1;
-      h->run_sub(sx, sc, off.data() + f0, poses.data() + 12 * f0, f1 - f0, true, out ? out + f0 : nullptr);
-      f0 = f1;
-    }
+    integrate_staged(h, {}, sx, sc, any_rgb, off.data(), poses.data(), F, true, out);
   });
 }
 
