@@ -120,6 +120,31 @@ int vxg_reset(vxg_handle* h);
 int vxg_register_consumer(vxg_handle* h, const char* name);
 int vxg_drain_updated(vxg_handle* h, const char* name, int32_t* idx, uint64_t cap, uint64_t* n_out);
 
+/* ---- sharded map: block-key ownership across ranks.
+ * Every rank bundles the whole batch (identical ray order), walks a
+ * record-balanced slice of the global ray order, routes each update record to
+ * the owner of its block (owner = mix64(block) mod world) with an all-to-all,
+ * and owners sort + fold. The union of the shards equals the 1-GPU layer
+ * bit-for-bit. */
+/* NCCL unique id (128 bytes) made by rank 0 and broadcast by the caller. */
+int vxg_nccl_unique_id(uint8_t* out);
+/* Makes h the shard `rank` of `world` (one process per GPU); world > 1 creates
+ * an NCCL communicator from id_bytes. vxg_integrate_* then run sharded and
+ * return the global per-frame counters on every rank. */
+int vxg_shard_init(vxg_handle* h, int rank, int world, const uint8_t* id_bytes);
+/* Loopback group: `world` shards on ONE device in one process, exchanging
+ * records with device-to-device copies (the sharded kernels without NVLink);
+ * used to test the sharded path on a single GPU. */
+typedef struct vxg_group vxg_group;
+int vxg_group_create(const vxg_tsdf_config* config, float voxel_size, int voxels_per_side, int device, int world,
+                     uint64_t block_capacity, vxg_group** out);
+int vxg_group_destroy(vxg_group* g);
+int vxg_group_shard(vxg_group* g, int i, vxg_handle** out);
+int vxg_group_set_config(vxg_group* g, const vxg_tsdf_config* config);
+int vxg_group_integrate_packed(vxg_group* g, const float* xyz, const uint8_t* rgb, const uint64_t* offsets,
+                               const float* poses, uint64_t n_frames, int flags, vxg_stats* out);
+int vxg_group_serialize_vxblx(vxg_group* g, uint8_t* buf, uint64_t cap, uint64_t* need);
+
 /* Stage profiling: when enabled, every batch records CUDA events around each
  * pipeline stage on the handle's stream. vxg_stage_times returns, per stage,
  * the accumulated milliseconds and launches since the last reset (names in

@@ -190,10 +190,19 @@ struct vxo_layer {
 
 namespace {
 
+struct TraceRec {  // one update_tsdf_voxel call, in reference order
+  int32_t ray;
+  int32_t g[3];
+  float d;
+  float w;
+  uint32_t color;  // r | g<<8 | b<<16 | has_color<<31
+};
+
 struct Integrator {
   const vxg_tsdf_config& c;
   vxo_layer* layer;
   uint64_t raycasts = 0;
+  std::vector<TraceRec>* trace = nullptr;  // test hook: record the update sequence
   Key3 cached_index{0, 0, 0};
   std::vector<vxg_voxel>* cached_block = nullptr;
 
@@ -232,6 +241,12 @@ struct Integrator {
       const size_t lin = static_cast<size_t>(local[0]) +
                          static_cast<size_t>(vps) * (static_cast<size_t>(local[1]) + static_cast<size_t>(vps) * static_cast<size_t>(local[2]));
       update_voxel(&(*cached_block)[lin], d, w, c.truncation, c.max_weight, color);
+      if (trace != nullptr) {
+        const uint32_t col = color != nullptr ? (static_cast<uint32_t>(color[0]) | (static_cast<uint32_t>(color[1]) << 8) |
+                                                 (static_cast<uint32_t>(color[2]) << 16) | 0x80000000u)
+                                              : 0u;
+        trace->push_back(TraceRec{static_cast<int32_t>(raycasts - 1), {g[0], g[1], g[2]}, d, w, col});
+      }
       ++updates;
     }
     return updates;
@@ -314,10 +329,13 @@ void vxo_layer_destroy(vxo_layer* l) { delete l; }
 
 size_t vxo_block_count(const vxo_layer* l) { return l->blocks.size(); }
 
+static std::vector<TraceRec>* g_trace = nullptr;
+
 int vxo_integrate(vxo_layer* l, const vxg_tsdf_config* c, const float* xyz, const uint8_t* rgb, size_t n,
                   const float pose[12], vxg_stats* out) {
   if (vxo_config_validate(c, nullptr, 0) != VXG_OK) return VXG_EINVAL;
   Integrator it{*c, l};
+  it.trace = g_trace;
   const float origin[3] = {pose[3], pose[7], pose[11]};
   uint64_t updates = 0, skipped = 0;
   if (c->merge_mode == VXG_MERGE_SIMPLE) {
@@ -362,6 +380,29 @@ int vxo_integrate(vxo_layer* l, const vxg_tsdf_config* c, const float* xyz, cons
     out->skipped = skipped;
   }
   return VXG_OK;
+}
+
+// Test hook: integrates one scan like vxo_integrate and returns the ordered
+// sequence of update_tsdf_voxel calls as records of 7 x 32-bit words
+// (ray index in ray order, gx, gy, gz, d (f32 bits), w (f32 bits), colour).
+size_t vxo_trace_updates(vxo_layer* l, const vxg_tsdf_config* c, const float* xyz, const uint8_t* rgb, size_t n,
+                         const float pose[12], uint32_t* out, size_t cap) {
+  std::vector<TraceRec> tr;
+  g_trace = &tr;
+  vxg_stats st;
+  vxo_integrate(l, c, xyz, rgb, n, pose, &st);
+  g_trace = nullptr;
+  for (size_t i = 0; i < tr.size() && i < cap; ++i) {
+    uint32_t* o = out + 7 * i;
+    o[0] = static_cast<uint32_t>(tr[i].ray);
+    o[1] = static_cast<uint32_t>(tr[i].g[0]);
+    o[2] = static_cast<uint32_t>(tr[i].g[1]);
+    o[3] = static_cast<uint32_t>(tr[i].g[2]);
+    std::memcpy(&o[4], &tr[i].d, 4);
+    std::memcpy(&o[5], &tr[i].w, 4);
+    o[6] = tr[i].color;
+  }
+  return tr.size();
 }
 
 size_t vxo_export_blocks(const vxo_layer* l, int32_t* idx, vxg_voxel* voxels, size_t cap) {

@@ -68,6 +68,12 @@ void vxo_global_index(const float p[3], float voxel_size, int32_t out[3]);
 /* IndexHash (core.h:68-74). */
 uint64_t vxo_index_hash(int32_t x, int32_t y, int32_t z);
 
+/* Test hook: integrates one scan like vxo_integrate and writes the ordered
+ * update_tsdf_voxel call sequence as 7-word records (ray index in ray order,
+ * gx, gy, gz, d bits, w bits, colour | has_colour<<31); returns the count. */
+size_t vxo_trace_updates(vxo_layer* l, const vxg_tsdf_config* c, const float* xyz, const uint8_t* rgb, size_t n,
+                         const float pose[12], uint32_t* out, size_t cap);
+
 /* Grouped-mode ray order: the terminal voxel keys of the in-range points in
  * IndexMap<PointBucket> iteration order (tsdf_integrator.cpp:199-223), i.e.
  * std::unordered_map itself after reserve(n/4+1). Writes up to cap keys

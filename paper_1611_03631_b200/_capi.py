@@ -72,6 +72,15 @@ SIGNATURES = [
     ("vxg_stage_times", c_int, [c_void_p, POINTER(c_double), POINTER(c_uint64), POINTER(c_uint64), c_int]),
     ("vxg_batch_info", c_int, [c_void_p, POINTER(c_uint64), c_int]),
     ("vxg_kernel_launches", c_int, [c_void_p, POINTER(c_uint64), c_int]),
+    ("vxg_nccl_unique_id", c_int, [c_void_p]),
+    ("vxg_shard_init", c_int, [c_void_p, c_int, c_int, c_void_p]),
+    ("vxg_group_create", c_int, [POINTER(VxgTsdfConfig), c_float, c_int, c_int, c_int, c_uint64, POINTER(c_void_p)]),
+    ("vxg_group_destroy", c_int, [c_void_p]),
+    ("vxg_group_shard", c_int, [c_void_p, c_int, POINTER(c_void_p)]),
+    ("vxg_group_set_config", c_int, [c_void_p, POINTER(VxgTsdfConfig)]),
+    ("vxg_group_integrate_packed", c_int,
+     [c_void_p, c_void_p, c_void_p, POINTER(c_uint64), POINTER(c_float), c_uint64, c_int, POINTER(VxgStats)]),
+    ("vxg_group_serialize_vxblx", c_int, [c_void_p, c_void_p, c_uint64, POINTER(c_uint64)]),
     ("vxg_selftest_fold", c_int, [c_int, c_uint64, c_uint64, c_uint32, c_uint64, POINTER(c_uint64)]),
     ("vxg_debug_top_runs", c_int, [c_void_p, POINTER(c_uint32), POINTER(c_uint32), c_uint32]),
     ("vxg_eval_projective_distance", c_int, [c_int, c_void_p, c_void_p, c_void_p, c_uint64, c_void_p]),

@@ -581,6 +581,191 @@ __global__ void __launch_bounds__(128) k_emit(uint32_t R0, uint32_t R1, const ui
   }
 }
 
+// ---------------------------------------------------------------- sharded map (multi-GPU)
+// Update records travelling between shards carry a global voxel key:
+// (bx + 2^14) << 49 | (by + 2^14) << 34 | (bz + 2^14) << 19 | local linear
+// index (vps <= 64). The owner of a block is mix64(packed block) % world.
+constexpr int32_t kGBias = 1 << 14;
+
+__device__ __host__ __forceinline__ bool gkey_encode(int b0, int b1, int b2, uint32_t lin, uint64_t* out) {
+  if (b0 < -kGBias || b0 >= kGBias || b1 < -kGBias || b1 >= kGBias || b2 < -kGBias || b2 >= kGBias) return false;
+  *out = (static_cast<uint64_t>(b0 + kGBias) << 49) | (static_cast<uint64_t>(b1 + kGBias) << 34) |
+         (static_cast<uint64_t>(b2 + kGBias) << 19) | static_cast<uint64_t>(lin);
+  return true;
+}
+
+__device__ __host__ __forceinline__ void gkey_decode(uint64_t k, int* b, uint32_t* lin) {
+  b[0] = static_cast<int>((k >> 49) & 0x7FFF) - kGBias;
+  b[1] = static_cast<int>((k >> 34) & 0x7FFF) - kGBias;
+  b[2] = static_cast<int>((k >> 19) & 0x7FFF) - kGBias;
+  *lin = static_cast<uint32_t>(k & 0x7FFFF);
+}
+
+__device__ __host__ __forceinline__ uint32_t block_owner(int b0, int b1, int b2, uint32_t world) {
+  return static_cast<uint32_t>(mix64(pack_block(b0, b1, b2)) % world);
+}
+
+// k_emit for one rank's slice [R0, R1) of the global ray order: same walk and
+// weights, but records carry (global voxel key, ray) and the block's owner;
+// no block allocation here (the owner allocates on receipt).
+__global__ void __launch_bounds__(128) k_emit_sharded(uint32_t R0, uint32_t R1, const RayInfo* __restrict__ rays,
+                                                      const unsigned long long* __restrict__ roff, uint64_t base,
+                                                      const float* __restrict__ poses, TsdfParams tp, int vps,
+                                                      uint32_t world, TermView tv,
+                                                      unsigned long long* __restrict__ gkeys,
+                                                      uint32_t* __restrict__ gvals, uint32_t* __restrict__ owner,
+                                                      uint32_t* __restrict__ counters) {
+  const float v = tp.voxel_size;
+  const bool anti = tp.merge_mode == VXG_MERGE_GROUPED_ANTI_GRAZE;
+  for (uint32_t j = R0 + blockIdx.x * blockDim.x + threadIdx.x; j < R1; j += gridDim.x * blockDim.x) {
+    const RayInfo r = rays[j];
+    const float* Pm = poses + 12 * r.frame;
+    const float o0 = Pm[3], o1 = Pm[7], o2 = Pm[11];
+    const float depth = r.depth;
+    if (!(r.valid == 1u && !(depth <= 0.0f))) continue;
+    const float ray0 = fsub(r.p[0], o0), ray1 = fsub(r.p[1], o1), ray2 = fsub(r.p[2], o2);
+    const float s = fdiv(tp.truncation, depth);
+    Walk wk;
+    uint32_t span = 0;
+    walk_axis_init(o0, fadd(r.p[0], fmul(ray0, s)), v, &wk.c0, &wk.e0, &wk.s0, &wk.m0, &wk.d0, &span);
+    walk_axis_init(o1, fadd(r.p[1], fmul(ray1, s)), v, &wk.c1, &wk.e1, &wk.s1, &wk.m1, &wk.d1, &span);
+    walk_axis_init(o2, fadd(r.p[2], fmul(ray2, s)), v, &wk.c2, &wk.e2, &wk.s2, &wk.m2, &wk.d2, &span);
+    const uint32_t count = span + 1u;
+    const uint64_t out0 = roff[j] - base;
+    int og0 = 0, og1 = 0, og2 = 0;
+    if (anti) {
+      og0 = gidx(o0, v);
+      og1 = gidx(o1, v);
+      og2 = gidx(o2, v);
+    }
+    float x0 = vcenter(wk.c0, v), x1 = vcenter(wk.c1, v), x2 = vcenter(wk.c2, v);
+    int b0 = floor_div(wk.c0, vps), b1 = floor_div(wk.c1, vps), b2 = floor_div(wk.c2, vps);
+    int l0 = wk.c0 - b0 * vps, l1 = wk.c1 - b1 * vps, l2 = wk.c2 - b2 * vps;
+    int cb0 = 0x7fffffff, cb1 = 0, cb2 = 0;
+    uint32_t cown = 0;
+    for (uint32_t k = 0; k < count; ++k) {
+      unsigned long long key = ~0ull;
+      uint32_t own = world;
+      bool skip = false;
+      if (anti) {
+        const int g[3] = {wk.c0, wk.c1, wk.c2};
+        const int og[3] = {og0, og1, og2};
+        skip = !(wk.c0 == r.term[0] && wk.c1 == r.term[1] && wk.c2 == r.term[2]) && is_terminal(tv, r.frame, og, g);
+      }
+      if (!skip) {
+        const float t0 = fsub(r.p[0], x0), t1 = fsub(r.p[1], x1), t2 = fsub(r.p[2], x2);
+        const float magnitude = norm3(t0, t1, t2);
+        const float along = dot3(t0, t1, t2, ray0, ray1, ray2);
+        const float d = along < 0.0f ? -magnitude : magnitude;
+        const float w = fmul(mweight_base(tp.weight_mode, r.base, d, tp.truncation, tp.dropoff_epsilon), r.weight);
+        if (!(w <= 0.0f)) {
+          if (b0 != cb0 || b1 != cb1 || b2 != cb2) {
+            cb0 = b0;
+            cb1 = b1;
+            cb2 = b2;
+            cown = block_owner(b0, b1, b2, world);
+          }
+          uint64_t gk;
+          if (gkey_encode(b0, b1, b2, static_cast<uint32_t>(l0 + vps * (l1 + vps * l2)), &gk)) {
+            key = gk;
+            own = cown;
+          } else {
+            atomicOr(&counters[1], static_cast<uint32_t>(kErrKeyRange));
+          }
+        }
+      }
+      const uint64_t o_idx = out0 + k;
+      gkeys[o_idx] = key;
+      gvals[o_idx] = j;
+      owner[o_idx] = own;
+      if (k + 1 < count && !(wk.c0 == wk.e0 && wk.c1 == wk.e1 && wk.c2 == wk.e2)) {
+        const bool a1 = wk.m1 < wk.m0;
+        const float mlo = a1 ? wk.m1 : wk.m0;
+        const bool a2 = wk.m2 < mlo;
+        if (a2) {
+          wk.c2 += wk.s2;
+          wk.m2 = fadd(wk.m2, wk.d2);
+          x2 = vcenter(wk.c2, v);
+          l2 += wk.s2;
+          if (l2 == vps) { l2 = 0; ++b2; } else if (l2 < 0) { l2 = vps - 1; --b2; }
+        } else if (a1) {
+          wk.c1 += wk.s1;
+          wk.m1 = fadd(wk.m1, wk.d1);
+          x1 = vcenter(wk.c1, v);
+          l1 += wk.s1;
+          if (l1 == vps) { l1 = 0; ++b1; } else if (l1 < 0) { l1 = vps - 1; --b1; }
+        } else {
+          wk.c0 += wk.s0;
+          wk.m0 = fadd(wk.m0, wk.d0);
+          x0 = vcenter(wk.c0, v);
+          l0 += wk.s0;
+          if (l0 == vps) { l0 = 0; ++b0; } else if (l0 < 0) { l0 = vps - 1; --b0; }
+        }
+      }
+    }
+  }
+}
+
+// bounds[o] = first position of owner o in the owner-sorted records (o <= world).
+__global__ void k_owner_bounds(uint64_t n, const uint32_t* __restrict__ sorted_owner, uint32_t world,
+                               unsigned long long* __restrict__ bounds) {
+  const uint32_t o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o > world) return;
+  uint64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (sorted_owner[mid] < o) lo = mid + 1; else hi = mid;
+  }
+  bounds[o] = lo;
+}
+
+// Ray range of a record range: first ray whose record offset is >= lo / >= hi.
+__global__ void k_ray_bounds(uint32_t R, const unsigned long long* __restrict__ roff, uint64_t lo_rec, uint64_t hi_rec,
+                             unsigned long long* __restrict__ out) {
+  const uint32_t t = threadIdx.x;
+  if (t > 1) return;
+  const uint64_t target = t == 0 ? lo_rec : hi_rec;
+  uint32_t lo = 0, hi = R;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (roff[mid] < target) lo = mid + 1; else hi = mid;
+  }
+  out[t] = lo;
+}
+
+// Packs the owner-sorted records into 16-byte messages {key lo, key hi, ray, 0}.
+__global__ void k_gather_send(uint64_t n, const uint32_t* __restrict__ perm, const unsigned long long* __restrict__ gkeys,
+                              const uint32_t* __restrict__ gvals, uint4* __restrict__ send) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t p = perm[i];
+    const unsigned long long k = gkeys[p];
+    send[i] = make_uint4(static_cast<uint32_t>(k), static_cast<uint32_t>(k >> 32), gvals[p], 0u);
+  }
+}
+
+// Owner side: global voxel key -> this shard's slot (allocating on first
+// update, like get_or_allocate_block) -> u32 record key; counts updates per frame.
+__global__ void k_localize(uint64_t n, const uint4* __restrict__ recv, MapView map, const RayInfo* __restrict__ rays,
+                           uint32_t* __restrict__ rkeys, uint32_t* __restrict__ rvals,
+                           unsigned long long* __restrict__ updates) {
+  __shared__ unsigned long long bcache[kBlockCacheSize];
+  for (int i = threadIdx.x; i < kBlockCacheSize; i += blockDim.x) bcache[i] = ~0ull;
+  __syncthreads();
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint4 m = recv[i];
+    const uint64_t k = static_cast<uint64_t>(m.x) | (static_cast<uint64_t>(m.y) << 32);
+    int b[3];
+    uint32_t lin;
+    gkey_decode(k, b, &lin);
+    const int32_t slot = cached_find_or_insert(bcache, map, b[0], b[1], b[2]);
+    rkeys[i] = slot >= 0 ? static_cast<uint32_t>(slot) * static_cast<uint32_t>(map.nvox) + lin : kInvalidRecord;
+    rvals[i] = m.z;
+    warp_add_by_key(updates, rays[m.z].frame, 1u);
+  }
+}
+
 // update_tsdf_voxel applied per voxel in (frame, ray-order) order. Records are
 // stably sorted by voxel key into runs (one per voxel), handed out longest
 // first. A run's fold is an inherently serial chain, so the kernel keeps

@@ -8,6 +8,11 @@
 //            -> K5 stable radix sort by voxel -> K7 ordered fold
 // Sorting/scans use CUB (CCCL 2.8, header-only, compiled into this library).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <array>
+#include <mutex>
 
 #include <algorithm>
 #include <cmath>
@@ -233,12 +238,14 @@ struct vxg_handle {
     pending.clear();
   }
 
+  // CUB device algorithm; n_kernels = kernels it launches (for the launch count).
   template <typename Fn>
-  void cub(Fn fn) {
+  void cub(Fn fn, int n_kernels = 1) {
     size_t bytes = 0;
     CU(fn(nullptr, bytes));
     if (bytes == 0) bytes = 1;
     CU(fn(cub_tmp.ensure(bytes), bytes));
+    launches += static_cast<uint64_t>(n_kernels);
   }
 
   // ---------------------------------------------------------------- map
@@ -375,6 +382,25 @@ struct vxg_handle {
   void order_rehash_frame(uint32_t f, uint32_t K, uint32_t seg0, uint64_t n_points, const Schedule& sch,
                           uint32_t ray0, int pb);
   void emit_and_apply(uint32_t R, uint32_t F, const TermView& tv);
+  uint64_t count_rays(uint32_t R, uint32_t F);
+  void sort_fold(uint64_t T);
+  bool grew_after_attempt(int attempt);
+  void begin_batch(const float* xyz, const uint8_t* rgb, const uint64_t* offsets, const float* poses, uint64_t F,
+                   uint32_t* R_out, TermView* tv);
+  void end_batch(uint64_t F, vxg_stats* out);
+  // ---- sharded map (multi-GPU / loopback group)
+  int shard_rank = 0;
+  int shard_world = 1;
+  void* nccl_comm = nullptr;
+  std::vector<uint64_t> send_counts, send_offsets, recv_counts;
+  uint64_t recv_total = 0;
+  DBuf<unsigned long long> gkeys, sbounds, obounds, dev_counts;
+  DBuf<uint32_t> gvals, gowner, gowner2, giota, gperm;
+  DBuf<uint4> send_buf, recv_buf;
+  void shard_front(uint32_t R, uint32_t F, const TermView& tv);
+  void shard_back(const uint4* recv, uint64_t n, uint32_t F);
+  void nccl_exchange();
+  void nccl_reduce_updates(uint32_t F);
 };
 
 void vxg_handle::build_rays_simple(const float* dxyz, const uint8_t* drgb, uint64_t P, uint32_t F, uint32_t* R_out) {
@@ -387,7 +413,7 @@ void vxg_handle::build_rays_simple(const float* dxyz, const uint8_t* drgb, uint6
   CU(cudaGetLastError());
   cub([&](void* t, size_t& b) {
     return cub::DeviceScan::ExclusiveSum(t, b, flags.p, ray_idx.p, static_cast<int>(P), st);
-  });
+  }, 2);
   uint32_t last_idx = 0, last_flag = 0;
   CU(cudaMemcpyAsync(&last_idx, ray_idx.p + (P - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   CU(cudaMemcpyAsync(&last_flag, flags.p + (P - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
@@ -478,10 +504,10 @@ void vxg_handle::build_rays_grouped(const float* dxyz, const uint8_t* drgb, uint
     CU(cudaGetLastError());
     cub([&](void* t, size_t& b) {
       return cub::DeviceRadixSort::SortPairs(t, b, k32, k32b, pvals.p, pvals2.p, static_cast<int>(P), 0, end_bit, st);
-    });
+    }, 2 + (end_bit + 7) / 8);
     cub([&](void* t, size_t& b) {
       return cub::DeviceRunLengthEncode::Encode(t, b, k32b, u32, ucounts.p, num_runs.p, static_cast<int>(P), st);
-    });
+    }, 2);
     k_widen_keys<<<grid_for(P), 256, 0, st>>>(num_runs.p, u32, ukeys.p);
     ++launches;
     CU(cudaGetLastError());
@@ -495,11 +521,11 @@ void vxg_handle::build_rays_grouped(const float* dxyz, const uint8_t* drgb, uint
     cub([&](void* t, size_t& b) {
       return cub::DeviceRadixSort::SortPairs(t, b, pkeys.p, pkeys2.p, pvals.p, pvals2.p, static_cast<int>(P), 0,
                                              end_bit, st);
-    });
+    }, 2 + (end_bit + 7) / 8);
     cub([&](void* t, size_t& b) {
       return cub::DeviceRunLengthEncode::Encode(t, b, pkeys2.p, ukeys.p, ucounts.p, num_runs.p, static_cast<int>(P),
                                                 st);
-    });
+    }, 2);
   }
   uint32_t S = 0;
   CU(cudaMemcpyAsync(&S, num_runs.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
@@ -507,7 +533,7 @@ void vxg_handle::build_rays_grouped(const float* dxyz, const uint8_t* drgb, uint
   uoffs.ensure(std::max<uint32_t>(S, 1));
   cub([&](void* t, size_t& b) {
     return cub::DeviceScan::ExclusiveSum(t, b, ucounts.p, uoffs.p, static_cast<int>(S), st);
-  });
+  }, 2);
   segs.ensure(std::max<uint32_t>(S, 1));
   seg_count.ensure(F);
   seg_start.ensure(F);
@@ -560,7 +586,7 @@ void vxg_handle::build_rays_grouped(const float* dxyz, const uint8_t* drgb, uint
   const int obits = std::min(64, fb + 2 * pb + 1);
   cub([&](void* t, size_t& b) {
     return cub::DeviceRadixSort::SortPairs(t, b, okeys.p, okeys2.p, ovals.p, ovals2.p, static_cast<int>(S), 0, obits, st);
-  });
+  }, 2 + (obits + 7) / 8);
   std::swap(ovals.p, ovals2.p);
   std::swap(ovals.cap, ovals2.cap);
   for (uint32_t f = 0; f < F; ++f) {
@@ -581,7 +607,7 @@ void vxg_handle::build_rays_grouped(const float* dxyz, const uint8_t* drgb, uint
   *R_out = R;
 }
 
-void vxg_handle::emit_and_apply(uint32_t R, uint32_t F, const TermView& tv) {
+uint64_t vxg_handle::count_rays(uint32_t R, uint32_t F) {
   const TsdfParams tp = params();
   begin(ST_RAYS);
   rcount.ensure(R);
@@ -591,13 +617,103 @@ void vxg_handle::emit_and_apply(uint32_t R, uint32_t F, const TermView& tv) {
   CU(cudaGetLastError());
   cub([&](void* t, size_t& b) {
     return cub::DeviceScan::ExclusiveSum(t, b, rcount.p, roff.p, static_cast<int>(R), st);
-  });
+  }, 2);
   unsigned long long tail[2] = {0, 0};
   CU(cudaMemcpyAsync(&tail[0], roff.p + (R - 1), sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   CU(cudaMemcpyAsync(&tail[1], rcount.p + (R - 1), sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
-  end(R, 2);
-  const uint64_t total = tail[0] + tail[1];
+  end(R, 3);
+  return tail[0] + tail[1];
+}
+
+// Stable sort of T records (rkeys = u32 voxel key, rvals = ray index) by voxel
+// key, runs (one per voxel) longest first, then the ordered fold.
+void vxg_handle::sort_fold(uint64_t T) {
+  const TsdfParams tp = params();
+  begin(ST_SORT);
+  const int kbits = bits_for(cap_blocks * static_cast<uint64_t>(nvox));
+  const int sort_passes = (kbits + 7) / 8;
+  cub([&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortPairs(t, b, rkeys.p, rkeys2.p, rvals.p, rvals2.p, static_cast<int>(T), 0, kbits,
+                                           st);
+  }, 2 + sort_passes);
+  // runs = one per voxel (plus at most one run of invalid keys)
+  const uint64_t max_runs = std::min<uint64_t>(T, cap_blocks * static_cast<uint64_t>(nvox) + 1);
+  run_keys.ensure(max_runs);
+  run_len.ensure(max_runs);
+  num_runs.ensure(1);
+  cub([&](void* t, size_t& b) {
+    return cub::DeviceRunLengthEncode::Encode(t, b, rkeys2.p, run_keys.p, run_len.p, num_runs.p, static_cast<int>(T),
+                                              st);
+  }, 2);
+  uint32_t nruns = 0;
+  CU(cudaMemcpyAsync(&nruns, num_runs.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  run_start.ensure(nruns);
+  run_len2.ensure(nruns);
+  run_order.ensure(nruns);
+  run_iota.ensure(nruns);
+  cub([&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, run_len.p, run_start.p, static_cast<int>(nruns), st);
+  }, 2);
+  k_iota<<<grid_for(nruns), 256, 0, st>>>(nruns, run_iota.p);
+  ++launches;
+  const int lbits = bits_for(T);
+  cub([&](void* t, size_t& b) {  // longest runs first: they bound the fold's critical path
+    return cub::DeviceRadixSort::SortPairsDescending(t, b, run_len.p, run_len2.p, run_iota.p, run_order.p,
+                                                     static_cast<int>(nruns), 0, lbits, st);
+  }, 2 + (lbits + 7) / 8);
+  end(T, 0);
+  begin(ST_APPLY);
+  uint8_t* tch = consumers.empty() ? nullptr : touched.p;
+  work.ensure(2);
+  CU(cudaMemsetAsync(work.p, 0, 2 * sizeof(uint32_t), st));
+  int dev_sms = 148;
+  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
+  int per_sm = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fold_runs, 256, 0));
+  const unsigned fold_grid = static_cast<unsigned>(std::max<uint64_t>(
+      1, std::min<uint64_t>(static_cast<uint64_t>(dev_sms) * std::max(per_sm, 1), (nruns + 255) / 256)));
+  k_fold_runs<<<fold_grid, 256, 0, st>>>(num_runs.p, run_order.p, run_len2.p, run_keys.p, run_start.p, run_len.p,
+                                          rvals2.p, rays.p, d_poses.p, view(), tp, tch, work.p);
+  ++launches;
+  CU(cudaGetLastError());
+  end(T, 1);
+  // longest valid chain: the invalid-key run (if any) is the last run by key
+  uint32_t top[2] = {0, 0}, ord0 = 0, lastkey = 0;
+  const uint32_t ntop = std::min<uint32_t>(nruns, 2);
+  if (nruns) {
+    CU(cudaMemcpyAsync(top, run_len2.p, ntop * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(&ord0, run_order.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(&lastkey, run_keys.p + (nruns - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  }
+  CU(cudaStreamSynchronize(st));
+  const bool has_invalid = nruns && lastkey == kInvalidRecord;
+  const uint32_t mr = (has_invalid && ord0 == nruns - 1) ? top[1] : top[0];
+  info_records += T;
+  info_runs += nruns - (has_invalid ? 1 : 0);
+  info_max_run = std::max<uint64_t>(info_max_run, mr);
+}
+
+// After a produce+sort_fold attempt: true if the map had to grow (the caller
+// re-produces the records; the slab was not modified by the failed attempt).
+bool vxg_handle::grew_after_attempt(int attempt) {
+  uint32_t c[2];
+  read_counters(c);
+  if (c[1] & kErrKeyRange) throw VxgError(VXG_ERANGE, "voxel block index outside the supported range");
+  if (c[1] & (kErrSlabFull | kErrHashFull)) {
+    if (attempt > 64) throw VxgError(VXG_ENOMEM, "block allocation did not converge");
+    if (c[1] & kErrHashFull) rehash(hcap * 2);
+    grow_map(std::max<uint64_t>(c[0], cap_blocks + 1));
+    ensure_touched();
+    return true;
+  }
+  return false;
+}
+
+void vxg_handle::emit_and_apply(uint32_t R, uint32_t F, const TermView& tv) {
+  const TsdfParams tp = params();
+  const uint64_t total = count_rays(R, F);
   // chunk rays so one chunk's records stay addressable and within memory
   const uint64_t kMaxRecords = 1ull << 29;
   std::vector<unsigned long long> h_roff;
@@ -606,7 +722,9 @@ void vxg_handle::emit_and_apply(uint32_t R, uint32_t F, const TermView& tv) {
     CU(cudaMemcpyAsync(h_roff.data(), roff.p, R * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
   }
-  auto roff_at = [&](uint32_t r) -> uint64_t { return r >= R ? total : (h_roff.empty() ? (r == 0 ? 0 : total) : h_roff[r]); };
+  auto roff_at = [&](uint32_t r) -> uint64_t {
+    return r >= R ? total : (h_roff.empty() ? (r == 0 ? 0 : total) : h_roff[r]);
+  };
   // emission order: rays by decreasing record count (balanced warps); the
   // records still land at their ray-order offsets.
   ray_perm.ensure(R);
@@ -617,7 +735,7 @@ void vxg_handle::emit_and_apply(uint32_t R, uint32_t F, const TermView& tv) {
   cub([&](void* t, size_t& b) {
     return cub::DeviceRadixSort::SortPairsDescending(t, b, rcount.p, rcount2.p, ray_iota.p, ray_perm.p,
                                                      static_cast<int>(R), 0, 16, st);
-  });
+  }, 4);
   ensure_touched();
   uint32_t r0 = 0;
   while (r0 < R) {
@@ -653,82 +771,8 @@ void vxg_handle::emit_and_apply(uint32_t R, uint32_t F, const TermView& tv) {
       ++launches;
       CU(cudaGetLastError());
       end(T, 1);
-      begin(ST_SORT);
-      const int kbits = bits_for(cap_blocks * static_cast<uint64_t>(nvox));
-      cub([&](void* t, size_t& b) {
-        return cub::DeviceRadixSort::SortPairs(t, b, rkeys.p, rkeys2.p, rvals.p, rvals2.p, static_cast<int>(T), 0,
-                                               kbits, st);
-      });
-      // runs = one per voxel (plus at most one run of invalid keys)
-      const uint64_t max_runs = std::min<uint64_t>(T, cap_blocks * static_cast<uint64_t>(nvox) + 1);
-      run_keys.ensure(max_runs);
-      run_len.ensure(max_runs);
-      num_runs.ensure(1);
-      cub([&](void* t, size_t& b) {
-        return cub::DeviceRunLengthEncode::Encode(t, b, rkeys2.p, run_keys.p, run_len.p, num_runs.p,
-                                                  static_cast<int>(T), st);
-      });
-      uint32_t nruns = 0;
-      CU(cudaMemcpyAsync(&nruns, num_runs.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-      CU(cudaStreamSynchronize(st));
-      run_start.ensure(nruns);
-      run_len2.ensure(nruns);
-      run_order.ensure(nruns);
-      run_iota.ensure(nruns);
-      cub([&](void* t, size_t& b) {
-        return cub::DeviceScan::ExclusiveSum(t, b, run_len.p, run_start.p, static_cast<int>(nruns), st);
-      });
-      k_iota<<<grid_for(nruns), 256, 0, st>>>(nruns, run_iota.p);
-      ++launches;
-      const int lbits = bits_for(T);
-      cub([&](void* t, size_t& b) {  // longest runs first: they bound the fold's critical path
-        return cub::DeviceRadixSort::SortPairsDescending(t, b, run_len.p, run_len2.p, run_iota.p, run_order.p,
-                                                         static_cast<int>(nruns), 0, lbits, st);
-      });
-      end(T, 6);
-      begin(ST_APPLY);
-      uint8_t* tch = consumers.empty() ? nullptr : touched.p;
-      work.ensure(2);
-      CU(cudaMemsetAsync(work.p, 0, 2 * sizeof(uint32_t), st));
-      int dev_sms = 148;
-      cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
-      int per_sm = 0;
-      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fold_runs, 256, 0));
-      const unsigned fold_grid = static_cast<unsigned>(
-          std::max<uint64_t>(1, std::min<uint64_t>(static_cast<uint64_t>(dev_sms) * std::max(per_sm, 1),
-                                                   (nruns + 255) / 256)));
-      k_fold_runs<<<fold_grid, 256, 0, st>>>(num_runs.p, run_order.p, run_len2.p, run_keys.p, run_start.p,
-                                              run_len.p, rvals2.p, rays.p, d_poses.p, view(), tp, tch, work.p);
-      ++launches;
-      CU(cudaGetLastError());
-      end(T, 1);
-      {
-        // longest valid chain: the invalid-key run (if any) is the last run by key
-        uint32_t top[2] = {0, 0}, ord0 = 0, lastkey = 0;
-        const uint32_t ntop = std::min<uint32_t>(nruns, 2);
-        if (nruns) {
-          CU(cudaMemcpyAsync(top, run_len2.p, ntop * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-          CU(cudaMemcpyAsync(&ord0, run_order.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-          CU(cudaMemcpyAsync(&lastkey, run_keys.p + (nruns - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-        }
-        CU(cudaStreamSynchronize(st));
-        const bool has_invalid = nruns && lastkey == kInvalidRecord;
-        const uint32_t mr = (has_invalid && ord0 == nruns - 1) ? top[1] : top[0];
-        info_records += T;
-        info_runs += nruns - (has_invalid ? 1 : 0);
-        info_max_run = std::max<uint64_t>(info_max_run, mr);
-      }
-      uint32_t c[2];
-      read_counters(c);
-      if (c[1] & kErrKeyRange) throw VxgError(VXG_ERANGE, "voxel block index outside the supported range (+-2^20 blocks)");
-      if (c[1] & (kErrSlabFull | kErrHashFull)) {
-        if (attempt > 64) throw VxgError(VXG_ENOMEM, "block allocation did not converge");
-        if (c[1] & kErrHashFull) rehash(hcap * 2);
-        grow_map(std::max<uint64_t>(c[0], cap_blocks + 1));
-        ensure_touched();
-        continue;
-      }
-      break;
+      sort_fold(T);
+      if (!grew_after_attempt(attempt)) break;
     }
     // fold this chunk's per-frame update counts into the stats
     k_add_u64<<<grid_for(F), 256, 0, st>>>(F, d_stats.p, d_upd.p);
@@ -738,8 +782,9 @@ void vxg_handle::emit_and_apply(uint32_t R, uint32_t F, const TermView& tv) {
   }
 }
 
-void vxg_handle::run_sub(const float* xyz, const uint8_t* rgb, const uint64_t* offsets, const float* poses,
-                         uint64_t F, bool device_input, vxg_stats* out) {
+// Stages the batch metadata and builds the rays (bundling + ray order).
+void vxg_handle::begin_batch(const float* xyz, const uint8_t* rgb, const uint64_t* offsets, const float* poses,
+                             uint64_t F, uint32_t* R_out, TermView* tv) {
   const uint64_t P = offsets[F] - offsets[0];
   std::vector<uint64_t> h_off(F + 1);
   for (uint64_t f = 0; f <= F; ++f) h_off[f] = offsets[f] - offsets[0];
@@ -753,21 +798,22 @@ void vxg_handle::run_sub(const float* xyz, const uint8_t* rgb, const uint64_t* o
   CU(cudaMemsetAsync(counters.p + 1, 0, sizeof(uint32_t), st));
   const float* dxyz = xyz + 3 * offsets[0];
   const uint8_t* drgb = rgb != nullptr ? rgb + 3 * offsets[0] : nullptr;
-  if (!device_input) throw VxgError(VXG_EINVAL, "internal: run_sub expects staged device inputs");
   end(P * (drgb ? 15 : 12), 0);
-  if (P > 0) {
-    uint32_t R = 0;
-    TermView tv{nullptr, nullptr, nullptr, 0, 0};
-    if (cfg.merge_mode == VXG_MERGE_SIMPLE) {
-      build_rays_simple(dxyz, drgb, P, static_cast<uint32_t>(F), &R);
-    } else {
-      build_rays_grouped(dxyz, drgb, P, h_off.data(), static_cast<uint32_t>(F), &R, &tv);
-    }
-    uint32_t c[2];
-    read_counters(c);
-    if (c[1] & kErrKeyRange) throw VxgError(VXG_ERANGE, "terminal voxel outside the bundling key range");
-    if (R > 0) emit_and_apply(R, static_cast<uint32_t>(F), tv);
+  *R_out = 0;
+  *tv = TermView{nullptr, nullptr, nullptr, 0, 0};
+  if (P == 0) return;
+  if (cfg.merge_mode == VXG_MERGE_SIMPLE) {
+    build_rays_simple(dxyz, drgb, P, static_cast<uint32_t>(F), R_out);
+  } else {
+    build_rays_grouped(dxyz, drgb, P, h_off.data(), static_cast<uint32_t>(F), R_out, tv);
   }
+  uint32_t c[2];
+  read_counters(c);
+  if (c[1] & kErrKeyRange) throw VxgError(VXG_ERANGE, "terminal voxel outside the bundling key range");
+}
+
+// Reads the per-frame stats back and feeds the updated-block consumers.
+void vxg_handle::end_batch(uint64_t F, vxg_stats* out) {
   begin(ST_D2H);
   std::vector<unsigned long long> s(3 * F);
   CU(cudaMemcpyAsync(s.data(), d_stats.p, 3 * F * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
@@ -797,11 +843,250 @@ void vxg_handle::run_sub(const float* xyz, const uint8_t* rgb, const uint64_t* o
   }
 }
 
+void vxg_handle::run_sub(const float* xyz, const uint8_t* rgb, const uint64_t* offsets, const float* poses,
+                         uint64_t F, bool device_input, vxg_stats* out) {
+  if (!device_input) throw VxgError(VXG_EINVAL, "internal: run_sub expects staged device inputs");
+  uint32_t R = 0;
+  TermView tv;
+  begin_batch(xyz, rgb, offsets, poses, F, &R, &tv);
+  if (shard_world > 1) {
+    if (nccl_comm == nullptr) throw VxgError(VXG_EINVAL, "sharded handle without a communicator (vxg_shard_init)");
+    shard_front(R, static_cast<uint32_t>(F), tv);
+    nccl_exchange();
+    shard_back(recv_buf.p, recv_total, static_cast<uint32_t>(F));
+    nccl_reduce_updates(static_cast<uint32_t>(F));
+  } else if (R > 0) {
+    emit_and_apply(R, static_cast<uint32_t>(F), tv);
+  }
+  end_batch(F, out);
+}
+
+// ---------------------------------------------------------------- sharded map
+// Every shard bundles the whole batch (identical rays and ray order), walks a
+// record-balanced contiguous slice of the global ray order, and partitions the
+// slice's update records by block owner. Concatenating what an owner receives
+// in source-rank order preserves ray order, so the owner's stable sort + fold
+// reproduce the single-GPU result for its blocks exactly.
+void vxg_handle::shard_front(uint32_t R, uint32_t F, const TermView& tv) {
+  send_counts.assign(shard_world, 0);
+  send_offsets.assign(shard_world, 0);
+  if (R == 0) return;
+  const TsdfParams tp = params();
+  const uint64_t total = count_rays(R, F);
+  // this rank's ray slice: records [rank*total/world, (rank+1)*total/world)
+  sbounds.ensure(2);
+  const uint64_t lo_rec = total * static_cast<uint64_t>(shard_rank) / shard_world;
+  const uint64_t hi_rec = total * static_cast<uint64_t>(shard_rank + 1) / shard_world;
+  k_ray_bounds<<<1, 32, 0, st>>>(R, roff.p, lo_rec, hi_rec, sbounds.p);
+  ++launches;
+  unsigned long long hb[2];
+  CU(cudaMemcpyAsync(hb, sbounds.p, sizeof(hb), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  const uint32_t R0 = static_cast<uint32_t>(hb[0]), R1 = static_cast<uint32_t>(hb[1]);
+  unsigned long long base = 0, endrec = total;
+  if (R0 < R) CU(cudaMemcpy(&base, roff.p + R0, sizeof(base), cudaMemcpyDeviceToHost));
+  else base = total;
+  if (R1 < R) CU(cudaMemcpy(&endrec, roff.p + R1, sizeof(endrec), cudaMemcpyDeviceToHost));
+  const uint64_t T = endrec - base;
+  if (T == 0) return;
+  begin(ST_EMIT);
+  gkeys.ensure(T);
+  gvals.ensure(T);
+  gowner.ensure(T);
+  gowner2.ensure(T);
+  giota.ensure(T);
+  gperm.ensure(T);
+  k_emit_sharded<<<grid_for(R1 - R0, 128), 128, 0, st>>>(R0, R1, rays.p, roff.p, base, d_poses.p, tp, vps,
+                                                          static_cast<uint32_t>(shard_world), tv, gkeys.p, gvals.p,
+                                                          gowner.p, counters.p);
+  k_iota<<<grid_for(T), 256, 0, st>>>(static_cast<uint32_t>(T), giota.p);
+  launches += 2;
+  CU(cudaGetLastError());
+  const int obits = bits_for(static_cast<uint64_t>(shard_world));
+  cub([&](void* t, size_t& b) {  // stable partition by owner (invalid records: owner == world, last)
+    return cub::DeviceRadixSort::SortPairs(t, b, gowner.p, gowner2.p, giota.p, gperm.p, static_cast<int>(T), 0, obits,
+                                           st);
+  }, 3);
+  obounds.ensure(shard_world + 1);
+  k_owner_bounds<<<1, 64, 0, st>>>(T, gowner2.p, static_cast<uint32_t>(shard_world), obounds.p);
+  ++launches;
+  std::vector<unsigned long long> bnd(shard_world + 1);
+  CU(cudaMemcpyAsync(bnd.data(), obounds.p, (shard_world + 1) * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  uint32_t c[2];
+  read_counters(c);
+  if (c[1] & kErrKeyRange) throw VxgError(VXG_ERANGE, "voxel block index outside the sharded key range (+-2^14 blocks)");
+  const uint64_t n_valid = bnd[shard_world];
+  send_buf.ensure(std::max<uint64_t>(n_valid, 1));
+  if (n_valid) {
+    k_gather_send<<<grid_for(n_valid), 256, 0, st>>>(n_valid, gperm.p, gkeys.p, gvals.p, send_buf.p);
+    ++launches;
+    CU(cudaGetLastError());
+  }
+  for (int o = 0; o < shard_world; ++o) {
+    send_offsets[o] = bnd[o];
+    send_counts[o] = bnd[o + 1] - bnd[o];
+  }
+  end(T, 0);
+}
+
+// Owner side: localize the received records (allocating owned blocks), then
+// the same stable sort + ordered fold as one GPU; updates counted per frame.
+void vxg_handle::shard_back(const uint4* recv, uint64_t n, uint32_t F) {
+  d_upd.ensure(F);
+  CU(cudaMemsetAsync(d_upd.p, 0, F * sizeof(unsigned long long), st));
+  if (n > 0) {
+    ensure_touched();
+    rkeys.ensure(n);
+    rkeys2.ensure(n);
+    rvals.ensure(n);
+    rvals2.ensure(n);
+    for (int attempt = 0;; ++attempt) {
+      CU(cudaMemsetAsync(counters.p + 1, 0, sizeof(uint32_t), st));
+      CU(cudaMemsetAsync(d_upd.p, 0, F * sizeof(unsigned long long), st));
+      k_localize<<<grid_for(n), 256, 0, st>>>(n, recv, view(), rays.p, rkeys.p, rvals.p, d_upd.p);
+      ++launches;
+      CU(cudaGetLastError());
+      sort_fold(n);
+      if (!grew_after_attempt(attempt)) break;
+    }
+  }
+  k_add_u64<<<grid_for(F), 256, 0, st>>>(F, d_stats.p, d_upd.p);
+  ++launches;
+  CU(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+// NCCL is loaded at run time (libnccl.so.2: torch's or the system's) so the
+// library has no link-time dependency on it; only sharded multi-GPU handles use it.
+namespace {
+
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi* nccl() {
+  static NcclApi api;
+  static bool loaded = false;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (loaded) return &api;
+  void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (lib == nullptr) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (lib == nullptr) throw VxgError(VXG_ECUDA, "cannot load libnccl.so.2 for the sharded path");
+  auto sym = [&](const char* n) {
+    void* p = dlsym(lib, n);
+    if (p == nullptr) throw VxgError(VXG_ECUDA, std::string("libnccl lacks ") + n);
+    return p;
+  };
+  api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+  api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+  api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+  api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+  api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
+  api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+  api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
+  api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
+  api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+  loaded = true;
+  return &api;
+}
+
+#define NC(x)                                                                                   \
+  do {                                                                                          \
+    ncclResult_t r_ = (x);                                                                      \
+    if (r_ != ncclSuccess) throw VxgError(VXG_ECUDA, std::string("NCCL: ") + nccl()->GetErrorString(r_)); \
+  } while (0)
+
+}  // namespace
+
+// All-to-all of the per-owner record buffers over NVLink (ncclSend/ncclRecv
+// group): counts first, then the 16-byte records, received in source-rank
+// order into one contiguous buffer.
+void vxg_handle::nccl_exchange() {
+  NcclApi* nc = nccl();
+  auto comm = static_cast<ncclComm_t>(nccl_comm);
+  const int W = shard_world;
+  dev_counts.ensure(2 * W);
+  std::vector<unsigned long long> sc(W);
+  for (int p = 0; p < W; ++p) sc[p] = send_counts[p];
+  CU(cudaMemcpyAsync(dev_counts.p, sc.data(), W * sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
+  NC(nc->GroupStart());
+  for (int p = 0; p < W; ++p) {
+    NC(nc->Send(dev_counts.p + p, 1, ncclUint64, p, comm, st));
+    NC(nc->Recv(dev_counts.p + W + p, 1, ncclUint64, p, comm, st));
+  }
+  NC(nc->GroupEnd());
+  std::vector<unsigned long long> rc(W);
+  CU(cudaMemcpyAsync(rc.data(), dev_counts.p + W, W * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  recv_counts.assign(W, 0);
+  recv_total = 0;
+  std::vector<uint64_t> roffs(W);
+  for (int p = 0; p < W; ++p) {
+    recv_counts[p] = rc[p];
+    roffs[p] = recv_total;
+    recv_total += rc[p];
+  }
+  recv_buf.ensure(std::max<uint64_t>(recv_total, 1));
+  send_buf.ensure(1);
+  NC(nc->GroupStart());
+  for (int p = 0; p < W; ++p) {
+    if (send_counts[p]) NC(nc->Send(send_buf.p + send_offsets[p], send_counts[p] * sizeof(uint4), ncclUint8, p, comm, st));
+    if (recv_counts[p]) NC(nc->Recv(recv_buf.p + roffs[p], recv_counts[p] * sizeof(uint4), ncclUint8, p, comm, st));
+  }
+  NC(nc->GroupEnd());
+}
+
+// Per-frame update counts are partial per owner: sum them over the shards.
+void vxg_handle::nccl_reduce_updates(uint32_t F) {
+  NC(nccl()->AllReduce(d_stats.p, d_stats.p, F, ncclUint64, ncclSum, static_cast<ncclComm_t>(nccl_comm), st));
+}
+
+// Loopback exchange for a group of shards on ONE device (all on one stream):
+// the same sharded kernels, with device-to-device copies standing in for NVLink.
+struct vxg_group {
+  std::vector<vxg_handle*> shards;
+};
+
+namespace {
+
+void group_exchange(vxg_group* g) {
+  const int W = static_cast<int>(g->shards.size());
+  cudaStream_t st = g->shards[0]->st;
+  for (int dst = 0; dst < W; ++dst) {
+    vxg_handle* d = g->shards[dst];
+    uint64_t total = 0;
+    for (int src = 0; src < W; ++src) total += g->shards[src]->send_counts.empty() ? 0 : g->shards[src]->send_counts[dst];
+    d->recv_buf.ensure(std::max<uint64_t>(total, 1));
+    d->recv_total = total;
+    uint64_t at = 0;
+    for (int src = 0; src < W; ++src) {
+      vxg_handle* s = g->shards[src];
+      if (s->send_counts.empty() || s->send_counts[dst] == 0) continue;
+      CU(cudaMemcpyAsync(d->recv_buf.p + at, s->send_buf.p + s->send_offsets[dst], s->send_counts[dst] * sizeof(uint4),
+                         cudaMemcpyDeviceToDevice, st));
+      at += s->send_counts[dst];
+    }
+  }
+}
+
+}  // namespace
+
 // ============================================================================ C ABI
 namespace {
 
 template <typename Fn>
 int guarded(Fn fn) {
+  cudaGetLastError();  // do not inherit a stale, non-sticky error from an unrelated earlier call
   try {
     fn();
     return VXG_OK;
@@ -898,7 +1183,8 @@ int vxg_destroy(vxg_handle* h) {
   if (h == nullptr) return VXG_OK;
   return guarded([&] {
     cudaSetDevice(h->device);
-    cudaStreamSynchronize(h->st);
+    if (h->st != nullptr && h->st == h->own) cudaStreamSynchronize(h->st);
+    if (h->own) cudaStreamSynchronize(h->own);
     for (auto& pe : h->pending) {
       cudaEventDestroy(pe.second.first);
       cudaEventDestroy(pe.second.second);
@@ -909,6 +1195,7 @@ int vxg_destroy(vxg_handle* h) {
       cudaStreamDestroy(h->copy_st);
     }
     for (cudaEvent_t e : h->copy_events) cudaEventDestroy(e);
+    if (h->nccl_comm) nccl()->CommDestroy(static_cast<ncclComm_t>(h->nccl_comm));
     if (h->own) cudaStreamDestroy(h->own);
     delete h;
   });
@@ -1426,6 +1713,174 @@ int vxg_kernel_launches(vxg_handle* h, uint64_t* out, int reset) {
   if (out) *out = h->launches;
   if (reset) h->launches = 0;
   return VXG_OK;
+}
+
+int vxg_nccl_unique_id(uint8_t* out) {
+  return guarded([&] {
+    ncclUniqueId id;
+    NC(nccl()->GetUniqueId(&id));
+    std::memcpy(out, id.internal, NCCL_UNIQUE_ID_BYTES);
+  });
+}
+
+int vxg_shard_init(vxg_handle* h, int rank, int world, const uint8_t* id_bytes) {
+  return guarded([&] {
+    if (world < 1 || rank < 0 || rank >= world) throw VxgError(VXG_EINVAL, "invalid shard rank / world");
+    set_device(h);
+    if (world > 1) {
+      ncclUniqueId id;
+      std::memcpy(id.internal, id_bytes, NCCL_UNIQUE_ID_BYTES);
+      ncclComm_t comm;
+      NC(nccl()->CommInitRank(&comm, world, id, rank));
+      h->nccl_comm = comm;
+    }
+    h->shard_rank = rank;
+    h->shard_world = world;
+  });
+}
+
+int vxg_group_create(const vxg_tsdf_config* config, float voxel_size, int vps, int device, int world,
+                     uint64_t block_capacity, vxg_group** out) {
+  return guarded([&] {
+    if (world < 1) throw VxgError(VXG_EINVAL, "group needs world >= 1");
+    auto* g = new vxg_group;
+    for (int r = 0; r < world; ++r) {
+      vxg_handle* h = nullptr;
+      const int rc = vxg_create(config, voxel_size, vps, device, block_capacity, &h);
+      if (rc != VXG_OK) {
+        for (vxg_handle* x : g->shards) vxg_destroy(x);
+        delete g;
+        throw VxgError(rc, g_err);
+      }
+      h->shard_rank = r;
+      h->shard_world = world;
+      if (r > 0) h->st = g->shards[0]->st;  // one stream: phases run in order
+      g->shards.push_back(h);
+    }
+    *out = g;
+  });
+}
+
+int vxg_group_destroy(vxg_group* g) {
+  if (g == nullptr) return VXG_OK;
+  // shards 1.. run on shard 0's stream: destroy them before shard 0
+  for (size_t i = g->shards.size(); i-- > 0;) vxg_destroy(g->shards[i]);
+  delete g;
+  return VXG_OK;
+}
+
+int vxg_group_shard(vxg_group* g, int i, vxg_handle** out) {
+  if (g == nullptr || i < 0 || i >= static_cast<int>(g->shards.size())) return VXG_EINVAL;
+  *out = g->shards[i];
+  return VXG_OK;
+}
+
+int vxg_group_set_config(vxg_group* g, const vxg_tsdf_config* config) {
+  for (vxg_handle* h : g->shards) {
+    const int rc = vxg_set_config(h, config);
+    if (rc != VXG_OK) return rc;
+  }
+  return VXG_OK;
+}
+
+int vxg_group_integrate_packed(vxg_group* g, const float* xyz, const uint8_t* rgb, const uint64_t* offsets,
+                               const float* poses, uint64_t F, int flags, vxg_stats* out) {
+  return guarded([&] {
+    if (g == nullptr || offsets == nullptr || poses == nullptr) throw VxgError(VXG_EINVAL, "null argument");
+    if (F == 0) return;
+    vxg_handle* h0 = g->shards[0];
+    set_device(h0);
+    const uint64_t P = offsets[F] - offsets[0];
+    const float* dx = xyz;
+    const uint8_t* dc = rgb;
+    std::vector<uint64_t> off(offsets, offsets + F + 1);
+    if (!(flags & VXG_INPUT_DEVICE) && P > 0) {
+      float* sx = h0->in_xyz.ensure(3 * P);
+      CU(cudaMemcpyAsync(sx, xyz + 3 * offsets[0], 3 * P * sizeof(float), cudaMemcpyHostToDevice, h0->st));
+      uint8_t* sc = nullptr;
+      if (rgb) {
+        sc = h0->in_rgb.ensure(3 * P);
+        CU(cudaMemcpyAsync(sc, rgb + 3 * offsets[0], 3 * P, cudaMemcpyHostToDevice, h0->st));
+      }
+      dx = sx;
+      dc = sc;
+      for (auto& o : off) o -= offsets[0];
+    }
+    const auto parts = plan_subbatches(off.data(), F, false);
+    const int W = static_cast<int>(g->shards.size());
+    std::vector<std::vector<vxg_stats>> st(W);
+    for (const auto& part : parts) {
+      const uint64_t f0 = part.first, f1 = part.second, nF = f1 - f0;
+      std::vector<uint32_t> R(W);
+      std::vector<TermView> tv(W);
+      for (int r = 0; r < W; ++r) g->shards[r]->begin_batch(dx, dc, off.data() + f0, poses + 12 * f0, nF, &R[r], &tv[r]);
+      for (int r = 0; r < W; ++r) g->shards[r]->shard_front(R[r], static_cast<uint32_t>(nF), tv[r]);
+      group_exchange(g);
+      for (int r = 0; r < W; ++r) g->shards[r]->shard_back(g->shards[r]->recv_buf.p, g->shards[r]->recv_total,
+                                                           static_cast<uint32_t>(nF));
+      for (int r = 0; r < W; ++r) {
+        st[r].assign(nF, vxg_stats{0, 0, 0});
+        g->shards[r]->end_batch(nF, st[r].data());
+      }
+      if (out) {
+        for (uint64_t f = 0; f < nF; ++f) {
+          vxg_stats s = st[0][f];  // raycasts / skipped: identical on every shard
+          s.updates = 0;
+          for (int r = 0; r < W; ++r) s.updates += st[r][f].updates;
+          out[f0 + f] = s;
+        }
+      }
+    }
+  });
+}
+
+// VXBLX of the union of the shards (ownership is disjoint).
+int vxg_group_serialize_vxblx(vxg_group* g, uint8_t* buf, uint64_t cap, uint64_t* need) {
+  return guarded([&] {
+    vxg_handle* h0 = g->shards[0];
+    const uint64_t nv = static_cast<uint64_t>(h0->nvox);
+    std::vector<std::pair<std::array<int32_t, 3>, std::pair<int, uint64_t>>> all;
+    std::vector<std::vector<vxg_voxel>> vox(g->shards.size());
+    for (size_t s = 0; s < g->shards.size(); ++s) {
+      uint64_t nb = 0;
+      if (vxg_block_count(g->shards[s], &nb) != VXG_OK) throw VxgError(VXG_ECUDA, g_err);
+      std::vector<int32_t> idx(3 * nb + 3);
+      vox[s].resize(nb * nv + 1);
+      uint64_t got = 0;
+      if (vxg_export_blocks(g->shards[s], idx.data(), vox[s].data(), nb, &got) != VXG_OK) throw VxgError(VXG_ECUDA, g_err);
+      for (uint64_t k = 0; k < got; ++k) all.push_back({{idx[3 * k], idx[3 * k + 1], idx[3 * k + 2]}, {static_cast<int>(s), k}});
+    }
+    std::sort(all.begin(), all.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    const uint64_t total = 31 + all.size() * (24 + nv * 12);
+    if (need) *need = total;
+    if (buf == nullptr || cap < total) return;
+    uint8_t* o = buf;
+    auto put = [&](const void* src, size_t len) {
+      std::memcpy(o, src, len);
+      o += len;
+    };
+    const char magic[6] = {'V', 'X', 'B', 'L', 'X', '\0'};
+    const uint32_t version = 1;
+    const double vs = static_cast<double>(h0->voxel_size);
+    const uint32_t vps = static_cast<uint32_t>(h0->vps);
+    const uint8_t kind = 0;
+    const uint64_t nb = all.size();
+    put(magic, 6);
+    put(&version, 4);
+    put(&vs, 8);
+    put(&vps, 4);
+    put(&kind, 1);
+    put(&nb, 8);
+    for (const auto& e : all) {
+      for (int a = 0; a < 3; ++a) {
+        const int64_t v = e.first[a];
+        put(&v, 8);
+      }
+      vxg_voxel* src = vox[e.second.first].data() + e.second.second * nv;
+      for (uint64_t i = 0; i < nv; ++i) src[i].pad = 0;
+      put(src, nv * sizeof(vxg_voxel));
+    }
+  });
 }
 
 // ---------------------------------------------------------------- free functions on device

@@ -241,6 +241,12 @@ class TsdfLayer:
         check(lib().vxg_batch_info(self._h, out, 1 if reset else 0))
         return {"records": int(out[0]), "n_vox": int(out[1]), "max_chain": int(out[2]), "blocks": int(out[3])}
 
+    def shard_init(self, rank: int, world: int, nccl_id: bytes = b"") -> None:
+        """Makes this layer shard `rank` of `world` (one process per GPU, NCCL
+        all-to-all of update records between shards)."""
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id.ljust(128, b"\0")[:128])
+        check(lib().vxg_shard_init(self._h, int(rank), int(world), buf))
+
     def set_stream(self, stream_ptr: Optional[int]) -> None:
         check(lib().vxg_set_stream(self._h, ctypes.c_void_p(stream_ptr) if stream_ptr else None))
 
@@ -320,6 +326,73 @@ class TsdfIntegrator:
         return out
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id for vxg_shard_init (rank 0 makes it, the caller broadcasts it)."""
+    buf = (ctypes.c_uint8 * 128)()
+    check(lib().vxg_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+class ShardGroup:
+    """`world` map shards on ONE device exchanging update records in-process
+    (the sharded kernels with device-to-device copies in place of NVLink) —
+    the single-GPU test vehicle of the multi-GPU path (vxg_group_*)."""
+
+    def __init__(self, config: TsdfConfig, voxel_size: float, voxels_per_side: int = 16, world: int = 2,
+                 device: int = 0, block_capacity: int = 0):
+        config.validate()
+        self._voxel_size = float(np.float32(voxel_size))
+        self._vps = int(voxels_per_side)
+        self._g = ctypes.c_void_p()
+        c = config.to_c()
+        check(lib().vxg_group_create(ctypes.byref(c), self._voxel_size, self._vps, int(device), int(world),
+                                     int(block_capacity), ctypes.byref(self._g)))
+        self.world = int(world)
+
+    def __del__(self):
+        g = getattr(self, "_g", None)
+        if g is not None and g.value:
+            try:
+                lib().vxg_group_destroy(g)
+            except Exception:
+                pass
+            self._g = None
+
+    def shard_block_counts(self):
+        out = []
+        for i in range(self.world):
+            h = ctypes.c_void_p()
+            check(lib().vxg_group_shard(self._g, i, ctypes.byref(h)))
+            n = ctypes.c_uint64()
+            check(lib().vxg_block_count(h, ctypes.byref(n)))
+            out.append(int(n.value))
+        return out
+
+    def integrate_batch(self, scans: Sequence[Scan]) -> np.ndarray:
+        F = len(scans)
+        xyz = np.ascontiguousarray(np.concatenate([s.points for s in scans]) if F else np.zeros((0, 3), np.float32))
+        has = all(s.colors is not None for s in scans)
+        if not has and any(s.colors is not None for s in scans):
+            raise ValueError("ShardGroup.integrate_batch needs colours on all scans or none")
+        rgb = np.ascontiguousarray(np.concatenate([s.colors for s in scans])) if (has and F) else None
+        offsets = np.zeros(F + 1, dtype=np.uint64)
+        offsets[1:] = np.cumsum([len(s.points) for s in scans])
+        poses = np.ascontiguousarray(np.stack([s.pose for s in scans]).astype(np.float32)) if F else np.zeros((0, 12), np.float32)
+        stats = (VxgStats * max(F, 1))()
+        check(lib().vxg_group_integrate_packed(self._g, _ptr(xyz), _ptr(rgb),
+                                               offsets.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                                               poses.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), F,
+                                               VXG_INPUT_HOST, stats))
+        return np.array([[s.updates, s.raycasts, s.skipped] for s in stats[:F]], dtype=np.uint64).reshape(F, 3)
+
+    def save_bytes(self) -> bytes:
+        need = ctypes.c_uint64()
+        check(lib().vxg_group_serialize_vxblx(self._g, None, 0, ctypes.byref(need)))
+        buf = np.zeros(need.value, dtype=np.uint8)
+        check(lib().vxg_group_serialize_vxblx(self._g, _ptr(buf), need.value, ctypes.byref(need)))
+        return buf.tobytes()
+
+
 # ---- the reference's public free functions, evaluated on the device (batched)
 def projective_distance(x, p, s, device: int = 0) -> np.ndarray:
     """tsdf_integrator.cpp:22-27 for n (x, p, s) triples."""
@@ -374,5 +447,6 @@ def raycast(start, end, voxel_size: float, device: int = 0):
 
 
 __all__ = ["WeightMode", "MergeMode", "TsdfConfig", "Scan", "TsdfLayer", "TsdfIntegrator", "ParseError",
+           "ShardGroup", "nccl_unique_id",
            "projective_distance", "measurement_weight", "update_tsdf_voxels", "raycast", "VOXEL_DTYPE",
            "K_TSDF_OBSERVED_WEIGHT", "pose_3x4"]
