@@ -37,6 +37,16 @@ struct alignas(16) RayInfo {  // one cast_and_update call (tsdf_integrator.cpp:1
   uint32_t valid;
 };
 
+// The fields the fold's weighing needs, one 32-byte sector per ray.
+struct alignas(32) FoldRay {
+  float p[3];
+  float weight;
+  uint32_t color;
+  uint32_t frame;
+  float base;
+  float pad;
+};
+
 struct alignas(16) Record {
   float d;
   float w;
@@ -337,7 +347,7 @@ __device__ __forceinline__ float mweight_base(int mode, float base, float d, flo
 // the ray's depth and hoisted 1/depth^2.
 __global__ void k_ray_count(uint32_t R, RayInfo* __restrict__ rays, const float* __restrict__ poses,
                             TsdfParams tp, unsigned long long* __restrict__ counts,
-                            unsigned long long* __restrict__ raycasts) {
+                            unsigned long long* __restrict__ raycasts, FoldRay* __restrict__ fray) {
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < R; j += gridDim.x * blockDim.x) {
     const RayInfo r = rays[j];
     uint64_t c = 0;
@@ -347,7 +357,18 @@ __global__ void k_ray_count(uint32_t R, RayInfo* __restrict__ rays, const float*
       const float ray[3] = {fsub(r.p[0], Pm[3]), fsub(r.p[1], Pm[7]), fsub(r.p[2], Pm[11])};
       const float depth = norm3(ray[0], ray[1], ray[2]);
       rays[j].depth = depth;
-      rays[j].base = tp.weight_mode == VXG_WEIGHT_CONSTANT ? 1.0f : fdiv(1.0f, fmul(depth, depth));
+      const float base = tp.weight_mode == VXG_WEIGHT_CONSTANT ? 1.0f : fdiv(1.0f, fmul(depth, depth));
+      rays[j].base = base;
+      FoldRay fr;
+      fr.p[0] = r.p[0];
+      fr.p[1] = r.p[1];
+      fr.p[2] = r.p[2];
+      fr.weight = r.weight;
+      fr.color = r.color;
+      fr.frame = r.frame;
+      fr.base = base;
+      fr.pad = depth;
+      fray[j] = fr;
       if (!(depth <= 0.0f)) {
         cast = 1u;
         const float s = fdiv(tp.truncation, depth);
@@ -746,7 +767,7 @@ __global__ void k_gather_send(uint64_t n, const uint32_t* __restrict__ perm, con
 
 // Owner side: global voxel key -> this shard's slot (allocating on first
 // update, like get_or_allocate_block) -> u32 record key; counts updates per frame.
-__global__ void k_localize(uint64_t n, const uint4* __restrict__ recv, MapView map, const RayInfo* __restrict__ rays,
+__global__ void k_localize(uint64_t n, const uint4* __restrict__ recv, MapView map, const FoldRay* __restrict__ rays,
                            uint32_t* __restrict__ rkeys, uint32_t* __restrict__ rvals,
                            unsigned long long* __restrict__ updates) {
   __shared__ unsigned long long bcache[kBlockCacheSize];
@@ -789,6 +810,17 @@ struct alignas(16) Upd {
 };
 
 __device__ __forceinline__ Upd weigh(const RayInfo& ry, const float* __restrict__ poses, float x0, float x1, float x2,
+                                     const TsdfParams& tp) {
+  const float* Pm = poses + 12 * ry.frame;
+  Upd u;
+  u.d = projective_distance(x0, x1, x2, ry.p[0], ry.p[1], ry.p[2], Pm[3], Pm[7], Pm[11]);
+  u.w = fmul(mweight_base(tp.weight_mode, ry.base, u.d, tp.truncation, tp.dropoff_epsilon), ry.weight);
+  u.c = ry.color;
+  u.pad = 0u;
+  return u;
+}
+
+__device__ __forceinline__ Upd weigh(const FoldRay& ry, const float* __restrict__ poses, float x0, float x1, float x2,
                                      const TsdfParams& tp) {
   const float* Pm = poses + 12 * ry.frame;
   Upd u;
@@ -888,15 +920,176 @@ __device__ __forceinline__ bool sat_prepare(const Upd& x, float cr, float cg, fl
   return ok;
 }
 
+// Warp-mode general step, one channel per lane (ch = lane & 3: 0 = distance,
+// 1..3 = colour r, g, b): the four quotients of update_tsdf_voxel are
+// independent given W and total = W + w, so each lane carries one chain
+// (W is replicated). Straight-line; `ok` as in step_fast (the caller re-runs
+// the chunk with step_exact when any lane cleared it).
+__device__ __forceinline__ void quad_step(float& s, float& W, int ch, float d, float w, uint32_t col, float truncation,
+                                          float max_weight, bool& ok) {
+  const bool live = w > 0.0f;
+  const bool colour = ch != 0;
+  const bool active = !colour || (col >> 31) != 0u;
+  const float n = colour ? __uint2float_rn((col >> (8 * (ch - 1))) & 0xffu)
+                         : (d < -truncation ? -truncation : (truncation < d ? truncation : d));
+  const float total = __fadd_rn(W, w);
+  const Recip rt = make_recip(total);
+  const float a = __fadd_rn(__fmul_rn(W, s), __fmul_rn(w, n));
+  const float q = fast_quot0(a, rt);
+  ok = ok & (!live | !active | ((w < 0x1p100f) & rt.ok & quot_ok(a) & (!colour | (q < 0x1p22f))));
+  const float sn = colour ? fminf(round_half_away_pos(q), 255.0f) : q;
+  s = (live & active) ? sn : s;
+  W = live ? (max_weight < total ? max_weight : total) : W;
+}
+
+// ---- warp-specialised long-run fold (phase 1)
+// Each long run is processed by a PAIR of warps: the producer gathers and
+// weighs 32 records per chunk (ids two chunks ahead, rays one chunk ahead)
+// into a kRingStages-deep shared-memory ring; the consumer only folds. mbarrier
+// full/empty per stage hand chunks over, so the consumer's serial chain never
+// waits on global memory or on the weighing arithmetic.
+constexpr int kRingStages = 4;
+
+struct alignas(16) StageRec {
+  float d;
+  float w;
+  uint32_t c;
+  uint32_t ok;  // sat-lane constants valid (w and T in the fast range)
+  float wc;     // RN(w * clamp(d))
+  float T;      // RN(max_weight + w)
+  float r1;     // refined reciprocal of T
+  float pad;
+};
+
+struct alignas(16) PreRec {  // one record as handed to the long-run consumer
+  float W;   // weight before this update (the producer's W scan)
+  float T;   // RN(W + w)
+  float r1;  // refined reciprocal of T
+  float wc;  // RN(w * clamp(d))
+  float wn0, wn1, wn2;  // RN(w * new colour channel)
+  uint32_t c;           // colour word (has_color << 31)
+  float w, d;           // raw (for the stationarity vote and the exact fallback)
+  uint32_t ok, pad;     // w in (0, 2^100) and T in the fast-division range
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "VXG_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra VXG_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ StageRec stage_rec(const RayInfo& ry, const float* __restrict__ poses, const RunCtx& c,
+                                              const TsdfParams& tp) {
+  const Upd u = weigh(ry, poses, c.x0, c.x1, c.x2, tp);
+  StageRec s;
+  s.d = u.d;
+  s.w = u.w;
+  s.c = u.c;
+  const float clamped = u.d < -tp.truncation ? -tp.truncation : (tp.truncation < u.d ? tp.truncation : u.d);
+  s.T = __fadd_rn(tp.max_weight, u.w);
+  const Recip rt = make_recip(s.T);
+  s.wc = __fmul_rn(u.w, clamped);
+  s.r1 = rt.r1;
+  s.ok = ((u.w > 0.0f) & (u.w < 0x1p100f) & rt.ok) ? 1u : 0u;
+  s.pad = 0.0f;
+  return s;
+}
+
+// (d, w, colour) of every sorted record, computed once by a fully parallel
+// pass (coalesced reads of the sorted keys/ray ids, one ray gather, coalesced
+// 16-byte write), so the serial fold loops only stream their run's records.
+// Same arithmetic as emission (projective_distance, measurement_weight).
+__global__ void k_weigh_records(uint64_t T, const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ svals,
+                                const FoldRay* __restrict__ rays, const float* __restrict__ poses, MapView map,
+                                TsdfParams tp, uint4* __restrict__ recs) {
+  const int vps = map.vps;
+  constexpr int kU = 4;  // independent records in flight per thread
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i0 < T; i0 += kU * stride) {
+    uint32_t key[kU], val[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint64_t i = i0 + u * stride;
+      key[u] = i < T ? skeys[i] : kInvalidRecord;
+      val[u] = i < T ? svals[i] : 0u;
+    }
+    FoldRay ry[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (key[u] != kInvalidRecord) ry[u] = rays[val[u]];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint64_t i = i0 + u * stride;
+      if (i >= T) continue;
+      if (key[u] == kInvalidRecord) {
+        recs[i] = make_uint4(0u, 0u, 0u, 0u);
+        continue;
+      }
+      const uint32_t slot = key[u] / static_cast<uint32_t>(map.nvox);
+      const uint32_t lin = key[u] - slot * static_cast<uint32_t>(map.nvox);
+      const int l0 = static_cast<int>(lin % vps), l1 = static_cast<int>((lin / vps) % vps),
+                l2 = static_cast<int>(lin / (vps * vps));
+      const float x0 = vcenter(map.block_idx[3 * slot + 0] * vps + l0, tp.voxel_size);
+      const float x1 = vcenter(map.block_idx[3 * slot + 1] * vps + l1, tp.voxel_size);
+      const float x2 = vcenter(map.block_idx[3 * slot + 2] * vps + l2, tp.voxel_size);
+      const Upd w = weigh(ry[u], poses, x0, x1, x2, tp);
+      recs[i] = make_uint4(__float_as_uint(w.d), __float_as_uint(w.w), w.c, 0u);
+    }
+  }
+}
+
+__device__ __forceinline__ Upd rec_upd(const uint4 r) {
+  Upd u;
+  u.d = __uint_as_float(r.x);
+  u.w = __uint_as_float(r.y);
+  u.c = r.z;
+  u.pad = 0u;
+  return u;
+}
+
+__device__ __forceinline__ StageRec stage_from(const Upd& u, const TsdfParams& tp) {
+  StageRec s;
+  s.d = u.d;
+  s.w = u.w;
+  s.c = u.c;
+  const float clamped = u.d < -tp.truncation ? -tp.truncation : (tp.truncation < u.d ? tp.truncation : u.d);
+  s.T = __fadd_rn(tp.max_weight, u.w);
+  const Recip rt = make_recip(s.T);
+  s.wc = __fmul_rn(u.w, clamped);
+  s.r1 = rt.r1;
+  s.ok = ((u.w > 0.0f) & (u.w < 0x1p100f) & rt.ok) ? 1u : 0u;
+  s.pad = 0.0f;
+  return s;
+}
+
 __global__ void __launch_bounds__(256) k_fold_runs(
     const uint32_t* __restrict__ num_runs_p, const uint32_t* __restrict__ order,
     const uint32_t* __restrict__ sorted_len, const uint32_t* __restrict__ ukeys, const uint32_t* __restrict__ ustart,
-    const uint32_t* __restrict__ ulen, const uint32_t* __restrict__ svals, const RayInfo* __restrict__ rays,
-    const float* __restrict__ poses, MapView map, TsdfParams tp, uint8_t* __restrict__ touched,
-    uint32_t* __restrict__ work) {
-  __shared__ Upd sbuf[8][2][32];
-  __shared__ SatRec ssat[8][32];
+    const uint32_t* __restrict__ ulen, const uint4* __restrict__ recs, MapView map, TsdfParams tp,
+    uint8_t* __restrict__ touched, uint32_t* __restrict__ work, unsigned long long* __restrict__ dbg) {
+  __shared__ PreRec ring[4][kRingStages][32];
+  __shared__ unsigned long long ring_full[4][kRingStages];
+  __shared__ unsigned long long ring_empty[4][kRingStages];
+  __shared__ uint32_t pair_run[4];
   if (map.counters[1] != 0u) return;  // emission failed (slab/hash full): host grows and replays
+  if (threadIdx.x < 4 * kRingStages) {
+    mbar_init(&ring_full[threadIdx.x / kRingStages][threadIdx.x % kRingStages], 32);
+    mbar_init(&ring_empty[threadIdx.x / kRingStages][threadIdx.x % kRingStages], 32);
+  }
+  __syncthreads();
   const uint32_t nruns = *num_runs_p;
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
@@ -905,87 +1098,160 @@ __global__ void __launch_bounds__(256) k_fold_runs(
   n_long = __shfl_sync(0xffffffffu, n_long, 0);
   const float Wmax = tp.max_weight;
 
-  // ---- phase 1: long runs, one warp per run
-  while (true) {
-    uint32_t r = 0;
-    if (lane == 0) r = atomicAdd(&work[0], 1u);
-    r = __shfl_sync(0xffffffffu, r, 0);
-    if (r >= n_long) break;
-    const RunCtx c = run_ctx(map, tp, ukeys, ustart, ulen, order[r]);
-    if (c.key == kInvalidRecord) continue;
-    vxg_voxel* vp = map.slab + c.key;
-    VoxState st = load_vox(vp);
-    const uint32_t nchunks = (c.len + 31) >> 5;
-    Upd x0{0.0f, 0.0f, 0u, 0u};
-    if (lane < c.len) x0 = weigh(rays[svals[c.start + lane]], poses, c.x0, c.x1, c.x2, tp);
-    sbuf[wid][0][lane] = x0;
-    uint32_t id_next = 0;
-    if (32 + lane < c.len) id_next = svals[c.start + 32 + lane];
-    bool sat_ok;
-    {
-      SatRec sr;
-      const bool ok = sat_prepare(x0, st.cr, st.cg, st.cb, tp, &sr) || lane >= c.len;
-      ssat[wid][lane] = sr;
-      sat_ok = __all_sync(0xffffffffu, ok) && st.W == Wmax;
-    }
-    __syncwarp();
-    for (uint32_t k = 0; k < nchunks; ++k) {
-      const uint32_t j1 = (k + 1) * 32 + lane, j2 = (k + 2) * 32 + lane;
-      RayInfo ry1;
-      const bool has1 = j1 < c.len;
-      if (has1) ry1 = rays[id_next];
-      uint32_t id2 = 0;
-      if (j2 < c.len) id2 = svals[c.start + j2];
-      const uint32_t cnt = min(32u, c.len - k * 32);
-      const Upd* ub = sbuf[wid][k & 1];
-      bool done = false;
-      if (sat_ok) {
-        // D-only chain; verify the numerators' fast range afterwards
-        float D = st.D;
-        bool all = true;
-        if (cnt == 32) {
+  // ---- phase 1: long runs, one producer/consumer warp pair per run
+  {
+    // consumers are warps 4..7 (highest ids: the warp arbiter favours them);
+    // pair p = consumer 4+p (sub-partition p) + producer (p+1)&3 (another one)
+    const bool producer = wid < 4;
+    const int pair = producer ? ((wid + 3) & 3) : (wid - 4);
+    uint32_t kk = 0;  // chunk counter of this pair across its runs (ring position / phase)
+    while (true) {
+      if (!producer && lane == 0) pair_run[pair] = atomicAdd(&work[0], 1u);
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
+      const uint32_t r = pair_run[pair];
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");  // pair_run is rewritten next run
+      if (r >= n_long) break;
+      const RunCtx c = run_ctx(map, tp, ukeys, ustart, ulen, order[r]);
+      if (c.key == kInvalidRecord) continue;
+      const uint32_t nchunks = (c.len + 31) >> 5;
+      vxg_voxel* vp = map.slab + c.key;
+      if (producer) {
+        // The weight chain W_{i+1} = min(W_i + w_i, Wmax) does not depend on
+        // the distance or the colours: run it here and hand each record its
+        // W_i, T_i = RN(W_i + w_i), reciprocal, RN(w clamp(d)), RN(w n_c).
+        float W = vp->weight;
+        uint4 r_k = lane < c.len ? recs[c.start + lane] : make_uint4(0u, 0u, 0u, 0u);
+        for (uint32_t k = 0; k < nchunks; ++k, ++kk) {
+          const uint32_t j = k * 32 + lane;
+          const uint4 r_k1 = j + 32 < c.len ? recs[c.start + j + 32] : make_uint4(0u, 0u, 0u, 0u);
+          const uint32_t cnt = min(32u, c.len - k * 32);
+          const float w = __uint_as_float(r_k.y);
+          float Wmine = W;
+          for (uint32_t u = 0; u < cnt; ++u) {  // sequential W scan (replicated on all lanes)
+            const float wu = __shfl_sync(0xffffffffu, w, u);
+            if (static_cast<uint32_t>(lane) == u) Wmine = W;
+            if (wu > 0.0f) {
+              const float t = __fadd_rn(W, wu);
+              W = Wmax < t ? Wmax : t;
+            }
+          }
+          PreRec pr;
+          const float d = __uint_as_float(r_k.x);
+          const float clamped = d < -tp.truncation ? -tp.truncation : (tp.truncation < d ? tp.truncation : d);
+          pr.W = Wmine;
+          pr.T = __fadd_rn(Wmine, w);
+          const Recip rt = make_recip(pr.T);
+          pr.r1 = rt.r1;
+          pr.wc = __fmul_rn(w, clamped);
+          pr.wn0 = __fmul_rn(w, __uint2float_rn(r_k.z & 0xffu));
+          pr.wn1 = __fmul_rn(w, __uint2float_rn((r_k.z >> 8) & 0xffu));
+          pr.wn2 = __fmul_rn(w, __uint2float_rn((r_k.z >> 16) & 0xffu));
+          pr.c = r_k.z;
+          pr.w = w;
+          pr.d = d;
+          pr.ok = ((w > 0.0f) & (w < 0x1p100f) & rt.ok) ? 1u : 0u;
+          pr.pad = 0u;
+          const int s = static_cast<int>(kk % kRingStages);
+          if (kk >= kRingStages) mbar_wait(&ring_empty[pair][s], ((kk / kRingStages) - 1) & 1u);
+          ring[pair][s][lane] = pr;
+          mbar_arrive(&ring_full[pair][s]);
+          r_k = r_k1;
+        }
+      } else {
+        VoxState st = load_vox(vp);
+        unsigned long long t_start = 0, n_sat = 0;
+        if (dbg != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+        for (uint32_t k = 0; k < nchunks; ++k, ++kk) {
+          const int s = static_cast<int>(kk % kRingStages);
+          mbar_wait(&ring_full[pair][s], (kk / kRingStages) & 1u);
+          const PreRec* rb = ring[pair][s];
+          const uint32_t cnt = min(32u, c.len - k * 32);
+          const float Wlast_T = rb[cnt - 1].T, Wlast_w = rb[cnt - 1].w, Wlast_W = rb[cnt - 1].W;
+          const float W_end = Wlast_w > 0.0f ? (Wmax < Wlast_T ? Wmax : Wlast_T) : Wlast_W;
+          // colours provably unchanged over the whole chunk? (each lane votes for its record)
+          bool vote = true;
+          if (static_cast<uint32_t>(lane) < cnt) {
+            const PreRec x = rb[lane];
+            vote = x.ok != 0u;
+            if (x.c >> 31) {
+              const float thr = __fmul_rn(0.499f, x.T);
+              vote = vote & colour_stationary(thr, x.w, st.cr, __uint2float_rn(x.c & 0xffu)) &
+                     colour_stationary(thr, x.w, st.cg, __uint2float_rn((x.c >> 8) & 0xffu)) &
+                     colour_stationary(thr, x.w, st.cb, __uint2float_rn((x.c >> 16) & 0xffu));
+            }
+          }
+          const bool stationary = __all_sync(0xffffffffu, vote);
+          bool done = false;
+          if (stationary) {  // distance chain only: FMUL, FADD, 3-FMA quotient per step
+            float D = st.D;
+            bool all = true;
+            if (cnt == 32) {
 #pragma unroll 16
-          for (int u = 0; u < 32; ++u) {
-            const SatRec sr = ssat[wid][u];
-            const float a = __fadd_rn(__fmul_rn(Wmax, D), sr.wc);
-            all = all & fast_range(a);
-            const float q0 = __fmul_rn(a, sr.r1);
-            D = __fmaf_rn(sr.r1, __fmaf_rn(-sr.T, q0, a), q0);
+              for (int u = 0; u < 32; ++u) {
+                const float a = __fadd_rn(__fmul_rn(rb[u].W, D), rb[u].wc);
+                all = all & quot_ok(a);
+                D = fast_quot0(a, Recip{rb[u].T, rb[u].r1, true});
+              }
+            } else {
+              for (uint32_t u = 0; u < cnt; ++u) {
+                const float a = __fadd_rn(__fmul_rn(rb[u].W, D), rb[u].wc);
+                all = all & quot_ok(a);
+                D = fast_quot0(a, Recip{rb[u].T, rb[u].r1, true});
+              }
+            }
+            if (all) {
+              st.D = D;
+              st.W = W_end;
+              done = true;
+              n_sat += cnt;
+            }
+          } else {  // one chain per lane: ch = lane & 3 (distance, r, g, b), W precomputed
+            const int ch = lane & 3;
+            float qs = ch == 0 ? st.D : (ch == 1 ? st.cr : (ch == 2 ? st.cg : st.cb));
+            bool ok = true;
+            bool all_col = true;
+            for (uint32_t u = 0; u < cnt; ++u) {
+              const PreRec& x = rb[u];
+              const bool has_col = (x.c >> 31) != 0u;
+              const float add = ch == 0 ? x.wc : (ch == 1 ? x.wn0 : (ch == 2 ? x.wn1 : x.wn2));
+              const float a = __fadd_rn(__fmul_rn(x.W, qs), add);
+              const float q = fast_quot0(a, Recip{x.T, x.r1, true});
+              const bool colour = ch != 0;
+              ok = ok & (x.ok != 0u) & (!(colour & !has_col) ? (quot_ok(a) & (!colour | (q < 0x1p22f))) : true);
+              const float sn = colour ? fminf(round_half_away_pos(q), 255.0f) : q;
+              qs = (!colour | has_col) ? sn : qs;
+              all_col = all_col & has_col;
+            }
+            (void)all_col;
+            if (__all_sync(0xffffffffu, ok)) {
+              st.D = __shfl_sync(0xffffffffu, qs, 0);
+              st.cr = __shfl_sync(0xffffffffu, qs, 1);
+              st.cg = __shfl_sync(0xffffffffu, qs, 2);
+              st.cb = __shfl_sync(0xffffffffu, qs, 3);
+              st.W = W_end;
+              done = true;
+            }
           }
-        } else {
-          for (uint32_t u = 0; u < cnt; ++u) {
-            const SatRec sr = ssat[wid][u];
-            const float a = __fadd_rn(__fmul_rn(Wmax, D), sr.wc);
-            all = all & fast_range(a);
-            const float q0 = __fmul_rn(a, sr.r1);
-            D = __fmaf_rn(sr.r1, __fmaf_rn(-sr.T, q0, a), q0);
+          if (!done) {  // rare: exact re-run of the chunk from its start state
+            for (uint32_t u = 0; u < cnt; ++u)
+              step_exact(st.D, st.W, st.cr, st.cg, st.cb, rb[u].d, rb[u].w, rb[u].c, tp.truncation, Wmax);
           }
+          __syncwarp();
+          mbar_arrive(&ring_empty[pair][s]);
         }
-        if (all) {
-          st.D = D;
-          done = true;
+        if (lane == 0) {
+          store_vox(vp, st);
+          if (touched != nullptr) touched[c.key / static_cast<uint32_t>(map.nvox)] = 1u;
+          if (dbg != nullptr) {
+            unsigned long long t_end;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+            dbg[4 * r + 0] = t_start;
+            dbg[4 * r + 1] = t_end;
+            dbg[4 * r + 2] = c.len;
+            dbg[4 * r + 3] = n_sat;
+          }
         }
       }
-      if (!done) {  // general path (also the replay of a chunk whose fast lane bailed out)
-        for (uint32_t u = 0; u < cnt; ++u) {
-          const Upd x = ub[u];
-          update_voxel_fast(st.D, st.W, st.cr, st.cg, st.cb, x.d, x.w, x.c, tp.truncation, tp.max_weight);
-        }
-      }
-      __syncwarp();
-      Upd x1{0.0f, 0.0f, 0u, 0u};
-      if (has1) x1 = weigh(ry1, poses, c.x0, c.x1, c.x2, tp);
-      sbuf[wid][(k + 1) & 1][lane] = x1;
-      SatRec sr;
-      const bool ok = sat_prepare(x1, st.cr, st.cg, st.cb, tp, &sr) || !has1;
-      ssat[wid][lane] = sr;
-      sat_ok = __all_sync(0xffffffffu, ok) && st.W == Wmax;
-      id_next = id2;
-      __syncwarp();
-    }
-    if (lane == 0) {
-      store_vox(vp, st);
-      if (touched != nullptr) touched[c.key / static_cast<uint32_t>(map.nvox)] = 1u;
     }
   }
 
@@ -1005,16 +1271,31 @@ __global__ void __launch_bounds__(256) k_fold_runs(
       Upd xs[kFoldChunk];
 #pragma unroll
       for (int u = 0; u < kFoldChunk; ++u) {
-        if (j + u < c.len) xs[u] = weigh(rays[svals[c.start + j + u]], poses, c.x0, c.x1, c.x2, tp);
+        if (j + u < c.len) xs[u] = rec_upd(recs[c.start + j + u]);
       }
+      const VoxState s0 = st;
+      bool ok = true;
 #pragma unroll
       for (int u = 0; u < kFoldChunk; ++u) {
         if (j + u < c.len)
-          update_voxel_fast(st.D, st.W, st.cr, st.cg, st.cb, xs[u].d, xs[u].w, xs[u].c, tp.truncation, tp.max_weight);
+          step_fast(st.D, st.W, st.cr, st.cg, st.cb, xs[u].d, xs[u].w, xs[u].c, tp.truncation, tp.max_weight, ok);
+      }
+      if (!ok) {  // rare: exact re-run of the chunk from its start state
+        st = s0;
+        for (int u = 0; u < kFoldChunk; ++u) {
+          if (j + u < c.len)
+            step_exact(st.D, st.W, st.cr, st.cg, st.cb, xs[u].d, xs[u].w, xs[u].c, tp.truncation, tp.max_weight);
+        }
       }
     }
     store_vox(vp, st);
     if (touched != nullptr) touched[c.key / static_cast<uint32_t>(map.nvox)] = 1u;
+  }
+  if (dbg != nullptr && lane == 0) {  // when this warp ran out of work
+    unsigned long long t_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    atomicMax(&dbg[4 * nruns], t_end);
+    atomicMin(&dbg[4 * nruns + 1], t_end);
   }
 }
 

@@ -161,6 +161,11 @@ struct vxg_handle {
   DBuf<uint64_t> tbl_off, bcs;
   DBuf<uint32_t> rkeys, rkeys2, rvals, rvals2;
   DBuf<uint32_t> run_keys, run_len, run_start, run_len2, run_order, run_iota, work;
+  DBuf<uint4> fold_recs;
+  DBuf<FoldRay> fold_rays;
+  bool debug_fold = false;  // globaltimer trace of the fold (vxg_debug_fold)
+  DBuf<unsigned long long> fold_dbg;
+  uint32_t fold_dbg_n = 0;
   uint64_t info_records = 0, info_runs = 0, info_max_run = 0;  // since the last vxg_batch_info reset
 
   // ---- profiling
@@ -612,7 +617,8 @@ uint64_t vxg_handle::count_rays(uint32_t R, uint32_t F) {
   begin(ST_RAYS);
   rcount.ensure(R);
   roff.ensure(R);
-  k_ray_count<<<grid_for(R), 256, 0, st>>>(R, rays.p, d_poses.p, tp, rcount.p, d_stats.p + F);
+  fold_rays.ensure(R);
+  k_ray_count<<<grid_for(R), 256, 0, st>>>(R, rays.p, d_poses.p, tp, rcount.p, d_stats.p + F, fold_rays.p);
   ++launches;
   CU(cudaGetLastError());
   cub([&](void* t, size_t& b) {
@@ -674,8 +680,20 @@ void vxg_handle::sort_fold(uint64_t T) {
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fold_runs, 256, 0));
   const unsigned fold_grid = static_cast<unsigned>(std::max<uint64_t>(
       1, std::min<uint64_t>(static_cast<uint64_t>(dev_sms) * std::max(per_sm, 1), (nruns + 255) / 256)));
+  unsigned long long* dbg = nullptr;
+  if (debug_fold) {
+    fold_dbg.ensure(4 * nruns + 2);
+    CU(cudaMemsetAsync(fold_dbg.p, 0, (4 * nruns + 2) * sizeof(unsigned long long), st));
+    CU(cudaMemsetAsync(fold_dbg.p + 4 * nruns + 1, 0xFF, sizeof(unsigned long long), st));
+    dbg = fold_dbg.p;
+    fold_dbg_n = nruns;
+  }
+  fold_recs.ensure(T);
+  k_weigh_records<<<grid_for(T), 256, 0, st>>>(T, rkeys2.p, rvals2.p, fold_rays.p, d_poses.p, view(), tp,
+                                                fold_recs.p);
   k_fold_runs<<<fold_grid, 256, 0, st>>>(num_runs.p, run_order.p, run_len2.p, run_keys.p, run_start.p, run_len.p,
-                                          rvals2.p, rays.p, d_poses.p, view(), tp, tch, work.p);
+                                          fold_recs.p, view(), tp, tch, work.p, dbg);
+  ++launches;
   ++launches;
   CU(cudaGetLastError());
   end(T, 1);
@@ -944,7 +962,7 @@ void vxg_handle::shard_back(const uint4* recv, uint64_t n, uint32_t F) {
     for (int attempt = 0;; ++attempt) {
       CU(cudaMemsetAsync(counters.p + 1, 0, sizeof(uint32_t), st));
       CU(cudaMemsetAsync(d_upd.p, 0, F * sizeof(unsigned long long), st));
-      k_localize<<<grid_for(n), 256, 0, st>>>(n, recv, view(), rays.p, rkeys.p, rvals.p, d_upd.p);
+      k_localize<<<grid_for(n), 256, 0, st>>>(n, recv, view(), fold_rays.p, rkeys.p, rvals.p, d_upd.p);
       ++launches;
       CU(cudaGetLastError());
       sort_fold(n);
@@ -1695,6 +1713,20 @@ extern "C" int vxg_selftest_fold(int device, uint64_t n, uint64_t n_seq, uint32_
     CU(cudaMemcpy(h, mm.p, sizeof(h), cudaMemcpyDeviceToHost));
     out[0] = h[0];
     out[1] = h[1];
+  });
+}
+
+// Debug: enable the fold trace / read it: out = 4*nruns+2 u64 (per long run:
+// start ns, end ns, length, records folded on the saturated lane; then the
+// latest and earliest warp exit time). Returns nruns in *n.
+extern "C" int vxg_debug_fold(vxg_handle* h, int enable, unsigned long long* out, uint64_t cap, uint64_t* n) {
+  return guarded([&] {
+    h->debug_fold = enable != 0;
+    if (n) *n = h->fold_dbg_n;
+    if (out && h->fold_dbg.p) {
+      const uint64_t m = std::min<uint64_t>(cap, 4ull * h->fold_dbg_n + 2);
+      CU(cudaMemcpy(out, h->fold_dbg.p, m * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    }
   });
 }
 

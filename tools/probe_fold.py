@@ -1,0 +1,34 @@
+"""Dev probe: globaltimer trace of the fold kernel on the cfg1 100-frame batch."""
+import ctypes, sys
+import numpy as np
+sys.path.insert(0, '.')
+import torch
+from paper_1611_03631_b200 import TsdfIntegrator, TsdfLayer
+from paper_1611_03631_b200 import workload as W
+from paper_1611_03631_b200._capi import lib
+L = lib()
+L.vxg_debug_fold.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
+wc = W.CONFIGS[1]
+xyz, rgb, off, poses = W.pack(W.frames(1, count=100))
+layer = TsdfLayer(wc.voxel_size, 16, block_capacity=1024)
+integ = TsdfIntegrator(W.tsdf_config(wc), layer)
+dx = torch.from_numpy(xyz).cuda(); dc = torch.from_numpy(rgb).cuda()
+integ.integrate_packed(dx.data_ptr(), dc.data_ptr(), off, poses, True)
+layer.reset()
+L.vxg_debug_fold(layer.handle, 1, None, 0, None)
+layer.profile(True); layer.stage_times(True)
+integ.integrate_packed(dx.data_ptr(), dc.data_ptr(), off, poses, True)
+print('apply ms', layer.stage_times(True)['apply'][0])
+n = ctypes.c_uint64()
+L.vxg_debug_fold(layer.handle, 0, None, 0, ctypes.byref(n))
+buf = np.zeros(4 * n.value + 2, np.uint64)
+L.vxg_debug_fold(layer.handle, 0, buf.ctypes.data, len(buf), ctypes.byref(n))
+d = buf[:4 * n.value].reshape(-1, 4).astype(np.int64)
+long_ = d[d[:, 1] > 0]
+t0 = long_[:, 0].min()
+print('long runs', len(long_), 'first start', 0, 'last long end (us)', (long_[:, 1].max() - t0) / 1e3)
+print('warp exits: earliest (us)', (int(buf[-1]) - t0) / 1e3, 'latest (us)', (int(buf[-2]) - t0) / 1e3)
+dur = (long_[:, 1] - long_[:, 0])
+for i in np.argsort(-long_[:, 2])[:8]:
+    print(f'len {long_[i,2]:6d} sat {long_[i,3]:6d} start {(long_[i,0]-t0)/1e3:8.1f}us dur {dur[i]/1e3:8.1f}us  ns/step {dur[i]/long_[i,2]:.1f}')
+print('median ns/step over long runs', np.median(dur / long_[:, 2]), 'sat fraction', long_[:, 3].sum() / long_[:, 2].sum())
