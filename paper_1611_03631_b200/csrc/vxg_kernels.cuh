@@ -809,26 +809,48 @@ struct alignas(16) Upd {
   uint32_t pad;
 };
 
-__device__ __forceinline__ Upd weigh(const RayInfo& ry, const float* __restrict__ poses, float x0, float x1, float x2,
+// org: sensor origins, 3 floats per frame (the fold kernels stage them in
+// shared memory so the only global latency per record is the ray gather).
+// mweight_base with the dropoff division by the constant (truncation - eps)
+// through its precomputed reciprocal (exact inside the fast range, else the
+// IEEE division itself).
+__device__ __forceinline__ float mweight_base_r(int mode, float base, float d, float truncation, float eps,
+                                                const Recip& den) {
+  if (mode == VXG_WEIGHT_CONSTANT) return 1.0f;
+  if (mode == VXG_WEIGHT_INVERSE_Z2) return base;
+  if (mode != VXG_WEIGHT_INVERSE_Z2_DROPOFF) return 0.0f;
+  if (d > -eps) return base;
+  if (d < -truncation) return 0.0f;
+  const float n = fmul(base, fadd(d, truncation));
+  if (den.ok && fast_range(n)) return fast_quot(n, den);
+  return fdiv(n, den.b);
+}
+
+__device__ __forceinline__ Upd weigh(const FoldRay& ry, const float* org, float x0, float x1, float x2,
                                      const TsdfParams& tp) {
-  const float* Pm = poses + 12 * ry.frame;
+  const float* O = org + 3 * ry.frame;
   Upd u;
-  u.d = projective_distance(x0, x1, x2, ry.p[0], ry.p[1], ry.p[2], Pm[3], Pm[7], Pm[11]);
-  u.w = fmul(mweight_base(tp.weight_mode, ry.base, u.d, tp.truncation, tp.dropoff_epsilon), ry.weight);
+  u.d = projective_distance(x0, x1, x2, ry.p[0], ry.p[1], ry.p[2], O[0], O[1], O[2]);
+  const Recip den = make_recip(fsub(tp.truncation, tp.dropoff_epsilon));  // loop-invariant
+  u.w = fmul(mweight_base_r(tp.weight_mode, ry.base, u.d, tp.truncation, tp.dropoff_epsilon, den), ry.weight);
   u.c = ry.color;
   u.pad = 0u;
   return u;
 }
 
-__device__ __forceinline__ Upd weigh(const FoldRay& ry, const float* __restrict__ poses, float x0, float x1, float x2,
-                                     const TsdfParams& tp) {
-  const float* Pm = poses + 12 * ry.frame;
-  Upd u;
-  u.d = projective_distance(x0, x1, x2, ry.p[0], ry.p[1], ry.p[2], Pm[3], Pm[7], Pm[11]);
-  u.w = fmul(mweight_base(tp.weight_mode, ry.base, u.d, tp.truncation, tp.dropoff_epsilon), ry.weight);
-  u.c = ry.color;
-  u.pad = 0u;
-  return u;
+constexpr uint32_t kOrgCache = 1024;  // frames whose origins fit the fold kernels' smem table
+
+__global__ void k_origins(uint32_t F, const float* __restrict__ poses, float* __restrict__ org) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < 3 * F; i += gridDim.x * blockDim.x)
+    org[i] = poses[12 * (i / 3) + 3 + 4 * (i % 3)];
+}
+
+// Stages the origin table in shared memory when it fits; returns the table to use.
+__device__ __forceinline__ const float* stage_origins(float* s_org, const float* __restrict__ g_org, uint32_t F) {
+  if (F > kOrgCache) return g_org;
+  for (uint32_t i = threadIdx.x; i < 3 * F; i += blockDim.x) s_org[i] = g_org[i];
+  __syncthreads();
+  return s_org;
 }
 
 struct RunCtx {
@@ -886,62 +908,6 @@ __device__ __forceinline__ uint32_t count_long_runs(const uint32_t* __restrict__
   return lo;
 }
 
-// Saturated, colour-stationary lane: when W == max_weight at the start of a
-// 32-record chunk, W stays max_weight (total = Wmax + w > Wmax) and, if every
-// record of the chunk leaves every colour channel unchanged
-// (colour_stationary), a step reduces to
-//   D <- RN(RN(RN(Wmax*D) + wc) / T),  wc = RN(w*clamp(d)), T = RN(Wmax + w)
-// whose wc, T and reciprocal are per-record constants the lanes precompute in
-// parallel. The serial chain is then FMUL, FADD and the 3-FMA quotient.
-struct alignas(16) SatRec {
-  float wc;
-  float T;
-  float r1;
-  float pad;
-};
-
-__device__ __forceinline__ bool sat_prepare(const Upd& x, float cr, float cg, float cb, const TsdfParams& tp,
-                                            SatRec* out) {
-  const float w = x.w;
-  const float clamped = x.d < -tp.truncation ? -tp.truncation : (tp.truncation < x.d ? tp.truncation : x.d);
-  const float T = __fadd_rn(tp.max_weight, w);
-  const Recip rt = make_recip(T);
-  out->wc = __fmul_rn(w, clamped);
-  out->T = T;
-  out->r1 = rt.r1;
-  out->pad = 0.0f;
-  bool ok = (w > 0.0f) & (w < 0x1p100f) & rt.ok;
-  if (x.c >> 31) {
-    const float thr = __fmul_rn(0.499f, T);
-    ok = ok & colour_stationary(thr, w, cr, __uint2float_rn(x.c & 0xffu)) &
-         colour_stationary(thr, w, cg, __uint2float_rn((x.c >> 8) & 0xffu)) &
-         colour_stationary(thr, w, cb, __uint2float_rn((x.c >> 16) & 0xffu));
-  }
-  return ok;
-}
-
-// Warp-mode general step, one channel per lane (ch = lane & 3: 0 = distance,
-// 1..3 = colour r, g, b): the four quotients of update_tsdf_voxel are
-// independent given W and total = W + w, so each lane carries one chain
-// (W is replicated). Straight-line; `ok` as in step_fast (the caller re-runs
-// the chunk with step_exact when any lane cleared it).
-__device__ __forceinline__ void quad_step(float& s, float& W, int ch, float d, float w, uint32_t col, float truncation,
-                                          float max_weight, bool& ok) {
-  const bool live = w > 0.0f;
-  const bool colour = ch != 0;
-  const bool active = !colour || (col >> 31) != 0u;
-  const float n = colour ? __uint2float_rn((col >> (8 * (ch - 1))) & 0xffu)
-                         : (d < -truncation ? -truncation : (truncation < d ? truncation : d));
-  const float total = __fadd_rn(W, w);
-  const Recip rt = make_recip(total);
-  const float a = __fadd_rn(__fmul_rn(W, s), __fmul_rn(w, n));
-  const float q = fast_quot0(a, rt);
-  ok = ok & (!live | !active | ((w < 0x1p100f) & rt.ok & quot_ok(a) & (!colour | (q < 0x1p22f))));
-  const float sn = colour ? fminf(round_half_away_pos(q), 255.0f) : q;
-  s = (live & active) ? sn : s;
-  W = live ? (max_weight < total ? max_weight : total) : W;
-}
-
 // ---- warp-specialised long-run fold (phase 1)
 // Each long run is processed by a PAIR of warps: the producer gathers and
 // weighs 32 records per chunk (ids two chunks ahead, rays one chunk ahead)
@@ -949,17 +915,6 @@ __device__ __forceinline__ void quad_step(float& s, float& W, int ch, float d, f
 // full/empty per stage hand chunks over, so the consumer's serial chain never
 // waits on global memory or on the weighing arithmetic.
 constexpr int kRingStages = 4;
-
-struct alignas(16) StageRec {
-  float d;
-  float w;
-  uint32_t c;
-  uint32_t ok;  // sat-lane constants valid (w and T in the fast range)
-  float wc;     // RN(w * clamp(d))
-  float T;      // RN(max_weight + w)
-  float r1;     // refined reciprocal of T
-  float pad;
-};
 
 struct alignas(16) PreRec {  // one record as handed to the long-run consumer
   float W;   // weight before this update (the producer's W scan)
@@ -991,96 +946,50 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t pari
       : "memory");
 }
 
-__device__ __forceinline__ StageRec stage_rec(const RayInfo& ry, const float* __restrict__ poses, const RunCtx& c,
-                                              const TsdfParams& tp) {
-  const Upd u = weigh(ry, poses, c.x0, c.x1, c.x2, tp);
-  StageRec s;
-  s.d = u.d;
-  s.w = u.w;
-  s.c = u.c;
-  const float clamped = u.d < -tp.truncation ? -tp.truncation : (tp.truncation < u.d ? tp.truncation : u.d);
-  s.T = __fadd_rn(tp.max_weight, u.w);
-  const Recip rt = make_recip(s.T);
-  s.wc = __fmul_rn(u.w, clamped);
-  s.r1 = rt.r1;
-  s.ok = ((u.w > 0.0f) & (u.w < 0x1p100f) & rt.ok) ? 1u : 0u;
-  s.pad = 0.0f;
-  return s;
-}
-
-// (d, w, colour) of every sorted record, computed once by a fully parallel
-// pass (coalesced reads of the sorted keys/ray ids, one ray gather, coalesced
-// 16-byte write), so the serial fold loops only stream their run's records.
-// Same arithmetic as emission (projective_distance, measurement_weight).
-__global__ void k_weigh_records(uint64_t T, const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ svals,
-                                const FoldRay* __restrict__ rays, const float* __restrict__ poses, MapView map,
-                                TsdfParams tp, uint4* __restrict__ recs) {
-  const int vps = map.vps;
-  constexpr int kU = 4;  // independent records in flight per thread
+// Run marks of the sorted records: voxel k's records are [dense_start[k],
+// dense_end[k]) (dense_end[k] stays 0 for a voxel without records).
+__global__ void k_run_marks(uint64_t T, const uint32_t* __restrict__ skeys, uint32_t* __restrict__ dense_start,
+                            uint32_t* __restrict__ dense_end) {
+  // 4 keys per thread (16-byte loads); neighbours across threads by shuffle
+  const uint64_t n4 = (T + 3) / 4;
+  const uint32_t lane = threadIdx.x & 31u;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i0 < T; i0 += kU * stride) {
-    uint32_t key[kU], val[kU];
+  for (uint64_t q0 = blockIdx.x * static_cast<uint64_t>(blockDim.x); q0 < n4; q0 += stride) {
+    const uint64_t q = q0 + threadIdx.x;  // warp-uniform trip count (full-warp shuffles)
+    uint32_t k[4];
+    if (4 * q + 3 < T) {
+      const uint4 v = reinterpret_cast<const uint4*>(skeys)[q];
+      k[0] = v.x; k[1] = v.y; k[2] = v.z; k[3] = v.w;
+    } else {
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const uint64_t i = i0 + u * stride;
-      key[u] = i < T ? skeys[i] : kInvalidRecord;
-      val[u] = i < T ? svals[i] : 0u;
+      for (int u = 0; u < 4; ++u) k[u] = 4 * q + u < T ? skeys[4 * q + u] : kInvalidRecord;
     }
-    FoldRay ry[kU];
+    uint32_t prev = __shfl_up_sync(0xffffffffu, k[3], 1);
+    uint32_t next = __shfl_down_sync(0xffffffffu, k[0], 1);
+    if (lane == 0u) prev = q > 0 && 4 * q - 1 < T ? skeys[4 * q - 1] : kInvalidRecord;
+    if (lane == 31u) next = 4 * q + 4 < T ? skeys[4 * q + 4] : kInvalidRecord;
 #pragma unroll
-    for (int u = 0; u < kU; ++u)
-      if (key[u] != kInvalidRecord) ry[u] = rays[val[u]];
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const uint64_t i = i0 + u * stride;
-      if (i >= T) continue;
-      if (key[u] == kInvalidRecord) {
-        recs[i] = make_uint4(0u, 0u, 0u, 0u);
-        continue;
-      }
-      const uint32_t slot = key[u] / static_cast<uint32_t>(map.nvox);
-      const uint32_t lin = key[u] - slot * static_cast<uint32_t>(map.nvox);
-      const int l0 = static_cast<int>(lin % vps), l1 = static_cast<int>((lin / vps) % vps),
-                l2 = static_cast<int>(lin / (vps * vps));
-      const float x0 = vcenter(map.block_idx[3 * slot + 0] * vps + l0, tp.voxel_size);
-      const float x1 = vcenter(map.block_idx[3 * slot + 1] * vps + l1, tp.voxel_size);
-      const float x2 = vcenter(map.block_idx[3 * slot + 2] * vps + l2, tp.voxel_size);
-      const Upd w = weigh(ry[u], poses, x0, x1, x2, tp);
-      recs[i] = make_uint4(__float_as_uint(w.d), __float_as_uint(w.w), w.c, 0u);
+    for (int u = 0; u < 4; ++u) {
+      const uint64_t i = 4 * q + u;
+      const uint32_t key = k[u];
+      if (i >= T || key == kInvalidRecord) continue;  // invalid keys sort after every run; never folded
+      const uint32_t before = u == 0 ? prev : k[u - 1];
+      const uint32_t after = u == 3 ? next : k[u + 1];
+      if (i == 0 || before != key) dense_start[key] = static_cast<uint32_t>(i);
+      if (i + 1 == T || after != key) dense_end[key] = static_cast<uint32_t>(i + 1);
     }
   }
-}
-
-__device__ __forceinline__ Upd rec_upd(const uint4 r) {
-  Upd u;
-  u.d = __uint_as_float(r.x);
-  u.w = __uint_as_float(r.y);
-  u.c = r.z;
-  u.pad = 0u;
-  return u;
-}
-
-__device__ __forceinline__ StageRec stage_from(const Upd& u, const TsdfParams& tp) {
-  StageRec s;
-  s.d = u.d;
-  s.w = u.w;
-  s.c = u.c;
-  const float clamped = u.d < -tp.truncation ? -tp.truncation : (tp.truncation < u.d ? tp.truncation : u.d);
-  s.T = __fadd_rn(tp.max_weight, u.w);
-  const Recip rt = make_recip(s.T);
-  s.wc = __fmul_rn(u.w, clamped);
-  s.r1 = rt.r1;
-  s.ok = ((u.w > 0.0f) & (u.w < 0x1p100f) & rt.ok) ? 1u : 0u;
-  s.pad = 0.0f;
-  return s;
 }
 
 __global__ void __launch_bounds__(256) k_fold_runs(
     const uint32_t* __restrict__ num_runs_p, const uint32_t* __restrict__ order,
     const uint32_t* __restrict__ sorted_len, const uint32_t* __restrict__ ukeys, const uint32_t* __restrict__ ustart,
-    const uint32_t* __restrict__ ulen, const uint4* __restrict__ recs, MapView map, TsdfParams tp,
-    uint8_t* __restrict__ touched, uint32_t* __restrict__ work, unsigned long long* __restrict__ dbg) {
+    const uint32_t* __restrict__ ulen, const uint32_t* __restrict__ svals, const FoldRay* __restrict__ rays,
+    const float* __restrict__ g_org, uint32_t F, MapView map, TsdfParams tp, uint8_t* __restrict__ touched,
+    uint32_t* __restrict__ work, unsigned long long* __restrict__ dbg) {
   __shared__ PreRec ring[4][kRingStages][32];
+  __shared__ float s_org[3 * kOrgCache];
+  const float* poses = stage_origins(s_org, g_org, F);
   __shared__ unsigned long long ring_full[4][kRingStages];
   __shared__ unsigned long long ring_empty[4][kRingStages];
   __shared__ uint32_t pair_run[4];
@@ -1091,6 +1000,7 @@ __global__ void __launch_bounds__(256) k_fold_runs(
   }
   __syncthreads();
   const uint32_t nruns = *num_runs_p;
+  const uint32_t n_all = nruns;
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
   uint32_t n_long = 0;
@@ -1119,55 +1029,125 @@ __global__ void __launch_bounds__(256) k_fold_runs(
         // The weight chain W_{i+1} = min(W_i + w_i, Wmax) does not depend on
         // the distance or the colours: run it here and hand each record its
         // W_i, T_i = RN(W_i + w_i), reciprocal, RN(w clamp(d)), RN(w n_c).
+        long long pwait = 0, pbusy0 = dbg != nullptr ? clock64() : 0, pt_weigh = 0, pt_scan = 0;
         float W = vp->weight;
-        uint4 r_k = lane < c.len ? recs[c.start + lane] : make_uint4(0u, 0u, 0u, 0u);
+        // pipeline (gather latency ~ a whole chunk of the consumer's chain):
+        // rays three chunks ahead, their ids five chunks ahead
+        const FoldRay zr{};
+        const uint32_t* ids = svals + c.start;
+        auto id_at = [&](uint32_t jj) { return jj < c.len ? ids[jj] : 0u; };
+        auto ray_at = [&](uint32_t jj, uint32_t v) { return jj < c.len ? rays[v] : zr; };
+        auto weigh_at = [&](uint32_t jj, const FoldRay& r) {
+          Upd x;
+          if (jj < c.len) {
+            x = weigh(r, poses, c.x0, c.x1, c.x2, tp);
+          } else {
+            x.d = 0.0f;
+            x.w = 0.0f;
+            x.c = 0u;
+            x.pad = 0u;
+          }
+          return x;
+        };
+        FoldRay ry1 = ray_at(32 + lane, id_at(32 + lane));
+        FoldRay ry2 = ray_at(64 + lane, id_at(64 + lane));
+        uint32_t v3 = id_at(96 + lane), v4 = id_at(128 + lane);
+        // records are weighed one chunk ahead of their hand-over
+        Upd u_next = weigh_at(lane, ray_at(lane, id_at(lane)));
         for (uint32_t k = 0; k < nchunks; ++k, ++kk) {
           const uint32_t j = k * 32 + lane;
-          const uint4 r_k1 = j + 32 < c.len ? recs[c.start + j + 32] : make_uint4(0u, 0u, 0u, 0u);
+          const FoldRay ry3 = ray_at(j + 96, v3);
+          v3 = v4;
+          v4 = id_at(j + 160);
           const uint32_t cnt = min(32u, c.len - k * 32);
-          const float w = __uint_as_float(r_k.y);
+          const Upd u = u_next;
+          const long long tp0 = dbg != nullptr ? clock64() : 0;
+          u_next = weigh_at(j + 32, ry1);
+          if (dbg != nullptr) {  // force the weighing to complete before the timestamp
+            asm volatile("" ::"f"(u_next.d), "f"(u_next.w));
+            pt_weigh += clock64() - tp0;
+          }
+          const long long tp1 = dbg != nullptr ? clock64() : 0;
+          // The weight chain W_{i+1} = min(RN(W_i + w_i), Wmax) (w_i > 0) does
+          // not depend on the distance or the colours: run it here and hand
+          // each record its W_i, T_i = RN(W_i + w_i) and reciprocal. The clamp
+          // commutes out of the chain: with S_0 = W_0, S_{i+1} = RN(S_i + w+_i)
+          // (w+ = w > 0 ? w : 0, and RN(S + 0) = S), W_i = min(S_i, Wmax) —
+          // before saturation S_i = W_i, and once S_k >= Wmax every later
+          // S >= Wmax while W stays Wmax. The serial part is one FADD per record.
+          const float w = u.w;
           float Wmine = W;
-          for (uint32_t u = 0; u < cnt; ++u) {  // sequential W scan (replicated on all lanes)
-            const float wu = __shfl_sync(0xffffffffu, w, u);
-            if (static_cast<uint32_t>(lane) == u) Wmine = W;
-            if (wu > 0.0f) {
-              const float t = __fadd_rn(W, wu);
-              W = Wmax < t ? Wmax : t;
+          if (W != Wmax) {  // W is warp-uniform (replicated scan)
+            const float wp = w > 0.0f ? w : 0.0f;
+            float S = W, Smine = W;
+            if (cnt == 32) {
+#pragma unroll
+              for (int q = 0; q < 32; ++q) {
+                const float wu = __shfl_sync(0xffffffffu, wp, q);
+                Smine = lane == q ? S : Smine;
+                S = __fadd_rn(S, wu);
+              }
+            } else {
+              for (uint32_t q = 0; q < cnt; ++q) {
+                const float wu = __shfl_sync(0xffffffffu, wp, q);
+                Smine = static_cast<uint32_t>(lane) == q ? S : Smine;
+                S = __fadd_rn(S, wu);
+              }
             }
+            Wmine = fminf(Smine, Wmax);
+            W = fminf(S, Wmax);
+          }
+          // else saturated: W_i = min(RN(Wmax + w), Wmax) = Wmax for w > 0 and
+          // unchanged for w <= 0, so every record sees Wmax and W stays Wmax
+          if (dbg != nullptr) {
+            asm volatile("" ::"f"(W), "f"(Wmine));
+            pt_scan += clock64() - tp1;
           }
           PreRec pr;
-          const float d = __uint_as_float(r_k.x);
-          const float clamped = d < -tp.truncation ? -tp.truncation : (tp.truncation < d ? tp.truncation : d);
+          const float clamped = u.d < -tp.truncation ? -tp.truncation : (tp.truncation < u.d ? tp.truncation : u.d);
           pr.W = Wmine;
           pr.T = __fadd_rn(Wmine, w);
           const Recip rt = make_recip(pr.T);
           pr.r1 = rt.r1;
           pr.wc = __fmul_rn(w, clamped);
-          pr.wn0 = __fmul_rn(w, __uint2float_rn(r_k.z & 0xffu));
-          pr.wn1 = __fmul_rn(w, __uint2float_rn((r_k.z >> 8) & 0xffu));
-          pr.wn2 = __fmul_rn(w, __uint2float_rn((r_k.z >> 16) & 0xffu));
-          pr.c = r_k.z;
+          pr.wn0 = __fmul_rn(w, __uint2float_rn(u.c & 0xffu));
+          pr.wn1 = __fmul_rn(w, __uint2float_rn((u.c >> 8) & 0xffu));
+          pr.wn2 = __fmul_rn(w, __uint2float_rn((u.c >> 16) & 0xffu));
+          pr.c = u.c;
           pr.w = w;
-          pr.d = d;
+          pr.d = u.d;
           pr.ok = ((w > 0.0f) & (w < 0x1p100f) & rt.ok) ? 1u : 0u;
           pr.pad = 0u;
           const int s = static_cast<int>(kk % kRingStages);
+          const long long tw0 = dbg != nullptr ? clock64() : 0;
           if (kk >= kRingStages) mbar_wait(&ring_empty[pair][s], ((kk / kRingStages) - 1) & 1u);
+          if (dbg != nullptr) pwait += clock64() - tw0;
           ring[pair][s][lane] = pr;
           mbar_arrive(&ring_full[pair][s]);
-          r_k = r_k1;
+          ry1 = ry2;
+          ry2 = ry3;
+        }
+        if (dbg != nullptr && lane == 0) {
+          atomicAdd(&dbg[4 * n_all + 4], static_cast<unsigned long long>(pwait));
+          atomicAdd(&dbg[4 * n_all + 5], static_cast<unsigned long long>(clock64() - pbusy0));
+          atomicAdd(&dbg[4 * n_all + 6], static_cast<unsigned long long>(pt_weigh));
+          atomicAdd(&dbg[4 * n_all + 7], static_cast<unsigned long long>(pt_scan));
         }
       } else {
         VoxState st = load_vox(vp);
         unsigned long long t_start = 0, n_sat = 0;
+        long long cwait = 0, cbusy0 = dbg != nullptr ? clock64() : 0, ct_vote = 0, ct_chain = 0;
         if (dbg != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
         for (uint32_t k = 0; k < nchunks; ++k, ++kk) {
           const int s = static_cast<int>(kk % kRingStages);
+          const long long tw0 = dbg != nullptr ? clock64() : 0;
           mbar_wait(&ring_full[pair][s], (kk / kRingStages) & 1u);
+          if (dbg != nullptr) cwait += clock64() - tw0;
+          const long long tc0 = dbg != nullptr ? clock64() : 0;
           const PreRec* rb = ring[pair][s];
           const uint32_t cnt = min(32u, c.len - k * 32);
           const float Wlast_T = rb[cnt - 1].T, Wlast_w = rb[cnt - 1].w, Wlast_W = rb[cnt - 1].W;
-          const float W_end = Wlast_w > 0.0f ? (Wmax < Wlast_T ? Wmax : Wlast_T) : Wlast_W;
+          const float W_end = Wlast_w > 0.0f ? fminf(Wlast_T, Wmax) : Wlast_W;
           // colours provably unchanged over the whole chunk? (each lane votes for its record)
           bool vote = true;
           if (static_cast<uint32_t>(lane) < cnt) {
@@ -1181,25 +1161,30 @@ __global__ void __launch_bounds__(256) k_fold_runs(
             }
           }
           const bool stationary = __all_sync(0xffffffffu, vote);
+          const long long tc1 = dbg != nullptr ? clock64() : 0;
           bool done = false;
           if (stationary) {  // distance chain only: FMUL, FADD, 3-FMA quotient per step
             float D = st.D;
-            bool all = true;
+            QuotRange qr;  // range checks accumulate off the chain (no predicate chain)
+            const float4* rq = reinterpret_cast<const float4*>(rb);
+            constexpr int kStride = sizeof(PreRec) / sizeof(float4);
             if (cnt == 32) {
-#pragma unroll 16
+#pragma unroll
               for (int u = 0; u < 32; ++u) {
-                const float a = __fadd_rn(__fmul_rn(rb[u].W, D), rb[u].wc);
-                all = all & quot_ok(a);
-                D = fast_quot0(a, Recip{rb[u].T, rb[u].r1, true});
+                const float4 x = rq[u * kStride];  // (W, T, r1, wc)
+                const float a = __fadd_rn(__fmul_rn(x.x, D), x.w);
+                qr_add(qr, a);
+                D = fast_quot0(a, Recip{x.y, x.z, true});
               }
             } else {
               for (uint32_t u = 0; u < cnt; ++u) {
-                const float a = __fadd_rn(__fmul_rn(rb[u].W, D), rb[u].wc);
-                all = all & quot_ok(a);
-                D = fast_quot0(a, Recip{rb[u].T, rb[u].r1, true});
+                const float4 x = rq[u * kStride];
+                const float a = __fadd_rn(__fmul_rn(x.x, D), x.w);
+                qr_add(qr, a);
+                D = fast_quot0(a, Recip{x.y, x.z, true});
               }
             }
-            if (all) {
+            if (qr_ok(qr)) {
               st.D = D;
               st.W = W_end;
               done = true;
@@ -1207,22 +1192,28 @@ __global__ void __launch_bounds__(256) k_fold_runs(
             }
           } else {  // one chain per lane: ch = lane & 3 (distance, r, g, b), W precomputed
             const int ch = lane & 3;
+            const bool colour = ch != 0;
             float qs = ch == 0 ? st.D : (ch == 1 ? st.cr : (ch == 2 ? st.cg : st.cb));
-            bool ok = true;
-            bool all_col = true;
+            QuotRange qr;
+            float qmax = 0.0f;
+            bool bad = false;
             for (uint32_t u = 0; u < cnt; ++u) {
               const PreRec& x = rb[u];
-              const bool has_col = (x.c >> 31) != 0u;
+              const bool live = x.w > 0.0f;
+              const bool active = !colour || (x.c >> 31) != 0u;
               const float add = ch == 0 ? x.wc : (ch == 1 ? x.wn0 : (ch == 2 ? x.wn1 : x.wn2));
               const float a = __fadd_rn(__fmul_rn(x.W, qs), add);
               const float q = fast_quot0(a, Recip{x.T, x.r1, true});
-              const bool colour = ch != 0;
-              ok = ok & (x.ok != 0u) & (!(colour & !has_col) ? (quot_ok(a) & (!colour | (q < 0x1p22f))) : true);
+              if (live & active) {
+                bad |= x.ok == 0u;
+                qr_add(qr, a);
+                if (colour) qmax = fmaxf(qmax, q);
+              }
               const float sn = colour ? fminf(round_half_away_pos(q), 255.0f) : q;
-              qs = (!colour | has_col) ? sn : qs;
-              all_col = all_col & has_col;
+              qs = (live & active) ? sn : qs;
             }
-            (void)all_col;
+            // q < 2^22 for colours (round_half_away_pos); NaN q fails the range check of a
+            const bool ok = !bad & qr_ok(qr) & (qmax < 0x1p22f);
             if (__all_sync(0xffffffffu, ok)) {
               st.D = __shfl_sync(0xffffffffu, qs, 0);
               st.cr = __shfl_sync(0xffffffffu, qs, 1);
@@ -1236,8 +1227,19 @@ __global__ void __launch_bounds__(256) k_fold_runs(
             for (uint32_t u = 0; u < cnt; ++u)
               step_exact(st.D, st.W, st.cr, st.cg, st.cb, rb[u].d, rb[u].w, rb[u].c, tp.truncation, Wmax);
           }
+          if (dbg != nullptr) {
+            asm volatile("" ::"f"(st.D));
+            ct_chain += clock64() - tc1;
+            ct_vote += tc1 - tc0;
+          }
           __syncwarp();
           mbar_arrive(&ring_empty[pair][s]);
+        }
+        if (dbg != nullptr && lane == 0) {
+          atomicAdd(&dbg[4 * n_all + 2], static_cast<unsigned long long>(cwait));
+          atomicAdd(&dbg[4 * n_all + 3], static_cast<unsigned long long>(clock64() - cbusy0));
+          atomicAdd(&dbg[4 * n_all + 8], static_cast<unsigned long long>(ct_vote));
+          atomicAdd(&dbg[4 * n_all + 9], static_cast<unsigned long long>(ct_chain));
         }
         if (lane == 0) {
           store_vox(vp, st);
@@ -1255,7 +1257,32 @@ __global__ void __launch_bounds__(256) k_fold_runs(
     }
   }
 
-  // ---- phase 2: short runs, one thread per run
+  if (dbg != nullptr && lane == 0) {  // when this warp ran out of work
+    unsigned long long t_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    atomicMax(&dbg[4 * nruns], t_end);
+    atomicMin(&dbg[4 * nruns + 1], t_end);
+  }
+}
+
+// Short runs (< kLongRun records): one thread per run, launched on a second
+// stream next to k_fold_runs (disjoint voxels), with its own register budget
+// so more warps hide the ray-id -> ray gather latency.
+template <int kMinBlocks, int kC>
+__global__ void __launch_bounds__(256, kMinBlocks) k_fold_short(
+    const uint32_t* __restrict__ num_runs_p, const uint32_t* __restrict__ order,
+    const uint32_t* __restrict__ sorted_len, const uint32_t* __restrict__ ukeys, const uint32_t* __restrict__ ustart,
+    const uint32_t* __restrict__ ulen, const uint32_t* __restrict__ svals, const FoldRay* __restrict__ rays,
+    const float* __restrict__ g_org, uint32_t F, MapView map, TsdfParams tp, uint8_t* __restrict__ touched,
+    uint32_t* __restrict__ work) {
+  __shared__ float s_org[3 * kOrgCache];
+  const float* poses = stage_origins(s_org, g_org, F);
+  if (map.counters[1] != 0u) return;
+  const uint32_t nruns = *num_runs_p;
+  const int lane = threadIdx.x & 31;
+  uint32_t n_long = 0;
+  if (lane == 0) n_long = count_long_runs(sorted_len, nruns);
+  n_long = __shfl_sync(0xffffffffu, n_long, 0);
   while (true) {
     uint32_t base = 0;
     if (lane == 0) base = atomicAdd(&work[1], 32u);
@@ -1267,22 +1294,28 @@ __global__ void __launch_bounds__(256) k_fold_runs(
     if (c.key == kInvalidRecord) continue;
     vxg_voxel* vp = map.slab + c.key;
     VoxState st = load_vox(vp);
-    for (uint32_t j = 0; j < c.len; j += kFoldChunk) {
-      Upd xs[kFoldChunk];
+    for (uint32_t j = 0; j < c.len; j += kC) {
+      Upd xs[kC];
+      FoldRay ry[kC];
 #pragma unroll
-      for (int u = 0; u < kFoldChunk; ++u) {
-        if (j + u < c.len) xs[u] = rec_upd(recs[c.start + j + u]);
+      for (int u = 0; u < kC; ++u) {
+        if (j + u < c.len) ry[u] = rays[svals[c.start + j + u]];
+      }
+#pragma unroll
+      for (int u = 0; u < kC; ++u) {
+        if (j + u < c.len) xs[u] = weigh(ry[u], poses, c.x0, c.x1, c.x2, tp);
       }
       const VoxState s0 = st;
       bool ok = true;
 #pragma unroll
-      for (int u = 0; u < kFoldChunk; ++u) {
+      for (int u = 0; u < kC; ++u) {
         if (j + u < c.len)
-          step_fast(st.D, st.W, st.cr, st.cg, st.cb, xs[u].d, xs[u].w, xs[u].c, tp.truncation, tp.max_weight, ok);
+          step_fast_skip(st.D, st.W, st.cr, st.cg, st.cb, xs[u].d, xs[u].w, xs[u].c, tp.truncation, tp.max_weight,
+                         ok);
       }
       if (!ok) {  // rare: exact re-run of the chunk from its start state
         st = s0;
-        for (int u = 0; u < kFoldChunk; ++u) {
+        for (int u = 0; u < kC; ++u) {
           if (j + u < c.len)
             step_exact(st.D, st.W, st.cr, st.cg, st.cb, xs[u].d, xs[u].w, xs[u].c, tp.truncation, tp.max_weight);
         }
@@ -1290,12 +1323,6 @@ __global__ void __launch_bounds__(256) k_fold_runs(
     }
     store_vox(vp, st);
     if (touched != nullptr) touched[c.key / static_cast<uint32_t>(map.nvox)] = 1u;
-  }
-  if (dbg != nullptr && lane == 0) {  // when this warp ran out of work
-    unsigned long long t_end;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
-    atomicMax(&dbg[4 * nruns], t_end);
-    atomicMin(&dbg[4 * nruns + 1], t_end);
   }
 }
 

@@ -1,0 +1,201 @@
+// Stable LSD radix sort of the fold's (voxel key, ray id) records.
+//
+// The keys of one batch are dense: slot * vps^3 + local < blocks * vps^3, i.e.
+// 21 bits for the 450-block cfg1 layer. One reduce-then-scan pass per digit of
+// up to 11 bits (two passes for keys up to 22 bits, where an 8-bit onesweep
+// needs three):
+//   k_sort_upsweep   per super-tile digit histogram   (reads 4 B/record)
+//   ExclusiveSum     digit-major [digit][super-tile]  -> global output bases
+//   k_sort_downsweep per sub-tile: warp-private match_any ranking (stable),
+//                    smem staging in digit order, coalesced scatter
+//                                                      (reads 8 B, writes 8 B)
+// Records within a voxel keep their emission (= ray) order, which is what the
+// ordered fold (tsdf_integrator.cpp:246, one update_tsdf_voxel per ray in
+// order) needs. Invalid records (key 0xFFFFFFFF) have all-ones digits and land
+// after every valid key as long as every valid key < 2^kbits - 1.
+#pragma once
+#include <cstdint>
+
+namespace vxg {
+
+constexpr int kSortThreads = 256;
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kSortIpt = 24;
+constexpr int kSortSub = kSortThreads * kSortIpt;           // records per sub-tile
+constexpr int kSortNsub = 8;                                // sub-tiles per super-tile (one CTA)
+constexpr uint32_t kSortSuper = static_cast<uint32_t>(kSortSub) * kSortNsub;
+constexpr int kSortMaxBits = 11;
+constexpr int kSortMaxBins = 1 << kSortMaxBits;
+constexpr int kSortWcStride = kSortMaxBins + 2;             // + overflow bin for the tail, even
+constexpr int kSortScanPer = (kSortMaxBins + 1 + kSortThreads - 1) / kSortThreads;
+
+struct SortSmem {
+  uint16_t wcnt[kSortWarps][kSortWcStride];  // per-warp digit counts, then cross-warp prefixes
+  uint32_t tcount[kSortMaxBins + 1];         // sub-tile digit counts
+  uint32_t tstart[kSortMaxBins + 1];         // sub-tile digit starts (exclusive scan of tcount)
+  uint32_t gbase[kSortMaxBins];              // global output position of the digit's next record
+  uint32_t wsum[kSortWarps];
+  uint32_t stage_k[kSortSub];
+  uint32_t stage_v[kSortSub];
+};
+
+__global__ void __launch_bounds__(kSortThreads) k_sort_upsweep(const uint32_t* __restrict__ keys, uint64_t n,
+                                                               int shift, uint32_t mask, uint32_t S,
+                                                               uint32_t* __restrict__ counts) {
+  __shared__ uint32_t h[kSortMaxBins];
+  const uint32_t bins = mask + 1u;
+  for (uint32_t d = threadIdx.x; d < bins; d += kSortThreads) h[d] = 0u;
+  __syncthreads();
+  const uint64_t lo = static_cast<uint64_t>(blockIdx.x) * kSortSuper;
+  const uint32_t cnt = static_cast<uint32_t>(min(static_cast<uint64_t>(kSortSuper), n - lo));
+  const uint4* k4 = reinterpret_cast<const uint4*>(keys + lo);  // lo % 4 == 0, buffers 256-B aligned
+  const uint32_t n4 = cnt / 4u;
+  for (uint32_t i = threadIdx.x; i < n4; i += kSortThreads) {  // spread-address ATOMS (MATCH.ANY is slower)
+    const uint4 k = k4[i];
+    atomicAdd(&h[(k.x >> shift) & mask], 1u);
+    atomicAdd(&h[(k.y >> shift) & mask], 1u);
+    atomicAdd(&h[(k.z >> shift) & mask], 1u);
+    atomicAdd(&h[(k.w >> shift) & mask], 1u);
+  }
+  for (uint32_t i = 4u * n4 + threadIdx.x; i < cnt; i += kSortThreads) atomicAdd(&h[(keys[lo + i] >> shift) & mask], 1u);
+  __syncthreads();
+  for (uint32_t d = threadIdx.x; d < bins; d += kSortThreads) counts[static_cast<uint64_t>(d) * S + blockIdx.x] = h[d];
+}
+
+// Lanes of the warp holding the same digit d (< 2^12): one ballot per bit
+// (MATCH.ANY is several times slower on sm_100).
+__device__ __forceinline__ uint32_t digit_peers(uint32_t d) {
+  uint32_t peers = 0xffffffffu;
+#pragma unroll
+  for (int b = 0; b <= kSortMaxBits; ++b) {
+    const uint32_t v = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+    peers &= ((d >> b) & 1u) ? v : ~v;
+  }
+  return peers;
+}
+
+template <bool kBallot>
+__global__ void __launch_bounds__(kSortThreads, 2)
+    k_sort_downsweep(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
+                     uint32_t* __restrict__ vout, uint64_t n, int shift, uint32_t mask, uint32_t S,
+                     const uint32_t* __restrict__ offs) {
+  extern __shared__ __align__(16) uint8_t sort_smem_raw[];
+  SortSmem& sm = *reinterpret_cast<SortSmem*>(sort_smem_raw);
+  const uint32_t bins = mask + 1u;
+  const int tid = threadIdx.x, w = tid >> 5;
+  const uint32_t lane = tid & 31u, lt = (1u << lane) - 1u;
+  for (uint32_t d = tid; d < bins; d += kSortThreads) sm.gbase[d] = offs[static_cast<uint64_t>(d) * S + blockIdx.x];
+  const uint64_t super0 = static_cast<uint64_t>(blockIdx.x) * kSortSuper;
+  uint32_t* wc32 = reinterpret_cast<uint32_t*>(&sm.wcnt[0][0]);
+  for (int t = 0; t < kSortNsub; ++t) {
+    const uint64_t base = super0 + static_cast<uint64_t>(t) * kSortSub;
+    if (base >= n) break;  // CTA-uniform
+    const uint32_t nv = static_cast<uint32_t>(min(static_cast<uint64_t>(kSortSub), n - base));
+    for (int i = tid; i < kSortWarps * kSortWcStride / 2; i += kSortThreads) wc32[i] = 0u;
+    // load: warp w owns sub-tile items [w*IPT*32, (w+1)*IPT*32), item (j, lane) = j*32 + lane
+    uint32_t key[kSortIpt], val[kSortIpt];
+    const uint32_t i0 = static_cast<uint32_t>(w) * (kSortIpt * 32) + lane;
+#pragma unroll
+    for (int j = 0; j < kSortIpt; ++j) {
+      const uint32_t i = i0 + j * 32;
+      key[j] = i < nv ? kin[base + i] : 0u;
+      val[j] = i < nv ? vin[base + i] : 0u;
+    }
+    __syncthreads();  // wcnt zeroed; previous sub-tile's gbase update visible
+    // stable warp-private ranking: (j, lane) order == item order
+    uint32_t rk[kSortIpt];
+#pragma unroll
+    for (int j = 0; j < kSortIpt; ++j) {
+      const uint32_t d = i0 + j * 32 < nv ? (key[j] >> shift) & mask : bins;
+      const uint32_t peers = kBallot ? digit_peers(d) : __match_any_sync(0xffffffffu, d);
+      const uint32_t pre = sm.wcnt[w][d];
+      __syncwarp();
+      if ((peers & lt) == 0u) sm.wcnt[w][d] = static_cast<uint16_t>(pre + __popc(peers));
+      __syncwarp();
+      rk[j] = pre + __popc(peers & lt);
+    }
+    __syncthreads();
+    // cross-warp exclusive prefixes (in place) and sub-tile digit counts
+    for (uint32_t d = tid; d <= bins; d += kSortThreads) {
+      uint32_t run = 0;
+#pragma unroll
+      for (int q = 0; q < kSortWarps; ++q) {
+        const uint32_t c = sm.wcnt[q][d];
+        sm.wcnt[q][d] = static_cast<uint16_t>(run);
+        run += c;
+      }
+      sm.tcount[d] = run;
+    }
+    __syncthreads();
+    {  // exclusive scan tcount[0..bins] -> tstart
+      const uint32_t nb = bins + 1u;
+      uint32_t loc[kSortScanPer], sum = 0;
+#pragma unroll
+      for (int q = 0; q < kSortScanPer; ++q) {
+        const uint32_t idx = static_cast<uint32_t>(tid) * kSortScanPer + q;
+        loc[q] = idx < nb ? sm.tcount[idx] : 0u;
+        sum += loc[q];
+      }
+      uint32_t x = sum;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, off);
+        if (lane >= static_cast<uint32_t>(off)) x += y;
+      }
+      if (lane == 31u) sm.wsum[w] = x;
+      __syncthreads();
+      uint32_t run = x - sum;
+      for (int q = 0; q < w; ++q) run += sm.wsum[q];
+#pragma unroll
+      for (int q = 0; q < kSortScanPer; ++q) {
+        const uint32_t idx = static_cast<uint32_t>(tid) * kSortScanPer + q;
+        if (idx < nb) sm.tstart[idx] = run;
+        run += loc[q];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kSortIpt; ++j) {
+      if (i0 + j * 32 < nv) {
+        const uint32_t d = (key[j] >> shift) & mask;
+        const uint32_t p = sm.tstart[d] + sm.wcnt[w][d] + rk[j];
+        sm.stage_k[p] = key[j];
+        sm.stage_v[p] = val[j];
+      }
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < nv; i += kSortThreads) {
+      const uint32_t k = sm.stage_k[i];
+      const uint32_t d = (k >> shift) & mask;
+      const uint32_t p = sm.gbase[d] + (i - sm.tstart[d]);
+      kout[p] = k;
+      vout[p] = sm.stage_v[i];
+    }
+    __syncthreads();
+    for (uint32_t d = tid; d < bins; d += kSortThreads) sm.gbase[d] += sm.tcount[d];
+  }
+}
+
+// Runs of the sorted records, one per voxel, from the dense per-key head/tail
+// marks the weigh pass wrote (dense_end[k] == 0: voxel k has no record).
+__global__ void k_run_flags(uint32_t K, const uint32_t* __restrict__ dense_end, uint32_t* __restrict__ flag) {
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x)
+    flag[k] = dense_end[k] != 0u ? 1u : 0u;
+}
+
+__global__ void k_run_scatter(uint32_t K, const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos,
+                              const uint32_t* __restrict__ dense_start, const uint32_t* __restrict__ dense_end,
+                              uint32_t* __restrict__ run_keys, uint32_t* __restrict__ run_start,
+                              uint32_t* __restrict__ run_len, uint32_t* __restrict__ nruns) {
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x) {
+    if (flag[k]) {
+      const uint32_t j = pos[k];
+      run_keys[j] = k;
+      run_start[j] = dense_start[k];
+      run_len[j] = dense_end[k] - dense_start[k];
+    }
+    if (k == K - 1) *nruns = pos[k] + flag[k];
+  }
+}
+
+}  // namespace vxg

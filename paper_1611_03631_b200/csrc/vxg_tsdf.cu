@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <map>
@@ -32,6 +33,7 @@
 
 #include "../../include/vxg.h"
 #include "vxg_kernels.cuh"
+#include "vxg_sort.cuh"
 
 namespace vxg {
 using Schedule = std::vector<std::pair<uint64_t, uint64_t>>;
@@ -125,6 +127,8 @@ struct vxg_handle {
   cudaStream_t own = nullptr;
   cudaStream_t st = nullptr;
   cudaStream_t copy_st = nullptr;         // H2D staging of host inputs (overlaps compute)
+  cudaStream_t fold_st = nullptr;         // short-run fold beside the long-run fold
+  cudaEvent_t fold_fork = nullptr, fold_join = nullptr;
   std::vector<cudaEvent_t> copy_events;
 
   // ---- map (slab + block hash)
@@ -161,8 +165,9 @@ struct vxg_handle {
   DBuf<uint64_t> tbl_off, bcs;
   DBuf<uint32_t> rkeys, rkeys2, rvals, rvals2;
   DBuf<uint32_t> run_keys, run_len, run_start, run_len2, run_order, run_iota, work;
-  DBuf<uint4> fold_recs;
+  DBuf<uint32_t> sort_counts, sort_offs, dense_start, dense_end, run_flag, run_pos;
   DBuf<FoldRay> fold_rays;
+  DBuf<float> d_org;  // sensor origins, 3 floats per frame
   bool debug_fold = false;  // globaltimer trace of the fold (vxg_debug_fold)
   DBuf<unsigned long long> fold_dbg;
   uint32_t fold_dbg_n = 0;
@@ -388,7 +393,9 @@ struct vxg_handle {
                           uint32_t ray0, int pb);
   void emit_and_apply(uint32_t R, uint32_t F, const TermView& tv);
   uint64_t count_rays(uint32_t R, uint32_t F);
-  void sort_fold(uint64_t T);
+  void sort_fold(uint64_t T, uint64_t nslots, uint32_t F);
+  void sort_records(uint64_t T, int kbits, uint32_t** sk, uint32_t** sv);
+  uint64_t last_blocks = 0;  // blocks allocated after the last produce attempt
   bool grew_after_attempt(int attempt);
   void begin_batch(const float* xyz, const uint8_t* rgb, const uint64_t* offsets, const float* poses, uint64_t F,
                    uint32_t* R_out, TermView* tv);
@@ -634,83 +641,177 @@ uint64_t vxg_handle::count_rays(uint32_t R, uint32_t F) {
 
 // Stable sort of T records (rkeys = u32 voxel key, rvals = ray index) by voxel
 // key, runs (one per voxel) longest first, then the ordered fold.
-void vxg_handle::sort_fold(uint64_t T) {
+// Stable sort of the T records by voxel key (vxg_sort.cuh); returns the
+// buffers holding the sorted keys / ray ids.
+void vxg_handle::sort_records(uint64_t T, int kbits, uint32_t** sk, uint32_t** sv) {
+  static bool attr = false;
+  if (!attr) {
+    CU(cudaFuncSetAttribute(k_sort_downsweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(sizeof(SortSmem))));
+    attr = true;
+  }
+  static const bool use_cub = [] {
+    const char* e = getenv("VXG_SORT");
+    return !(e && std::string(e) == "lsd11");
+  }();
+  if (use_cub) {
+    const int nb = std::max(kbits, 1);
+    cub([&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, rkeys.p, rkeys2.p, rvals.p, rvals2.p, static_cast<int>(T), 0, nb,
+                                             st);
+    }, 2 + (nb + 7) / 8);
+    *sk = rkeys2.p;
+    *sv = rvals2.p;
+    return;
+  }
+  const int passes = std::max(1, (kbits + kSortMaxBits - 1) / kSortMaxBits);
+  const uint32_t S = static_cast<uint32_t>((T + kSortSuper - 1) / kSortSuper);
+  uint32_t *ki = rkeys.p, *vi = rvals.p, *ko = rkeys2.p, *vo = rvals2.p;
+  int shift = 0;
+  for (int p = 0; p < passes; ++p) {
+    const int bits = (kbits - shift + (passes - p) - 1) / (passes - p);
+    const uint32_t mask = bits ? (bits >= 32 ? 0xFFFFFFFFu : (1u << bits) - 1u) : 0u;
+    const uint64_t nc = static_cast<uint64_t>(mask + 1u) * S;
+    sort_counts.ensure(nc);
+    sort_offs.ensure(nc);
+    k_sort_upsweep<<<S, kSortThreads, 0, st>>>(ki, T, shift, mask, S, sort_counts.p);
+    ++launches;
+    cub([&](void* t, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, sort_counts.p, sort_offs.p, static_cast<int>(nc), st);
+    }, 2);
+    k_sort_downsweep<true><<<S, kSortThreads, sizeof(SortSmem), st>>>(ki, vi, ko, vo, T, shift, mask, S, sort_offs.p);
+    ++launches;
+    CU(cudaGetLastError());
+    std::swap(ki, ko);
+    std::swap(vi, vo);
+    shift += bits;
+  }
+  *sk = ki;
+  *sv = vi;
+}
+
+// Sorts the T records of one attempt (keys < nslots * vps^3, or invalid) and
+// folds every voxel's run in ray order.
+void vxg_handle::sort_fold(uint64_t T, uint64_t nslots, uint32_t F) {
   const TsdfParams tp = params();
   begin(ST_SORT);
-  const int kbits = bits_for(cap_blocks * static_cast<uint64_t>(nvox));
-  const int sort_passes = (kbits + 7) / 8;
-  cub([&](void* t, size_t& b) {
-    return cub::DeviceRadixSort::SortPairs(t, b, rkeys.p, rkeys2.p, rvals.p, rvals2.p, static_cast<int>(T), 0, kbits,
-                                           st);
-  }, 2 + sort_passes);
-  // runs = one per voxel (plus at most one run of invalid keys)
-  const uint64_t max_runs = std::min<uint64_t>(T, cap_blocks * static_cast<uint64_t>(nvox) + 1);
-  run_keys.ensure(max_runs);
-  run_len.ensure(max_runs);
+  const uint64_t K = std::max<uint64_t>(1, std::min<uint64_t>(nslots, cap_blocks) * static_cast<uint64_t>(nvox));
+  const int kbits = bits_for(K);  // every valid key < K <= 2^kbits - 1: the invalid key sorts last
+  if (const char* dump = getenv("VXG_DUMP_RECORDS")) {  // dev hook: unsorted records for tools/sort_lab.cu
+    std::vector<uint32_t> hk(T), hv(T);
+    CU(cudaMemcpyAsync(hk.data(), rkeys.p, T * 4, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(hv.data(), rvals.p, T * 4, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    if (FILE* f = fopen(dump, "wb")) {
+      const uint64_t hdr[2] = {T, static_cast<uint64_t>(kbits)};
+      fwrite(hdr, sizeof(hdr), 1, f);
+      fwrite(hk.data(), 4, T, f);
+      fwrite(hv.data(), 4, T, f);
+      fclose(f);
+    }
+  }
+  uint32_t *skeys = nullptr, *svals = nullptr;
+  sort_records(T, kbits, &skeys, &svals);
+  end(T, 0);
+  begin(ST_APPLY);
+  // mark each voxel's run [start, end) (dense by key)
+  dense_start.ensure(K);
+  dense_end.ensure(K);
+  CU(cudaMemsetAsync(dense_end.p, 0, K * sizeof(uint32_t), st));
+  k_run_marks<<<grid_for((T + 3) / 4), 256, 0, st>>>(T, skeys, dense_start.p, dense_end.p);
+  ++launches;
+  // compact the runs in key order
+  run_flag.ensure(K);
+  run_pos.ensure(K);
+  run_keys.ensure(K);
+  run_len.ensure(K);
+  run_start.ensure(K);
   num_runs.ensure(1);
+  k_run_flags<<<grid_for(K), 256, 0, st>>>(static_cast<uint32_t>(K), dense_end.p, run_flag.p);
+  ++launches;
   cub([&](void* t, size_t& b) {
-    return cub::DeviceRunLengthEncode::Encode(t, b, rkeys2.p, run_keys.p, run_len.p, num_runs.p, static_cast<int>(T),
-                                              st);
+    return cub::DeviceScan::ExclusiveSum(t, b, run_flag.p, run_pos.p, static_cast<int>(K), st);
   }, 2);
+  k_run_scatter<<<grid_for(K), 256, 0, st>>>(static_cast<uint32_t>(K), run_flag.p, run_pos.p, dense_start.p,
+                                              dense_end.p, run_keys.p, run_start.p, run_len.p, num_runs.p);
+  ++launches;
+  CU(cudaGetLastError());
   uint32_t nruns = 0;
   CU(cudaMemcpyAsync(&nruns, num_runs.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
-  run_start.ensure(nruns);
-  run_len2.ensure(nruns);
-  run_order.ensure(nruns);
-  run_iota.ensure(nruns);
-  cub([&](void* t, size_t& b) {
-    return cub::DeviceScan::ExclusiveSum(t, b, run_len.p, run_start.p, static_cast<int>(nruns), st);
-  }, 2);
-  k_iota<<<grid_for(nruns), 256, 0, st>>>(nruns, run_iota.p);
-  ++launches;
-  const int lbits = bits_for(T);
-  cub([&](void* t, size_t& b) {  // longest runs first: they bound the fold's critical path
-    return cub::DeviceRadixSort::SortPairsDescending(t, b, run_len.p, run_len2.p, run_iota.p, run_order.p,
-                                                     static_cast<int>(nruns), 0, lbits, st);
-  }, 2 + (lbits + 7) / 8);
-  end(T, 0);
-  begin(ST_APPLY);
+  run_len2.ensure(std::max<uint32_t>(nruns, 1));
+  run_order.ensure(std::max<uint32_t>(nruns, 1));
+  run_iota.ensure(std::max<uint32_t>(nruns, 1));
+  if (nruns) {
+    k_iota<<<grid_for(nruns), 256, 0, st>>>(nruns, run_iota.p);
+    ++launches;
+    const int lbits = bits_for(T);
+    cub([&](void* t, size_t& b) {  // longest runs first: they bound the fold's critical path
+      return cub::DeviceRadixSort::SortPairsDescending(t, b, run_len.p, run_len2.p, run_iota.p, run_order.p,
+                                                       static_cast<int>(nruns), 0, lbits, st);
+    }, 2 + (lbits + 7) / 8);
+  }
   uint8_t* tch = consumers.empty() ? nullptr : touched.p;
   work.ensure(2);
   CU(cudaMemsetAsync(work.p, 0, 2 * sizeof(uint32_t), st));
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
-  int per_sm = 0;
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fold_runs, 256, 0));
-  const unsigned fold_grid = static_cast<unsigned>(std::max<uint64_t>(
-      1, std::min<uint64_t>(static_cast<uint64_t>(dev_sms) * std::max(per_sm, 1), (nruns + 255) / 256)));
+  // long runs: one CTA (4 producer/consumer pairs) per SM on st; short runs:
+  // k_fold_short on fold_st beside it (disjoint voxels), filling the rest
+  const unsigned long_grid = static_cast<unsigned>(std::max<uint64_t>(
+      1, std::min<uint64_t>(static_cast<uint64_t>(dev_sms), (nruns + 3) / 4)));
   unsigned long long* dbg = nullptr;
   if (debug_fold) {
-    fold_dbg.ensure(4 * nruns + 2);
-    CU(cudaMemsetAsync(fold_dbg.p, 0, (4 * nruns + 2) * sizeof(unsigned long long), st));
+    fold_dbg.ensure(4 * nruns + 10);
+    CU(cudaMemsetAsync(fold_dbg.p, 0, (4 * nruns + 10) * sizeof(unsigned long long), st));
     CU(cudaMemsetAsync(fold_dbg.p + 4 * nruns + 1, 0xFF, sizeof(unsigned long long), st));
     dbg = fold_dbg.p;
     fold_dbg_n = nruns;
   }
-  fold_recs.ensure(T);
-  k_weigh_records<<<grid_for(T), 256, 0, st>>>(T, rkeys2.p, rvals2.p, fold_rays.p, d_poses.p, view(), tp,
-                                                fold_recs.p);
-  k_fold_runs<<<fold_grid, 256, 0, st>>>(num_runs.p, run_order.p, run_len2.p, run_keys.p, run_start.p, run_len.p,
-                                          fold_recs.p, view(), tp, tch, work.p, dbg);
-  ++launches;
-  ++launches;
+  if (nruns) {
+    if (fold_st == nullptr) {
+      CU(cudaStreamCreateWithFlags(&fold_st, cudaStreamNonBlocking));
+      CU(cudaEventCreateWithFlags(&fold_fork, cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&fold_join, cudaEventDisableTiming));
+    }
+    d_org.ensure(3 * std::max<uint32_t>(F, 1));
+    k_origins<<<grid_for(3 * F), 256, 0, st>>>(F, d_poses.p, d_org.p);
+    ++launches;
+    CU(cudaEventRecord(fold_fork, st));
+    CU(cudaStreamWaitEvent(fold_st, fold_fork, 0));
+    k_fold_runs<<<long_grid, 256, 0, st>>>(num_runs.p, run_order.p, run_len2.p, run_keys.p, run_start.p, run_len.p,
+                                            svals, fold_rays.p, d_org.p, F, view(), tp, tch, work.p, dbg);
+    static const int short_blocks = [] {
+      const char* e = getenv("VXG_FOLD_SHORT_BLOCKS");
+      return e ? atoi(e) : 3;
+    }();
+    static const bool serial = getenv("VXG_FOLD_SERIAL") != nullptr;  // dev: long runs uncontended
+    cudaStream_t sst = serial ? st : fold_st;
+    const unsigned short_grid = static_cast<unsigned>(std::max<uint64_t>(
+        1, std::min<uint64_t>(static_cast<uint64_t>(dev_sms) * 4, (nruns + 255) / 256)));
+#define VXG_FOLD_SHORT(MB, C)                                                                                 \
+  k_fold_short<MB, C><<<short_grid, 256, 0, sst>>>(num_runs.p, run_order.p, run_len2.p, run_keys.p, run_start.p, \
+                                                       run_len.p, svals, fold_rays.p, d_org.p, F, view(), tp, tch, \
+                                                       work.p)
+    switch (short_blocks) {
+      case 2: VXG_FOLD_SHORT(2, 8); break;
+      case 4: VXG_FOLD_SHORT(4, 4); break;
+      case 5: VXG_FOLD_SHORT(3, 8); break;
+      default: VXG_FOLD_SHORT(3, 4); break;
+    }
+#undef VXG_FOLD_SHORT
+    CU(cudaEventRecord(fold_join, fold_st));
+    CU(cudaStreamWaitEvent(st, fold_join, 0));
+    launches += 2;
+  }
   CU(cudaGetLastError());
   end(T, 1);
-  // longest valid chain: the invalid-key run (if any) is the last run by key
-  uint32_t top[2] = {0, 0}, ord0 = 0, lastkey = 0;
-  const uint32_t ntop = std::min<uint32_t>(nruns, 2);
-  if (nruns) {
-    CU(cudaMemcpyAsync(top, run_len2.p, ntop * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-    CU(cudaMemcpyAsync(&ord0, run_order.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-    CU(cudaMemcpyAsync(&lastkey, run_keys.p + (nruns - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-  }
+  uint32_t top = 0;
+  if (nruns) CU(cudaMemcpyAsync(&top, run_len2.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
-  const bool has_invalid = nruns && lastkey == kInvalidRecord;
-  const uint32_t mr = (has_invalid && ord0 == nruns - 1) ? top[1] : top[0];
   info_records += T;
-  info_runs += nruns - (has_invalid ? 1 : 0);
-  info_max_run = std::max<uint64_t>(info_max_run, mr);
+  info_runs += nruns;
+  info_max_run = std::max<uint64_t>(info_max_run, top);
 }
 
 // After a produce+sort_fold attempt: true if the map had to grow (the caller
@@ -718,6 +819,7 @@ void vxg_handle::sort_fold(uint64_t T) {
 bool vxg_handle::grew_after_attempt(int attempt) {
   uint32_t c[2];
   read_counters(c);
+  last_blocks = c[0];
   if (c[1] & kErrKeyRange) throw VxgError(VXG_ERANGE, "voxel block index outside the supported range");
   if (c[1] & (kErrSlabFull | kErrHashFull)) {
     if (attempt > 64) throw VxgError(VXG_ENOMEM, "block allocation did not converge");
@@ -789,8 +891,9 @@ void vxg_handle::emit_and_apply(uint32_t R, uint32_t F, const TermView& tv) {
       ++launches;
       CU(cudaGetLastError());
       end(T, 1);
-      sort_fold(T);
-      if (!grew_after_attempt(attempt)) break;
+      if (grew_after_attempt(attempt)) continue;
+      sort_fold(T, last_blocks, F);
+      break;
     }
     // fold this chunk's per-frame update counts into the stats
     k_add_u64<<<grid_for(F), 256, 0, st>>>(F, d_stats.p, d_upd.p);
@@ -827,6 +930,7 @@ void vxg_handle::begin_batch(const float* xyz, const uint8_t* rgb, const uint64_
   }
   uint32_t c[2];
   read_counters(c);
+  last_blocks = c[0];
   if (c[1] & kErrKeyRange) throw VxgError(VXG_ERANGE, "terminal voxel outside the bundling key range");
 }
 
@@ -933,6 +1037,7 @@ void vxg_handle::shard_front(uint32_t R, uint32_t F, const TermView& tv) {
   CU(cudaStreamSynchronize(st));
   uint32_t c[2];
   read_counters(c);
+  last_blocks = c[0];
   if (c[1] & kErrKeyRange) throw VxgError(VXG_ERANGE, "voxel block index outside the sharded key range (+-2^14 blocks)");
   const uint64_t n_valid = bnd[shard_world];
   send_buf.ensure(std::max<uint64_t>(n_valid, 1));
@@ -965,8 +1070,9 @@ void vxg_handle::shard_back(const uint4* recv, uint64_t n, uint32_t F) {
       k_localize<<<grid_for(n), 256, 0, st>>>(n, recv, view(), fold_rays.p, rkeys.p, rvals.p, d_upd.p);
       ++launches;
       CU(cudaGetLastError());
-      sort_fold(n);
-      if (!grew_after_attempt(attempt)) break;
+      if (grew_after_attempt(attempt)) continue;
+      sort_fold(n, last_blocks, F);
+      break;
     }
   }
   k_add_u64<<<grid_for(F), 256, 0, st>>>(F, d_stats.p, d_upd.p);
@@ -1213,6 +1319,12 @@ int vxg_destroy(vxg_handle* h) {
       cudaStreamDestroy(h->copy_st);
     }
     for (cudaEvent_t e : h->copy_events) cudaEventDestroy(e);
+    if (h->fold_st) {
+      cudaStreamSynchronize(h->fold_st);
+      cudaStreamDestroy(h->fold_st);
+      cudaEventDestroy(h->fold_fork);
+      cudaEventDestroy(h->fold_join);
+    }
     if (h->nccl_comm) nccl()->CommDestroy(static_cast<ncclComm_t>(h->nccl_comm));
     if (h->own) cudaStreamDestroy(h->own);
     delete h;
@@ -1724,7 +1836,7 @@ extern "C" int vxg_debug_fold(vxg_handle* h, int enable, unsigned long long* out
     h->debug_fold = enable != 0;
     if (n) *n = h->fold_dbg_n;
     if (out && h->fold_dbg.p) {
-      const uint64_t m = std::min<uint64_t>(cap, 4ull * h->fold_dbg_n + 2);
+      const uint64_t m = std::min<uint64_t>(cap, 4ull * h->fold_dbg_n + 10);
       CU(cudaMemcpy(out, h->fold_dbg.p, m * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     }
   });

@@ -1,0 +1,119 @@
+// Dev lab: time record-sort variants on a real record dump (VXG_DUMP_RECORDS)
+// and check each against CUB's stable SortPairs.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_1611_03631_b200/csrc tools/sort_lab.cu -o build/sort_lab
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include "vxg_sort.cuh"
+using namespace vxg;
+
+#define CK(x) do { cudaError_t err_ = (x); if (err_ != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(err_)); exit(1); } } while (0)
+
+// upsweep variant: plain per-CTA smem atomics, no match
+__global__ void __launch_bounds__(256) up_atom(const uint32_t* __restrict__ keys, uint64_t n, int shift, uint32_t mask,
+                                               uint32_t S, uint32_t* __restrict__ counts) {
+  __shared__ uint32_t h[kSortMaxBins];
+  const uint32_t bins = mask + 1u;
+  for (uint32_t d = threadIdx.x; d < bins; d += 256) h[d] = 0u;
+  __syncthreads();
+  const uint64_t lo = static_cast<uint64_t>(blockIdx.x) * kSortSuper;
+  const uint32_t cnt = static_cast<uint32_t>(min(static_cast<uint64_t>(kSortSuper), n - lo));
+  const uint4* k4 = reinterpret_cast<const uint4*>(keys + lo);
+  const uint32_t n4 = cnt / 4u;
+  for (uint32_t i = threadIdx.x; i < n4; i += 256) {
+    const uint4 k = k4[i];
+    atomicAdd(&h[(k.x >> shift) & mask], 1u);
+    atomicAdd(&h[(k.y >> shift) & mask], 1u);
+    atomicAdd(&h[(k.z >> shift) & mask], 1u);
+    atomicAdd(&h[(k.w >> shift) & mask], 1u);
+  }
+  for (uint32_t i = 4u * n4 + threadIdx.x; i < cnt; i += 256) atomicAdd(&h[(keys[lo + i] >> shift) & mask], 1u);
+  __syncthreads();
+  for (uint32_t d = threadIdx.x; d < bins; d += 256) counts[static_cast<uint64_t>(d) * S + blockIdx.x] = h[d];
+}
+
+int main(int argc, char** argv) {
+  FILE* f = fopen(argc > 1 ? argv[1] : "/tmp/records.bin", "rb");
+  if (!f) { printf("no dump\n"); return 1; }
+  uint64_t hdr[2];
+  fread(hdr, sizeof(hdr), 1, f);
+  const uint64_t T = hdr[0];
+  const int kbits = static_cast<int>(hdr[1]);
+  std::vector<uint32_t> hk(T), hv(T);
+  fread(hk.data(), 4, T, f);
+  fread(hv.data(), 4, T, f);
+  fclose(f);
+  printf("T=%llu kbits=%d\n", (unsigned long long)T, kbits);
+  uint32_t *k0, *v0, *k1, *v1, *k2, *v2, *rk, *rv;
+  CK(cudaMalloc(&k0, T * 4)); CK(cudaMalloc(&v0, T * 4)); CK(cudaMalloc(&k1, T * 4)); CK(cudaMalloc(&v1, T * 4));
+  CK(cudaMalloc(&k2, T * 4)); CK(cudaMalloc(&v2, T * 4)); CK(cudaMalloc(&rk, T * 4)); CK(cudaMalloc(&rv, T * 4));
+  CK(cudaMemcpy(k0, hk.data(), T * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(v0, hv.data(), T * 4, cudaMemcpyHostToDevice));
+  cudaEvent_t a, b;
+  cudaEventCreate(&a); cudaEventCreate(&b);
+  // reference: CUB
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, rk, v0, rv, (int)T, 0, kbits);
+  void* tmp; CK(cudaMalloc(&tmp, tb + (64 << 20)));
+  float ms;
+  for (int r = 0; r < 2; ++r) cub::DeviceRadixSort::SortPairs(tmp, tb, k0, rk, v0, rv, (int)T, 0, kbits);
+  cudaEventRecord(a);
+  for (int r = 0; r < 5; ++r) cub::DeviceRadixSort::SortPairs(tmp, tb, k0, rk, v0, rv, (int)T, 0, kbits);
+  cudaEventRecord(b); cudaEventSynchronize(b); cudaEventElapsedTime(&ms, a, b);
+  printf("cub   : %.3f ms\n", ms / 5);
+  std::vector<uint32_t> ck(T), cv(T), tk(T), tv(T);
+  CK(cudaMemcpy(ck.data(), rk, T * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(cv.data(), rv, T * 4, cudaMemcpyDeviceToHost));
+
+  const int passes = std::max(1, (kbits + kSortMaxBits - 1) / kSortMaxBits);
+  const uint32_t S = static_cast<uint32_t>((T + kSortSuper - 1) / kSortSuper);
+  uint32_t *counts, *offs;
+  CK(cudaMalloc(&counts, (size_t)kSortMaxBins * S * 4)); CK(cudaMalloc(&offs, (size_t)kSortMaxBins * S * 4));
+  CK(cudaFuncSetAttribute(k_sort_downsweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SortSmem)));
+  CK(cudaFuncSetAttribute(k_sort_downsweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SortSmem)));
+  size_t stb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, stb, counts, offs, kSortMaxBins * (int)S);
+  for (int variant = 0; variant < 2; ++variant) {
+    float t_up = 0, t_scan = 0, t_down = 0;
+    cudaEvent_t e[4];
+    for (auto& x : e) cudaEventCreate(&x);
+    for (int rep = 0; rep < 4; ++rep) {
+      uint32_t *ki = k0, *vi = v0, *ko = k1, *vo = v1;
+      int shift = 0;
+      for (int p = 0; p < passes; ++p) {
+        const int bits = (kbits - shift + (passes - p) - 1) / (passes - p);
+        const uint32_t mask = (1u << bits) - 1u;
+        const int nc = (int)((mask + 1u) * S);
+        cudaEventRecord(e[0]);
+        if (variant == 0) k_sort_upsweep<<<S, 256>>>(ki, T, shift, mask, S, counts);
+        else up_atom<<<S, 256>>>(ki, T, shift, mask, S, counts);
+        cudaEventRecord(e[1]);
+        cub::DeviceScan::ExclusiveSum(tmp, stb, counts, offs, nc);
+        cudaEventRecord(e[2]);
+        if (variant == 0) k_sort_downsweep<false><<<S, 256, sizeof(SortSmem)>>>(ki, vi, ko, vo, T, shift, mask, S, offs);
+        else k_sort_downsweep<true><<<S, 256, sizeof(SortSmem)>>>(ki, vi, ko, vo, T, shift, mask, S, offs);
+        cudaEventRecord(e[3]);
+        CK(cudaEventSynchronize(e[3]));
+        float x;
+        if (rep) {
+          cudaEventElapsedTime(&x, e[0], e[1]); t_up += x;
+          cudaEventElapsedTime(&x, e[1], e[2]); t_scan += x;
+          cudaEventElapsedTime(&x, e[2], e[3]); t_down += x;
+        }
+        ki = ko; vi = vo; ko = (ko == k1) ? k2 : k1; vo = (vo == v1) ? v2 : v1;
+        shift += bits;
+      }
+      if (rep == 3) {
+        CK(cudaMemcpy(tk.data(), ki, T * 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(tv.data(), vi, T * 4, cudaMemcpyDeviceToHost));
+      }
+    }
+    CK(cudaGetLastError());
+    const bool ok = tk == ck && tv == cv;
+    printf("lsd11 v%d: up %.3f scan %.3f down %.3f total %.3f ms (%d passes) %s\n", variant, t_up / 3, t_scan / 3,
+           t_down / 3, (t_up + t_scan + t_down) / 3, passes, ok ? "OK" : "MISMATCH");
+  }
+  return 0;
+}
