@@ -845,9 +845,11 @@ __global__ void k_origins(uint32_t F, const float* __restrict__ poses, float* __
     org[i] = poses[12 * (i / 3) + 3 + 4 * (i % 3)];
 }
 
-// Stages the origin table in shared memory when it fits; returns the table to use.
+// Stages the origin table in shared memory (kSmem: the host launched the
+// variant only when F <= kOrgCache, so the loads compile to LDS).
+template <bool kSmem>
 __device__ __forceinline__ const float* stage_origins(float* s_org, const float* __restrict__ g_org, uint32_t F) {
-  if (F > kOrgCache) return g_org;
+  if (!kSmem) return g_org;
   for (uint32_t i = threadIdx.x; i < 3 * F; i += blockDim.x) s_org[i] = g_org[i];
   __syncthreads();
   return s_org;
@@ -927,6 +929,27 @@ struct alignas(16) PreRec {  // one record as handed to the long-run consumer
   uint32_t ok, pad;     // w in (0, 2^100) and T in the fast-division range
 };
 
+// Per-chunk summary the producer publishes with the chunk: the weight after
+// it, whether every record is in the fast range, and per colour channel the
+// interval of current colours o for which every record of the chunk is
+// stationary: RN(|n - o| w) < RN(0.499 T) <=> |n - o| <= k with
+// k = max{k : RN(k w) < RN(0.499 T)} (RN(k w) is monotone in k).
+struct alignas(16) ChunkHdr {
+  float W_end;
+  uint32_t ok;
+  int lo[3];
+  int hi[3];
+};
+
+// k = max{k in [0, 255] : RN(k w) < thr}, for w > 0 and thr > 0 (k = 0 always qualifies).
+__device__ __forceinline__ int stationary_radius(float w, float thr) {
+  int k = static_cast<int>(fminf(floorf(__fdividef(thr, w)), 255.0f));
+  k = k < 0 ? 0 : k;
+  while (k > 0 && !(__fmul_rn(static_cast<float>(k), w) < thr)) --k;
+  while (k < 255 && __fmul_rn(static_cast<float>(k + 1), w) < thr) ++k;
+  return k;
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -981,20 +1004,26 @@ __global__ void k_run_marks(uint64_t T, const uint32_t* __restrict__ skeys, uint
   }
 }
 
-__global__ void __launch_bounds__(256) k_fold_runs(
+// kP producer/consumer pairs per CTA (64 kP threads). kSep: consumers only on
+// sub-partitions 0 and 1 (warp & 3 < 2), producers on 2 and 3, so no consumer
+// shares its scheduler with a producer.
+template <int kP, bool kSep, bool kSmemOrg>
+__global__ void __launch_bounds__(64 * kP, 1) k_fold_runs(
     const uint32_t* __restrict__ num_runs_p, const uint32_t* __restrict__ order,
     const uint32_t* __restrict__ sorted_len, const uint32_t* __restrict__ ukeys, const uint32_t* __restrict__ ustart,
     const uint32_t* __restrict__ ulen, const uint32_t* __restrict__ svals, const FoldRay* __restrict__ rays,
     const float* __restrict__ g_org, uint32_t F, MapView map, TsdfParams tp, uint8_t* __restrict__ touched,
     uint32_t* __restrict__ work, unsigned long long* __restrict__ dbg) {
-  __shared__ PreRec ring[4][kRingStages][32];
+  __shared__ PreRec ring[kP][kRingStages][32];
   __shared__ float s_org[3 * kOrgCache];
-  const float* poses = stage_origins(s_org, g_org, F);
-  __shared__ unsigned long long ring_full[4][kRingStages];
-  __shared__ unsigned long long ring_empty[4][kRingStages];
-  __shared__ uint32_t pair_run[4];
+  const float* poses = stage_origins<kSmemOrg>(s_org, g_org, F);
+  __shared__ unsigned long long ring_full[kP][kRingStages];
+  __shared__ unsigned long long ring_empty[kP][kRingStages];
+  __shared__ uint32_t pair_run[kP];
+  __shared__ float4 wscan[kP][8];
+  __shared__ ChunkHdr ring_hdr[kP][kRingStages];  // the chunk's 32 weights, broadcast to the producer lanes
   if (map.counters[1] != 0u) return;  // emission failed (slab/hash full): host grows and replays
-  if (threadIdx.x < 4 * kRingStages) {
+  if (threadIdx.x < kP * kRingStages) {
     mbar_init(&ring_full[threadIdx.x / kRingStages][threadIdx.x % kRingStages], 32);
     mbar_init(&ring_empty[threadIdx.x / kRingStages][threadIdx.x % kRingStages], 32);
   }
@@ -1010,10 +1039,11 @@ __global__ void __launch_bounds__(256) k_fold_runs(
 
   // ---- phase 1: long runs, one producer/consumer warp pair per run
   {
-    // consumers are warps 4..7 (highest ids: the warp arbiter favours them);
-    // pair p = consumer 4+p (sub-partition p) + producer (p+1)&3 (another one)
-    const bool producer = wid < 4;
-    const int pair = producer ? ((wid + 3) & 3) : (wid - 4);
+    // default (kP = 4): consumers are warps 4..7 (highest ids: the warp
+    // arbiter favours them); pair p = consumer 4+p (sub-partition p) +
+    // producer (p+1)&3 (another one)
+    const bool producer = kSep ? (wid & 3) >= 2 : wid < kP;
+    const int pair = kSep ? ((wid >> 2) * 2 + (wid & 1)) : (producer ? ((wid + kP - 1) % kP) : (wid - kP));
     uint32_t kk = 0;  // chunk counter of this pair across its runs (ring position / phase)
     while (true) {
       if (!producer && lane == 0) pair_run[pair] = atomicAdd(&work[0], 1u);
@@ -1080,20 +1110,29 @@ __global__ void __launch_bounds__(256) k_fold_runs(
           if (W != Wmax) {  // W is warp-uniform (replicated scan)
             const float wp = w > 0.0f ? w : 0.0f;
             float S = W, Smine = W;
-            if (cnt == 32) {
+            reinterpret_cast<float*>(wscan[pair])[lane] = wp;
+            __syncwarp();
+            float4 wq[8];
 #pragma unroll
-              for (int q = 0; q < 32; ++q) {
-                const float wu = __shfl_sync(0xffffffffu, wp, q);
+            for (int q = 0; q < 8; ++q) wq[q] = wscan[pair][q];
+            if (__float_as_uint(W) != 0x80000000u) {
+#pragma unroll
+              for (int q = 0; q < 32; ++q) {  // records >= cnt carry w+ = 0: RN(S + 0) = S
+                const float4 v = wq[q >> 2];
+                const float wu = (q & 3) == 0 ? v.x : ((q & 3) == 1 ? v.y : ((q & 3) == 2 ? v.z : v.w));
                 Smine = lane == q ? S : Smine;
                 S = __fadd_rn(S, wu);
               }
-            } else {
-              for (uint32_t q = 0; q < cnt; ++q) {
-                const float wu = __shfl_sync(0xffffffffu, wp, q);
-                Smine = static_cast<uint32_t>(lane) == q ? S : Smine;
-                S = __fadd_rn(S, wu);
+            } else {  // W = -0 (imported layer): RN(-0 + 0) = +0, so skip the zero terms explicitly
+#pragma unroll
+              for (int q = 0; q < 32; ++q) {
+                const float4 v = wq[q >> 2];
+                const float wu = (q & 3) == 0 ? v.x : ((q & 3) == 1 ? v.y : ((q & 3) == 2 ? v.z : v.w));
+                Smine = lane == q ? S : Smine;
+                S = wu > 0.0f ? __fadd_rn(S, wu) : S;
               }
             }
+            __syncwarp();
             Wmine = fminf(Smine, Wmax);
             W = fminf(S, Wmax);
           }
@@ -1118,11 +1157,35 @@ __global__ void __launch_bounds__(256) k_fold_runs(
           pr.d = u.d;
           pr.ok = ((w > 0.0f) & (w < 0x1p100f) & rt.ok) ? 1u : 0u;
           pr.pad = 0u;
+          // chunk summary (records >= cnt do not constrain it)
+          int lo0 = -1024, lo1 = -1024, lo2 = -1024, hi0 = 1024, hi1 = 1024, hi2 = 1024;
+          const bool in_chunk = static_cast<uint32_t>(lane) < cnt;
+          if (in_chunk && pr.ok && (u.c >> 31)) {
+            const int kr = stationary_radius(w, __fmul_rn(0.499f, pr.T));
+            const int n0 = static_cast<int>(u.c & 0xffu), n1 = static_cast<int>((u.c >> 8) & 0xffu),
+                      n2 = static_cast<int>((u.c >> 16) & 0xffu);
+            lo0 = n0 - kr;
+            hi0 = n0 + kr;
+            lo1 = n1 - kr;
+            hi1 = n1 + kr;
+            lo2 = n2 - kr;
+            hi2 = n2 + kr;
+          }
+          ChunkHdr hd;
+          hd.W_end = W;
+          hd.ok = __all_sync(0xffffffffu, !in_chunk || pr.ok) ? 1u : 0u;
+          hd.lo[0] = __reduce_max_sync(0xffffffffu, lo0);
+          hd.lo[1] = __reduce_max_sync(0xffffffffu, lo1);
+          hd.lo[2] = __reduce_max_sync(0xffffffffu, lo2);
+          hd.hi[0] = __reduce_min_sync(0xffffffffu, hi0);
+          hd.hi[1] = __reduce_min_sync(0xffffffffu, hi1);
+          hd.hi[2] = __reduce_min_sync(0xffffffffu, hi2);
           const int s = static_cast<int>(kk % kRingStages);
           const long long tw0 = dbg != nullptr ? clock64() : 0;
           if (kk >= kRingStages) mbar_wait(&ring_empty[pair][s], ((kk / kRingStages) - 1) & 1u);
           if (dbg != nullptr) pwait += clock64() - tw0;
           ring[pair][s][lane] = pr;
+          if (lane == 0) ring_hdr[pair][s] = hd;
           mbar_arrive(&ring_full[pair][s]);
           ry1 = ry2;
           ry2 = ry3;
@@ -1146,21 +1209,13 @@ __global__ void __launch_bounds__(256) k_fold_runs(
           const long long tc0 = dbg != nullptr ? clock64() : 0;
           const PreRec* rb = ring[pair][s];
           const uint32_t cnt = min(32u, c.len - k * 32);
-          const float Wlast_T = rb[cnt - 1].T, Wlast_w = rb[cnt - 1].w, Wlast_W = rb[cnt - 1].W;
-          const float W_end = Wlast_w > 0.0f ? fminf(Wlast_T, Wmax) : Wlast_W;
-          // colours provably unchanged over the whole chunk? (each lane votes for its record)
-          bool vote = true;
-          if (static_cast<uint32_t>(lane) < cnt) {
-            const PreRec x = rb[lane];
-            vote = x.ok != 0u;
-            if (x.c >> 31) {
-              const float thr = __fmul_rn(0.499f, x.T);
-              vote = vote & colour_stationary(thr, x.w, st.cr, __uint2float_rn(x.c & 0xffu)) &
-                     colour_stationary(thr, x.w, st.cg, __uint2float_rn((x.c >> 8) & 0xffu)) &
-                     colour_stationary(thr, x.w, st.cb, __uint2float_rn((x.c >> 16) & 0xffu));
-            }
-          }
-          const bool stationary = __all_sync(0xffffffffu, vote);
+          const ChunkHdr hd = ring_hdr[pair][s];
+          const float W_end = hd.W_end;
+          // colours provably unchanged over the whole chunk? (intervals from the producer)
+          const int o0 = static_cast<int>(st.cr), o1 = static_cast<int>(st.cg), o2 = static_cast<int>(st.cb);
+          const bool vote = hd.ok != 0u && hd.lo[0] <= o0 && o0 <= hd.hi[0] && hd.lo[1] <= o1 && o1 <= hd.hi[1] &&
+                            hd.lo[2] <= o2 && o2 <= hd.hi[2];
+          const bool stationary = vote;  // warp-uniform
           const long long tc1 = dbg != nullptr ? clock64() : 0;
           bool done = false;
           if (stationary) {  // distance chain only: FMUL, FADD, 3-FMA quotient per step
@@ -1169,9 +1224,14 @@ __global__ void __launch_bounds__(256) k_fold_runs(
             const float4* rq = reinterpret_cast<const float4*>(rb);
             constexpr int kStride = sizeof(PreRec) / sizeof(float4);
             if (cnt == 32) {
+              constexpr int kAhead = 6;  // (W, T, r1, wc) loaded kAhead steps before use
+              float4 buf[kAhead];
+#pragma unroll
+              for (int u = 0; u < kAhead; ++u) buf[u] = rq[u * kStride];
 #pragma unroll
               for (int u = 0; u < 32; ++u) {
-                const float4 x = rq[u * kStride];  // (W, T, r1, wc)
+                const float4 x = buf[u % kAhead];
+                if (u + kAhead < 32) buf[u % kAhead] = rq[(u + kAhead) * kStride];
                 const float a = __fadd_rn(__fmul_rn(x.x, D), x.w);
                 qr_add(qr, a);
                 D = fast_quot0(a, Recip{x.y, x.z, true});
@@ -1268,7 +1328,7 @@ __global__ void __launch_bounds__(256) k_fold_runs(
 // Short runs (< kLongRun records): one thread per run, launched on a second
 // stream next to k_fold_runs (disjoint voxels), with its own register budget
 // so more warps hide the ray-id -> ray gather latency.
-template <int kMinBlocks, int kC>
+template <int kMinBlocks, int kC, bool kSmemOrg>
 __global__ void __launch_bounds__(256, kMinBlocks) k_fold_short(
     const uint32_t* __restrict__ num_runs_p, const uint32_t* __restrict__ order,
     const uint32_t* __restrict__ sorted_len, const uint32_t* __restrict__ ukeys, const uint32_t* __restrict__ ustart,
@@ -1276,7 +1336,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_fold_short(
     const float* __restrict__ g_org, uint32_t F, MapView map, TsdfParams tp, uint8_t* __restrict__ touched,
     uint32_t* __restrict__ work) {
   __shared__ float s_org[3 * kOrgCache];
-  const float* poses = stage_origins(s_org, g_org, F);
+  const float* poses = stage_origins<kSmemOrg>(s_org, g_org, F);
   if (map.counters[1] != 0u) return;
   const uint32_t nruns = *num_runs_p;
   const int lane = threadIdx.x & 31;
@@ -1294,16 +1354,35 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_fold_short(
     if (c.key == kInvalidRecord) continue;
     vxg_voxel* vp = map.slab + c.key;
     VoxState st = load_vox(vp);
+    // software pipeline over chunks of kC records: rays gathered two chunks
+    // ahead, weighed one chunk ahead of their fold steps
+    const uint32_t* ids = svals + c.start;
+    FoldRay rn[kC];
+    Upd xn[kC], xs[kC];
+#pragma unroll
+    for (int u = 0; u < kC; ++u) {
+      if (u < c.len) rn[u] = rays[ids[u]];
+    }
+#pragma unroll
+    for (int u = 0; u < kC; ++u) {
+      xn[u].w = 0.0f;
+      if (u < c.len) xn[u] = weigh(rn[u], poses, c.x0, c.x1, c.x2, tp);
+    }
+#pragma unroll
+    for (int u = 0; u < kC; ++u) {
+      if (kC + u < c.len) rn[u] = rays[ids[kC + u]];
+    }
     for (uint32_t j = 0; j < c.len; j += kC) {
-      Upd xs[kC];
-      FoldRay ry[kC];
+#pragma unroll
+      for (int u = 0; u < kC; ++u) xs[u] = xn[u];
+      // weigh chunk j+kC (gathered last iteration), gather chunk j+2kC
 #pragma unroll
       for (int u = 0; u < kC; ++u) {
-        if (j + u < c.len) ry[u] = rays[svals[c.start + j + u]];
+        if (j + kC + u < c.len) xn[u] = weigh(rn[u], poses, c.x0, c.x1, c.x2, tp);
       }
 #pragma unroll
       for (int u = 0; u < kC; ++u) {
-        if (j + u < c.len) xs[u] = weigh(ry[u], poses, c.x0, c.x1, c.x2, tp);
+        if (j + 2 * kC + u < c.len) rn[u] = rays[ids[j + 2 * kC + u]];
       }
       const VoxState s0 = st;
       bool ok = true;

@@ -779,26 +779,50 @@ void vxg_handle::sort_fold(uint64_t T, uint64_t nslots, uint32_t F) {
     ++launches;
     CU(cudaEventRecord(fold_fork, st));
     CU(cudaStreamWaitEvent(fold_st, fold_fork, 0));
-    k_fold_runs<<<long_grid, 256, 0, st>>>(num_runs.p, run_order.p, run_len2.p, run_keys.p, run_start.p, run_len.p,
-                                            svals, fold_rays.p, d_org.p, F, view(), tp, tch, work.p, dbg);
+    static const int long_layout = [] {
+      const char* e = getenv("VXG_LONG_LAYOUT");
+      return e ? atoi(e) : 0;
+    }();
+    static const int long_smem = [] {
+      const char* e = getenv("VXG_LONG_SMEM");
+      return e ? atoi(e) : 0;
+    }();
+    static const int long_ctas = [] {
+      const char* e = getenv("VXG_LONG_CTAS");
+      return e ? atoi(e) : 0;
+    }();
+    const unsigned lg = long_ctas > 0 ? static_cast<unsigned>(long_ctas) : long_grid;
+    const bool smem_org = F <= kOrgCache;
+#define VXG_FOLD_LONG(P, SEP, THREADS)                                                                              \
+  do {                                                                                                           \
+    auto kern = smem_org ? k_fold_runs<P, SEP, true> : k_fold_runs<P, SEP, false>;                              \
+    if (long_smem) CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, long_smem));      \
+    kern<<<lg, THREADS, long_smem, st>>>(num_runs.p, run_order.p, run_len2.p, run_keys.p, run_start.p, run_len.p, \
+                                         svals, fold_rays.p, d_org.p, F, view(), tp, tch, work.p, dbg);           \
+  } while (0)
+    if (long_layout == 2)
+      VXG_FOLD_LONG(2, true, 128);
+    else
+      VXG_FOLD_LONG(4, false, 256);
+#undef VXG_FOLD_LONG
     static const int short_blocks = [] {
       const char* e = getenv("VXG_FOLD_SHORT_BLOCKS");
-      return e ? atoi(e) : 3;
+      return e ? atoi(e) : 5;
     }();
     static const bool serial = getenv("VXG_FOLD_SERIAL") != nullptr;  // dev: long runs uncontended
     cudaStream_t sst = serial ? st : fold_st;
     const unsigned short_grid = static_cast<unsigned>(std::max<uint64_t>(
         1, std::min<uint64_t>(static_cast<uint64_t>(dev_sms) * 4, (nruns + 255) / 256)));
 #define VXG_FOLD_SHORT(MB, C)                                                                                 \
-  k_fold_short<MB, C><<<short_grid, 256, 0, sst>>>(num_runs.p, run_order.p, run_len2.p, run_keys.p, run_start.p, \
-                                                       run_len.p, svals, fold_rays.p, d_org.p, F, view(), tp, tch, \
-                                                       work.p)
-    switch (short_blocks) {
-      case 2: VXG_FOLD_SHORT(2, 8); break;
-      case 4: VXG_FOLD_SHORT(4, 4); break;
-      case 5: VXG_FOLD_SHORT(3, 8); break;
-      default: VXG_FOLD_SHORT(3, 4); break;
-    }
+  do {                                                                                                        \
+    auto kern = smem_org ? k_fold_short<MB, C, true> : k_fold_short<MB, C, false>;                           \
+    kern<<<short_grid, 256, 0, sst>>>(num_runs.p, run_order.p, run_len2.p, run_keys.p, run_start.p, run_len.p, \
+                                      svals, fold_rays.p, d_org.p, F, view(), tp, tch, work.p);                \
+  } while (0)
+    if (short_blocks == 1)
+      VXG_FOLD_SHORT(3, 4);
+    else
+      VXG_FOLD_SHORT(2, 4);
 #undef VXG_FOLD_SHORT
     CU(cudaEventRecord(fold_join, fold_st));
     CU(cudaStreamWaitEvent(st, fold_join, 0));
