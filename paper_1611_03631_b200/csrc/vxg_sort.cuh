@@ -20,37 +20,41 @@ namespace vxg {
 
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kSortIpt = 24;
-constexpr int kSortSub = kSortThreads * kSortIpt;           // records per sub-tile
-constexpr int kSortNsub = 8;                                // sub-tiles per super-tile (one CTA)
-constexpr uint32_t kSortSuper = static_cast<uint32_t>(kSortSub) * kSortNsub;
-constexpr int kSortMaxBits = 11;
-constexpr int kSortMaxBins = 1 << kSortMaxBits;
-constexpr int kSortWcStride = kSortMaxBins + 2;             // + overflow bin for the tail, even
-constexpr int kSortScanPer = (kSortMaxBins + 1 + kSortThreads - 1) / kSortThreads;
 
-struct SortSmem {
-  uint16_t wcnt[kSortWarps][kSortWcStride];  // per-warp digit counts, then cross-warp prefixes
-  uint32_t tcount[kSortMaxBins + 1];         // sub-tile digit counts
-  uint32_t tstart[kSortMaxBins + 1];         // sub-tile digit starts (exclusive scan of tcount)
-  uint32_t gbase[kSortMaxBins];              // global output position of the digit's next record
-  uint32_t wsum[kSortWarps];
-  uint32_t stage_k[kSortSub];
-  uint32_t stage_v[kSortSub];
+// kBits: largest digit of a pass; kIpt: records per thread per sub-tile.
+template <int kBits, int kIpt>
+struct SortCfg {
+  static constexpr int kBins = 1 << kBits;
+  static constexpr int kSub = kSortThreads * kIpt;                  // records per sub-tile
+  static constexpr int kNsub = 8;                                   // sub-tiles per super-tile (one CTA)
+  static constexpr uint32_t kSuper = static_cast<uint32_t>(kSub) * kNsub;
+  static constexpr int kWcStride = kBins + 2;                       // + overflow bin for the tail, even
+  static constexpr int kScanPer = (kBins + 1 + kSortThreads - 1) / kSortThreads;
+  struct Smem {
+    uint16_t wcnt[kSortWarps][kWcStride];  // per-warp digit counts, then cross-warp prefixes
+    uint32_t tcount[kBins + 1];            // sub-tile digit counts
+    uint32_t tstart[kBins + 1];            // sub-tile digit starts (exclusive scan of tcount)
+    uint32_t gbase[kBins];                 // global output position of the digit's next record
+    uint32_t wsum[kSortWarps];
+    uint32_t stage_k[kSub];
+    uint32_t stage_v[kSub];
+  };
 };
 
+template <int kBits, int kIpt>
 __global__ void __launch_bounds__(kSortThreads) k_sort_upsweep(const uint32_t* __restrict__ keys, uint64_t n,
                                                                int shift, uint32_t mask, uint32_t S,
                                                                uint32_t* __restrict__ counts) {
-  __shared__ uint32_t h[kSortMaxBins];
+  using C = SortCfg<kBits, kIpt>;
+  __shared__ uint32_t h[C::kBins];
   const uint32_t bins = mask + 1u;
   for (uint32_t d = threadIdx.x; d < bins; d += kSortThreads) h[d] = 0u;
   __syncthreads();
-  const uint64_t lo = static_cast<uint64_t>(blockIdx.x) * kSortSuper;
-  const uint32_t cnt = static_cast<uint32_t>(min(static_cast<uint64_t>(kSortSuper), n - lo));
+  const uint64_t lo = static_cast<uint64_t>(blockIdx.x) * C::kSuper;
+  const uint32_t cnt = static_cast<uint32_t>(min(static_cast<uint64_t>(C::kSuper), n - lo));
   const uint4* k4 = reinterpret_cast<const uint4*>(keys + lo);  // lo % 4 == 0, buffers 256-B aligned
   const uint32_t n4 = cnt / 4u;
-  for (uint32_t i = threadIdx.x; i < n4; i += kSortThreads) {  // spread-address ATOMS (MATCH.ANY is slower)
+  for (uint32_t i = threadIdx.x; i < n4; i += kSortThreads) {  // shared-memory atomics (MATCH.ANY is slower)
     const uint4 k = k4[i];
     atomicAdd(&h[(k.x >> shift) & mask], 1u);
     atomicAdd(&h[(k.y >> shift) & mask], 1u);
@@ -62,52 +66,57 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_upsweep(const uint32_t* _
   for (uint32_t d = threadIdx.x; d < bins; d += kSortThreads) counts[static_cast<uint64_t>(d) * S + blockIdx.x] = h[d];
 }
 
-// Lanes of the warp holding the same digit d (< 2^12): one ballot per bit
-// (MATCH.ANY is several times slower on sm_100).
+// Lanes of the warp holding the same digit d (< 2^(kB+1)): one ballot per bit.
+template <int kB>
 __device__ __forceinline__ uint32_t digit_peers(uint32_t d) {
   uint32_t peers = 0xffffffffu;
 #pragma unroll
-  for (int b = 0; b <= kSortMaxBits; ++b) {
+  for (int b = 0; b <= kB; ++b) {
     const uint32_t v = __ballot_sync(0xffffffffu, (d >> b) & 1u);
     peers &= ((d >> b) & 1u) ? v : ~v;
   }
   return peers;
 }
 
-template <bool kBallot>
-__global__ void __launch_bounds__(kSortThreads, 2)
+template <int kBits, int kIpt, int kMinBlocks, bool kPrefetch = false>
+__global__ void __launch_bounds__(kSortThreads, kMinBlocks)
     k_sort_downsweep(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
                      uint32_t* __restrict__ vout, uint64_t n, int shift, uint32_t mask, uint32_t S,
                      const uint32_t* __restrict__ offs) {
+  using C = SortCfg<kBits, kIpt>;
   extern __shared__ __align__(16) uint8_t sort_smem_raw[];
-  SortSmem& sm = *reinterpret_cast<SortSmem*>(sort_smem_raw);
+  typename C::Smem& sm = *reinterpret_cast<typename C::Smem*>(sort_smem_raw);
   const uint32_t bins = mask + 1u;
   const int tid = threadIdx.x, w = tid >> 5;
   const uint32_t lane = tid & 31u, lt = (1u << lane) - 1u;
   for (uint32_t d = tid; d < bins; d += kSortThreads) sm.gbase[d] = offs[static_cast<uint64_t>(d) * S + blockIdx.x];
-  const uint64_t super0 = static_cast<uint64_t>(blockIdx.x) * kSortSuper;
+  const uint64_t super0 = static_cast<uint64_t>(blockIdx.x) * C::kSuper;
   uint32_t* wc32 = reinterpret_cast<uint32_t*>(&sm.wcnt[0][0]);
-  for (int t = 0; t < kSortNsub; ++t) {
-    const uint64_t base = super0 + static_cast<uint64_t>(t) * kSortSub;
-    if (base >= n) break;  // CTA-uniform
-    const uint32_t nv = static_cast<uint32_t>(min(static_cast<uint64_t>(kSortSub), n - base));
-    for (int i = tid; i < kSortWarps * kSortWcStride / 2; i += kSortThreads) wc32[i] = 0u;
-    // load: warp w owns sub-tile items [w*IPT*32, (w+1)*IPT*32), item (j, lane) = j*32 + lane
-    uint32_t key[kSortIpt], val[kSortIpt];
-    const uint32_t i0 = static_cast<uint32_t>(w) * (kSortIpt * 32) + lane;
+  // warp w owns sub-tile items [w*IPT*32, (w+1)*IPT*32), item (j, lane) = j*32 + lane
+  const uint32_t i0 = static_cast<uint32_t>(w) * (kIpt * 32) + lane;
+  uint32_t key[kIpt], val[kIpt];
+  auto load_sub = [&](uint64_t b, uint32_t nvv) {
 #pragma unroll
-    for (int j = 0; j < kSortIpt; ++j) {
+    for (int j = 0; j < kIpt; ++j) {
       const uint32_t i = i0 + j * 32;
-      key[j] = i < nv ? kin[base + i] : 0u;
-      val[j] = i < nv ? vin[base + i] : 0u;
+      key[j] = i < nvv ? kin[b + i] : 0u;
+      if (kPrefetch) val[j] = i < nvv ? vin[b + i] : 0u;
     }
+  };
+  if (kPrefetch && super0 < n) load_sub(super0, static_cast<uint32_t>(min(static_cast<uint64_t>(C::kSub), n - super0)));
+  for (int t = 0; t < C::kNsub; ++t) {
+    const uint64_t base = super0 + static_cast<uint64_t>(t) * C::kSub;
+    if (base >= n) break;  // CTA-uniform
+    const uint32_t nv = static_cast<uint32_t>(min(static_cast<uint64_t>(C::kSub), n - base));
+    for (int i = tid; i < kSortWarps * C::kWcStride / 2; i += kSortThreads) wc32[i] = 0u;
+    if (!kPrefetch) load_sub(base, nv);
     __syncthreads();  // wcnt zeroed; previous sub-tile's gbase update visible
     // stable warp-private ranking: (j, lane) order == item order
-    uint32_t rk[kSortIpt];
+    uint32_t rk[kIpt];
 #pragma unroll
-    for (int j = 0; j < kSortIpt; ++j) {
+    for (int j = 0; j < kIpt; ++j) {
       const uint32_t d = i0 + j * 32 < nv ? (key[j] >> shift) & mask : bins;
-      const uint32_t peers = kBallot ? digit_peers(d) : __match_any_sync(0xffffffffu, d);
+      const uint32_t peers = digit_peers<kBits>(d);
       const uint32_t pre = sm.wcnt[w][d];
       __syncwarp();
       if ((peers & lt) == 0u) sm.wcnt[w][d] = static_cast<uint16_t>(pre + __popc(peers));
@@ -129,10 +138,10 @@ __global__ void __launch_bounds__(kSortThreads, 2)
     __syncthreads();
     {  // exclusive scan tcount[0..bins] -> tstart
       const uint32_t nb = bins + 1u;
-      uint32_t loc[kSortScanPer], sum = 0;
+      uint32_t loc[C::kScanPer], sum = 0;
 #pragma unroll
-      for (int q = 0; q < kSortScanPer; ++q) {
-        const uint32_t idx = static_cast<uint32_t>(tid) * kSortScanPer + q;
+      for (int q = 0; q < C::kScanPer; ++q) {
+        const uint32_t idx = static_cast<uint32_t>(tid) * C::kScanPer + q;
         loc[q] = idx < nb ? sm.tcount[idx] : 0u;
         sum += loc[q];
       }
@@ -147,21 +156,26 @@ __global__ void __launch_bounds__(kSortThreads, 2)
       uint32_t run = x - sum;
       for (int q = 0; q < w; ++q) run += sm.wsum[q];
 #pragma unroll
-      for (int q = 0; q < kSortScanPer; ++q) {
-        const uint32_t idx = static_cast<uint32_t>(tid) * kSortScanPer + q;
+      for (int q = 0; q < C::kScanPer; ++q) {
+        const uint32_t idx = static_cast<uint32_t>(tid) * C::kScanPer + q;
         if (idx < nb) sm.tstart[idx] = run;
         run += loc[q];
       }
     }
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < kSortIpt; ++j) {
-      if (i0 + j * 32 < nv) {
+    for (int j = 0; j < kIpt; ++j) {
+      const uint32_t i = i0 + j * 32;
+      if (i < nv) {
         const uint32_t d = (key[j] >> shift) & mask;
         const uint32_t p = sm.tstart[d] + sm.wcnt[w][d] + rk[j];
         sm.stage_k[p] = key[j];
-        sm.stage_v[p] = val[j];
+        sm.stage_v[p] = kPrefetch ? val[j] : vin[base + i];
       }
+    }
+    if (kPrefetch) {  // next sub-tile's loads overlap this one's scatter
+      const uint64_t nb = base + C::kSub;
+      if (t + 1 < C::kNsub && nb < n) load_sub(nb, static_cast<uint32_t>(min(static_cast<uint64_t>(C::kSub), n - nb)));
     }
     __syncthreads();
     for (uint32_t i = tid; i < nv; i += kSortThreads) {

@@ -395,6 +395,8 @@ struct vxg_handle {
   uint64_t count_rays(uint32_t R, uint32_t F);
   void sort_fold(uint64_t T, uint64_t nslots, uint32_t F);
   void sort_records(uint64_t T, int kbits, uint32_t** sk, uint32_t** sv);
+  template <int kBits, int kIpt, int kMB>
+  void lsd_sort(uint64_t T, int kbits, uint32_t** sk, uint32_t** sv);
   uint64_t last_blocks = 0;  // blocks allocated after the last produce attempt
   bool grew_after_attempt(int attempt);
   void begin_batch(const float* xyz, const uint8_t* rgb, const uint64_t* offsets, const float* poses, uint64_t F,
@@ -639,20 +641,48 @@ uint64_t vxg_handle::count_rays(uint32_t R, uint32_t F) {
   return tail[0] + tail[1];
 }
 
-// Stable sort of T records (rkeys = u32 voxel key, rvals = ray index) by voxel
-// key, runs (one per voxel) longest first, then the ordered fold.
-// Stable sort of the T records by voxel key (vxg_sort.cuh); returns the
-// buffers holding the sorted keys / ray ids.
-void vxg_handle::sort_records(uint64_t T, int kbits, uint32_t** sk, uint32_t** sv) {
+// Stable LSD radix sort of the T records by voxel key (vxg_sort.cuh): digits
+// of up to kBits bits (3 passes for the <= 21-bit keys of a 512-block layer
+// of 16^3 voxels); returns the buffers holding the sorted keys / ray ids.
+template <int kBits, int kIpt, int kMB>
+void vxg_handle::lsd_sort(uint64_t T, int kbits, uint32_t** sk, uint32_t** sv) {
+  using C = SortCfg<kBits, kIpt>;
   static bool attr = false;
   if (!attr) {
-    CU(cudaFuncSetAttribute(k_sort_downsweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(sizeof(SortSmem))));
+    CU(cudaFuncSetAttribute(k_sort_downsweep<kBits, kIpt, kMB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(sizeof(typename C::Smem))));
     attr = true;
   }
-  static const bool use_cub = [] {
+  const int passes = std::max(1, (kbits + kBits - 1) / kBits);
+  const uint32_t S = static_cast<uint32_t>((T + C::kSuper - 1) / C::kSuper);
+  uint32_t *ki = rkeys.p, *vi = rvals.p, *ko = rkeys2.p, *vo = rvals2.p;
+  int shift = 0;
+  for (int p = 0; p < passes; ++p) {
+    const int bits = (kbits - shift + (passes - p) - 1) / (passes - p);
+    const uint32_t mask = bits ? (1u << bits) - 1u : 0u;
+    const uint64_t nc = static_cast<uint64_t>(mask + 1u) * S;
+    sort_counts.ensure(nc);
+    sort_offs.ensure(nc);
+    k_sort_upsweep<kBits, kIpt><<<S, kSortThreads, 0, st>>>(ki, T, shift, mask, S, sort_counts.p);
+    cub([&](void* t, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, sort_counts.p, sort_offs.p, static_cast<int>(nc), st);
+    }, 2);
+    k_sort_downsweep<kBits, kIpt, kMB, true><<<S, kSortThreads, sizeof(typename C::Smem), st>>>(
+        ki, vi, ko, vo, T, shift, mask, S, sort_offs.p);
+    launches += 2;
+    CU(cudaGetLastError());
+    std::swap(ki, ko);
+    std::swap(vi, vo);
+    shift += bits;
+  }
+  *sk = ki;
+  *sv = vi;
+}
+
+void vxg_handle::sort_records(uint64_t T, int kbits, uint32_t** sk, uint32_t** sv) {
+  static const bool use_cub = [] {  // dev A/B: VXG_SORT=cub
     const char* e = getenv("VXG_SORT");
-    return !(e && std::string(e) == "lsd11");
+    return e && std::string(e) == "cub";
   }();
   if (use_cub) {
     const int nb = std::max(kbits, 1);
@@ -664,30 +694,10 @@ void vxg_handle::sort_records(uint64_t T, int kbits, uint32_t** sk, uint32_t** s
     *sv = rvals2.p;
     return;
   }
-  const int passes = std::max(1, (kbits + kSortMaxBits - 1) / kSortMaxBits);
-  const uint32_t S = static_cast<uint32_t>((T + kSortSuper - 1) / kSortSuper);
-  uint32_t *ki = rkeys.p, *vi = rvals.p, *ko = rkeys2.p, *vo = rvals2.p;
-  int shift = 0;
-  for (int p = 0; p < passes; ++p) {
-    const int bits = (kbits - shift + (passes - p) - 1) / (passes - p);
-    const uint32_t mask = bits ? (bits >= 32 ? 0xFFFFFFFFu : (1u << bits) - 1u) : 0u;
-    const uint64_t nc = static_cast<uint64_t>(mask + 1u) * S;
-    sort_counts.ensure(nc);
-    sort_offs.ensure(nc);
-    k_sort_upsweep<<<S, kSortThreads, 0, st>>>(ki, T, shift, mask, S, sort_counts.p);
-    ++launches;
-    cub([&](void* t, size_t& b) {
-      return cub::DeviceScan::ExclusiveSum(t, b, sort_counts.p, sort_offs.p, static_cast<int>(nc), st);
-    }, 2);
-    k_sort_downsweep<true><<<S, kSortThreads, sizeof(SortSmem), st>>>(ki, vi, ko, vo, T, shift, mask, S, sort_offs.p);
-    ++launches;
-    CU(cudaGetLastError());
-    std::swap(ki, ko);
-    std::swap(vi, vo);
-    shift += bits;
-  }
-  *sk = ki;
-  *sv = vi;
+  if (kbits <= 21)
+    lsd_sort<7, 12, 4>(T, kbits, sk, sv);
+  else
+    lsd_sort<8, 12, 4>(T, kbits, sk, sv);
 }
 
 // Sorts the T records of one attempt (keys < nslots * vps^3, or invalid) and

@@ -11,27 +11,56 @@ using namespace vxg;
 
 #define CK(x) do { cudaError_t err_ = (x); if (err_ != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(err_)); exit(1); } } while (0)
 
-// upsweep variant: plain per-CTA smem atomics, no match
-__global__ void __launch_bounds__(256) up_atom(const uint32_t* __restrict__ keys, uint64_t n, int shift, uint32_t mask,
-                                               uint32_t S, uint32_t* __restrict__ counts) {
-  __shared__ uint32_t h[kSortMaxBins];
-  const uint32_t bins = mask + 1u;
-  for (uint32_t d = threadIdx.x; d < bins; d += 256) h[d] = 0u;
-  __syncthreads();
-  const uint64_t lo = static_cast<uint64_t>(blockIdx.x) * kSortSuper;
-  const uint32_t cnt = static_cast<uint32_t>(min(static_cast<uint64_t>(kSortSuper), n - lo));
-  const uint4* k4 = reinterpret_cast<const uint4*>(keys + lo);
-  const uint32_t n4 = cnt / 4u;
-  for (uint32_t i = threadIdx.x; i < n4; i += 256) {
-    const uint4 k = k4[i];
-    atomicAdd(&h[(k.x >> shift) & mask], 1u);
-    atomicAdd(&h[(k.y >> shift) & mask], 1u);
-    atomicAdd(&h[(k.z >> shift) & mask], 1u);
-    atomicAdd(&h[(k.w >> shift) & mask], 1u);
+template <int kBits, int kIpt, int kMB, bool kPF = false>
+void run_lsd(const char* name, uint64_t T, int kbits, uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
+             uint32_t* k2, uint32_t* v2, void* tmp, const std::vector<uint32_t>& ck, const std::vector<uint32_t>& cv) {
+  using C = SortCfg<kBits, kIpt>;
+  const int passes = std::max(1, (kbits + kBits - 1) / kBits);
+  const uint32_t S = static_cast<uint32_t>((T + C::kSuper - 1) / C::kSuper);
+  uint32_t *counts, *offs;
+  CK(cudaMalloc(&counts, (size_t)C::kBins * S * 4)); CK(cudaMalloc(&offs, (size_t)C::kBins * S * 4));
+  CK(cudaFuncSetAttribute(k_sort_downsweep<kBits, kIpt, kMB, kPF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)sizeof(typename C::Smem)));
+  size_t stb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, stb, counts, offs, C::kBins * (int)S);
+  float t_up = 0, t_scan = 0, t_down = 0;
+  cudaEvent_t e[4];
+  for (auto& x : e) cudaEventCreate(&x);
+  std::vector<uint32_t> tk(T), tv(T);
+  for (int rep = 0; rep < 4; ++rep) {
+    uint32_t *ki = k0, *vi = v0, *ko = k1, *vo = v1;
+    int shift = 0;
+    for (int p = 0; p < passes; ++p) {
+      const int bits = (kbits - shift + (passes - p) - 1) / (passes - p);
+      const uint32_t mask = (1u << bits) - 1u;
+      const int nc = (int)((mask + 1u) * S);
+      cudaEventRecord(e[0]);
+      k_sort_upsweep<kBits, kIpt><<<S, 256>>>(ki, T, shift, mask, S, counts);
+      cudaEventRecord(e[1]);
+      cub::DeviceScan::ExclusiveSum(tmp, stb, counts, offs, nc);
+      cudaEventRecord(e[2]);
+      k_sort_downsweep<kBits, kIpt, kMB, kPF><<<S, 256, sizeof(typename C::Smem)>>>(ki, vi, ko, vo, T, shift, mask, S, offs);
+      cudaEventRecord(e[3]);
+      CK(cudaEventSynchronize(e[3]));
+      float x;
+      if (rep) {
+        cudaEventElapsedTime(&x, e[0], e[1]); t_up += x;
+        cudaEventElapsedTime(&x, e[1], e[2]); t_scan += x;
+        cudaEventElapsedTime(&x, e[2], e[3]); t_down += x;
+      }
+      ki = ko; vi = vo; ko = (ko == k1) ? k2 : k1; vo = (vo == v1) ? v2 : v1;
+      shift += bits;
+    }
+    if (rep == 3) {
+      CK(cudaMemcpy(tk.data(), ki, T * 4, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(tv.data(), vi, T * 4, cudaMemcpyDeviceToHost));
+    }
   }
-  for (uint32_t i = 4u * n4 + threadIdx.x; i < cnt; i += 256) atomicAdd(&h[(keys[lo + i] >> shift) & mask], 1u);
-  __syncthreads();
-  for (uint32_t d = threadIdx.x; d < bins; d += 256) counts[static_cast<uint64_t>(d) * S + blockIdx.x] = h[d];
+  CK(cudaGetLastError());
+  const bool ok = tk == ck && tv == cv;
+  printf("%-14s: up %.3f scan %.3f down %.3f total %.3f ms (%d passes, smem %zu B) %s\n", name, t_up / 3, t_scan / 3,
+         t_down / 3, (t_up + t_scan + t_down) / 3, passes, sizeof(typename C::Smem), ok ? "OK" : "MISMATCH");
+  cudaFree(counts); cudaFree(offs);
 }
 
 int main(int argc, char** argv) {
@@ -67,53 +96,11 @@ int main(int argc, char** argv) {
   CK(cudaMemcpy(ck.data(), rk, T * 4, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(cv.data(), rv, T * 4, cudaMemcpyDeviceToHost));
 
-  const int passes = std::max(1, (kbits + kSortMaxBits - 1) / kSortMaxBits);
-  const uint32_t S = static_cast<uint32_t>((T + kSortSuper - 1) / kSortSuper);
-  uint32_t *counts, *offs;
-  CK(cudaMalloc(&counts, (size_t)kSortMaxBins * S * 4)); CK(cudaMalloc(&offs, (size_t)kSortMaxBins * S * 4));
-  CK(cudaFuncSetAttribute(k_sort_downsweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SortSmem)));
-  CK(cudaFuncSetAttribute(k_sort_downsweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SortSmem)));
-  size_t stb = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, stb, counts, offs, kSortMaxBins * (int)S);
-  for (int variant = 0; variant < 2; ++variant) {
-    float t_up = 0, t_scan = 0, t_down = 0;
-    cudaEvent_t e[4];
-    for (auto& x : e) cudaEventCreate(&x);
-    for (int rep = 0; rep < 4; ++rep) {
-      uint32_t *ki = k0, *vi = v0, *ko = k1, *vo = v1;
-      int shift = 0;
-      for (int p = 0; p < passes; ++p) {
-        const int bits = (kbits - shift + (passes - p) - 1) / (passes - p);
-        const uint32_t mask = (1u << bits) - 1u;
-        const int nc = (int)((mask + 1u) * S);
-        cudaEventRecord(e[0]);
-        if (variant == 0) k_sort_upsweep<<<S, 256>>>(ki, T, shift, mask, S, counts);
-        else up_atom<<<S, 256>>>(ki, T, shift, mask, S, counts);
-        cudaEventRecord(e[1]);
-        cub::DeviceScan::ExclusiveSum(tmp, stb, counts, offs, nc);
-        cudaEventRecord(e[2]);
-        if (variant == 0) k_sort_downsweep<false><<<S, 256, sizeof(SortSmem)>>>(ki, vi, ko, vo, T, shift, mask, S, offs);
-        else k_sort_downsweep<true><<<S, 256, sizeof(SortSmem)>>>(ki, vi, ko, vo, T, shift, mask, S, offs);
-        cudaEventRecord(e[3]);
-        CK(cudaEventSynchronize(e[3]));
-        float x;
-        if (rep) {
-          cudaEventElapsedTime(&x, e[0], e[1]); t_up += x;
-          cudaEventElapsedTime(&x, e[1], e[2]); t_scan += x;
-          cudaEventElapsedTime(&x, e[2], e[3]); t_down += x;
-        }
-        ki = ko; vi = vo; ko = (ko == k1) ? k2 : k1; vo = (vo == v1) ? v2 : v1;
-        shift += bits;
-      }
-      if (rep == 3) {
-        CK(cudaMemcpy(tk.data(), ki, T * 4, cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(tv.data(), vi, T * 4, cudaMemcpyDeviceToHost));
-      }
-    }
-    CK(cudaGetLastError());
-    const bool ok = tk == ck && tv == cv;
-    printf("lsd11 v%d: up %.3f scan %.3f down %.3f total %.3f ms (%d passes) %s\n", variant, t_up / 3, t_scan / 3,
-           t_down / 3, (t_up + t_scan + t_down) / 3, passes, ok ? "OK" : "MISMATCH");
-  }
+  run_lsd<7, 16, 4>("b7 ipt16 mb4", T, kbits, k0, v0, k1, v1, k2, v2, tmp, ck, cv);
+  run_lsd<7, 16, 3, true>("b7 i16 mb3 pf", T, kbits, k0, v0, k1, v1, k2, v2, tmp, ck, cv);
+  run_lsd<7, 12, 4, true>("b7 i12 mb4 pf", T, kbits, k0, v0, k1, v1, k2, v2, tmp, ck, cv);
+  run_lsd<7, 8, 4, true>("b7 i8 mb4 pf", T, kbits, k0, v0, k1, v1, k2, v2, tmp, ck, cv);
+  run_lsd<7, 16, 2, true>("b7 i16 mb2 pf", T, kbits, k0, v0, k1, v1, k2, v2, tmp, ck, cv);
+  run_lsd<7, 32, 2, true>("b7 i32 mb2 pf", T, kbits, k0, v0, k1, v1, k2, v2, tmp, ck, cv);
   return 0;
 }
