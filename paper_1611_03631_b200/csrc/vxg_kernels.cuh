@@ -164,10 +164,38 @@ __global__ void k_widen_keys(const uint32_t* __restrict__ num_p, const uint32_t*
 // (independent loads and weights ahead of the dependent fp64 sums).
 constexpr int kSegChunk = 8;
 
+// Per-point terms of the bucket sums, computed in sorted order by a fully
+// parallel pass (one gather per point) so the per-bucket sequential fp64 sums
+// stream contiguous memory: world point p = T_f * x and its weight 1/|p - o|^2.
+template <typename KeyT>
+__global__ void k_point_prep(uint64_t P, const KeyT* __restrict__ skeys, const uint32_t* __restrict__ svals,
+                             const float* __restrict__ xyz, const uint8_t* __restrict__ rgb,
+                             const float* __restrict__ poses, TsdfParams tp, int kb, float4* __restrict__ pw,
+                             uint32_t* __restrict__ cc) {
+  const uint64_t field_mask = (1ull << (3 * kb)) - 1ull;
+  for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < P;
+       j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t key = static_cast<uint64_t>(skeys[j]);
+    if ((key & field_mask) == field_mask) continue;  // out-of-range point: its bucket is skipped
+    const uint32_t f = static_cast<uint32_t>(key >> (3 * kb));
+    const uint32_t i = svals[j];
+    const float* Pm = poses + 12 * f;
+    float pp[3];
+    transform_point(Pm, xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], pp);
+    const float depth = norm3(fsub(pp[0], Pm[3]), fsub(pp[1], Pm[7]), fsub(pp[2], Pm[11]));
+    const float ww = tp.weight_mode == VXG_WEIGHT_CONSTANT ? 1.0f : fdiv(1.0f, fmul(depth, depth));
+    pw[j] = make_float4(pp[0], pp[1], pp[2], ww);
+    if (rgb != nullptr)
+      cc[j] = static_cast<uint32_t>(rgb[3 * i]) | (static_cast<uint32_t>(rgb[3 * i + 1]) << 8) |
+              (static_cast<uint32_t>(rgb[3 * i + 2]) << 16);
+  }
+}
+
 __global__ void k_seg_reduce(const uint32_t* __restrict__ num_segs_p, const unsigned long long* __restrict__ ukeys,
                              const uint32_t* __restrict__ uoffs, const uint32_t* __restrict__ ucounts,
-                             const uint32_t* __restrict__ svals, const float* __restrict__ xyz,
-                             const uint8_t* __restrict__ rgb, const uint64_t* __restrict__ off,
+                             const uint32_t* __restrict__ svals, const float4* __restrict__ pw,
+                             const uint32_t* __restrict__ cc, const uint8_t* __restrict__ rgb,
+                             const uint64_t* __restrict__ off,
                              const float* __restrict__ poses, TsdfParams tp, int rb, int kb,
                              SegInfo* __restrict__ segs, uint32_t* __restrict__ seg_count,
                              uint32_t* __restrict__ seg_start, unsigned long long* __restrict__ skipped) {
@@ -201,38 +229,18 @@ __global__ void k_seg_reduce(const uint32_t* __restrict__ num_segs_p, const unsi
     const float o[3] = {Pm[3], Pm[7], Pm[11]};
     double wp[3] = {0.0, 0.0, 0.0}, wc[3] = {0.0, 0.0, 0.0}, W = 0.0;
     const uint32_t first = svals[start];
-    for (uint32_t j0 = 0; j0 < cnt; j0 += kSegChunk) {
-      float pp[kSegChunk][3];
-      float ww[kSegChunk];
-      uint32_t cc[kSegChunk];
+    for (uint32_t j = 0; j < cnt; ++j) {  // point order within the bucket (stable sort)
+      const float4 q = pw[start + j];
+      const double wd = static_cast<double>(q.w);
+      wp[0] = __dadd_rn(wp[0], __dmul_rn(wd, static_cast<double>(q.x)));
+      wp[1] = __dadd_rn(wp[1], __dmul_rn(wd, static_cast<double>(q.y)));
+      wp[2] = __dadd_rn(wp[2], __dmul_rn(wd, static_cast<double>(q.z)));
+      if (rgb != nullptr) {
+        const uint32_t c = cc[start + j];
 #pragma unroll
-      for (int u = 0; u < kSegChunk; ++u) {
-        ww[u] = 0.0f;
-        cc[u] = 0u;
-        if (j0 + u < cnt) {
-          const uint32_t i = svals[start + j0 + u];
-          transform_point(Pm, xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], pp[u]);
-          const float depth = norm3(fsub(pp[u][0], o[0]), fsub(pp[u][1], o[1]), fsub(pp[u][2], o[2]));
-          ww[u] = tp.weight_mode == VXG_WEIGHT_CONSTANT ? 1.0f : fdiv(1.0f, fmul(depth, depth));
-          if (rgb != nullptr)
-            cc[u] = static_cast<uint32_t>(rgb[3 * i]) | (static_cast<uint32_t>(rgb[3 * i + 1]) << 8) |
-                    (static_cast<uint32_t>(rgb[3 * i + 2]) << 16);
-        }
+        for (int k = 0; k < 3; ++k) wc[k] = __dadd_rn(wc[k], __dmul_rn(wd, static_cast<double>((c >> (8 * k)) & 0xffu)));
       }
-#pragma unroll
-      for (int u = 0; u < kSegChunk; ++u) {
-        if (j0 + u < cnt) {
-          const double wd = static_cast<double>(ww[u]);
-#pragma unroll
-          for (int k = 0; k < 3; ++k) wp[k] = __dadd_rn(wp[k], __dmul_rn(wd, static_cast<double>(pp[u][k])));
-          if (rgb != nullptr) {
-#pragma unroll
-            for (int k = 0; k < 3; ++k)
-              wc[k] = __dadd_rn(wc[k], __dmul_rn(wd, static_cast<double>((cc[u] >> (8 * k)) & 0xffu)));
-          }
-          W = __dadd_rn(W, wd);
-        }
-      }
+      W = __dadd_rn(W, wd);
     }
 #pragma unroll
     for (int k = 0; k < 3; ++k) out.mean[k] = __double2float_rn(__ddiv_rn(wp[k], W));

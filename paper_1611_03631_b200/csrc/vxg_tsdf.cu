@@ -167,6 +167,8 @@ struct vxg_handle {
   DBuf<uint32_t> run_keys, run_len, run_start, run_len2, run_order, run_iota, work;
   DBuf<uint32_t> sort_counts, sort_offs, dense_start, dense_end, run_flag, run_pos;
   DBuf<FoldRay> fold_rays;
+  DBuf<float4> pt_w;    // bundling: per sorted point (world point, weight)
+  DBuf<uint32_t> pt_c;  // bundling: per sorted point colour
   DBuf<float> d_org;  // sensor origins, 3 floats per frame
   bool debug_fold = false;  // globaltimer trace of the fold (vxg_debug_fold)
   DBuf<unsigned long long> fold_dbg;
@@ -524,6 +526,11 @@ void vxg_handle::build_rays_grouped(const float* dxyz, const uint8_t* drgb, uint
     }, 2);
     k_widen_keys<<<grid_for(P), 256, 0, st>>>(num_runs.p, u32, ukeys.p);
     ++launches;
+    pt_w.ensure(P);
+    pt_c.ensure(P);
+    k_point_prep<uint32_t><<<grid_for(P), 256, 0, st>>>(P, k32b, pvals2.p, dxyz, drgb, d_poses.p, tp, kb, pt_w.p,
+                                                        pt_c.p);
+    ++launches;
     CU(cudaGetLastError());
   } else {
     pkeys.ensure(P);
@@ -540,6 +547,12 @@ void vxg_handle::build_rays_grouped(const float* dxyz, const uint8_t* drgb, uint
       return cub::DeviceRunLengthEncode::Encode(t, b, pkeys2.p, ukeys.p, ucounts.p, num_runs.p, static_cast<int>(P),
                                                 st);
     }, 2);
+    pt_w.ensure(P);
+    pt_c.ensure(P);
+    k_point_prep<unsigned long long><<<grid_for(P), 256, 0, st>>>(P, pkeys2.p, pvals2.p, dxyz, drgb, d_poses.p, tp, kb,
+                                                                  pt_w.p, pt_c.p);
+    ++launches;
+    CU(cudaGetLastError());
   }
   uint32_t S = 0;
   CU(cudaMemcpyAsync(&S, num_runs.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
@@ -553,7 +566,8 @@ void vxg_handle::build_rays_grouped(const float* dxyz, const uint8_t* drgb, uint
   seg_start.ensure(F);
   CU(cudaMemsetAsync(seg_count.p, 0, F * sizeof(uint32_t), st));
   CU(cudaMemsetAsync(seg_start.p, 0xFF, F * sizeof(uint32_t), st));
-  k_seg_reduce<<<grid_for(S), 256, 0, st>>>(num_runs.p, ukeys.p, uoffs.p, ucounts.p, pvals2.p, dxyz, drgb, d_off.p,
+  k_seg_reduce<<<grid_for(S), 256, 0, st>>>(num_runs.p, ukeys.p, uoffs.p, ucounts.p, pvals2.p, pt_w.p, pt_c.p, drgb,
+                                            d_off.p,
                                             d_poses.p, tp, rb, kb, segs.p, seg_count.p, seg_start.p, d_stats.p + 2 * F);
   ++launches;
   CU(cudaGetLastError());
@@ -561,7 +575,7 @@ void vxg_handle::build_rays_grouped(const float* dxyz, const uint8_t* drgb, uint
   CU(cudaMemcpyAsync(K.data(), seg_count.p, F * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   CU(cudaMemcpyAsync(start.data(), seg_start.p, F * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
-  end(P, 6);
+  end(P, 7);
 
   // ---- K3 ray order
   begin(ST_ORDER);
