@@ -2,11 +2,13 @@
 //
 // The keys of one batch are dense: slot * vps^3 + local < blocks * vps^3, i.e.
 // 21 bits for the 450-block cfg1 layer. One reduce-then-scan pass per digit of
-// up to 11 bits (two passes for keys up to 22 bits, where an 8-bit onesweep
-// needs three):
+// 7 bits (8 above 21 key bits): three passes at ~3.3 TB/s each on B200, where
+// CUB's 8-bit onesweep runs three at ~1.9 TB/s. Wider digits (11 bits: two
+// passes) fragment the scatter and cost more per bin than they save.
 //   k_sort_upsweep   per super-tile digit histogram   (reads 4 B/record)
 //   ExclusiveSum     digit-major [digit][super-tile]  -> global output bases
 //   k_sort_downsweep per sub-tile: warp-private match_any ranking (stable),
+//                    next sub-tile's keys/ids loaded during this one's scatter,
 //                    smem staging in digit order, coalesced scatter
 //                                                      (reads 8 B, writes 8 B)
 // Records within a voxel keep their emission (= ray) order, which is what the
@@ -78,7 +80,7 @@ __device__ __forceinline__ uint32_t digit_peers(uint32_t d) {
   return peers;
 }
 
-template <int kBits, int kIpt, int kMinBlocks, bool kPrefetch = false>
+template <int kBits, int kIpt, int kMinBlocks, bool kPrefetch = false, bool kMatch = false>
 __global__ void __launch_bounds__(kSortThreads, kMinBlocks)
     k_sort_downsweep(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
                      uint32_t* __restrict__ vout, uint64_t n, int shift, uint32_t mask, uint32_t S,
@@ -116,7 +118,7 @@ __global__ void __launch_bounds__(kSortThreads, kMinBlocks)
 #pragma unroll
     for (int j = 0; j < kIpt; ++j) {
       const uint32_t d = i0 + j * 32 < nv ? (key[j] >> shift) & mask : bins;
-      const uint32_t peers = digit_peers<kBits>(d);
+      const uint32_t peers = kMatch ? __match_any_sync(0xffffffffu, d) : digit_peers<kBits>(d);
       const uint32_t pre = sm.wcnt[w][d];
       __syncwarp();
       if ((peers & lt) == 0u) sm.wcnt[w][d] = static_cast<uint16_t>(pre + __popc(peers));

@@ -663,7 +663,7 @@ void vxg_handle::lsd_sort(uint64_t T, int kbits, uint32_t** sk, uint32_t** sv) {
   using C = SortCfg<kBits, kIpt>;
   static bool attr = false;
   if (!attr) {
-    CU(cudaFuncSetAttribute(k_sort_downsweep<kBits, kIpt, kMB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CU(cudaFuncSetAttribute(k_sort_downsweep<kBits, kIpt, kMB, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(sizeof(typename C::Smem))));
     attr = true;
   }
@@ -681,7 +681,7 @@ void vxg_handle::lsd_sort(uint64_t T, int kbits, uint32_t** sk, uint32_t** sv) {
     cub([&](void* t, size_t& b) {
       return cub::DeviceScan::ExclusiveSum(t, b, sort_counts.p, sort_offs.p, static_cast<int>(nc), st);
     }, 2);
-    k_sort_downsweep<kBits, kIpt, kMB, true><<<S, kSortThreads, sizeof(typename C::Smem), st>>>(
+    k_sort_downsweep<kBits, kIpt, kMB, true, true><<<S, kSortThreads, sizeof(typename C::Smem), st>>>(
         ki, vi, ko, vo, T, shift, mask, S, sort_offs.p);
     launches += 2;
     CU(cudaGetLastError());
