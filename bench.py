@@ -267,21 +267,36 @@ def main():
     h2d = P * 12 + (P * 3 if rgb is not None else 0) + 8 * (F + 1) + 48 * F
     d2h = 24 * F
 
-    # ---- roofline of the dominant kernel (apply = ordered fold)
+    # ---- rooflines (SURVEY.md 8d accounting): HBM-bound stages,
+    # achieved = algorithmic bytes / the stage's CUDA-event time on the launching stream
     peak, peak_src = _peaks()
     dom = max(("emit", "record_sort", "apply", "bundle", "ray_order", "ray_setup"), key=lambda k: stages[k][0])
-    apply_ms = stages["apply"][0] / max(stages["apply"][1], 1)
     n_upd = updates_per_step
     n_vox = info["n_vox"] / args.steps
+    n_rec = info["records"] / args.steps
+    passes = info["sort_passes"]
     prof_path = os.path.join(ROOT, "profiles", "roofline_inputs.json")
-    traffic = None
+    prof = {}
     try:
         with open(prof_path) as f:
-            traffic = json.load(f).get("apply_dram_bytes_per_launch")
+            prof = json.load(f)
     except Exception:
         pass
-    apply_bytes = 16.0 * n_upd + 24.0 * n_vox
-    achieved = apply_bytes / (apply_ms / 1e3) / 1e9 if apply_ms > 0 else 0.0
+
+    def roof(stage, kernels, alg_bytes, model):
+        t_ms = stages[stage][0] / args.steps
+        ach = alg_bytes / (t_ms / 1e3) / 1e9 if t_ms > 0 else 0.0
+        return {"bound": "hbm", "kernel": kernels, "stage": stage, "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak, "traffic": prof.get(f"{stage}_dram_bytes_per_step"),
+                "algorithmic_bytes": alg_bytes, "ms_per_step": t_ms, "peak_source": peak_src, "model": model}
+
+    roof_sort = roof("record_sort", "k_sort_upsweep + k_sort_downsweep (x passes)", 20.0 * n_rec * passes,
+                     f"LSD radix sort of 8-byte (voxel key, ray id) records, {passes} passes x (4 B upsweep read "
+                     f"+ 8 B read + 8 B write) per record")
+    roof_apply = roof("apply", "k_run_marks + k_fold_runs + k_fold_short", 16.0 * n_upd + 24.0 * n_vox,
+                      "16 B/update + 24 B/distinct voxel (SURVEY.md 8d); bound in practice by the longest "
+                      "per-voxel chain (work.longest_fold_chain sequential steps)")
+    roofline = roof_sort if stages["record_sort"][0] >= stages["apply"][0] else roof_apply
 
     # ---- CPU baseline (the reference, rank 0, N=1 only, bounded sample)
     cpu = None
@@ -306,14 +321,11 @@ def main():
                                        f"records" if world > 1 else "1 GPU")},
             "e2e": {"value": total_updates / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
-            "roofline": {"bound": "hbm", "kernel": "k_fold (apply)", "achieved": achieved, "peak": peak,
-                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                         "algorithmic_bytes": apply_bytes, "peak_source": peak_src,
-                         "model": "16 B/update + 24 B/distinct voxel (SURVEY.md 8d)",
-                         "apply_ms_per_launch": apply_ms},
+            "roofline": roofline,
+            "roofline_stages": {"record_sort": roof_sort, "apply": roof_apply},
             "stages_ms_per_step": {k: v[0] / args.steps for k, v in stages.items()},
-            "work": {"records_per_step": info["records"] / args.steps, "n_vox_per_step": n_vox,
-                     "longest_fold_chain": info["max_chain"], "blocks": info["blocks"]},
+            "work": {"records_per_step": n_rec, "n_vox_per_step": n_vox,
+                     "longest_fold_chain": info["max_chain"], "blocks": info["blocks"], "sort_passes": passes},
             "dominant_stage": dom,
             "gpu_launches": launches,
             "clocks": clocks.summary(),

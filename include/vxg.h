@@ -155,7 +155,8 @@ const char* vxg_stage_name(int stage);
 int vxg_stage_times(vxg_handle* h, double* ms, uint64_t* launches, uint64_t* units, int reset);
 /* Work counters since the last reset: out[0] = candidate records emitted,
  * out[1] = distinct voxels folded (N_vox), out[2] = longest per-voxel fold
- * chain (records), out[3] = allocated blocks. */
+ * chain (records), out[3] = allocated blocks, out[4] = radix passes of the
+ * last record sort (out must hold 5 values). */
 int vxg_batch_info(vxg_handle* h, uint64_t* out, int reset);
 /* Kernel launches issued by the library since the last call (and reset). */
 int vxg_kernel_launches(vxg_handle* h, uint64_t* out, int reset);

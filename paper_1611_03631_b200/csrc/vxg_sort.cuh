@@ -37,9 +37,9 @@ struct SortCfg {
     uint32_t tcount[kBins + 1];            // sub-tile digit counts
     uint32_t tstart[kBins + 1];            // sub-tile digit starts (exclusive scan of tcount)
     uint32_t gbase[kBins];                 // global output position of the digit's next record
+    uint32_t gdelta[kBins];                // gbase - tstart: staged index -> output position
     uint32_t wsum[kSortWarps];
-    uint32_t stage_k[kSub];
-    uint32_t stage_v[kSub];
+    uint2 stage[kSub];                     // (key, ray id) in digit order
   };
 };
 
@@ -165,14 +165,20 @@ __global__ void __launch_bounds__(kSortThreads, kMinBlocks)
       }
     }
     __syncthreads();
+    // fold the sub-tile digit starts into the per-warp prefixes (one lookup per
+    // record below) and the global bases into per-digit deltas
+    for (uint32_t e = tid; e < kSortWarps * (bins + 1u); e += kSortThreads) {
+      const uint32_t q = e / (bins + 1u), d = e - q * (bins + 1u);
+      sm.wcnt[q][d] = static_cast<uint16_t>(sm.wcnt[q][d] + sm.tstart[d]);
+    }
+    for (uint32_t d = tid; d < bins; d += kSortThreads) sm.gdelta[d] = sm.gbase[d] - sm.tstart[d];
+    __syncthreads();
 #pragma unroll
     for (int j = 0; j < kIpt; ++j) {
       const uint32_t i = i0 + j * 32;
       if (i < nv) {
         const uint32_t d = (key[j] >> shift) & mask;
-        const uint32_t p = sm.tstart[d] + sm.wcnt[w][d] + rk[j];
-        sm.stage_k[p] = key[j];
-        sm.stage_v[p] = kPrefetch ? val[j] : vin[base + i];
+        sm.stage[sm.wcnt[w][d] + rk[j]] = make_uint2(key[j], kPrefetch ? val[j] : vin[base + i]);
       }
     }
     if (kPrefetch) {  // next sub-tile's loads overlap this one's scatter
@@ -181,11 +187,10 @@ __global__ void __launch_bounds__(kSortThreads, kMinBlocks)
     }
     __syncthreads();
     for (uint32_t i = tid; i < nv; i += kSortThreads) {
-      const uint32_t k = sm.stage_k[i];
-      const uint32_t d = (k >> shift) & mask;
-      const uint32_t p = sm.gbase[d] + (i - sm.tstart[d]);
-      kout[p] = k;
-      vout[p] = sm.stage_v[i];
+      const uint2 kv = sm.stage[i];
+      const uint32_t p = sm.gdelta[(kv.x >> shift) & mask] + i;
+      kout[p] = kv.x;
+      vout[p] = kv.y;
     }
     __syncthreads();
     for (uint32_t d = tid; d < bins; d += kSortThreads) sm.gbase[d] += sm.tcount[d];

@@ -174,6 +174,7 @@ struct vxg_handle {
   DBuf<unsigned long long> fold_dbg;
   uint32_t fold_dbg_n = 0;
   uint64_t info_records = 0, info_runs = 0, info_max_run = 0;  // since the last vxg_batch_info reset
+  uint64_t info_sort_passes = 0;
 
   // ---- profiling
   bool profile = false;
@@ -668,6 +669,7 @@ void vxg_handle::lsd_sort(uint64_t T, int kbits, uint32_t** sk, uint32_t** sv) {
     attr = true;
   }
   const int passes = std::max(1, (kbits + kBits - 1) / kBits);
+  info_sort_passes = static_cast<uint64_t>(passes);
   const uint32_t S = static_cast<uint32_t>((T + C::kSuper - 1) / C::kSuper);
   uint32_t *ki = rkeys.p, *vi = rvals.p, *ko = rkeys2.p, *vo = rvals2.p;
   int shift = 0;
@@ -704,6 +706,7 @@ void vxg_handle::sort_records(uint64_t T, int kbits, uint32_t** sk, uint32_t** s
       return cub::DeviceRadixSort::SortPairs(t, b, rkeys.p, rkeys2.p, rvals.p, rvals2.p, static_cast<int>(T), 0, nb,
                                              st);
     }, 2 + (nb + 7) / 8);
+    info_sort_passes = static_cast<uint64_t>((nb + 7) / 8);
     *sk = rkeys2.p;
     *sv = rvals2.p;
     return;
@@ -1413,12 +1416,18 @@ struct Copy {
 // Frame-aligned sub-batches: <= 2^30 points each (32-bit point indices).
 std::vector<std::pair<uint64_t, uint64_t>> plan_subbatches(const uint64_t* off, uint64_t F, bool host_input) {
   const uint64_t P = off[F] - off[0];
-  // One sub-batch whenever it fits: the fold's critical path is set by the
-  // hottest voxels' chains, which do not shrink with smaller batches, so
-  // splitting only to overlap the H2D copy costs more than it hides.
-  (void)P;
-  (void)host_input;
-  const uint64_t target = 1ull << 30;
+  // Device input: one sub-batch whenever it fits. Host input: split so the H2D
+  // copy of part k+1 overlaps the compute of part k.
+  // Two parts for large host batches: measured on B200 (cfg1, 100 frames,
+  // 460 MB over PCIe) 20.1 ms vs 21.7 ms for one part; more parts lose more in
+  // the fold (fewer records per voxel per launch) than they hide.
+  static const int env_parts = [] {
+    const char* e = getenv("VXG_H2D_PARTS");
+    return e ? std::max(1, atoi(e)) : 0;
+  }();
+  const uint64_t h2d_parts = env_parts > 0 ? static_cast<uint64_t>(env_parts) : (P >= (1ull << 24) ? 2ull : 1ull);
+  uint64_t target = 1ull << 30;
+  if (host_input && h2d_parts > 1) target = std::max<uint64_t>(1, (P + h2d_parts - 1) / h2d_parts);
   std::vector<std::pair<uint64_t, uint64_t>> parts;
   uint64_t f0 = 0;
   while (f0 < F) {
@@ -1850,6 +1859,7 @@ int vxg_batch_info(vxg_handle* h, uint64_t* out, int reset) {
   out[1] = h->info_runs;
   out[2] = h->info_max_run;
   out[3] = h->n_blocks;
+  out[4] = h->info_sort_passes;
   if (reset) h->info_records = h->info_runs = h->info_max_run = 0;
   return VXG_OK;
 }

@@ -236,10 +236,11 @@ class TsdfLayer:
         return int(n.value)
 
     def batch_info(self, reset: bool = True) -> Dict[str, int]:
-        """records emitted, distinct voxels folded (N_vox), longest fold chain, blocks."""
-        out = (ctypes.c_uint64 * 4)()
+        """records emitted, distinct voxels folded (N_vox), longest fold chain, blocks, record-sort passes."""
+        out = (ctypes.c_uint64 * 5)()
         check(lib().vxg_batch_info(self._h, out, 1 if reset else 0))
-        return {"records": int(out[0]), "n_vox": int(out[1]), "max_chain": int(out[2]), "blocks": int(out[3])}
+        return {"records": int(out[0]), "n_vox": int(out[1]), "max_chain": int(out[2]), "blocks": int(out[3]),
+                "sort_passes": int(out[4])}
 
     def shard_init(self, rank: int, world: int, nccl_id: bytes = b"") -> None:
         """Makes this layer shard `rank` of `world` (one process per GPU, NCCL
