@@ -72,6 +72,10 @@ struct DBuf {
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
   ~DBuf() { release(); }
+  void swap(DBuf& o) {
+    std::swap(p, o.p);
+    std::swap(cap, o.cap);
+  }
   void release() {
     if (p) cudaFree(p);
     p = nullptr;
@@ -399,7 +403,9 @@ struct vxg_handle {
   void sort_fold(uint64_t T, uint64_t nslots, uint32_t F);
   void sort_records(uint64_t T, int kbits, uint32_t** sk, uint32_t** sv);
   template <int kBits, int kIpt, int kMB>
-  void lsd_sort(uint64_t T, int kbits, uint32_t** sk, uint32_t** sv);
+  void lsd_sort(uint64_t T, int kbits, uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, uint32_t** sk,
+                uint32_t** sv);
+  int last_lsd_passes = 0;
   uint64_t last_blocks = 0;  // blocks allocated after the last produce attempt
   bool grew_after_attempt(int attempt);
   void begin_batch(const float* xyz, const uint8_t* rgb, const uint64_t* offsets, const float* poses, uint64_t F,
@@ -519,9 +525,15 @@ void vxg_handle::build_rays_grouped(const float* dxyz, const uint8_t* drgb, uint
                                                         counters.p);
     ++launches;
     CU(cudaGetLastError());
-    cub([&](void* t, size_t& b) {
-      return cub::DeviceRadixSort::SortPairs(t, b, k32, k32b, pvals.p, pvals2.p, static_cast<int>(P), 0, end_bit, st);
-    }, 2 + (end_bit + 7) / 8);
+    // stable sort by (frame, terminal voxel): the custom LSD sort, 8-bit digits
+    uint32_t *sk = nullptr, *sv = nullptr;
+    lsd_sort<8, 12, 4>(P, end_bit, k32, pvals.p, k32b, pvals2.p, &sk, &sv);
+    if (sk != k32b) {  // even pass count: the result is in the first buffers
+      pkeys.swap(pkeys2);
+      pvals.swap(pvals2);
+      k32 = reinterpret_cast<uint32_t*>(pkeys.p);
+      k32b = reinterpret_cast<uint32_t*>(pkeys2.p);
+    }
     cub([&](void* t, size_t& b) {
       return cub::DeviceRunLengthEncode::Encode(t, b, k32b, u32, ucounts.p, num_runs.p, static_cast<int>(P), st);
     }, 2);
@@ -660,7 +672,8 @@ uint64_t vxg_handle::count_rays(uint32_t R, uint32_t F) {
 // of up to kBits bits (3 passes for the <= 21-bit keys of a 512-block layer
 // of 16^3 voxels); returns the buffers holding the sorted keys / ray ids.
 template <int kBits, int kIpt, int kMB>
-void vxg_handle::lsd_sort(uint64_t T, int kbits, uint32_t** sk, uint32_t** sv) {
+void vxg_handle::lsd_sort(uint64_t T, int kbits, uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
+                          uint32_t** sk, uint32_t** sv) {
   using C = SortCfg<kBits, kIpt>;
   static bool attr = false;
   if (!attr) {
@@ -669,9 +682,9 @@ void vxg_handle::lsd_sort(uint64_t T, int kbits, uint32_t** sk, uint32_t** sv) {
     attr = true;
   }
   const int passes = std::max(1, (kbits + kBits - 1) / kBits);
-  info_sort_passes = static_cast<uint64_t>(passes);
+  last_lsd_passes = passes;
   const uint32_t S = static_cast<uint32_t>((T + C::kSuper - 1) / C::kSuper);
-  uint32_t *ki = rkeys.p, *vi = rvals.p, *ko = rkeys2.p, *vo = rvals2.p;
+  uint32_t *ki = k0, *vi = v0, *ko = k1, *vo = v1;
   int shift = 0;
   for (int p = 0; p < passes; ++p) {
     const int bits = (kbits - shift + (passes - p) - 1) / (passes - p);
@@ -712,9 +725,10 @@ void vxg_handle::sort_records(uint64_t T, int kbits, uint32_t** sk, uint32_t** s
     return;
   }
   if (kbits <= 21)
-    lsd_sort<7, 12, 4>(T, kbits, sk, sv);
+    lsd_sort<7, 12, 4>(T, kbits, rkeys.p, rvals.p, rkeys2.p, rvals2.p, sk, sv);
   else
-    lsd_sort<8, 12, 4>(T, kbits, sk, sv);
+    lsd_sort<8, 12, 4>(T, kbits, rkeys.p, rvals.p, rkeys2.p, rvals2.p, sk, sv);
+  info_sort_passes = static_cast<uint64_t>(last_lsd_passes);
 }
 
 // Sorts the T records of one attempt (keys < nslots * vps^3, or invalid) and
