@@ -504,6 +504,8 @@ __global__ void __launch_bounds__(128) k_emit(uint32_t R0, uint32_t R1, const ui
     if (r.valid == 1u && !(depth <= 0.0f)) {
       const float ray0 = fsub(r.p[0], o0), ray1 = fsub(r.p[1], o1), ray2 = fsub(r.p[2], o2);
       const float s = fdiv(tp.truncation, depth);
+      // mweight_base for any d >= 0 (d > -eps in the drop-off mode), times the ray weight
+      const float w_front = fmul(mweight_base(tp.weight_mode, r.base, 0.0f, tp.truncation, tp.dropoff_epsilon), r.weight);
       Walk wk;
       uint32_t span = 0;
       walk_axis_init(o0, fadd(r.p[0], fmul(ray0, s)), v, &wk.c0, &wk.e0, &wk.s0, &wk.m0, &wk.d0, &span);
@@ -543,12 +545,17 @@ __global__ void __launch_bounds__(128) k_emit(uint32_t R0, uint32_t R1, const ui
           skip = !(wk.c0 == r.term[0] && wk.c1 == r.term[1] && wk.c2 == r.term[2]) && is_terminal(tv, r.frame, og, g);
         }
         if (!skip) {
-          // projective_distance(x, p, s) (tsdf_integrator.cpp:22-27); p - s == ray
+          // projective_distance(x, p, s) (tsdf_integrator.cpp:22-27); p - s == ray.
+          // In front of the point (along >= 0) d = +|t| >= 0, where every weight
+          // mode gives the ray's constant w_front: the norm is needed only behind it.
           const float t0 = fsub(r.p[0], x0), t1 = fsub(r.p[1], x1), t2 = fsub(r.p[2], x2);
-          const float magnitude = norm3(t0, t1, t2);
           const float along = dot3(t0, t1, t2, ray0, ray1, ray2);
-          const float d = along < 0.0f ? -magnitude : magnitude;
-          const float w = fmul(mweight_base(tp.weight_mode, r.base, d, tp.truncation, tp.dropoff_epsilon), r.weight);
+          float w = w_front;
+          if (!(along >= 0.0f)) {
+            const float magnitude = norm3(t0, t1, t2);
+            const float d = along < 0.0f ? -magnitude : magnitude;
+            w = fmul(mweight_base(tp.weight_mode, r.base, d, tp.truncation, tp.dropoff_epsilon), r.weight);
+          }
           if (!(w <= 0.0f)) {
             if (b0 != cb0 || b1 != cb1 || b2 != cb2) {
               cb0 = b0;
@@ -654,6 +661,7 @@ __global__ void __launch_bounds__(128) k_emit_sharded(uint32_t R0, uint32_t R1, 
     if (!(r.valid == 1u && !(depth <= 0.0f))) continue;
     const float ray0 = fsub(r.p[0], o0), ray1 = fsub(r.p[1], o1), ray2 = fsub(r.p[2], o2);
     const float s = fdiv(tp.truncation, depth);
+    const float w_front = fmul(mweight_base(tp.weight_mode, r.base, 0.0f, tp.truncation, tp.dropoff_epsilon), r.weight);
     Walk wk;
     uint32_t span = 0;
     walk_axis_init(o0, fadd(r.p[0], fmul(ray0, s)), v, &wk.c0, &wk.e0, &wk.s0, &wk.m0, &wk.d0, &span);
@@ -683,10 +691,13 @@ __global__ void __launch_bounds__(128) k_emit_sharded(uint32_t R0, uint32_t R1, 
       }
       if (!skip) {
         const float t0 = fsub(r.p[0], x0), t1 = fsub(r.p[1], x1), t2 = fsub(r.p[2], x2);
-        const float magnitude = norm3(t0, t1, t2);
         const float along = dot3(t0, t1, t2, ray0, ray1, ray2);
-        const float d = along < 0.0f ? -magnitude : magnitude;
-        const float w = fmul(mweight_base(tp.weight_mode, r.base, d, tp.truncation, tp.dropoff_epsilon), r.weight);
+        float w = w_front;  // as in k_emit: d >= 0 in front of the point
+        if (!(along >= 0.0f)) {
+          const float magnitude = norm3(t0, t1, t2);
+          const float d = along < 0.0f ? -magnitude : magnitude;
+          w = fmul(mweight_base(tp.weight_mode, r.base, d, tp.truncation, tp.dropoff_epsilon), r.weight);
+        }
         if (!(w <= 0.0f)) {
           if (b0 != cb0 || b1 != cb1 || b2 != cb2) {
             cb0 = b0;
