@@ -92,9 +92,10 @@ struct DBuf {
   }
 };
 
-constexpr int kStages = 8;
-const char* kStageNames[kStages] = {"h2d", "bundle", "ray_order", "ray_setup", "emit", "record_sort", "apply", "d2h"};
-enum Stage { ST_H2D = 0, ST_BUNDLE, ST_ORDER, ST_RAYS, ST_EMIT, ST_SORT, ST_APPLY, ST_D2H };
+constexpr int kStages = 9;
+const char* kStageNames[kStages] = {"h2d",         "bundle", "ray_order", "ray_setup", "emit",
+                                    "record_sort", "runs",   "apply",     "d2h"};
+enum Stage { ST_H2D = 0, ST_BUNDLE, ST_ORDER, ST_RAYS, ST_EMIT, ST_SORT, ST_RUNS, ST_APPLY, ST_D2H };
 
 int bits_for(uint64_t v) {  // smallest b with v < 2^b
   int b = 0;
@@ -754,7 +755,7 @@ void vxg_handle::sort_fold(uint64_t T, uint64_t nslots, uint32_t F) {
   uint32_t *skeys = nullptr, *svals = nullptr;
   sort_records(T, kbits, &skeys, &svals);
   end(T, 0);
-  begin(ST_APPLY);
+  begin(ST_RUNS);
   // mark each voxel's run [start, end) (dense by key)
   dense_start.ensure(K);
   dense_end.ensure(K);
@@ -792,6 +793,8 @@ void vxg_handle::sort_fold(uint64_t T, uint64_t nslots, uint32_t F) {
                                                        static_cast<int>(nruns), 0, lbits, st);
     }, 2 + (lbits + 7) / 8);
   }
+  end(T, 0);
+  begin(ST_APPLY);
   uint8_t* tch = consumers.empty() ? nullptr : touched.p;
   work.ensure(2);
   CU(cudaMemsetAsync(work.p, 0, 2 * sizeof(uint32_t), st));

@@ -11,7 +11,7 @@ using namespace vxg;
 
 #define CK(x) do { cudaError_t err_ = (x); if (err_ != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(err_)); exit(1); } } while (0)
 
-template <int kBits, int kIpt, int kMB, bool kPF = false, bool kM = false>
+template <int kBits, int kIpt, int kMB, bool kPF = false, bool kM = false, int kMixed = 0>
 void run_lsd(const char* name, uint64_t T, int kbits, uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
              uint32_t* k2, uint32_t* v2, void* tmp, const std::vector<uint32_t>& ck, const std::vector<uint32_t>& cv) {
   using C = SortCfg<kBits, kIpt>;
@@ -19,7 +19,9 @@ void run_lsd(const char* name, uint64_t T, int kbits, uint32_t* k0, uint32_t* v0
   const uint32_t S = static_cast<uint32_t>((T + C::kSuper - 1) / C::kSuper);
   uint32_t *counts, *offs;
   CK(cudaMalloc(&counts, (size_t)C::kBins * S * 4)); CK(cudaMalloc(&offs, (size_t)C::kBins * S * 4));
-  CK(cudaFuncSetAttribute(k_sort_downsweep<kBits, kIpt, kMB, kPF, kM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  CK(cudaFuncSetAttribute(k_sort_downsweep<kBits, kIpt, kMB, kPF, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)sizeof(typename C::Smem)));
+  CK(cudaFuncSetAttribute(k_sort_downsweep<kBits, kIpt, kMB, kPF, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)sizeof(typename C::Smem)));
   size_t stb = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, stb, counts, offs, C::kBins * (int)S);
@@ -39,14 +41,18 @@ void run_lsd(const char* name, uint64_t T, int kbits, uint32_t* k0, uint32_t* v0
       cudaEventRecord(e[1]);
       cub::DeviceScan::ExclusiveSum(tmp, stb, counts, offs, nc);
       cudaEventRecord(e[2]);
-      k_sort_downsweep<kBits, kIpt, kMB, kPF, kM><<<S, 256, sizeof(typename C::Smem)>>>(ki, vi, ko, vo, T, shift, mask, S, offs);
+      const bool use_match = kMixed ? (p == passes - 1) : kM;
+      if (use_match)
+        k_sort_downsweep<kBits, kIpt, kMB, kPF, true><<<S, 256, sizeof(typename C::Smem)>>>(ki, vi, ko, vo, T, shift, mask, S, offs);
+      else
+        k_sort_downsweep<kBits, kIpt, kMB, kPF, false><<<S, 256, sizeof(typename C::Smem)>>>(ki, vi, ko, vo, T, shift, mask, S, offs);
       cudaEventRecord(e[3]);
       CK(cudaEventSynchronize(e[3]));
       float x;
       if (rep) {
         cudaEventElapsedTime(&x, e[0], e[1]); t_up += x;
         cudaEventElapsedTime(&x, e[1], e[2]); t_scan += x;
-        cudaEventElapsedTime(&x, e[2], e[3]); t_down += x;
+        cudaEventElapsedTime(&x, e[2], e[3]); t_down += x; if (rep == 3) printf("  pass %d down %.3f ms\n", p, x);
       }
       ki = ko; vi = vo; ko = (ko == k1) ? k2 : k1; vo = (vo == v1) ? v2 : v1;
       shift += bits;
@@ -96,9 +102,10 @@ int main(int argc, char** argv) {
   CK(cudaMemcpy(ck.data(), rk, T * 4, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(cv.data(), rv, T * 4, cudaMemcpyDeviceToHost));
 
-  run_lsd<7, 12, 4, true>("b7 i12 mb4 pf", T, kbits, k0, v0, k1, v1, k2, v2, tmp, ck, cv);
-  run_lsd<7, 12, 4, true, true>("b7 i12 pf match", T, kbits, k0, v0, k1, v1, k2, v2, tmp, ck, cv);
-  run_lsd<8, 12, 4, true, true>("b8 i12 pf match", T, kbits, k0, v0, k1, v1, k2, v2, tmp, ck, cv);
-  run_lsd<11, 12, 2, true, true>("b11 i12 pf match", T, kbits, k0, v0, k1, v1, k2, v2, tmp, ck, cv);
+  run_lsd<7, 12, 4, true, true>("b7 i12 mb4", T, kbits, k0, v0, k1, v1, k2, v2, tmp, ck, cv);
+  run_lsd<7, 8, 5, true, true>("b7 i8 mb5", T, kbits, k0, v0, k1, v1, k2, v2, tmp, ck, cv);
+  run_lsd<7, 8, 6, true, true>("b7 i8 mb6", T, kbits, k0, v0, k1, v1, k2, v2, tmp, ck, cv);
+  run_lsd<7, 6, 6, true, true>("b7 i6 mb6", T, kbits, k0, v0, k1, v1, k2, v2, tmp, ck, cv);
+  run_lsd<7, 16, 3, true, true>("b7 i16 mb3", T, kbits, k0, v0, k1, v1, k2, v2, tmp, ck, cv);
   return 0;
 }

@@ -95,7 +95,7 @@ def main():
     sort_caps = [m for m in caps if "k_sort_" in m["kernel"]]
     n_sort_launches = max(1, len([m for m in sort_caps if "downsweep" in m["kernel"]]))
     sort_step = dram(["k_sort_downsweep", "k_sort_upsweep"]) * passes / n_sort_launches
-    apply_step = dram(["k_run_marks", "k_fold_runs", "k_fold_short"])
+    apply_step = dram(["k_fold_runs", "k_fold_short"])
     inputs = {"record_sort_dram_bytes_per_step": sort_step, "apply_dram_bytes_per_step": apply_step,
               "source": f"profiles/{tag}_summary.json", "sort_passes": passes}
     lines += ["", f"DRAM bytes per step: record_sort {sort_step:.3e} ({passes} passes), apply {apply_step:.3e}."]
