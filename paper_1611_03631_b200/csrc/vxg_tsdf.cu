@@ -405,7 +405,7 @@ struct vxg_handle {
   void sort_records(uint64_t T, int kbits, uint32_t** sk, uint32_t** sv);
   template <int kBits, int kIpt, int kMB>
   void lsd_sort(uint64_t T, int kbits, uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, uint32_t** sk,
-                uint32_t** sv);
+                uint32_t** sv, bool grouped);
   int last_lsd_passes = 0;
   uint64_t last_blocks = 0;  // blocks allocated after the last produce attempt
   bool grew_after_attempt(int attempt);
@@ -528,7 +528,7 @@ void vxg_handle::build_rays_grouped(const float* dxyz, const uint8_t* drgb, uint
     CU(cudaGetLastError());
     // stable sort by (frame, terminal voxel): the custom LSD sort, 8-bit digits
     uint32_t *sk = nullptr, *sv = nullptr;
-    lsd_sort<8, 12, 4>(P, end_bit, k32, pvals.p, k32b, pvals2.p, &sk, &sv);
+    lsd_sort<8, 12, 4>(P, end_bit, k32, pvals.p, k32b, pvals2.p, &sk, &sv, false);  // frames stay contiguous
     if (sk != k32b) {  // even pass count: the result is in the first buffers
       pkeys.swap(pkeys2);
       pvals.swap(pvals2);
@@ -672,9 +672,15 @@ uint64_t vxg_handle::count_rays(uint32_t R, uint32_t F) {
 // Stable LSD radix sort of the T records by voxel key (vxg_sort.cuh): digits
 // of up to kBits bits (3 passes for the <= 21-bit keys of a 512-block layer
 // of 16^3 voxels); returns the buffers holding the sorted keys / ray ids.
+// grouped = true: only equal keys need to end up adjacent (ray order kept
+// inside each group), not in key order. The digits are then applied top digit
+// first — in emission (ray) order the top digit (block slot bits) is the most
+// clustered, so that pass scatters long coalesced segments and ranks few
+// distinct values — then the others from the bottom: groups come out ordered
+// by a bit-permuted key (measured 3.57 vs 4.14 ms on cfg1).
 template <int kBits, int kIpt, int kMB>
 void vxg_handle::lsd_sort(uint64_t T, int kbits, uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
-                          uint32_t** sk, uint32_t** sv) {
+                          uint32_t** sk, uint32_t** sv, bool grouped) {
   using C = SortCfg<kBits, kIpt>;
   static bool attr = false;
   if (!attr) {
@@ -686,9 +692,15 @@ void vxg_handle::lsd_sort(uint64_t T, int kbits, uint32_t* k0, uint32_t* v0, uin
   last_lsd_passes = passes;
   const uint32_t S = static_cast<uint32_t>((T + C::kSuper - 1) / C::kSuper);
   uint32_t *ki = k0, *vi = v0, *ko = k1, *vo = v1;
-  int shift = 0;
-  for (int p = 0; p < passes; ++p) {
-    const int bits = (kbits - shift + (passes - p) - 1) / (passes - p);
+  int dshift[8], dbits[8];  // natural digits, least significant first
+  for (int p = 0, sh = 0; p < passes; ++p) {
+    dbits[p] = (kbits - sh + (passes - p) - 1) / (passes - p);
+    dshift[p] = sh;
+    sh += dbits[p];
+  }
+  for (int q = 0; q < passes; ++q) {
+    const int p = !grouped ? q : (q == 0 ? passes - 1 : q - 1);
+    const int shift = dshift[p], bits = dbits[p];
     const uint32_t mask = bits ? (1u << bits) - 1u : 0u;
     const uint64_t nc = static_cast<uint64_t>(mask + 1u) * S;
     sort_counts.ensure(nc);
@@ -703,7 +715,6 @@ void vxg_handle::lsd_sort(uint64_t T, int kbits, uint32_t* k0, uint32_t* v0, uin
     CU(cudaGetLastError());
     std::swap(ki, ko);
     std::swap(vi, vo);
-    shift += bits;
   }
   *sk = ki;
   *sv = vi;
@@ -726,9 +737,9 @@ void vxg_handle::sort_records(uint64_t T, int kbits, uint32_t** sk, uint32_t** s
     return;
   }
   if (kbits <= 21)
-    lsd_sort<7, 12, 4>(T, kbits, rkeys.p, rvals.p, rkeys2.p, rvals2.p, sk, sv);
+    lsd_sort<7, 12, 4>(T, kbits, rkeys.p, rvals.p, rkeys2.p, rvals2.p, sk, sv, true);
   else
-    lsd_sort<8, 12, 4>(T, kbits, rkeys.p, rvals.p, rkeys2.p, rvals2.p, sk, sv);
+    lsd_sort<8, 12, 4>(T, kbits, rkeys.p, rvals.p, rkeys2.p, rvals2.p, sk, sv, true);
   info_sort_passes = static_cast<uint64_t>(last_lsd_passes);
 }
 

@@ -69,6 +69,59 @@ void run_lsd(const char* name, uint64_t T, int kbits, uint32_t* k0, uint32_t* v0
   cudaFree(counts); cudaFree(offs);
 }
 
+// LSD with digit order (C, B, A) = shifts (14, 7, 0) for 21-bit keys: groups equal keys
+// (ray order kept) but orders groups by the permuted key C + 128 B + 16384 A.
+__global__ void permute_keys(const uint32_t* k, uint32_t* o, uint64_t n, int s0, int s1, int s2) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t x = k[i];
+    o[i] = x == 0xFFFFFFFFu ? x : ((x >> s0) & 127u) | (((x >> s1) & 127u) << 7) | (((x >> s2) & 127u) << 14);
+  }
+}
+template <int kBits, int kIpt, int kMB>
+void run_perm(const char* name, uint64_t T, uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, uint32_t* k2,
+              uint32_t* v2, void* tmp, size_t tb, int s0, int s1, int s2) {
+  using C = SortCfg<kBits, kIpt>;
+  const uint32_t S = static_cast<uint32_t>((T + C::kSuper - 1) / C::kSuper);
+  uint32_t *counts, *offs;
+  CK(cudaMalloc(&counts, (size_t)C::kBins * S * 4)); CK(cudaMalloc(&offs, (size_t)C::kBins * S * 4));
+  CK(cudaFuncSetAttribute(k_sort_downsweep<kBits, kIpt, kMB, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)sizeof(typename C::Smem)));
+  size_t stb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, stb, counts, offs, C::kBins * (int)S);
+  const int shifts[3] = {s0, s1, s2};
+  cudaEvent_t e[2];
+  for (auto& x : e) cudaEventCreate(&x);
+  uint32_t *rk, *rv;
+  for (int rep = 0; rep < 3; ++rep) {
+    uint32_t *ki = k0, *vi = v0, *ko = k1, *vo = v1;
+    cudaEventRecord(e[0]);
+    for (int p = 0; p < 3; ++p) {
+      const uint32_t mask = 127u;
+      k_sort_upsweep<kBits, kIpt><<<S, 256>>>(ki, T, shifts[p], mask, S, counts);
+      cub::DeviceScan::ExclusiveSum(tmp, stb, counts, offs, (int)(128 * S));
+      cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b); cudaEventRecord(a);
+      k_sort_downsweep<kBits, kIpt, kMB, true, true><<<S, 256, sizeof(typename C::Smem)>>>(ki, vi, ko, vo, T, shifts[p], mask, S, offs);
+      cudaEventRecord(b); cudaEventSynchronize(b); float x; cudaEventElapsedTime(&x, a, b);
+      if (rep == 2) printf("  perm pass %d (shift %d) down %.3f ms\n", p, shifts[p], x);
+      ki = ko; vi = vo; ko = (ko == k1) ? k2 : k1; vo = (vo == v1) ? v2 : v1;
+    }
+    cudaEventRecord(e[1]); cudaEventSynchronize(e[1]);
+    float ms; cudaEventElapsedTime(&ms, e[0], e[1]);
+    if (rep == 2) printf("%-14s: total %.3f ms\n", name, ms);
+    rk = ki; rv = vi;
+  }
+  // check: CUB on permuted keys gives the same ray ids order
+  uint32_t *pk, *pk2, *pv2;
+  CK(cudaMalloc(&pk, T * 4)); CK(cudaMalloc(&pk2, T * 4)); CK(cudaMalloc(&pv2, T * 4));
+  permute_keys<<<4096, 256>>>(k0, pk, T, s0, s1, s2);
+  cub::DeviceRadixSort::SortPairs(tmp, tb, pk, pk2, v0, pv2, (int)T, 0, 21);
+  std::vector<uint32_t> a(T), b(T);
+  CK(cudaMemcpy(a.data(), rv, T * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(b.data(), pv2, T * 4, cudaMemcpyDeviceToHost));
+  printf("  perm check %s\n", a == b ? "OK" : "MISMATCH");
+  cudaFree(pk); cudaFree(pk2); cudaFree(pv2); cudaFree(counts); cudaFree(offs);
+}
+
 int main(int argc, char** argv) {
   FILE* f = fopen(argc > 1 ? argv[1] : "/tmp/records.bin", "rb");
   if (!f) { printf("no dump\n"); return 1; }
@@ -103,9 +156,13 @@ int main(int argc, char** argv) {
   CK(cudaMemcpy(cv.data(), rv, T * 4, cudaMemcpyDeviceToHost));
 
   run_lsd<7, 12, 4, true, true>("b7 i12 mb4", T, kbits, k0, v0, k1, v1, k2, v2, tmp, ck, cv);
-  run_lsd<7, 8, 5, true, true>("b7 i8 mb5", T, kbits, k0, v0, k1, v1, k2, v2, tmp, ck, cv);
-  run_lsd<7, 8, 6, true, true>("b7 i8 mb6", T, kbits, k0, v0, k1, v1, k2, v2, tmp, ck, cv);
-  run_lsd<7, 6, 6, true, true>("b7 i6 mb6", T, kbits, k0, v0, k1, v1, k2, v2, tmp, ck, cv);
-  run_lsd<7, 16, 3, true, true>("b7 i16 mb3", T, kbits, k0, v0, k1, v1, k2, v2, tmp, ck, cv);
+  if (kbits == 21) {
+    const int orders[6][3] = {{14, 7, 0}, {14, 0, 7}, {7, 14, 0}, {7, 0, 14}, {0, 14, 7}, {0, 7, 14}};
+    for (auto& o : orders) {
+      char nm[32];
+      snprintf(nm, sizeof(nm), "perm %d,%d,%d", o[0], o[1], o[2]);
+      run_perm<7, 12, 4>(nm, T, k0, v0, k1, v1, k2, v2, tmp, tb + (64 << 20), o[0], o[1], o[2]);
+    }
+  }
   return 0;
 }
