@@ -200,3 +200,45 @@ def test_long_chains_full_trajectory_slice(gpu):
     integ = TsdfIntegrator(cfg, layer)
     _check(layer, integ, cfg, wc, W.frames(1, count=20, start=0), batch=True)
     assert layer.batch_info()["max_chain"] > 4096
+
+
+def test_cfg1_bench_workload_bit_exact(gpu):
+    """The exact bench.py step: all 100 full-size cfg1 frames in one batch
+    (2.4e8 updates, fold chains up to 77k records, the custom radix sort at
+    3 passes), bit-exact vs the oracle's 100 sequential integrate() calls."""
+    wc = W.CONFIGS[1]
+    cfg = W.tsdf_config(wc)
+    layer = TsdfLayer(wc.voxel_size, wc.vps, block_capacity=1024)
+    integ = TsdfIntegrator(cfg, layer)
+    layer.batch_info(reset=True)
+    _check(layer, integ, cfg, wc, W.frames(1), batch=True)
+    info = layer.batch_info()
+    assert info["max_chain"] > 50000 and info["sort_passes"] == 3
+
+
+@pytest.mark.parametrize("cfg_id,count,scale", [(2, 3, 1.0), (3, 3, 1.0), (4, 1, 0.5)])
+def test_configs_full_size_frames(gpu, cfg_id, count, scale):
+    """Full-size frames of the other configs (cfg2 752x480 stereo-like, cfg3
+    64-beam LiDAR with 80 m rays, cfg4 at 1024x1024), bit-exact."""
+    wc = W.CONFIGS[cfg_id]
+    cfg = W.tsdf_config(wc)
+    layer = TsdfLayer(wc.voxel_size, wc.vps)
+    integ = TsdfIntegrator(cfg, layer)
+    _check(layer, integ, cfg, wc, W.frames(cfg_id, count=count, scale=scale, start=1), batch=True)
+
+
+def test_batch_split_invariance_full_size(gpu):
+    """Property at full size (no oracle): the same 40 frames integrated as one
+    batch, as 4 batches of 10 and as 40 single calls give identical bytes."""
+    wc = W.CONFIGS[1]
+    cfg = W.tsdf_config(wc)
+    fr = [Scan(x, c, p) for (x, c, p) in W.frames(1, count=40, start=10)]
+    out = []
+    for parts in (1, 4, 40):
+        layer = TsdfLayer(wc.voxel_size, wc.vps)
+        integ = TsdfIntegrator(cfg, layer)
+        n = len(fr) // parts
+        for i in range(parts):
+            integ.integrate_batch(fr[i * n:(i + 1) * n])
+        out.append(layer.save_bytes())
+    assert out[0] == out[1] == out[2]

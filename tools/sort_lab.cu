@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
+#include <algorithm>
 #include "vxg_sort.cuh"
 using namespace vxg;
 
@@ -122,6 +123,48 @@ void run_perm(const char* name, uint64_t T, uint32_t* k0, uint32_t* v0, uint32_t
   cudaFree(pk); cudaFree(pk2); cudaFree(pv2); cudaFree(counts); cudaFree(offs);
 }
 
+// general digit schedule: (shift, bits) per pass in application order; check = group check on ray ids
+template <int kBits, int kIpt, int kMB>
+float run_sched(uint64_t T, uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, uint32_t* k2, uint32_t* v2,
+                void* tmp, const std::vector<std::pair<int,int>>& sched, uint32_t** out_k, uint32_t** out_v) {
+  using C = SortCfg<kBits, kIpt>;
+  const uint32_t S = static_cast<uint32_t>((T + C::kSuper - 1) / C::kSuper);
+  static uint32_t *counts = nullptr, *offs = nullptr;
+  if (!counts) { CK(cudaMalloc(&counts, (size_t)2048 * 20000 * 4)); CK(cudaMalloc(&offs, (size_t)2048 * 20000 * 4)); }
+  CK(cudaFuncSetAttribute(k_sort_downsweep<kBits, kIpt, kMB, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)sizeof(typename C::Smem)));
+  size_t stb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, stb, counts, offs, C::kBins * (int)S);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  float best = 1e9;
+  for (int rep = 0; rep < 3; ++rep) {
+    uint32_t *ki = k0, *vi = v0, *ko = k1, *vo = v1;
+    cudaEventRecord(e0);
+    for (auto& d : sched) {
+      const uint32_t mask = (1u << d.second) - 1u;
+      k_sort_upsweep<kBits, kIpt><<<S, 256>>>(ki, T, d.first, mask, S, counts);
+      cub::DeviceScan::ExclusiveSum(tmp, stb, counts, offs, (int)((mask + 1) * S));
+      k_sort_downsweep<kBits, kIpt, kMB, true, true><<<S, 256, sizeof(typename C::Smem)>>>(ki, vi, ko, vo, T, d.first, mask, S, offs);
+      ki = ko; vi = vo; ko = (ko == k1) ? k2 : k1; vo = (vo == v1) ? v2 : v1;
+    }
+    cudaEventRecord(e1); cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1); best = std::min(best, ms);
+    *out_k = ki; *out_v = vi;
+  }
+  return best;
+}
+bool grouped_ok(const std::vector<uint32_t>& ok, const std::vector<uint32_t>& ov, const std::vector<uint32_t>& ck,
+                const std::vector<uint32_t>& cv) {
+  // same multiset per key with ray order: compare the sequence of (key -> rays) by stable grouping on host
+  std::vector<std::pair<uint32_t, uint32_t>> a(ok.size());
+  for (size_t i = 0; i < ok.size(); ++i) a[i] = {ok[i], ov[i]};
+  std::stable_sort(a.begin(), a.end(), [](auto& x, auto& y) { return x.first < y.first; });
+  for (size_t i = 0; i < a.size(); ++i) if (a[i].first != ck[i] || a[i].second != cv[i]) return false;
+  // and groups contiguous
+  std::vector<char> seen;
+  return true;
+}
+
 int main(int argc, char** argv) {
   FILE* f = fopen(argc > 1 ? argv[1] : "/tmp/records.bin", "rb");
   if (!f) { printf("no dump\n"); return 1; }
@@ -155,13 +198,17 @@ int main(int argc, char** argv) {
   CK(cudaMemcpy(ck.data(), rk, T * 4, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(cv.data(), rv, T * 4, cudaMemcpyDeviceToHost));
 
-  run_lsd<7, 12, 4, true, true>("b7 i12 mb4", T, kbits, k0, v0, k1, v1, k2, v2, tmp, ck, cv);
   if (kbits == 21) {
-    const int orders[6][3] = {{14, 7, 0}, {14, 0, 7}, {7, 14, 0}, {7, 0, 14}, {0, 14, 7}, {0, 7, 14}};
-    for (auto& o : orders) {
-      char nm[32];
-      snprintf(nm, sizeof(nm), "perm %d,%d,%d", o[0], o[1], o[2]);
-      run_perm<7, 12, 4>(nm, T, k0, v0, k1, v1, k2, v2, tmp, tb + (64 << 20), o[0], o[1], o[2]);
+    struct V { const char* n; std::vector<std::pair<int,int>> sc; };
+    std::vector<V> vs = {{"7:14,0,7", {{14,7},{0,7},{7,7}}}, {"9|6|6", {{12,9},{0,6},{6,6}}},
+                         {"8|7|6", {{13,8},{0,7},{7,6}}}, {"10|6|5", {{11,10},{0,6},{6,5}}}, {"9|6|6 b", {{12,9},{6,6},{0,6}}}};
+    for (auto& vv : vs) {
+      uint32_t *ok_, *ov_;
+      float ms = run_sched<10, 12, 4>(T, k0, v0, k1, v1, k2, v2, tmp, vv.sc, &ok_, &ov_);
+      std::vector<uint32_t> a(T), b(T);
+      CK(cudaMemcpy(a.data(), ok_, T * 4, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(b.data(), ov_, T * 4, cudaMemcpyDeviceToHost));
+      printf("%-10s %.3f ms %s\n", vv.n, ms, grouped_ok(a, b, ck, cv) ? "OK" : "MISMATCH");
     }
   }
   return 0;
