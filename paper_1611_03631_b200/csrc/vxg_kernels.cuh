@@ -1374,49 +1374,41 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_fold_short(
     vxg_voxel* vp = map.slab + c.key;
     VoxState st = load_vox(vp);
     // software pipeline over chunks of kC records: rays gathered two chunks
-    // ahead, weighed one chunk ahead of their fold steps
+    // ahead, weighed one chunk ahead of their fold steps. Positions past the
+    // run re-read its last record and carry w = 0 (a no-op step), so the
+    // loop body has no per-record guards.
     const uint32_t* ids = svals + c.start;
+    const uint32_t last = c.len - 1;
     FoldRay rn[kC];
     Upd xn[kC], xs[kC];
+    auto weigh_at = [&](uint32_t idx, const FoldRay& ry) {
+      Upd x = weigh(ry, poses, c.x0, c.x1, c.x2, tp);
+      x.w = idx <= last ? x.w : 0.0f;
+      return x;
+    };
 #pragma unroll
-    for (int u = 0; u < kC; ++u) {
-      if (u < c.len) rn[u] = rays[ids[u]];
-    }
+    for (int u = 0; u < kC; ++u) rn[u] = rays[ids[min(static_cast<uint32_t>(u), last)]];
 #pragma unroll
-    for (int u = 0; u < kC; ++u) {
-      xn[u].w = 0.0f;
-      if (u < c.len) xn[u] = weigh(rn[u], poses, c.x0, c.x1, c.x2, tp);
-    }
+    for (int u = 0; u < kC; ++u) xn[u] = weigh_at(u, rn[u]);
 #pragma unroll
-    for (int u = 0; u < kC; ++u) {
-      if (kC + u < c.len) rn[u] = rays[ids[kC + u]];
-    }
+    for (int u = 0; u < kC; ++u) rn[u] = rays[ids[min(static_cast<uint32_t>(kC + u), last)]];
     for (uint32_t j = 0; j < c.len; j += kC) {
 #pragma unroll
       for (int u = 0; u < kC; ++u) xs[u] = xn[u];
       // weigh chunk j+kC (gathered last iteration), gather chunk j+2kC
 #pragma unroll
-      for (int u = 0; u < kC; ++u) {
-        if (j + kC + u < c.len) xn[u] = weigh(rn[u], poses, c.x0, c.x1, c.x2, tp);
-      }
+      for (int u = 0; u < kC; ++u) xn[u] = weigh_at(j + kC + u, rn[u]);
 #pragma unroll
-      for (int u = 0; u < kC; ++u) {
-        if (j + 2 * kC + u < c.len) rn[u] = rays[ids[j + 2 * kC + u]];
-      }
+      for (int u = 0; u < kC; ++u) rn[u] = rays[ids[min(j + 2 * kC + u, last)]];
       const VoxState s0 = st;
       bool ok = true;
 #pragma unroll
-      for (int u = 0; u < kC; ++u) {
-        if (j + u < c.len)
-          step_fast_skip(st.D, st.W, st.cr, st.cg, st.cb, xs[u].d, xs[u].w, xs[u].c, tp.truncation, tp.max_weight,
-                         ok);
-      }
+      for (int u = 0; u < kC; ++u)
+        step_fast_skip(st.D, st.W, st.cr, st.cg, st.cb, xs[u].d, xs[u].w, xs[u].c, tp.truncation, tp.max_weight, ok);
       if (!ok) {  // rare: exact re-run of the chunk from its start state
         st = s0;
-        for (int u = 0; u < kC; ++u) {
-          if (j + u < c.len)
-            step_exact(st.D, st.W, st.cr, st.cg, st.cb, xs[u].d, xs[u].w, xs[u].c, tp.truncation, tp.max_weight);
-        }
+        for (int u = 0; u < kC; ++u)
+          step_exact(st.D, st.W, st.cr, st.cg, st.cb, xs[u].d, xs[u].w, xs[u].c, tp.truncation, tp.max_weight);
       }
     }
     store_vox(vp, st);
