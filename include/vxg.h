@@ -96,6 +96,17 @@ int vxg_export_blocks(vxg_handle* h, int32_t* idx, vxg_voxel* voxels, uint64_t c
  * mirror a host layer. */
 int vxg_import_blocks(vxg_handle* h, const int32_t* idx, const vxg_voxel* voxels, uint64_t n);
 
+/* interpolate_distance (interpolation.h:28-60) for n points pts[n*3] (world
+ * frame): trilinear over the 8 surrounding voxel centres; found[i] = 0 when
+ * any corner is unallocated or unobserved (std::nullopt). flags:
+ * VXG_INPUT_DEVICE = pts, d, found are device pointers. */
+int vxg_interpolate_distance(vxg_handle* h, const float* pts, uint64_t n, float* d, uint8_t* found, int flags);
+/* surface_error (analysis.cpp:41-59) of host points against the layer:
+ * out[5] = {rms, mean, max, count, unknown_fraction}. Interpolation on the
+ * GPU; the fp64 accumulation runs in point order on the host, as in the
+ * reference's Accumulator. */
+int vxg_surface_error(vxg_handle* h, const float* pts, uint64_t n, float truncation, double* out);
+
 /* Layer::voxel_ptr (layer.h:99-112) for n global voxel indices g[n*3]:
  * found[i] = 0 (block unallocated: absence, never a default voxel) or 1. */
 int vxg_query_voxels(vxg_handle* h, const int32_t* g, uint64_t n, vxg_voxel* out, uint8_t* found);

@@ -10,6 +10,8 @@
 #include <stdexcept>
 #include <string>
 
+#include "vxf/analysis.h"
+#include "vxf/interpolation.h"
 #include "vxf/layer.h"
 #include "vxf/serialization.h"
 #include "vxf/tsdf_integrator.h"
@@ -153,6 +155,28 @@ size_t vxr_raycast(const float start[3], const float end[3], float voxel_size, i
 
 uint64_t vxr_index_hash(int32_t x, int32_t y, int32_t z) {
   return static_cast<uint64_t>(vxf::IndexHash()(Eigen::Vector3i(x, y, z)));
+}
+
+// interpolate_distance (interpolation.h:28-60) per point: found[i] = 0 when absent.
+void vxr_interpolate(void* hp, const float* pts, size_t n, float* d, uint8_t* found) {
+  const auto& layer = static_cast<RefHandle*>(hp)->layer;
+  for (size_t i = 0; i < n; ++i) {
+    const auto r = vxf::interpolate_distance(layer, vxf::Point(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]));
+    found[i] = r.has_value() ? 1 : 0;
+    d[i] = r.has_value() ? *r : 0.0f;
+  }
+}
+
+// surface_error (analysis.cpp:41-59): out = {rms, mean, max, count, unknown_fraction}.
+void vxr_surface_error(void* hp, const float* pts, size_t n, float truncation, double out[5]) {
+  std::vector<vxf::Point> p(n);
+  for (size_t i = 0; i < n; ++i) p[i] = vxf::Point(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+  const vxf::ErrorStats s = vxf::surface_error(static_cast<RefHandle*>(hp)->layer, p, truncation);
+  out[0] = s.rms;
+  out[1] = s.mean;
+  out[2] = s.max;
+  out[3] = static_cast<double>(s.count);
+  out[4] = s.unknown_fraction;
 }
 
 }  // extern "C"

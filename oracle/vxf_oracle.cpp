@@ -559,3 +559,77 @@ size_t vxo_bucket_schedule(size_t n_points, size_t max_keys, uint64_t* out, size
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- read-side consumers
+// interpolate_distance (interpolation.h:28-60): q = p/v - 0.5 per axis (Eigen
+// Vector3f / scalar then - Constant), base = floor(q), frac = q - base; absent
+// when any of the 8 corners is unallocated or unobserved (weight <= 1e-4,
+// voxel.h:17, core.h:32); lerp along x, then y, then z, no FMA.
+static int oracle_interp(const vxo_layer* l, const float* p, float* out) {
+  const float v = l->voxel_size;
+  float q[3], frac[3];
+  int32_t base[3];
+  for (int i = 0; i < 3; ++i) {
+    q[i] = p[i] / v - 0.5f;
+    base[i] = static_cast<int32_t>(std::floor(q[i]));
+    frac[i] = q[i] - static_cast<float>(base[i]);
+  }
+  float corner[2][2][2];
+  for (int dz = 0; dz < 2; ++dz)
+    for (int dy = 0; dy < 2; ++dy)
+      for (int dx = 0; dx < 2; ++dx) {
+        vxg_voxel vx;
+        if (!vxo_voxel(l, base[0] + dx, base[1] + dy, base[2] + dz, &vx) || !(vx.weight > 1e-4f)) return 0;
+        corner[dx][dy][dz] = vx.distance;
+      }
+  float plane[2][2];
+  for (int dy = 0; dy < 2; ++dy)
+    for (int dz = 0; dz < 2; ++dz) {
+      const float diff = corner[1][dy][dz] - corner[0][dy][dz];
+      const float prod = frac[0] * diff;
+      plane[dy][dz] = corner[0][dy][dz] + prod;
+    }
+  float line[2];
+  for (int dz = 0; dz < 2; ++dz) {
+    const float diff = plane[1][dz] - plane[0][dz];
+    const float prod = frac[1] * diff;
+    line[dz] = plane[0][dz] + prod;
+  }
+  const float diff = line[1] - line[0];
+  const float prod = frac[2] * diff;
+  *out = line[0] + prod;
+  return 1;
+}
+
+extern "C" void vxo_interpolate(const vxo_layer* l, const float* pts, size_t n, float* d, uint8_t* found) {
+  for (size_t i = 0; i < n; ++i) {
+    float r = 0.0f;
+    found[i] = static_cast<uint8_t>(oracle_interp(l, pts + 3 * i, &r));
+    d[i] = found[i] ? r : 0.0f;
+  }
+}
+
+// surface_error (analysis.cpp:41-59, Accumulator :16-37): fp64 sequential sums
+// in point order of clamp(d, -truncation, truncation).
+extern "C" void vxo_surface_error(const vxo_layer* l, const float* pts, size_t n, float truncation, double out[5]) {
+  double sum = 0.0, sum_sq = 0.0, max_abs = 0.0;
+  size_t count = 0, unknown = 0;
+  for (size_t i = 0; i < n; ++i) {
+    float r;
+    if (!oracle_interp(l, pts + 3 * i, &r)) {
+      ++unknown;
+      continue;
+    }
+    const float c = r < -truncation ? -truncation : (truncation < r ? truncation : r);
+    const double e = static_cast<double>(c);
+    sum += e;
+    sum_sq += e * e;
+    max_abs = std::max(max_abs, std::abs(e));
+    ++count;
+  }
+  out[0] = count ? std::sqrt(sum_sq / static_cast<double>(count)) : 0.0;
+  out[1] = count ? sum / static_cast<double>(count) : 0.0;
+  out[2] = count ? max_abs : 0.0;
+  out[3] = static_cast<double>(count);
+  out[4] = n ? static_cast<double>(unknown) / static_cast<double>(n) : 0.0;
+}

@@ -86,6 +86,12 @@ size_t vxo_grouped_ray_order(const vxg_tsdf_config* c, float voxel_size, const f
  * pairs; entry 0 is (0, initial bucket count). Returns the number of entries. */
 size_t vxo_bucket_schedule(size_t n_points, size_t max_keys, uint64_t* out, size_t cap);
 
+/* Read-side consumers: interpolate_distance (interpolation.h:28-60) per point
+ * (found[i] = 0: absent) and surface_error (analysis.cpp:41-59), out =
+ * {rms, mean, max, count, unknown_fraction}. */
+void vxo_interpolate(const vxo_layer* l, const float* pts, size_t n, float* d, uint8_t* found);
+void vxo_surface_error(const vxo_layer* l, const float* pts, size_t n, float truncation, double out[5]);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1554,6 +1554,59 @@ __global__ void k_query(uint64_t n, const int32_t* __restrict__ g, MapView map, 
   }
 }
 
+// interpolate_distance (interpolation.h:28-60): trilinear over the 8 voxel
+// centres around p, absent when any corner is unallocated or unobserved
+// (weight <= kTsdfObservedWeight, voxel.h:17). One thread per point; the 8
+// corners share at most 8 blocks, looked up through the device hash.
+__device__ __forceinline__ bool corner_distance(const MapView& map, int gx, int gy, int gz, float* d) {
+  const int b0 = floor_div(gx, map.vps), b1 = floor_div(gy, map.vps), b2 = floor_div(gz, map.vps);
+  if (!block_in_range(b0, b1, b2)) return false;
+  const int32_t s = map.find(pack_block(b0, b1, b2));
+  if (s < 0 || static_cast<uint32_t>(s) >= map.cap_blocks) return false;
+  const vxg_voxel& v = map.slab[static_cast<uint64_t>(s) * map.nvox + (gx - b0 * map.vps) +
+                               map.vps * ((gy - b1 * map.vps) + map.vps * (gz - b2 * map.vps))];
+  if (!(v.weight > 1e-4f)) return false;
+  *d = v.distance;
+  return true;
+}
+
+__global__ void k_interpolate(uint64_t n, const float* __restrict__ pts, MapView map, float voxel_size,
+                              float* __restrict__ out, uint8_t* __restrict__ found) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    float q[3], frac[3];
+    int base[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {  // q = p / v - 0.5 (Eigen: per-component quotient, then difference)
+      q[a] = fsub(fdiv(pts[3 * i + a], voxel_size), 0.5f);
+      base[a] = static_cast<int>(floorf(q[a]));
+      frac[a] = fsub(q[a], static_cast<float>(base[a]));
+    }
+    float c[2][2][2];
+    bool ok = true;
+#pragma unroll
+    for (int dz = 0; dz < 2; ++dz)
+#pragma unroll
+      for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < 2; ++dx)
+          ok = ok && corner_distance(map, base[0] + dx, base[1] + dy, base[2] + dz, &c[dx][dy][dz]);
+    float r = 0.0f;
+    if (ok) {
+      float plane[2][2], line[2];
+#pragma unroll
+      for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+        for (int dz = 0; dz < 2; ++dz) plane[dy][dz] = fadd(c[0][dy][dz], fmul(frac[0], fsub(c[1][dy][dz], c[0][dy][dz])));
+#pragma unroll
+      for (int dz = 0; dz < 2; ++dz) line[dz] = fadd(plane[0][dz], fmul(frac[1], fsub(plane[1][dz], plane[0][dz])));
+      r = fadd(line[0], fmul(frac[2], fsub(line[1], line[0])));
+    }
+    out[i] = r;
+    found[i] = ok ? 1u : 0u;
+  }
+}
+
 // ---------------------------------------------------------------- free-function evaluation
 __global__ void k_eval_pd(uint64_t n, const float* x, const float* p, const float* s, float* out) {
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;

@@ -1690,6 +1690,66 @@ int vxg_query_voxels(vxg_handle* h, const int32_t* g, uint64_t n, vxg_voxel* out
   });
 }
 
+int vxg_interpolate_distance(vxg_handle* h, const float* pts, uint64_t n, float* d, uint8_t* found, int flags) {
+  return guarded([&] {
+    set_device(h);
+    if (n == 0) return;
+    if (pts == nullptr || d == nullptr || found == nullptr) throw VxgError(VXG_EINVAL, "null argument");
+    if (flags & VXG_INPUT_DEVICE) {
+      k_interpolate<<<grid_for(n), 256, 0, h->st>>>(n, pts, h->view(), h->voxel_size, d, found);
+      ++h->launches;
+      CU(cudaGetLastError());
+      CU(cudaStreamSynchronize(h->st));
+      return;
+    }
+    DBuf<float> dp, dd;
+    DBuf<uint8_t> df;
+    dp.ensure(3 * n);
+    dd.ensure(n);
+    df.ensure(n);
+    CU(cudaMemcpyAsync(dp.p, pts, 3 * n * sizeof(float), cudaMemcpyHostToDevice, h->st));
+    k_interpolate<<<grid_for(n), 256, 0, h->st>>>(n, dp.p, h->view(), h->voxel_size, dd.p, df.p);
+    ++h->launches;
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(d, dd.p, n * sizeof(float), cudaMemcpyDeviceToHost, h->st));
+    CU(cudaMemcpyAsync(found, df.p, n, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaStreamSynchronize(h->st));
+  });
+}
+
+int vxg_surface_error(vxg_handle* h, const float* pts, uint64_t n, float truncation, double* out) {
+  return guarded([&] {
+    if (out == nullptr) throw VxgError(VXG_EINVAL, "null argument");
+    std::vector<float> d(n);
+    std::vector<uint8_t> found(n);
+    if (n) {
+      const int rc = vxg_interpolate_distance(h, pts, n, d.data(), found.data(), 0);
+      if (rc != VXG_OK) throw VxgError(rc, vxg_last_error());
+    }
+    // Accumulator (analysis.cpp:16-37): fp64 sums in point order over the
+    // interpolated distances the GPU returned, clamped to the truncation.
+    double sum = 0.0, sum_sq = 0.0, max_abs = 0.0;
+    uint64_t count = 0, unknown = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+      if (!found[i]) {
+        ++unknown;
+        continue;
+      }
+      const float c = d[i] < -truncation ? -truncation : (truncation < d[i] ? truncation : d[i]);
+      const double e = static_cast<double>(c);
+      sum += e;
+      sum_sq += e * e;
+      max_abs = std::max(max_abs, std::abs(e));
+      ++count;
+    }
+    out[0] = count ? std::sqrt(sum_sq / static_cast<double>(count)) : 0.0;
+    out[1] = count ? sum / static_cast<double>(count) : 0.0;
+    out[2] = count ? max_abs : 0.0;
+    out[3] = static_cast<double>(count);
+    out[4] = n ? static_cast<double>(unknown) / static_cast<double>(n) : 0.0;
+  });
+}
+
 int vxg_serialize_vxblx(vxg_handle* h, uint8_t* buf, uint64_t cap, uint64_t* need) {
   return guarded([&] {
     set_device(h);

@@ -180,6 +180,25 @@ class TsdfLayer:
             check(lib().vxg_query_voxels(self._h, _ptr(g), len(g), _ptr(out), _ptr(found)))
         return out, found.astype(bool)
 
+    def interpolate_distance(self, points: np.ndarray) -> Tuple[np.ndarray, np.ndarray]:
+        """interpolate_distance (interpolation.h:28-60) for many world points:
+        (distance, found); found is False where the reference returns nullopt."""
+        p = np.ascontiguousarray(points, dtype=np.float32).reshape(-1, 3)
+        d = np.zeros(len(p), dtype=np.float32)
+        found = np.zeros(len(p), dtype=np.uint8)
+        if len(p):
+            check(lib().vxg_interpolate_distance(self._h, _ptr(p), len(p), _ptr(d), _ptr(found), 0))
+        return d, found.astype(bool)
+
+    def surface_error(self, ground_truth_points: np.ndarray, truncation: float) -> Dict[str, float]:
+        """surface_error (analysis.cpp:41-59): ErrorStats as a dict
+        (rms, mean, max, count, unknown_fraction)."""
+        p = np.ascontiguousarray(ground_truth_points, dtype=np.float32).reshape(-1, 3)
+        out = np.zeros(5, dtype=np.float64)
+        check(lib().vxg_surface_error(self._h, _ptr(p), len(p), float(truncation), _ptr(out)))
+        return {"rms": float(out[0]), "mean": float(out[1]), "max": float(out[2]), "count": int(out[3]),
+                "unknown_fraction": float(out[4])}
+
     def voxel_ptr(self, g) -> Optional[np.void]:
         """Layer::voxel_ptr (layer.h:99-112): None when the block is unallocated."""
         out, found = self.query(np.asarray(g, dtype=np.int32).reshape(1, 3))

@@ -56,6 +56,8 @@ def oracle_lib():
         L.vxo_grouped_ray_order.restype = c_size_t
         L.vxo_grouped_ray_order.argtypes = [POINTER(VxgTsdfConfig), c_float, c_void_p, c_size_t, POINTER(c_float),
                                             c_void_p, c_size_t]
+        L.vxo_interpolate.argtypes = [c_void_p, c_void_p, c_size_t, c_void_p, c_void_p]
+        L.vxo_surface_error.argtypes = [c_void_p, c_void_p, c_size_t, c_float, c_void_p]
         L.vxo_bucket_schedule.restype = c_size_t
         L.vxo_bucket_schedule.argtypes = [c_size_t, c_size_t, c_void_p, c_size_t]
         _oracle = L
@@ -89,6 +91,8 @@ def ref_lib():
         L.vxr_raycast.argtypes = [POINTER(c_float), POINTER(c_float), c_float, c_void_p, c_size_t]
         L.vxr_index_hash.restype = c_uint64
         L.vxr_index_hash.argtypes = [c_int32, c_int32, c_int32]
+        L.vxr_interpolate.argtypes = [c_void_p, c_void_p, c_size_t, c_void_p, c_void_p]
+        L.vxr_surface_error.argtypes = [c_void_p, c_void_p, c_size_t, c_float, c_void_p]
         _ref = L
     return _ref
 
@@ -128,6 +132,12 @@ class OracleLayer:
             raise ValueError("oracle rejected the config")
         return int(st.updates), int(st.raycasts), int(st.skipped)
 
+    def interpolate_distance(self, points):
+        return _interp(self.L.vxo_interpolate, self.h, points)
+
+    def surface_error(self, points, truncation):
+        return _surface_error(self.L.vxo_surface_error, self.h, points, truncation)
+
     def block_count(self):
         return int(self.L.vxo_block_count(self.h))
 
@@ -149,6 +159,22 @@ class OracleLayer:
         i = np.ascontiguousarray(idx, dtype=np.int32)
         v = np.ascontiguousarray(voxels)
         self.L.vxo_set_block(self.h, _vp(i), _vp(v))
+
+
+def _interp(fn, h, points):
+    p = np.ascontiguousarray(points, dtype=np.float32).reshape(-1, 3)
+    d = np.zeros(len(p), dtype=np.float32)
+    f = np.zeros(len(p), dtype=np.uint8)
+    fn(h, _vp(p), len(p), _vp(d), _vp(f))
+    return d, f.astype(bool)
+
+
+def _surface_error(fn, h, points, truncation):
+    p = np.ascontiguousarray(points, dtype=np.float32).reshape(-1, 3)
+    out = np.zeros(5, dtype=np.float64)
+    fn(h, _vp(p), len(p), float(truncation), _vp(out))
+    return {"rms": float(out[0]), "mean": float(out[1]), "max": float(out[2]), "count": int(out[3]),
+            "unknown_fraction": float(out[4])}
 
 
 class RefLayer:
@@ -175,6 +201,12 @@ class RefLayer:
         if rc != 0:
             raise ValueError(self.L.vxr_last_error().decode())
         return int(st.updates), int(st.raycasts), int(st.skipped)
+
+    def interpolate_distance(self, points):
+        return _interp(self.L.vxr_interpolate, self.h, points)
+
+    def surface_error(self, points, truncation):
+        return _surface_error(self.L.vxr_surface_error, self.h, points, truncation)
 
     def block_count(self):
         return int(self.L.vxr_block_count(self.h))
