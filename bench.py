@@ -164,6 +164,8 @@ def main():
     ap.add_argument("--ref-frames", type=int, default=10)
     ap.add_argument("--cpu-frames", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--replicated", action="store_true",
+                    help="N>1: replicated traversal (every rank walks all rays, no record exchange)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -198,7 +200,7 @@ def main():
         from paper_1611_03631_b200 import nccl_unique_id
         obj = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        layer.shard_init(rank, world, obj[0])
+        layer.shard_init(rank, world, obj[0], replicated=args.replicated)
     integ = TsdfIntegrator(cfg, layer)
 
     d_xyz = torch.from_numpy(xyz).cuda()
@@ -317,8 +319,10 @@ def main():
             "config": {"workload": wc.name, "frames_per_step": F, "points_per_step": P, "updates_per_step": n_upd,
                        "merge": "grouped", "weight": "inverse_z2_dropoff", "voxel_size": wc.voxel_size,
                        "truncation": wc.truncation, "l2": "inputs 460 MB > 126 MB L2 (no flush)",
-                       "parallelism": (f"map sharded by block owner over {world} ranks, NCCL all-to-all of update "
-                                       f"records" if world > 1 else "1 GPU")},
+                       "parallelism": ((f"map sharded by block owner over {world} ranks, replicated traversal "
+                                        f"(no record exchange)" if args.replicated else
+                                        f"map sharded by block owner over {world} ranks, NCCL all-to-all of update "
+                                        f"records") if world > 1 else "1 GPU")},
             "e2e": {"value": total_updates / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
             "roofline": roofline,

@@ -143,12 +143,21 @@ int vxg_nccl_unique_id(uint8_t* out);
  * an NCCL communicator from id_bytes. vxg_integrate_* then run sharded and
  * return the global per-frame counters on every rank. */
 int vxg_shard_init(vxg_handle* h, int rank, int world, const uint8_t* id_bytes);
+/* Sharding mode (SURVEY.md 8e fallback): on = replicated traversal — every
+ * rank walks ALL rays and keeps only the records of the blocks it owns, so no
+ * update records are exchanged (only the per-frame counters are summed) at the
+ * cost of G x the walk. off (default) = each rank walks its slice of the ray
+ * order and owners receive their records with one all-to-all. Same result
+ * either way. */
+int vxg_shard_set_replicated(vxg_handle* h, int on);
 /* Loopback group: `world` shards on ONE device in one process, exchanging
  * records with device-to-device copies (the sharded kernels without NVLink);
  * used to test the sharded path on a single GPU. */
 typedef struct vxg_group vxg_group;
 int vxg_group_create(const vxg_tsdf_config* config, float voxel_size, int voxels_per_side, int device, int world,
                      uint64_t block_capacity, vxg_group** out);
+/* vxg_shard_set_replicated for every shard of a loopback group. */
+int vxg_group_set_replicated(vxg_group* g, int on);
 int vxg_group_destroy(vxg_group* g);
 int vxg_group_shard(vxg_group* g, int i, vxg_handle** out);
 int vxg_group_set_config(vxg_group* g, const vxg_tsdf_config* config);

@@ -76,6 +76,8 @@ SIGNATURES = [
     ("vxg_kernel_launches", c_int, [c_void_p, POINTER(c_uint64), c_int]),
     ("vxg_nccl_unique_id", c_int, [c_void_p]),
     ("vxg_shard_init", c_int, [c_void_p, c_int, c_int, c_void_p]),
+    ("vxg_shard_set_replicated", c_int, [c_void_p, c_int]),
+    ("vxg_group_set_replicated", c_int, [c_void_p, c_int]),
     ("vxg_group_create", c_int, [POINTER(VxgTsdfConfig), c_float, c_int, c_int, c_int, c_uint64, POINTER(c_void_p)]),
     ("vxg_group_destroy", c_int, [c_void_p]),
     ("vxg_group_shard", c_int, [c_void_p, c_int, POINTER(c_void_p)]),

@@ -650,7 +650,8 @@ __global__ void __launch_bounds__(128) k_emit_sharded(uint32_t R0, uint32_t R1, 
                                                       uint32_t world, TermView tv,
                                                       unsigned long long* __restrict__ gkeys,
                                                       uint32_t* __restrict__ gvals, uint32_t* __restrict__ owner,
-                                                      uint32_t* __restrict__ counters) {
+                                                      uint32_t* __restrict__ counters, int keep_owner) {
+  // keep_owner >= 0 (replicated traversal): records of other owners are dropped
   const float v = tp.voxel_size;
   const bool anti = tp.merge_mode == VXG_MERGE_GROUPED_ANTI_GRAZE;
   for (uint32_t j = R0 + blockIdx.x * blockDim.x + threadIdx.x; j < R1; j += gridDim.x * blockDim.x) {
@@ -715,6 +716,7 @@ __global__ void __launch_bounds__(128) k_emit_sharded(uint32_t R0, uint32_t R1, 
         }
       }
       const uint64_t o_idx = out0 + k;
+      if (keep_owner >= 0 && own != static_cast<uint32_t>(keep_owner)) own = world;
       gkeys[o_idx] = key;
       gvals[o_idx] = j;
       owner[o_idx] = own;

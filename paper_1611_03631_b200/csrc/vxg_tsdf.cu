@@ -415,6 +415,14 @@ struct vxg_handle {
   // ---- sharded map (multi-GPU / loopback group)
   int shard_rank = 0;
   int shard_world = 1;
+  bool shard_replicated = false;  // replicated traversal, no record exchange
+  // records this rank folds: received (exchange) or its own partition (replicated)
+  const uint4* owned_records() const {
+    return shard_replicated ? send_buf.p + send_offsets[shard_rank] : recv_buf.p;
+  }
+  uint64_t owned_count() const {
+    return shard_replicated ? (send_counts.empty() ? 0 : send_counts[shard_rank]) : recv_total;
+  }
   void* nccl_comm = nullptr;
   std::vector<uint64_t> send_counts, send_offsets, recv_counts;
   uint64_t recv_total = 0;
@@ -1053,8 +1061,8 @@ void vxg_handle::run_sub(const float* xyz, const uint8_t* rgb, const uint64_t* o
   if (shard_world > 1) {
     if (nccl_comm == nullptr) throw VxgError(VXG_EINVAL, "sharded handle without a communicator (vxg_shard_init)");
     shard_front(R, static_cast<uint32_t>(F), tv);
-    nccl_exchange();
-    shard_back(recv_buf.p, recv_total, static_cast<uint32_t>(F));
+    if (!shard_replicated) nccl_exchange();
+    shard_back(owned_records(), owned_count(), static_cast<uint32_t>(F));
     nccl_reduce_updates(static_cast<uint32_t>(F));
   } else if (R > 0) {
     emit_and_apply(R, static_cast<uint32_t>(F), tv);
@@ -1074,20 +1082,24 @@ void vxg_handle::shard_front(uint32_t R, uint32_t F, const TermView& tv) {
   if (R == 0) return;
   const TsdfParams tp = params();
   const uint64_t total = count_rays(R, F);
-  // this rank's ray slice: records [rank*total/world, (rank+1)*total/world)
-  sbounds.ensure(2);
-  const uint64_t lo_rec = total * static_cast<uint64_t>(shard_rank) / shard_world;
-  const uint64_t hi_rec = total * static_cast<uint64_t>(shard_rank + 1) / shard_world;
-  k_ray_bounds<<<1, 32, 0, st>>>(R, roff.p, lo_rec, hi_rec, sbounds.p);
-  ++launches;
-  unsigned long long hb[2];
-  CU(cudaMemcpyAsync(hb, sbounds.p, sizeof(hb), cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
-  const uint32_t R0 = static_cast<uint32_t>(hb[0]), R1 = static_cast<uint32_t>(hb[1]);
+  uint32_t R0 = 0, R1 = R;
   unsigned long long base = 0, endrec = total;
-  if (R0 < R) CU(cudaMemcpy(&base, roff.p + R0, sizeof(base), cudaMemcpyDeviceToHost));
-  else base = total;
-  if (R1 < R) CU(cudaMemcpy(&endrec, roff.p + R1, sizeof(endrec), cudaMemcpyDeviceToHost));
+  if (!shard_replicated) {
+    // this rank's ray slice: records [rank*total/world, (rank+1)*total/world)
+    sbounds.ensure(2);
+    const uint64_t lo_rec = total * static_cast<uint64_t>(shard_rank) / shard_world;
+    const uint64_t hi_rec = total * static_cast<uint64_t>(shard_rank + 1) / shard_world;
+    k_ray_bounds<<<1, 32, 0, st>>>(R, roff.p, lo_rec, hi_rec, sbounds.p);
+    ++launches;
+    unsigned long long hb[2];
+    CU(cudaMemcpyAsync(hb, sbounds.p, sizeof(hb), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    R0 = static_cast<uint32_t>(hb[0]);
+    R1 = static_cast<uint32_t>(hb[1]);
+    if (R0 < R) CU(cudaMemcpy(&base, roff.p + R0, sizeof(base), cudaMemcpyDeviceToHost));
+    else base = total;
+    if (R1 < R) CU(cudaMemcpy(&endrec, roff.p + R1, sizeof(endrec), cudaMemcpyDeviceToHost));
+  }  // replicated traversal (SURVEY.md 8e fallback): every rank walks all rays, keeps its own blocks
   const uint64_t T = endrec - base;
   if (T == 0) return;
   begin(ST_EMIT);
@@ -1099,7 +1111,7 @@ void vxg_handle::shard_front(uint32_t R, uint32_t F, const TermView& tv) {
   gperm.ensure(T);
   k_emit_sharded<<<grid_for(R1 - R0, 128), 128, 0, st>>>(R0, R1, rays.p, roff.p, base, d_poses.p, tp, vps,
                                                           static_cast<uint32_t>(shard_world), tv, gkeys.p, gvals.p,
-                                                          gowner.p, counters.p);
+                                                          gowner.p, counters.p, shard_replicated ? shard_rank : -1);
   k_iota<<<grid_for(T), 256, 0, st>>>(static_cast<uint32_t>(T), giota.p);
   launches += 2;
   CU(cudaGetLastError());
@@ -2013,6 +2025,18 @@ int vxg_nccl_unique_id(uint8_t* out) {
   });
 }
 
+int vxg_shard_set_replicated(vxg_handle* h, int on) {
+  if (h == nullptr) return VXG_EINVAL;
+  h->shard_replicated = on != 0;
+  return VXG_OK;
+}
+
+int vxg_group_set_replicated(vxg_group* g, int on) {
+  if (g == nullptr) return VXG_EINVAL;
+  for (vxg_handle* h : g->shards) h->shard_replicated = on != 0;
+  return VXG_OK;
+}
+
 int vxg_shard_init(vxg_handle* h, int rank, int world, const uint8_t* id_bytes) {
   return guarded([&] {
     if (world < 1 || rank < 0 || rank >= world) throw VxgError(VXG_EINVAL, "invalid shard rank / world");
@@ -2105,8 +2129,8 @@ int vxg_group_integrate_packed(vxg_group* g, const float* xyz, const uint8_t* rg
       std::vector<TermView> tv(W);
       for (int r = 0; r < W; ++r) g->shards[r]->begin_batch(dx, dc, off.data() + f0, poses + 12 * f0, nF, &R[r], &tv[r]);
       for (int r = 0; r < W; ++r) g->shards[r]->shard_front(R[r], static_cast<uint32_t>(nF), tv[r]);
-      group_exchange(g);
-      for (int r = 0; r < W; ++r) g->shards[r]->shard_back(g->shards[r]->recv_buf.p, g->shards[r]->recv_total,
+      if (!g->shards[0]->shard_replicated) group_exchange(g);
+      for (int r = 0; r < W; ++r) g->shards[r]->shard_back(g->shards[r]->owned_records(), g->shards[r]->owned_count(),
                                                            static_cast<uint32_t>(nF));
       for (int r = 0; r < W; ++r) {
         st[r].assign(nF, vxg_stats{0, 0, 0});

@@ -261,11 +261,14 @@ class TsdfLayer:
         return {"records": int(out[0]), "n_vox": int(out[1]), "max_chain": int(out[2]), "blocks": int(out[3]),
                 "sort_passes": int(out[4])}
 
-    def shard_init(self, rank: int, world: int, nccl_id: bytes = b"") -> None:
+    def shard_init(self, rank: int, world: int, nccl_id: bytes = b"", replicated: bool = False) -> None:
         """Makes this layer shard `rank` of `world` (one process per GPU, NCCL
-        all-to-all of update records between shards)."""
+        all-to-all of update records between shards).
+        replicated=True: every rank walks all rays and keeps its own blocks'
+        records (no record exchange)."""
         buf = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id.ljust(128, b"\0")[:128])
         check(lib().vxg_shard_init(self._h, int(rank), int(world), buf))
+        check(lib().vxg_shard_set_replicated(self._h, 1 if replicated else 0))
 
     def set_stream(self, stream_ptr: Optional[int]) -> None:
         check(lib().vxg_set_stream(self._h, ctypes.c_void_p(stream_ptr) if stream_ptr else None))
@@ -359,7 +362,7 @@ class ShardGroup:
     the single-GPU test vehicle of the multi-GPU path (vxg_group_*)."""
 
     def __init__(self, config: TsdfConfig, voxel_size: float, voxels_per_side: int = 16, world: int = 2,
-                 device: int = 0, block_capacity: int = 0):
+                 device: int = 0, block_capacity: int = 0, replicated: bool = False):
         config.validate()
         self._voxel_size = float(np.float32(voxel_size))
         self._vps = int(voxels_per_side)
@@ -367,6 +370,7 @@ class ShardGroup:
         c = config.to_c()
         check(lib().vxg_group_create(ctypes.byref(c), self._voxel_size, self._vps, int(device), int(world),
                                      int(block_capacity), ctypes.byref(self._g)))
+        check(lib().vxg_group_set_replicated(self._g, 1 if replicated else 0))
         self.world = int(world)
 
     def __del__(self):

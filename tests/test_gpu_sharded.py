@@ -56,3 +56,21 @@ def test_sharded_full_frames(gpu):
     s4 = g.integrate_batch([Scan(*f) for f in frames])
     assert (s1 == s4).all()
     assert g.save_bytes() == single.save_bytes()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("cfg_id", [1, 3])
+def test_replicated_traversal_equals_oracle(gpu, world, cfg_id):
+    """SURVEY.md 8e fallback: every shard walks all rays and keeps only its own
+    blocks' records (no record exchange); same layer, same counters."""
+    wc = W.CONFIGS[cfg_id]
+    cfg = W.tsdf_config(wc)
+    frames = W.frames(cfg_id, count=3, scale=0.2, start=4)
+    ora = OracleLayer(cfg, wc.voxel_size, wc.vps)
+    o_stats = [list(ora.integrate(*f)) for f in frames]
+    g = ShardGroup(cfg, wc.voxel_size, wc.vps, world=world, replicated=True)
+    stats = [[int(v) for v in r] for r in g.integrate_batch([Scan(*f) for f in frames])]
+    assert stats == o_stats
+    got, exp = g.save_bytes(), ora.save_bytes()
+    assert got == exp, diff_report(got, exp)
+    assert sum(1 for c in g.shard_block_counts() if c > 0) > 1

@@ -89,7 +89,7 @@ def fold_records(recs, cfg, vps):
     return {k: bytes(v) for k, v in state.items()}
 
 
-def _worker(rank, world, port, cfg_id, vps, result_path):
+def _worker(rank, world, port, cfg_id, vps, result_path, replicated=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -97,25 +97,32 @@ def _worker(rank, world, port, cfg_id, vps, result_path):
         recs, lay, cfg, v = trace_scan(cfg_id, vps)  # step 1: identical on every rank
         T = len(recs)
         ray = recs[:, 0].astype(np.int64)
-        # step 2: ray-aligned slice of the record range
-        lo, hi = T * rank // world, T * (rank + 1) // world
-        starts = np.searchsorted(ray, np.unique(ray))  # record offset of each ray (records grouped by ray)
-        roff = np.append(starts, T)
-        first = lambda target: int(roff[np.searchsorted(roff, target)])  # first ray offset >= target
-        s0, s1 = first(lo), first(hi)
-        mine = recs[s0:s1]
-        # step 3: stable partition by block owner
-        g = mine[:, 1:4].view(np.int32)
-        owners = np.array([owner_of([floor_div(int(a), vps) for a in row], world) for row in g], np.int64)
-        send = [np.ascontiguousarray(mine[owners == o]) for o in range(world)]
-        # step 4: all-to-all (counts, then records)
-        sc = torch.tensor([len(s) for s in send], dtype=torch.int64)
-        rc = torch.zeros(world, dtype=torch.int64)
-        dist.all_to_all_single(rc, sc)
-        send_t = torch.from_numpy(np.concatenate(send).view(np.int32).reshape(-1, 7)) if T else torch.zeros((0, 7), dtype=torch.int32)
-        recv_t = torch.zeros((int(rc.sum()), 7), dtype=torch.int32)
-        dist.all_to_all_single(recv_t, send_t, output_split_sizes=rc.tolist(), input_split_sizes=sc.tolist())
-        got = recv_t.numpy().view(np.uint32)  # step 5: source-rank order preserved by all_to_all_single
+        if replicated:
+            # replicated traversal (SURVEY.md 8e fallback): every rank walks all
+            # rays and keeps the records of the blocks it owns; no exchange
+            g = recs[:, 1:4].view(np.int32)
+            owners = np.array([owner_of([floor_div(int(a), vps) for a in row], world) for row in g], np.int64)
+            got = np.ascontiguousarray(recs[owners == rank])
+        else:
+            # step 2: ray-aligned slice of the record range
+            lo, hi = T * rank // world, T * (rank + 1) // world
+            starts = np.searchsorted(ray, np.unique(ray))  # record offset of each ray (records grouped by ray)
+            roff = np.append(starts, T)
+            first = lambda target: int(roff[np.searchsorted(roff, target)])  # first ray offset >= target
+            s0, s1 = first(lo), first(hi)
+            mine = recs[s0:s1]
+            # step 3: stable partition by block owner
+            g = mine[:, 1:4].view(np.int32)
+            owners = np.array([owner_of([floor_div(int(a), vps) for a in row], world) for row in g], np.int64)
+            send = [np.ascontiguousarray(mine[owners == o]) for o in range(world)]
+            # step 4: all-to-all (counts, then records)
+            sc = torch.tensor([len(s) for s in send], dtype=torch.int64)
+            rc = torch.zeros(world, dtype=torch.int64)
+            dist.all_to_all_single(rc, sc)
+            send_t = torch.from_numpy(np.concatenate(send).view(np.int32).reshape(-1, 7)) if T else torch.zeros((0, 7), dtype=torch.int32)
+            recv_t = torch.zeros((int(rc.sum()), 7), dtype=torch.int32)
+            dist.all_to_all_single(recv_t, send_t, output_split_sizes=rc.tolist(), input_split_sizes=sc.tolist())
+            got = recv_t.numpy().view(np.uint32)  # step 5: source-rank order preserved by all_to_all_single
         shard = fold_records(got, cfg, vps)
         shards = [None] * world
         dist.all_gather_object(shards, shard)
@@ -150,10 +157,11 @@ def _free_port():
     return port
 
 
+@pytest.mark.parametrize("replicated", [False, True])
 @pytest.mark.parametrize("cfg_id,vps", [(1, 16), (3, 8)])
-def test_sharded_protocol_world2(tmp_path, cfg_id, vps):
+def test_sharded_protocol_world2(tmp_path, cfg_id, vps, replicated):
     result = tmp_path / "result.txt"
-    mp.spawn(_worker, args=(2, _free_port(), cfg_id, vps, str(result)), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), cfg_id, vps, str(result), replicated), nprocs=2, join=True)
     ok_fold, ok_layer, busy, nvox = map(int, result.read_text().split())
     assert nvox > 1000
     assert ok_layer, "single-process fold of the trace differs from the oracle layer"
