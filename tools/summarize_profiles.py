@@ -62,6 +62,9 @@ def full_capture(rep):
     return res
 
 
+RECORD_SORT = "<7,"
+
+
 def main():
     tag, launches, rep, passes = sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4])
     bench = json.load(open(sys.argv[5])) if len(sys.argv) > 5 else None
@@ -92,9 +95,11 @@ def main():
                    if any(n in m["kernel"] for n in names))
 
     # one launch of each sort kernel was captured per pass position; scale one pass by the pass count
-    sort_caps = [m for m in caps if "k_sort_" in m["kernel"]]
+    # (the record sort is the 7-bit-digit instantiation; <8, ...> is the bundling key sort)
+    sort_caps = [m for m in caps if "k_sort_" in m["kernel"] and RECORD_SORT in m["kernel"]]
     n_sort_launches = max(1, len([m for m in sort_caps if "downsweep" in m["kernel"]]))
-    sort_step = dram(["k_sort_downsweep", "k_sort_upsweep"]) * passes / n_sort_launches
+    sort_step = sum(m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
+                    for m in sort_caps) * passes / n_sort_launches
     apply_step = dram(["k_fold_runs", "k_fold_short"])
     inputs = {"record_sort_dram_bytes_per_step": sort_step, "apply_dram_bytes_per_step": apply_step,
               "source": f"profiles/{tag}_summary.json", "sort_passes": passes}
