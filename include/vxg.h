@@ -82,6 +82,20 @@ int vxg_integrate_batch(vxg_handle* h, const vxg_frame* frames, uint64_t n_frame
 int vxg_integrate_packed(vxg_handle* h, const float* xyz, const uint8_t* rgb, const uint64_t* offsets,
                          const float* poses, uint64_t n_frames, int flags, vxg_stats* out);
 
+/* Streaming ingestion (double-buffered staging of packed batches).
+ * vxg_stage_packed starts the asynchronous host->device copy of a packed batch
+ * (xyz/rgb in pinned host memory for a truly asynchronous copy; layout as in
+ * vxg_integrate_packed) into one of two staging slots on the handle's copy
+ * stream and returns at once (*slot = the slot id). vxg_integrate_staged then
+ * integrates that staged batch with n_frames poses: layer and stats identical
+ * to vxg_integrate_packed on the same inputs. Staging batch k+1 before
+ * integrating batch k overlaps its copy with batch k's compute. At most two
+ * batches may be staged and not yet integrated (VXG_EINVAL otherwise); the
+ * host buffers must stay valid until the matching vxg_integrate_staged returns. */
+int vxg_stage_packed(vxg_handle* h, const float* xyz, const uint8_t* rgb, const uint64_t* offsets,
+                     uint64_t n_frames, int* slot);
+int vxg_integrate_staged(vxg_handle* h, int slot, const float* poses, vxg_stats* out);
+
 /* Layer::block_count() (layer.h:72). */
 int vxg_block_count(vxg_handle* h, uint64_t* out);
 

@@ -56,6 +56,8 @@ SIGNATURES = [
     ("vxg_integrate_batch", c_int, [c_void_p, POINTER(VxgFrame), c_uint64, c_int, POINTER(VxgStats)]),
     ("vxg_integrate_packed", c_int,
      [c_void_p, c_void_p, c_void_p, POINTER(c_uint64), POINTER(c_float), c_uint64, c_int, POINTER(VxgStats)]),
+    ("vxg_stage_packed", c_int, [c_void_p, c_void_p, c_void_p, POINTER(c_uint64), c_uint64, POINTER(c_int)]),
+    ("vxg_integrate_staged", c_int, [c_void_p, c_int, POINTER(c_float), POINTER(VxgStats)]),
     ("vxg_block_count", c_int, [c_void_p, POINTER(c_uint64)]),
     ("vxg_export_blocks", c_int, [c_void_p, c_void_p, c_void_p, c_uint64, POINTER(c_uint64)]),
     ("vxg_import_blocks", c_int, [c_void_p, c_void_p, c_void_p, c_uint64]),

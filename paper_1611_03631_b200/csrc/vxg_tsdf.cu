@@ -135,6 +135,17 @@ struct vxg_handle {
   cudaStream_t fold_st = nullptr;         // short-run fold beside the long-run fold
   cudaEvent_t fold_fork = nullptr, fold_join = nullptr;
   std::vector<cudaEvent_t> copy_events;
+  // ---- streaming ingestion: two staging slots (vxg_stage_packed / vxg_integrate_staged)
+  struct StageSlot {
+    DBuf<float> xyz;
+    DBuf<uint8_t> rgb;
+    std::vector<uint64_t> off;  // rebased: off[0] = 0
+    bool has_rgb = false;
+    bool full = false;          // staged, not yet integrated
+    bool used = false;          // `released` has been recorded once
+    cudaEvent_t copied = nullptr, released = nullptr;
+  } stage_slot[2];
+  int next_stage = 0;
 
   // ---- map (slab + block hash)
   DBuf<vxg_voxel> slab;
@@ -1410,6 +1421,10 @@ int vxg_destroy(vxg_handle* h) {
       cudaStreamDestroy(h->copy_st);
     }
     for (cudaEvent_t e : h->copy_events) cudaEventDestroy(e);
+    for (auto& ss : h->stage_slot) {
+      if (ss.copied) cudaEventDestroy(ss.copied);
+      if (ss.released) cudaEventDestroy(ss.released);
+    }
     if (h->fold_st) {
       cudaStreamSynchronize(h->fold_st);
       cudaStreamDestroy(h->fold_st);
@@ -1550,6 +1565,60 @@ int vxg_integrate_packed(vxg_handle* h, const float* xyz, const uint8_t* rgb, co
                           offsets[f + 1] - offsets[f]});
     }
     integrate_staged(h, copies, xyz, rgb, rgb != nullptr, offsets, poses, F, dev, out);
+  });
+}
+
+int vxg_stage_packed(vxg_handle* h, const float* xyz, const uint8_t* rgb, const uint64_t* offsets, uint64_t F,
+                     int* slot) {
+  return guarded([&] {
+    if (h == nullptr || offsets == nullptr || slot == nullptr) throw VxgError(VXG_EINVAL, "null argument");
+    for (uint64_t f = 0; f < F; ++f)
+      if (offsets[f + 1] < offsets[f]) throw VxgError(VXG_EINVAL, "frame offsets must be non-decreasing");
+    const uint64_t P = F ? offsets[F] - offsets[0] : 0;
+    if (P > 0 && xyz == nullptr) throw VxgError(VXG_EINVAL, "null point buffer");
+    const int k = h->next_stage;
+    vxg_handle::StageSlot& ss = h->stage_slot[k];
+    if (ss.full) throw VxgError(VXG_EINVAL, "both staging slots hold batches not yet integrated");
+    set_device(h);
+    if (h->copy_st == nullptr) CU(cudaStreamCreateWithFlags(&h->copy_st, cudaStreamNonBlocking));
+    if (ss.copied == nullptr) {
+      CU(cudaEventCreateWithFlags(&ss.copied, cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&ss.released, cudaEventDisableTiming));
+    }
+    // the slot's buffers may still be read by the batch integrated from it last
+    if (ss.used) CU(cudaStreamWaitEvent(h->copy_st, ss.released, 0));
+    float* dx = ss.xyz.ensure(std::max<uint64_t>(3 * P, 3));
+    uint8_t* dc = rgb != nullptr ? ss.rgb.ensure(std::max<uint64_t>(3 * P, 3)) : nullptr;
+    if (P > 0) {
+      CU(cudaMemcpyAsync(dx, xyz + 3 * offsets[0], 3 * P * sizeof(float), cudaMemcpyHostToDevice, h->copy_st));
+      if (dc != nullptr)
+        CU(cudaMemcpyAsync(dc, rgb + 3 * offsets[0], 3 * P, cudaMemcpyHostToDevice, h->copy_st));
+    }
+    CU(cudaEventRecord(ss.copied, h->copy_st));
+    ss.off.assign(F + 1, 0);
+    for (uint64_t f = 0; f <= F; ++f) ss.off[f] = offsets[f] - offsets[0];
+    ss.has_rgb = rgb != nullptr;
+    ss.full = true;
+    h->next_stage = k ^ 1;
+    *slot = k;
+  });
+}
+
+int vxg_integrate_staged(vxg_handle* h, int slot, const float* poses, vxg_stats* out) {
+  return guarded([&] {
+    if (h == nullptr) throw VxgError(VXG_EINVAL, "null argument");
+    if (slot < 0 || slot > 1 || !h->stage_slot[slot].full) throw VxgError(VXG_EINVAL, "no batch staged in this slot");
+    vxg_handle::StageSlot& ss = h->stage_slot[slot];
+    const uint64_t F = ss.off.size() - 1;
+    if (F > 0 && poses == nullptr) throw VxgError(VXG_EINVAL, "null argument");
+    set_device(h);
+    ss.full = false;  // consumed even if the integration throws (the copy is complete or abandoned)
+    CU(cudaStreamWaitEvent(h->st, ss.copied, 0));
+    if (F > 0)
+      integrate_staged(h, {}, ss.xyz.p, ss.has_rgb ? ss.rgb.p : nullptr, ss.has_rgb, ss.off.data(), poses, F, true,
+                       out);
+    CU(cudaEventRecord(ss.released, h->st));
+    ss.used = true;
   });
 }
 

@@ -348,6 +348,32 @@ class TsdfIntegrator:
             self._raycasts, self._skipped = int(out[-1, 1]), int(out[-1, 2])
         return out
 
+    def stage_packed(self, xyz_ptr: int, rgb_ptr: Optional[int], offsets: np.ndarray) -> int:
+        """Streaming ingestion: start the asynchronous H2D copy of a packed batch
+        (pinned host pointers) into a staging slot; returns the slot id. The
+        host buffers must stay valid until integrate_staged(slot) returns."""
+        self._bind()
+        offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+        slot = ctypes.c_int()
+        check(lib().vxg_stage_packed(
+            self._layer.handle, ctypes.c_void_p(xyz_ptr), ctypes.c_void_p(rgb_ptr) if rgb_ptr else None,
+            offsets.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), len(offsets) - 1, ctypes.byref(slot)))
+        return slot.value
+
+    def integrate_staged(self, slot: int, poses: np.ndarray) -> np.ndarray:
+        """Integrate a batch staged by stage_packed (same results as integrate_packed)."""
+        self._bind()
+        poses = np.ascontiguousarray(poses, dtype=np.float32).reshape(-1, 12)
+        F = len(poses)
+        stats = (VxgStats * max(F, 1))()
+        check(lib().vxg_integrate_staged(self._layer.handle, int(slot),
+                                         poses.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), stats))
+        out = np.array([[s.updates, s.raycasts, s.skipped] for s in stats[:F]], dtype=np.uint64).reshape(F, 3)
+        if F:
+            self._raycasts, self._skipped = int(out[-1, 1]), int(out[-1, 2])
+        return out
+
+
 
 def nccl_unique_id() -> bytes:
     """128-byte NCCL unique id for vxg_shard_init (rank 0 makes it, the caller broadcasts it)."""

@@ -242,3 +242,33 @@ def test_batch_split_invariance_full_size(gpu):
             integ.integrate_batch(fr[i * n:(i + 1) * n])
         out.append(layer.save_bytes())
     assert out[0] == out[1] == out[2]
+
+
+def test_streaming_staged_equals_packed(gpu):
+    """Streaming ingestion: batches staged ahead (double-buffered H2D on the copy
+    stream, batch k+1 staged before batch k is integrated) give the same layer
+    bytes and stats as synchronous integrate_packed calls; staging a third
+    batch while two are pending is rejected."""
+    import torch
+    wc = W.CONFIGS[1]
+    cfg = W.tsdf_config(wc)
+    batches = [W.pack(W.frames(1, count=4, scale=0.5, start=4 * k)) for k in range(4)]
+    ref = TsdfLayer(wc.voxel_size, wc.vps)
+    iref = TsdfIntegrator(cfg, ref)
+    sref = [iref.integrate_packed(x.ctypes.data, c.ctypes.data, o, p, False) for (x, c, o, p) in batches]
+    pinned = [(torch.from_numpy(x).pin_memory(), torch.from_numpy(c).pin_memory(), o, p) for (x, c, o, p) in batches]
+    layer = TsdfLayer(wc.voxel_size, wc.vps)
+    integ = TsdfIntegrator(cfg, layer)
+    slot = integ.stage_packed(pinned[0][0].data_ptr(), pinned[0][1].data_ptr(), pinned[0][2])
+    got = []
+    for k in range(len(pinned)):
+        nxt = None
+        if k + 1 < len(pinned):
+            nxt = integ.stage_packed(pinned[k + 1][0].data_ptr(), pinned[k + 1][1].data_ptr(), pinned[k + 1][2])
+            with pytest.raises(Exception):  # two batches pending: no third slot
+                integ.stage_packed(pinned[k][0].data_ptr(), pinned[k][1].data_ptr(), pinned[k][2])
+        got.append(integ.integrate_staged(slot, pinned[k][3]))
+        slot = nxt
+    for a, b in zip(got, sref):
+        assert np.array_equal(a, b)
+    assert layer.save_bytes() == ref.save_bytes()
