@@ -96,6 +96,26 @@ int vxg_stage_packed(vxg_handle* h, const float* xyz, const uint8_t* rgb, const 
                      uint64_t n_frames, int* slot);
 int vxg_integrate_staged(vxg_handle* h, int slot, const float* poses, vxg_stats* out);
 
+/* ---- meshing on the device slab: vxf::MeshExtractor (mesh_extractor.cpp)
+ * Per-block marching cubes over the TSDF zero crossing (extract_block,
+ * mesh_extractor.cpp:85-151): cubes span 8 voxel centres and may straddle
+ * block boundaries; cubes with an unallocated or unobserved corner emit
+ * nothing; shared edges interpolate from the lower global index; vertex
+ * normals from central differences of interpolate_distance (vertex_normal,
+ * :69-83). vxg_mesh_extract computes the fragments of the given blocks
+ * (blocks = n x 3 block indices, unallocated ones skipped — extract_blocks
+ * :41-46), or of every allocated block when blocks == NULL (extract_all
+ * :48-52), keeps them on the device and returns the fragment and triangle
+ * counts; vxg_mesh_fetch copies them out, fragments sorted by block index
+ * (x, y, z): block_idx n_frag x 3, frag_tri (n_frag + 1) triangle offsets,
+ * vertices / normals n_tri x 9 floats (3 vertices per triangle, in the
+ * reference's emission order; the fragment's triangle t is (3t, 3t+1, 3t+2)),
+ * colors n_tri x 9 u8 (with_colors only; may be NULL). */
+int vxg_mesh_extract(vxg_handle* h, const vxg_mc_tables* tables, const int32_t* blocks, uint64_t n_blocks,
+                     int with_colors, uint64_t* n_frag, uint64_t* n_tri);
+int vxg_mesh_fetch(vxg_handle* h, int32_t* block_idx, uint64_t* frag_tri, float* vertices, float* normals,
+                   uint8_t* colors);
+
 /* Layer::block_count() (layer.h:72). */
 int vxg_block_count(vxg_handle* h, uint64_t* out);
 

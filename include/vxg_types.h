@@ -52,6 +52,17 @@ typedef struct vxg_voxel {
   uint8_t r, g, b, pad;
 } vxg_voxel;
 
+/* Marching-cubes case tables, supplied by the caller (the reference build's
+ * own vxf::mc_tables, marching_cubes_tables.h): corner offsets, the two corners
+ * of each edge, the crossed-edge mask and the triangle list (edge ids, -1
+ * terminated) of each of the 256 corner-sign configurations. */
+typedef struct vxg_mc_tables {
+  int32_t corner_offsets[8][3];
+  int32_t edge_corners[12][2];
+  uint16_t edge_table[256];
+  int8_t tri_table[256][16];
+} vxg_mc_tables;
+
 /* Status codes (SURVEY.md §8b error convention). */
 enum vxg_status {
   VXG_OK = 0,

@@ -13,6 +13,8 @@
 #include "vxf/analysis.h"
 #include "vxf/interpolation.h"
 #include "vxf/layer.h"
+#include "vxf/marching_cubes_tables.h"
+#include "vxf/mesh_extractor.h"
 #include "vxf/serialization.h"
 #include "vxf/tsdf_integrator.h"
 
@@ -177,6 +179,84 @@ void vxr_surface_error(void* hp, const float* pts, size_t n, float truncation, d
   out[2] = s.max;
   out[3] = static_cast<double>(s.count);
   out[4] = s.unknown_fraction;
+}
+
+// Layer block overwrite (for analytic fields in the meshing parity tests).
+void vxr_set_block(void* hp, const int32_t idx[3], const vxg_voxel* voxels) {
+  auto& layer = static_cast<RefHandle*>(hp)->layer;
+  auto& blk = layer.get_or_allocate_block(vxf::BlockIndex(idx[0], idx[1], idx[2]));
+  const int n = layer.voxels_per_side() * layer.voxels_per_side() * layer.voxels_per_side();
+  for (int i = 0; i < n; ++i) {
+    vxf::TsdfVoxel& v = blk.voxel(i);
+    v.distance = voxels[i].distance;
+    v.weight = voxels[i].weight;
+    v.color = vxf::Color{voxels[i].r, voxels[i].g, voxels[i].b};
+  }
+}
+
+// The reference build's marching-cubes case tables (marching_cubes_tables.h),
+// handed to the B200 path (vxg_mesh_extract takes them from its caller).
+void vxr_mc_tables(vxg_mc_tables* t) {
+  namespace mc = vxf::mc_tables;
+  for (int c = 0; c < 8; ++c)
+    for (int a = 0; a < 3; ++a) t->corner_offsets[c][a] = mc::kCornerOffsets[c][a];
+  for (int e = 0; e < 12; ++e)
+    for (int a = 0; a < 2; ++a) t->edge_corners[e][a] = mc::kEdgeCorners[e][a];
+  for (int i = 0; i < 256; ++i) {
+    t->edge_table[i] = mc::kEdgeTable[i];
+    for (int k = 0; k < 16; ++k) t->tri_table[i][k] = static_cast<int8_t>(mc::kTriTable[i][k]);
+  }
+}
+
+// MeshExtractor::extract_all / extract_blocks, then fragments() in (x,y,z)
+// block order; same output contract as vxo_mesh_extract. Returns n_frag, or
+// (size_t)-1 when a fragment's triangles are not (3t, 3t+1, 3t+2).
+size_t vxr_mesh_extract(void* hp, int with_colors, const int32_t* blocks, size_t n_req, int32_t* bidx,
+                        uint64_t* frag_tri, float* verts, float* normals, uint8_t* colors, size_t cap_frag,
+                        size_t cap_tri, uint64_t* n_tri) {
+  const auto& layer = static_cast<RefHandle*>(hp)->layer;
+  vxf::MeshExtractor ex(&layer, with_colors != 0);
+  if (blocks == nullptr) {
+    ex.extract_all();
+  } else {
+    vxf::IndexSet req;
+    for (size_t i = 0; i < n_req; ++i) req.insert(vxf::BlockIndex(blocks[3 * i], blocks[3 * i + 1], blocks[3 * i + 2]));
+    ex.extract_blocks(req);
+  }
+  std::vector<vxf::BlockIndex> order;
+  for (const auto& kv : ex.fragments()) order.push_back(kv.first);
+  std::sort(order.begin(), order.end(), [](const vxf::BlockIndex& a, const vxf::BlockIndex& b) {
+    return std::tie(a.x(), a.y(), a.z()) < std::tie(b.x(), b.y(), b.z());
+  });
+  uint64_t T = 0;
+  for (const auto& b : order) T += ex.fragments().at(b).triangles.size();
+  *n_tri = T;
+  if (cap_frag < order.size() || cap_tri < T) return order.size();
+  uint64_t o = 0;
+  for (size_t j = 0; j < order.size(); ++j) {
+    const vxf::Mesh& m = ex.fragments().at(order[j]);
+    if (bidx) {
+      bidx[3 * j] = order[j].x();
+      bidx[3 * j + 1] = order[j].y();
+      bidx[3 * j + 2] = order[j].z();
+    }
+    if (frag_tri) frag_tri[j] = o;
+    for (size_t k = 0; k < m.triangles.size(); ++k)
+      if (m.triangles[k][0] != 3 * k || m.triangles[k][1] != 3 * k + 1 || m.triangles[k][2] != 3 * k + 2)
+        return static_cast<size_t>(-1);
+    for (size_t q = 0; q < m.vertices.size(); ++q)
+      for (int a = 0; a < 3; ++a) {
+        if (verts) verts[9 * o + 3 * q + a] = m.vertices[q][a];
+        if (normals) normals[9 * o + 3 * q + a] = m.normals[q][a];
+        if (colors && with_colors) {
+          const vxf::Color& c = m.colors[q];
+          colors[9 * o + 3 * q + a] = a == 0 ? c.r : (a == 1 ? c.g : c.b);
+        }
+      }
+    o += m.triangles.size();
+  }
+  if (frag_tri) frag_tri[order.size()] = o;
+  return order.size();
 }
 
 }  // extern "C"

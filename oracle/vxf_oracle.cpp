@@ -633,3 +633,168 @@ extern "C" void vxo_surface_error(const vxo_layer* l, const float* pts, size_t n
   out[3] = static_cast<double>(count);
   out[4] = n ? static_cast<double>(unknown) / static_cast<double>(n) : 0.0;
 }
+
+// ---------------------------------------------------------------- meshing
+// MeshExtractor::extract_block (mesh_extractor.cpp:85-151), restated with plain
+// floats (the Eigen operations it uses are per-component; cross and norm in the
+// shim's order), case tables from the caller.
+namespace {
+
+struct McCorner {
+  int32_t g[3];
+  float d;
+  uint8_t rgb[3];
+};
+
+// edge_vertex (mesh_extractor.cpp:21-39): interpolate from the corner with the
+// lower (x, y, z) global index so shared edges agree bitwise.
+void mc_edge_vertex(const McCorner& a, const McCorner& b, float v, float* pos, uint8_t* col) {
+  const McCorner* lo = &a;
+  const McCorner* hi = &b;
+  if (std::lexicographical_compare(hi->g, hi->g + 3, lo->g, lo->g + 3)) std::swap(lo, hi);
+  const float t = lo->d / (lo->d - hi->d);
+  for (int i = 0; i < 3; ++i) {
+    const float plo = (static_cast<float>(lo->g[i]) + 0.5f) * v;  // voxel_center (core.h:50-52)
+    const float phi = (static_cast<float>(hi->g[i]) + 0.5f) * v;
+    const float diff = phi - plo;
+    const float step = t * diff;
+    pos[i] = plo + step;
+    const float clo = static_cast<float>(lo->rgb[i]);
+    const float span = static_cast<float>(hi->rgb[i]) - clo;
+    const float blend = clo + t * span;
+    const long r = std::lround(blend);
+    col[i] = static_cast<uint8_t>(std::clamp(r, 0l, 255l));
+  }
+}
+
+float mc_norm(const float* a) {
+  const float s12 = a[1] * a[1] + a[2] * a[2];
+  return std::sqrt(a[0] * a[0] + s12);
+}
+
+// vertex_normal (mesh_extractor.cpp:69-83)
+void mc_vertex_normal(const vxo_layer* l, const float* p, const float* face, float* out) {
+  const float h = l->voxel_size;
+  float grad[3];
+  for (int i = 0; i < 3; ++i) {
+    float lo[3] = {p[0], p[1], p[2]}, hi[3] = {p[0], p[1], p[2]};
+    lo[i] -= h;
+    hi[i] += h;
+    float dlo, dhi;
+    const int flo = oracle_interp(l, lo, &dlo);
+    const int fhi = oracle_interp(l, hi, &dhi);
+    if (!flo || !fhi) {
+      std::memcpy(out, face, 3 * sizeof(float));
+      return;
+    }
+    grad[i] = (dhi - dlo) / (2.0f * h);
+  }
+  const float n = mc_norm(grad);
+  if (n < 1e-10f) {
+    std::memcpy(out, face, 3 * sizeof(float));
+    return;
+  }
+  for (int i = 0; i < 3; ++i) out[i] = grad[i] / n;
+}
+
+struct McOut {
+  std::vector<float> v, n;
+  std::vector<uint8_t> c;
+};
+
+void mc_extract_block(const vxo_layer* l, const vxg_mc_tables* t, bool with_colors, const Key3& b, McOut* out) {
+  const int vps = l->vps;
+  const float v = l->voxel_size;
+  McCorner corners[8];
+  for (int z = 0; z < vps; ++z)
+    for (int y = 0; y < vps; ++y)
+      for (int x = 0; x < vps; ++x) {
+        int config = 0;
+        bool complete = true;
+        for (int c = 0; c < 8 && complete; ++c) {
+          const int32_t g[3] = {b[0] * vps + x + t->corner_offsets[c][0], b[1] * vps + y + t->corner_offsets[c][1],
+                                b[2] * vps + z + t->corner_offsets[c][2]};
+          vxg_voxel vx;
+          if (!vxo_voxel(l, g[0], g[1], g[2], &vx) || !(vx.weight > 1e-4f)) {  // voxel_ptr / observed()
+            complete = false;
+            break;
+          }
+          corners[c] = McCorner{{g[0], g[1], g[2]}, vx.distance, {vx.r, vx.g, vx.b}};
+          if (vx.distance < 0.0f) config |= 1 << c;
+        }
+        if (!complete || t->edge_table[config] == 0) continue;
+        float ep[12][3];
+        uint8_t ec[12][3];
+        for (int e = 0; e < 12; ++e)
+          if (t->edge_table[config] & (1 << e))
+            mc_edge_vertex(corners[t->edge_corners[e][0]], corners[t->edge_corners[e][1]], v, ep[e], ec[e]);
+        for (int k = 0; t->tri_table[config][k] != -1; k += 3) {
+          // table winding faces the negative side: (e0, e2, e1) (:116-122)
+          const int es[3] = {t->tri_table[config][k], t->tri_table[config][k + 2], t->tri_table[config][k + 1]};
+          const float* p0 = ep[es[0]];
+          const float* p1 = ep[es[1]];
+          const float* p2 = ep[es[2]];
+          const float a[3] = {p1[0] - p0[0], p1[1] - p0[1], p1[2] - p0[2]};
+          const float c[3] = {p2[0] - p0[0], p2[1] - p0[1], p2[2] - p0[2]};
+          float fnv[3];
+          for (int i = 0; i < 3; ++i) {  // cross product, component i = a_j c_k - a_k c_j
+            const int j = (i + 1) % 3, kk = (i + 2) % 3;
+            const float m1 = a[j] * c[kk];
+            const float m2 = a[kk] * c[j];
+            fnv[i] = m1 - m2;
+          }
+          const float fn = mc_norm(fnv);
+          if (fn > 1e-12f) {
+            for (int i = 0; i < 3; ++i) fnv[i] = fnv[i] / fn;
+          } else {
+            fnv[0] = 0.0f;
+            fnv[1] = 0.0f;
+            fnv[2] = 1.0f;
+          }
+          for (int q = 0; q < 3; ++q) {
+            const float* p = ep[es[q]];
+            float nrm[3];
+            mc_vertex_normal(l, p, fnv, nrm);
+            out->v.insert(out->v.end(), p, p + 3);
+            out->n.insert(out->n.end(), nrm, nrm + 3);
+            if (with_colors) out->c.insert(out->c.end(), ec[es[q]], ec[es[q]] + 3);
+          }
+        }
+      }
+}
+
+}  // namespace
+
+extern "C" size_t vxo_mesh_extract(const vxo_layer* l, const vxg_mc_tables* t, int with_colors, const int32_t* blocks,
+                                   size_t n_req, int32_t* bidx, uint64_t* frag_tri, float* verts, float* normals,
+                                   uint8_t* colors, size_t cap_frag, size_t cap_tri, uint64_t* n_tri) {
+  std::vector<Key3> order;
+  if (blocks == nullptr) {
+    for (const auto& kv : l->blocks) order.push_back(kv.first);
+  } else {
+    for (size_t i = 0; i < n_req; ++i) {
+      const Key3 k{blocks[3 * i], blocks[3 * i + 1], blocks[3 * i + 2]};
+      if (l->blocks.count(k)) order.push_back(k);
+    }
+  }
+  std::sort(order.begin(), order.end());
+  order.erase(std::unique(order.begin(), order.end()), order.end());
+  McOut out;
+  std::vector<uint64_t> frag(order.size() + 1, 0);
+  for (size_t j = 0; j < order.size(); ++j) {
+    mc_extract_block(l, t, with_colors != 0, order[j], &out);
+    frag[j + 1] = out.v.size() / 9;
+  }
+  const uint64_t T = frag.back();
+  *n_tri = T;
+  if (cap_frag >= order.size() && cap_tri >= T) {
+    for (size_t j = 0; j < order.size(); ++j)
+      for (int a = 0; a < 3; ++a)
+        if (bidx) bidx[3 * j + a] = order[j][a];
+    if (frag_tri) std::memcpy(frag_tri, frag.data(), frag.size() * sizeof(uint64_t));
+    if (verts && T) std::memcpy(verts, out.v.data(), 9 * T * sizeof(float));
+    if (normals && T) std::memcpy(normals, out.n.data(), 9 * T * sizeof(float));
+    if (colors && with_colors && T) std::memcpy(colors, out.c.data(), 9 * T);
+  }
+  return order.size();
+}

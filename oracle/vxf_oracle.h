@@ -92,6 +92,17 @@ size_t vxo_bucket_schedule(size_t n_points, size_t max_keys, uint64_t* out, size
 void vxo_interpolate(const vxo_layer* l, const float* pts, size_t n, float* d, uint8_t* found);
 void vxo_surface_error(const vxo_layer* l, const float* pts, size_t n, float truncation, double out[5]);
 
+/* MeshExtractor (mesh_extractor.cpp:41-151) restated: marching cubes per block
+ * with the caller's case tables. blocks == NULL: every block (extract_all),
+ * else the allocated ones among blocks[n_req x 3] (extract_blocks). Output in
+ * (x,y,z) block order: bidx[n_frag x 3], frag_tri[n_frag + 1] triangle
+ * offsets, verts / normals [n_tri x 9], colors [n_tri x 9] (with_colors).
+ * Returns n_frag and *n_tri; writes the arrays only when cap_frag >= n_frag
+ * and cap_tri >= n_tri (call once with zero caps to size them). */
+size_t vxo_mesh_extract(const vxo_layer* l, const vxg_mc_tables* t, int with_colors, const int32_t* blocks,
+                        size_t n_req, int32_t* bidx, uint64_t* frag_tri, float* verts, float* normals,
+                        uint8_t* colors, size_t cap_frag, size_t cap_tri, uint64_t* n_tri);
+
 #ifdef __cplusplus
 }
 #endif

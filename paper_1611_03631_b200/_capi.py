@@ -43,6 +43,11 @@ class VxgFrame(ctypes.Structure):
     _fields_ = [("xyz", c_void_p), ("rgb", c_void_p), ("n", c_uint64), ("pose", c_float * 12)]
 
 
+class VxgMcTables(ctypes.Structure):
+    _fields_ = [("corner_offsets", (c_int32 * 3) * 8), ("edge_corners", (c_int32 * 2) * 12),
+                ("edge_table", ctypes.c_uint16 * 256), ("tri_table", (ctypes.c_int8 * 16) * 256)]
+
+
 # (name, restype, argtypes) for every symbol include/vxg.h declares.
 SIGNATURES = [
     ("vxg_last_error", c_char_p, []),
@@ -58,6 +63,9 @@ SIGNATURES = [
      [c_void_p, c_void_p, c_void_p, POINTER(c_uint64), POINTER(c_float), c_uint64, c_int, POINTER(VxgStats)]),
     ("vxg_stage_packed", c_int, [c_void_p, c_void_p, c_void_p, POINTER(c_uint64), c_uint64, POINTER(c_int)]),
     ("vxg_integrate_staged", c_int, [c_void_p, c_int, POINTER(c_float), POINTER(VxgStats)]),
+    ("vxg_mesh_extract", c_int,
+     [c_void_p, POINTER(VxgMcTables), c_void_p, c_uint64, c_int, POINTER(c_uint64), POINTER(c_uint64)]),
+    ("vxg_mesh_fetch", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("vxg_block_count", c_int, [c_void_p, POINTER(c_uint64)]),
     ("vxg_export_blocks", c_int, [c_void_p, c_void_p, c_void_p, c_uint64, POINTER(c_uint64)]),
     ("vxg_import_blocks", c_int, [c_void_p, c_void_p, c_void_p, c_uint64]),

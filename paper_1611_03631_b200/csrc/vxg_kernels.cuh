@@ -1572,40 +1572,254 @@ __device__ __forceinline__ bool corner_distance(const MapView& map, int gx, int 
   return true;
 }
 
+// interpolate_distance at one point; false when absent.
+__device__ __forceinline__ bool interp_distance(const MapView& map, float voxel_size, const float* p, float* out) {
+  float q[3], frac[3];
+  int base[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {  // q = p / v - 0.5 (Eigen: per-component quotient, then difference)
+    q[a] = fsub(fdiv(p[a], voxel_size), 0.5f);
+    base[a] = static_cast<int>(floorf(q[a]));
+    frac[a] = fsub(q[a], static_cast<float>(base[a]));
+  }
+  float c[2][2][2];
+  bool ok = true;
+#pragma unroll
+  for (int dz = 0; dz < 2; ++dz)
+#pragma unroll
+    for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+      for (int dx = 0; dx < 2; ++dx)
+        ok = ok && corner_distance(map, base[0] + dx, base[1] + dy, base[2] + dz, &c[dx][dy][dz]);
+  if (!ok) return false;
+  float plane[2][2], line[2];
+#pragma unroll
+  for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+    for (int dz = 0; dz < 2; ++dz) plane[dy][dz] = fadd(c[0][dy][dz], fmul(frac[0], fsub(c[1][dy][dz], c[0][dy][dz])));
+#pragma unroll
+  for (int dz = 0; dz < 2; ++dz) line[dz] = fadd(plane[0][dz], fmul(frac[1], fsub(plane[1][dz], plane[0][dz])));
+  *out = fadd(line[0], fmul(frac[2], fsub(line[1], line[0])));
+  return true;
+}
+
 __global__ void k_interpolate(uint64_t n, const float* __restrict__ pts, MapView map, float voxel_size,
                               float* __restrict__ out, uint8_t* __restrict__ found) {
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    float q[3], frac[3];
-    int base[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {  // q = p / v - 0.5 (Eigen: per-component quotient, then difference)
-      q[a] = fsub(fdiv(pts[3 * i + a], voxel_size), 0.5f);
-      base[a] = static_cast<int>(floorf(q[a]));
-      frac[a] = fsub(q[a], static_cast<float>(base[a]));
-    }
-    float c[2][2][2];
-    bool ok = true;
-#pragma unroll
-    for (int dz = 0; dz < 2; ++dz)
-#pragma unroll
-      for (int dy = 0; dy < 2; ++dy)
-#pragma unroll
-        for (int dx = 0; dx < 2; ++dx)
-          ok = ok && corner_distance(map, base[0] + dx, base[1] + dy, base[2] + dz, &c[dx][dy][dz]);
     float r = 0.0f;
-    if (ok) {
-      float plane[2][2], line[2];
-#pragma unroll
-      for (int dy = 0; dy < 2; ++dy)
-#pragma unroll
-        for (int dz = 0; dz < 2; ++dz) plane[dy][dz] = fadd(c[0][dy][dz], fmul(frac[0], fsub(c[1][dy][dz], c[0][dy][dz])));
-#pragma unroll
-      for (int dz = 0; dz < 2; ++dz) line[dz] = fadd(plane[0][dz], fmul(frac[1], fsub(plane[1][dz], plane[0][dz])));
-      r = fadd(line[0], fmul(frac[2], fsub(line[1], line[0])));
-    }
-    out[i] = r;
+    const bool ok = interp_distance(map, voxel_size, pts + 3 * i, &r);
+    out[i] = ok ? r : 0.0f;
     found[i] = ok ? 1u : 0u;
+  }
+}
+
+// ---------------------------------------------------------------- meshing (MeshExtractor)
+// Marching cubes per block (mesh_extractor.cpp:85-151) on the slab. One thread
+// per cube of the requested blocks (cube = voxel (x, y, z) of the block and its
+// +1 neighbours, which may lie in adjacent blocks). Pass 1 counts each cube's
+// triangles; an exclusive scan over (block, cube) in the reference's loop
+// order (z, y, x) gives every cube its output position; pass 2 writes the
+// triangles. The case tables come from the caller (vxg_mc_tables) and are
+// staged in shared memory.
+struct McSmem {
+  int32_t coff[8][3];
+  int32_t ecorner[12][2];
+  uint16_t edge[256];
+  int8_t tri[256][16];
+  uint8_t ntri[256];
+};
+
+__device__ __forceinline__ void mc_stage(McSmem& sm, const vxg_mc_tables* __restrict__ t) {
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    sm.edge[i] = t->edge_table[i];
+    int n = 0;
+    for (int k = 0; k < 16; ++k) {
+      sm.tri[i][k] = t->tri_table[i][k];
+    }
+    while (n < 16 && t->tri_table[i][n] != -1) ++n;
+    sm.ntri[i] = static_cast<uint8_t>(n / 3);
+  }
+  if (threadIdx.x < 24) sm.coff[threadIdx.x / 3][threadIdx.x % 3] = t->corner_offsets[threadIdx.x / 3][threadIdx.x % 3];
+  if (threadIdx.x < 24) sm.ecorner[threadIdx.x / 2][threadIdx.x % 2] = t->edge_corners[threadIdx.x / 2][threadIdx.x % 2];
+  __syncthreads();
+}
+
+// Layer::voxel_ptr + observed() for a voxel of the cube; the cube's own block
+// is `slot` (the common case), others go through the block hash.
+__device__ __forceinline__ const vxg_voxel* mc_voxel(const MapView& map, int32_t slot, int bx, int by, int bz, int gx,
+                                                     int gy, int gz) {
+  const int vps = map.vps;
+  const int b0 = floor_div(gx, vps), b1 = floor_div(gy, vps), b2 = floor_div(gz, vps);
+  int32_t s = slot;
+  if (b0 != bx || b1 != by || b2 != bz) {
+    if (!block_in_range(b0, b1, b2)) return nullptr;
+    s = map.find(pack_block(b0, b1, b2));
+    if (s < 0 || static_cast<uint32_t>(s) >= map.cap_blocks) return nullptr;
+  }
+  const vxg_voxel* v = &map.slab[static_cast<uint64_t>(s) * map.nvox + (gx - b0 * vps) +
+                                 vps * ((gy - b1 * vps) + vps * (gz - b2 * vps))];
+  return v->weight > 1e-4f ? v : nullptr;  // TsdfVoxel::observed (voxel.h:17)
+}
+
+struct McCube {
+  int g[8][3];
+  float d[8];
+  uint8_t rgb[8][3];
+  int config;
+};
+
+// Corners of cube (x, y, z) of block slot; false when a corner is missing or
+// unobserved (mesh_extractor.cpp:96-108).
+__device__ __forceinline__ bool mc_cube(const MapView& map, const McSmem& sm, int32_t slot, const int* bidx, int lin,
+                                        McCube& c) {
+  const int vps = map.vps;
+  const int x = lin % vps, y = (lin / vps) % vps, z = lin / (vps * vps);
+  c.config = 0;
+  for (int k = 0; k < 8; ++k) {
+    const int gx = bidx[0] * vps + x + sm.coff[k][0], gy = bidx[1] * vps + y + sm.coff[k][1],
+              gz = bidx[2] * vps + z + sm.coff[k][2];
+    const vxg_voxel* v = mc_voxel(map, slot, bidx[0], bidx[1], bidx[2], gx, gy, gz);
+    if (v == nullptr) return false;
+    c.g[k][0] = gx;
+    c.g[k][1] = gy;
+    c.g[k][2] = gz;
+    c.d[k] = v->distance;
+    c.rgb[k][0] = v->r;
+    c.rgb[k][1] = v->g;
+    c.rgb[k][2] = v->b;
+    if (v->distance < 0.0f) c.config |= 1 << k;
+  }
+  return true;
+}
+
+__global__ void k_mc_count(uint64_t n_cubes, const int32_t* __restrict__ slots, MapView map,
+                           const vxg_mc_tables* __restrict__ tables, uint32_t* __restrict__ ntri) {
+  __shared__ McSmem sm;
+  mc_stage(sm, tables);
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n_cubes;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t b = i / static_cast<uint64_t>(map.nvox);
+    const int lin = static_cast<int>(i - b * static_cast<uint64_t>(map.nvox));
+    const int32_t slot = slots[b];
+    const int bidx[3] = {map.block_idx[3 * slot], map.block_idx[3 * slot + 1], map.block_idx[3 * slot + 2]};
+    McCube c;
+    uint32_t n = 0;
+    if (mc_cube(map, sm, slot, bidx, lin, c) && sm.edge[c.config] != 0) n = sm.ntri[c.config];
+    ntri[i] = n;
+  }
+}
+
+__global__ void k_gather_stride(uint64_t n, const uint32_t* __restrict__ src, uint64_t stride, uint32_t* __restrict__ dst) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    dst[i] = src[i * stride];
+}
+
+// vertex_normal (mesh_extractor.cpp:69-83): central differences of
+// interpolate_distance at +-h per axis; the face normal when any sample is
+// absent or the gradient vanishes.
+__device__ __forceinline__ void mc_vertex_normal(const MapView& map, float v, const float* p, const float* face,
+                                                 float* out) {
+  float grad[3];
+  for (int i = 0; i < 3; ++i) {
+    float lo[3] = {p[0], p[1], p[2]}, hi[3] = {p[0], p[1], p[2]};
+    lo[i] = fsub(lo[i], v);
+    hi[i] = fadd(hi[i], v);
+    float dlo, dhi;
+    if (!interp_distance(map, v, lo, &dlo) || !interp_distance(map, v, hi, &dhi)) {
+      out[0] = face[0];
+      out[1] = face[1];
+      out[2] = face[2];
+      return;
+    }
+    grad[i] = fdiv(fsub(dhi, dlo), fmul(2.0f, v));
+  }
+  const float norm = __fsqrt_rn(fadd(fmul(grad[0], grad[0]), fadd(fmul(grad[1], grad[1]), fmul(grad[2], grad[2]))));
+  if (norm < 1e-10f) {
+    out[0] = face[0];
+    out[1] = face[1];
+    out[2] = face[2];
+    return;
+  }
+  out[0] = fdiv(grad[0], norm);
+  out[1] = fdiv(grad[1], norm);
+  out[2] = fdiv(grad[2], norm);
+}
+
+__global__ void k_mc_emit(uint64_t n_cubes, const int32_t* __restrict__ slots, MapView map, float voxel_size,
+                          const vxg_mc_tables* __restrict__ tables, const uint32_t* __restrict__ ntri,
+                          const uint32_t* __restrict__ tri_off, int with_colors, float* __restrict__ verts,
+                          float* __restrict__ normals, uint8_t* __restrict__ colors) {
+  __shared__ McSmem sm;
+  mc_stage(sm, tables);
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n_cubes;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    if (ntri[i] == 0u) continue;
+    const uint64_t b = i / static_cast<uint64_t>(map.nvox);
+    const int lin = static_cast<int>(i - b * static_cast<uint64_t>(map.nvox));
+    const int32_t slot = slots[b];
+    const int bidx[3] = {map.block_idx[3 * slot], map.block_idx[3 * slot + 1], map.block_idx[3 * slot + 2]};
+    McCube c;
+    mc_cube(map, sm, slot, bidx, lin, c);
+    // edge vertices (edge_vertex, mesh_extractor.cpp:21-39): from the corner
+    // with the lower (x, y, z) global index
+    float ep[12][3];
+    uint8_t ec[12][3];
+    const uint16_t emask = sm.edge[c.config];
+    for (int e = 0; e < 12; ++e) {
+      if (!(emask & (1u << e))) continue;
+      int lo = sm.ecorner[e][0], hi = sm.ecorner[e][1];
+      const int* A = c.g[lo];
+      const int* B = c.g[hi];
+      const bool swap = B[0] != A[0] ? B[0] < A[0] : (B[1] != A[1] ? B[1] < A[1] : B[2] < A[2]);
+      if (swap) {
+        const int t = lo;
+        lo = hi;
+        hi = t;
+      }
+      const float t = fdiv(c.d[lo], fsub(c.d[lo], c.d[hi]));
+      for (int a = 0; a < 3; ++a) {
+        const float plo = vcenter(c.g[lo][a], voxel_size), phi = vcenter(c.g[hi][a], voxel_size);
+        ep[e][a] = fadd(plo, fmul(t, fsub(phi, plo)));
+        const float clo = static_cast<float>(c.rgb[lo][a]);
+        const long r = lroundf(fadd(clo, fmul(t, fsub(static_cast<float>(c.rgb[hi][a]), clo))));
+        ec[e][a] = static_cast<uint8_t>(r < 0 ? 0 : (r > 255 ? 255 : r));
+      }
+    }
+    uint64_t o = tri_off[i];
+    const int8_t* tt = sm.tri[c.config];
+    for (int t = 0; t < 16 && tt[t] != -1; t += 3, ++o) {
+      // the table winding faces the negative side: (e0, e2, e1) (:117-122)
+      const int es[3] = {tt[t], tt[t + 2], tt[t + 1]};
+      const float* p0 = ep[es[0]];
+      const float* p1 = ep[es[1]];
+      const float* p2 = ep[es[2]];
+      const float u[3] = {fsub(p1[0], p0[0]), fsub(p1[1], p0[1]), fsub(p1[2], p0[2])};
+      const float w[3] = {fsub(p2[0], p0[0]), fsub(p2[1], p0[1]), fsub(p2[2], p0[2])};
+      float fnv[3] = {fsub(fmul(u[1], w[2]), fmul(u[2], w[1])), fsub(fmul(u[2], w[0]), fmul(u[0], w[2])),
+                      fsub(fmul(u[0], w[1]), fmul(u[1], w[0]))};
+      const float fn = __fsqrt_rn(fadd(fmul(fnv[0], fnv[0]), fadd(fmul(fnv[1], fnv[1]), fmul(fnv[2], fnv[2]))));
+      if (fn > 1e-12f) {
+        fnv[0] = fdiv(fnv[0], fn);
+        fnv[1] = fdiv(fnv[1], fn);
+        fnv[2] = fdiv(fnv[2], fn);
+      } else {
+        fnv[0] = 0.0f;
+        fnv[1] = 0.0f;
+        fnv[2] = 1.0f;
+      }
+      for (int k = 0; k < 3; ++k) {
+        const float* p = ep[es[k]];
+        float nrm[3];
+        mc_vertex_normal(map, voxel_size, p, fnv, nrm);
+        for (int a = 0; a < 3; ++a) {
+          verts[9 * o + 3 * k + a] = p[a];
+          normals[9 * o + 3 * k + a] = nrm[a];
+          if (with_colors) colors[9 * o + 3 * k + a] = ec[es[k]][a];
+        }
+      }
+    }
   }
 }
 

@@ -24,6 +24,7 @@
 #include <set>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
 #include <utility>
 #include <vector>
 
@@ -146,6 +147,16 @@ struct vxg_handle {
     cudaEvent_t copied = nullptr, released = nullptr;
   } stage_slot[2];
   int next_stage = 0;
+  // ---- meshing results (vxg_mesh_extract / vxg_mesh_fetch)
+  DBuf<vxg_mc_tables> mesh_tab;
+  DBuf<int32_t> mesh_slots;
+  DBuf<uint32_t> mesh_ntri, mesh_off, mesh_frag_dev;
+  DBuf<float> mesh_v, mesh_n;
+  DBuf<uint8_t> mesh_c;
+  std::vector<int32_t> mesh_bidx;
+  std::vector<uint64_t> mesh_frag;
+  uint64_t mesh_T = 0;
+  bool mesh_colors = false, mesh_ready = false;
 
   // ---- map (slab + block hash)
   DBuf<vxg_voxel> slab;
@@ -1794,6 +1805,104 @@ int vxg_interpolate_distance(vxg_handle* h, const float* pts, uint64_t n, float*
     CU(cudaGetLastError());
     CU(cudaMemcpyAsync(d, dd.p, n * sizeof(float), cudaMemcpyDeviceToHost, h->st));
     CU(cudaMemcpyAsync(found, df.p, n, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaStreamSynchronize(h->st));
+  });
+}
+
+int vxg_mesh_extract(vxg_handle* h, const vxg_mc_tables* tables, const int32_t* blocks, uint64_t n_req,
+                     int with_colors, uint64_t* n_frag, uint64_t* n_tri) {
+  return guarded([&] {
+    if (h == nullptr || tables == nullptr || n_frag == nullptr || n_tri == nullptr)
+      throw VxgError(VXG_EINVAL, "null argument");
+    if (blocks == nullptr && n_req > 0) throw VxgError(VXG_EINVAL, "null block list");
+    set_device(h);
+    h->mesh_ready = false;
+    std::vector<uint32_t> order;
+    export_sorted(h, &order);  // every allocated block, sorted by (x, y, z)
+    std::vector<int32_t> slots;
+    if (blocks == nullptr) {
+      slots.assign(order.begin(), order.end());
+    } else {  // extract_blocks: the requested blocks that are allocated (block_ptr != nullptr)
+      std::unordered_map<uint64_t, uint32_t> rank;
+      rank.reserve(order.size());
+      for (uint32_t r = 0; r < order.size(); ++r) {
+        const int32_t* b = h->host_idx.data() + 3 * order[r];
+        rank.emplace(pack_block(b[0], b[1], b[2]), r);
+      }
+      std::vector<uint32_t> ranks;
+      for (uint64_t i = 0; i < n_req; ++i) {
+        const int32_t* b = blocks + 3 * i;
+        if (!block_in_range(b[0], b[1], b[2])) continue;
+        const auto it = rank.find(pack_block(b[0], b[1], b[2]));
+        if (it != rank.end()) ranks.push_back(it->second);
+      }
+      std::sort(ranks.begin(), ranks.end());
+      ranks.erase(std::unique(ranks.begin(), ranks.end()), ranks.end());
+      for (uint32_t r : ranks) slots.push_back(static_cast<int32_t>(order[r]));
+    }
+    const uint64_t B = slots.size();
+    h->mesh_bidx.resize(3 * B);
+    for (uint64_t j = 0; j < B; ++j)
+      for (int a = 0; a < 3; ++a) h->mesh_bidx[3 * j + a] = h->host_idx[3 * static_cast<uint64_t>(slots[j]) + a];
+    h->mesh_frag.assign(B + 1, 0);
+    h->mesh_T = 0;
+    h->mesh_colors = with_colors != 0;
+    if (B > 0) {
+      const uint64_t nc = B * static_cast<uint64_t>(h->nvox);
+      if (nc >= (1ull << 31)) throw VxgError(VXG_EINVAL, "too many blocks for one extraction");
+      CU(cudaMemcpyAsync(h->mesh_tab.ensure(1), tables, sizeof(vxg_mc_tables), cudaMemcpyHostToDevice, h->st));
+      CU(cudaMemcpyAsync(h->mesh_slots.ensure(B), slots.data(), B * sizeof(int32_t), cudaMemcpyHostToDevice, h->st));
+      h->mesh_ntri.ensure(nc + 1);
+      h->mesh_off.ensure(nc + 1);
+      const unsigned grid = grid_for(nc);
+      k_mc_count<<<grid, 256, 0, h->st>>>(nc, h->mesh_slots.p, h->view(), h->mesh_tab.p, h->mesh_ntri.p);
+      CU(cudaMemsetAsync(h->mesh_ntri.p + nc, 0, sizeof(uint32_t), h->st));
+      ++h->launches;
+      h->cub([&](void* t, size_t& b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, h->mesh_ntri.p, h->mesh_off.p, static_cast<int>(nc + 1), h->st);
+      }, 2);
+      // fragment boundaries: the scan at every block's first cube (+ the total)
+      h->mesh_frag_dev.ensure(B + 1);
+      k_gather_stride<<<grid_for(B + 1), 256, 0, h->st>>>(B + 1, h->mesh_off.p, static_cast<uint64_t>(h->nvox),
+                                                          h->mesh_frag_dev.p);
+      ++h->launches;
+      std::vector<uint32_t> fr(B + 1);
+      CU(cudaMemcpyAsync(fr.data(), h->mesh_frag_dev.p, (B + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, h->st));
+      CU(cudaStreamSynchronize(h->st));
+      for (uint64_t j = 0; j <= B; ++j) h->mesh_frag[j] = fr[j];
+      h->mesh_T = fr[B];
+      if (h->mesh_T > 0) {
+        h->mesh_v.ensure(9 * h->mesh_T);
+        h->mesh_n.ensure(9 * h->mesh_T);
+        if (h->mesh_colors) h->mesh_c.ensure(9 * h->mesh_T);
+        k_mc_emit<<<grid, 256, 0, h->st>>>(nc, h->mesh_slots.p, h->view(), h->voxel_size, h->mesh_tab.p,
+                                           h->mesh_ntri.p, h->mesh_off.p, with_colors, h->mesh_v.p, h->mesh_n.p,
+                                           h->mesh_colors ? h->mesh_c.p : nullptr);
+        ++h->launches;
+      }
+      CU(cudaGetLastError());
+      CU(cudaStreamSynchronize(h->st));
+    }
+    h->mesh_ready = true;
+    *n_frag = B;
+    *n_tri = h->mesh_T;
+  });
+}
+
+int vxg_mesh_fetch(vxg_handle* h, int32_t* block_idx, uint64_t* frag_tri, float* vertices, float* normals,
+                   uint8_t* colors) {
+  return guarded([&] {
+    if (h == nullptr) throw VxgError(VXG_EINVAL, "null argument");
+    if (!h->mesh_ready) throw VxgError(VXG_EINVAL, "no extracted mesh (call vxg_mesh_extract first)");
+    set_device(h);
+    const uint64_t B = h->mesh_bidx.size() / 3, T = h->mesh_T;
+    if (block_idx) std::memcpy(block_idx, h->mesh_bidx.data(), 3 * B * sizeof(int32_t));
+    if (frag_tri) std::memcpy(frag_tri, h->mesh_frag.data(), (B + 1) * sizeof(uint64_t));
+    if (T > 0) {
+      if (vertices) CU(cudaMemcpyAsync(vertices, h->mesh_v.p, 9 * T * sizeof(float), cudaMemcpyDeviceToHost, h->st));
+      if (normals) CU(cudaMemcpyAsync(normals, h->mesh_n.p, 9 * T * sizeof(float), cudaMemcpyDeviceToHost, h->st));
+      if (colors && h->mesh_colors) CU(cudaMemcpyAsync(colors, h->mesh_c.p, 9 * T, cudaMemcpyDeviceToHost, h->st));
+    }
     CU(cudaStreamSynchronize(h->st));
   });
 }

@@ -21,7 +21,8 @@ from typing import Dict, Optional, Sequence, Tuple
 
 import numpy as np
 
-from ._capi import (ParseError, VXG_INPUT_DEVICE, VXG_INPUT_HOST, VxgFrame, VxgStats, VxgTsdfConfig, VxgVoxel,
+from ._capi import (ParseError, VXG_INPUT_DEVICE, VXG_INPUT_HOST, VxgFrame, VxgMcTables, VxgStats, VxgTsdfConfig,
+                    VxgVoxel,
                     check, lib)
 
 VOXEL_DTYPE = np.dtype([("distance", "<f4"), ("weight", "<f4"), ("r", "u1"), ("g", "u1"), ("b", "u1"),
@@ -374,6 +375,88 @@ class TsdfIntegrator:
         return out
 
 
+
+@dataclass
+class Mesh:
+    """vxf::Mesh (mesh.h:13-33): triangle soup, 3 vertices per triangle in
+    emission order, per-vertex normals and optional colours."""
+    vertices: np.ndarray  # [V, 3] float32
+    normals: np.ndarray   # [V, 3] float32
+    colors: np.ndarray    # [V, 3] uint8 (empty without colours)
+    triangles: np.ndarray  # [T, 3] uint32
+
+    def empty(self) -> bool:
+        return len(self.triangles) == 0
+
+    def has_colors(self) -> bool:
+        return len(self.colors) > 0
+
+
+class MeshExtractor:
+    """vxf::MeshExtractor (mesh_extractor.h:13-35) on the device slab:
+    extract_blocks / extract_all replace the fragments of the blocks they
+    touch; fragments() maps block index -> Mesh; combined() concatenates the
+    fragments in (x, y, z) block order. The marching-cubes case tables are the
+    caller's (the reference build's mc_tables), as a VxgMcTables."""
+
+    def __init__(self, layer: TsdfLayer, tables, with_colors: bool = True):
+        self._layer = layer
+        self._tables = tables
+        self._with_colors = bool(with_colors)
+        self._fragments: Dict[Tuple[int, int, int], Mesh] = {}
+
+    def _run(self, blocks: Optional[np.ndarray]) -> None:
+        h = self._layer.handle
+        nf, nt = ctypes.c_uint64(), ctypes.c_uint64()
+        b = None if blocks is None else np.ascontiguousarray(blocks, dtype=np.int32).reshape(-1, 3)
+        check(lib().vxg_mesh_extract(h, ctypes.byref(self._tables), None if b is None else b.ctypes.data,
+                                     0 if b is None else len(b), int(self._with_colors), ctypes.byref(nf),
+                                     ctypes.byref(nt)))
+        B, T = nf.value, nt.value
+        bidx = np.zeros((B, 3), np.int32)
+        frag = np.zeros(B + 1, np.uint64)
+        v = np.zeros((3 * T, 3), np.float32)
+        n = np.zeros((3 * T, 3), np.float32)
+        c = np.zeros((3 * T, 3), np.uint8) if self._with_colors else np.zeros((0, 3), np.uint8)
+        check(lib().vxg_mesh_fetch(h, bidx.ctypes.data, frag.ctypes.data, v.ctypes.data, n.ctypes.data,
+                                   c.ctypes.data if self._with_colors else None))
+        for j in range(B):
+            t0, t1 = int(frag[j]), int(frag[j + 1])
+            k = t1 - t0
+            tri = np.arange(3 * k, dtype=np.uint32).reshape(k, 3)
+            self._fragments[tuple(int(x) for x in bidx[j])] = Mesh(
+                v[3 * t0:3 * t1].copy(), n[3 * t0:3 * t1].copy(),
+                c[3 * t0:3 * t1].copy() if self._with_colors else np.zeros((0, 3), np.uint8), tri)
+
+    def extract_blocks(self, blocks) -> None:
+        self._run(np.asarray(list(blocks), dtype=np.int32).reshape(-1, 3))
+
+    def extract_all(self) -> None:
+        self._run(None)
+
+    def fragments(self) -> Dict[Tuple[int, int, int], Mesh]:
+        return self._fragments
+
+    def combined(self) -> Mesh:
+        vs, ns, cs, ts = [], [], [], []
+        base = 0
+        for k in sorted(self._fragments):
+            m = self._fragments[k]
+            vs.append(m.vertices)
+            ns.append(m.normals)
+            cs.append(m.colors)
+            ts.append(m.triangles + base)
+            base += len(m.vertices)
+        cat = lambda xs, dt: np.concatenate(xs) if xs else np.zeros((0, 3), dt)  # noqa: E731
+        return Mesh(cat(vs, np.float32), cat(ns, np.float32),
+                    cat(cs, np.uint8) if self._with_colors else np.zeros((0, 3), np.uint8), cat(ts, np.uint32))
+
+
+def extract_mesh(layer: TsdfLayer, tables, with_colors: bool = True) -> Mesh:
+    """One-shot extraction over the whole layer (mesh_extractor.cpp:153-157)."""
+    ex = MeshExtractor(layer, tables, with_colors)
+    ex.extract_all()
+    return ex.combined()
 
 def nccl_unique_id() -> bytes:
     """128-byte NCCL unique id for vxg_shard_init (rank 0 makes it, the caller broadcasts it)."""

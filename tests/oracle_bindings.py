@@ -14,7 +14,7 @@ from ctypes import POINTER, c_char_p, c_float, c_int, c_int32, c_size_t, c_uint6
 
 import numpy as np
 
-from paper_1611_03631_b200._capi import VxgStats, VxgTsdfConfig, VxgVoxel
+from paper_1611_03631_b200._capi import VxgMcTables, VxgStats, VxgTsdfConfig, VxgVoxel
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 ORACLE_SO = os.path.join(ROOT, "oracle", "liboracle.so")
@@ -58,6 +58,9 @@ def oracle_lib():
                                             c_void_p, c_size_t]
         L.vxo_interpolate.argtypes = [c_void_p, c_void_p, c_size_t, c_void_p, c_void_p]
         L.vxo_surface_error.argtypes = [c_void_p, c_void_p, c_size_t, c_float, c_void_p]
+        L.vxo_mesh_extract.restype = c_size_t
+        L.vxo_mesh_extract.argtypes = [c_void_p, POINTER(VxgMcTables), c_int, c_void_p, c_size_t] + [c_void_p] * 5 + \
+            [c_size_t, c_size_t, POINTER(c_uint64)]
         L.vxo_bucket_schedule.restype = c_size_t
         L.vxo_bucket_schedule.argtypes = [c_size_t, c_size_t, c_void_p, c_size_t]
         _oracle = L
@@ -93,6 +96,11 @@ def ref_lib():
         L.vxr_index_hash.argtypes = [c_int32, c_int32, c_int32]
         L.vxr_interpolate.argtypes = [c_void_p, c_void_p, c_size_t, c_void_p, c_void_p]
         L.vxr_surface_error.argtypes = [c_void_p, c_void_p, c_size_t, c_float, c_void_p]
+        L.vxr_set_block.argtypes = [c_void_p, c_void_p, c_void_p]
+        L.vxr_mc_tables.argtypes = [POINTER(VxgMcTables)]
+        L.vxr_mesh_extract.restype = c_size_t
+        L.vxr_mesh_extract.argtypes = [c_void_p, c_int, c_void_p, c_size_t] + [c_void_p] * 5 + \
+            [c_size_t, c_size_t, POINTER(c_uint64)]
         _ref = L
     return _ref
 
@@ -160,6 +168,37 @@ class OracleLayer:
         v = np.ascontiguousarray(voxels)
         self.L.vxo_set_block(self.h, _vp(i), _vp(v))
 
+    def mesh_fragments(self, tables, with_colors=True, blocks=None):
+        b = None if blocks is None else np.ascontiguousarray(blocks, dtype=np.int32).reshape(-1, 3)
+        return _mesh(lambda *a: self.L.vxo_mesh_extract(self.h, ctypes.byref(tables), int(with_colors), _vp(b),
+                                                        0 if b is None else len(b), *a), with_colors)
+
+
+def mc_tables() -> VxgMcTables:
+    """The reference build's marching-cubes case tables (oracle/_ref)."""
+    t = VxgMcTables()
+    ref_lib().vxr_mc_tables(ctypes.byref(t))
+    return t
+
+
+def _mesh(call, with_colors):
+    """Run a two-call mesh extraction; returns {block: (verts[3T,3], normals, colors)}."""
+    nt = c_uint64()
+    nf = call(None, None, None, None, None, 0, 0, ctypes.byref(nt))
+    T = nt.value
+    bidx = np.zeros((nf, 3), np.int32)
+    frag = np.zeros(nf + 1, np.uint64)
+    v = np.zeros((3 * T, 3), np.float32)
+    n = np.zeros((3 * T, 3), np.float32)
+    c = np.zeros((3 * T, 3), np.uint8)
+    r = call(_vp(bidx), _vp(frag), _vp(v), _vp(n), _vp(c) if with_colors else None, nf, T, ctypes.byref(nt))
+    assert r == nf, "reference fragment triangles are not sequential"
+    out = {}
+    for j in range(nf):
+        a, b = 3 * int(frag[j]), 3 * int(frag[j + 1])
+        out[tuple(int(x) for x in bidx[j])] = (v[a:b], n[a:b], c[a:b] if with_colors else np.zeros((0, 3), np.uint8))
+    return out
+
 
 def _interp(fn, h, points):
     p = np.ascontiguousarray(points, dtype=np.float32).reshape(-1, 3)
@@ -210,6 +249,16 @@ class RefLayer:
 
     def block_count(self):
         return int(self.L.vxr_block_count(self.h))
+
+    def set_block(self, idx, voxels):
+        i = np.ascontiguousarray(idx, dtype=np.int32)
+        v = np.ascontiguousarray(voxels)
+        self.L.vxr_set_block(self.h, _vp(i), _vp(v))
+
+    def mesh_fragments(self, with_colors=True, blocks=None):
+        b = None if blocks is None else np.ascontiguousarray(blocks, dtype=np.int32).reshape(-1, 3)
+        return _mesh(lambda *a: self.L.vxr_mesh_extract(self.h, int(with_colors), _vp(b),
+                                                        0 if b is None else len(b), *a), with_colors)
 
     def save_bytes(self) -> bytes:
         need = self.L.vxr_save_vxblx(self.h, None, 0)
