@@ -31,7 +31,11 @@ $(OBJDIR)/bucket_schedule.o: $(CSRC)/bucket_schedule.cpp
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -x cu -c -o $@ $<
 
-$(LIB): $(OBJDIR)/vxg_tsdf.o $(OBJDIR)/bucket_schedule.o
+$(OBJDIR)/vxg_io.o: $(CSRC)/vxg_io.cu include/vxg.h include/vxg_types.h
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c -o $@ $<
+
+$(LIB): $(OBJDIR)/vxg_tsdf.o $(OBJDIR)/bucket_schedule.o $(OBJDIR)/vxg_io.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart_static -Xcompiler -fPIC
 
 $(PKG)/workload/libworkload.so: $(PKG)/workload/workload.c

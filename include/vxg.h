@@ -116,6 +116,28 @@ int vxg_mesh_extract(vxg_handle* h, const vxg_mc_tables* tables, const int32_t* 
 int vxg_mesh_fetch(vxg_handle* h, int32_t* block_idx, uint64_t* frag_tri, float* vertices, float* normals,
                    uint8_t* colors);
 
+/* ---- scan I/O (scan.h / scan.cpp), for the drop-in CLI flow (cmd_integrate)
+ * vxf::load_ply_points (scan.cpp:70-180): PLY point cloud, ascii or binary
+ * little-endian, vertex properties x,y,z[,red,green,blue] (others skipped).
+ * Two calls: xyz == NULL returns the vertex count *n and *has_color only;
+ * then xyz (n x 3) and rgb (n x 3, or NULL) receive the points — host
+ * pointers, or device pointers on `device` with flags = VXG_INPUT_DEVICE. A
+ * binary payload is decoded on the device. Errors carry the reference's
+ * std::runtime_error texts: VXG_EIO "cannot open PLY file: <path>", VXG_EPARSE
+ * for "not a PLY file", "unsupported PLY format", "list property on vertex
+ * element", "PLY vertex element lacks x/y/z properties", "truncated PLY vertex
+ * data", "malformed PLY vertex line", "unsupported PLY property/scalar type". */
+int vxg_ply_load(const char* path, int device, float* xyz, uint8_t* rgb, uint64_t cap, int flags, uint64_t* n,
+                 int* has_color);
+/* vxf::load_tum_trajectory (scan.cpp:182-211): `timestamp tx ty tz qx qy qz
+ * qw` per line, '#' comments; poses as row-major 3x4 [R | t] (R from the
+ * normalized quaternion). ts == poses == NULL: count only. Host-side text. */
+int vxg_tum_load(const char* path, double* ts, float* poses, uint64_t cap, uint64_t* n);
+/* vxf::save_ply_mesh (scan.cpp:213-240): binary little-endian PLY with
+ * normals and, when colors != NULL, colours; triangles n_triangles x 3. */
+int vxg_save_ply_mesh(const char* path, const float* vertices, const float* normals, const uint8_t* colors,
+                      uint64_t n_vertices, const uint32_t* triangles, uint64_t n_triangles);
+
 /* Layer::block_count() (layer.h:72). */
 int vxg_block_count(vxg_handle* h, uint64_t* out);
 

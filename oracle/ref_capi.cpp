@@ -15,6 +15,7 @@
 #include "vxf/layer.h"
 #include "vxf/marching_cubes_tables.h"
 #include "vxf/mesh_extractor.h"
+#include "vxf/scan.h"
 #include "vxf/serialization.h"
 #include "vxf/tsdf_integrator.h"
 
@@ -257,6 +258,68 @@ size_t vxr_mesh_extract(void* hp, int with_colors, const int32_t* blocks, size_t
   }
   if (frag_tri) frag_tri[order.size()] = o;
   return order.size();
+}
+
+// vxf::load_ply_points: two calls (xyz == NULL: count + has_color). Returns 0,
+// or 1 with the exception text in vxr_last_error().
+int vxr_load_ply(const char* path, float* xyz, uint8_t* rgb, uint64_t* n, int* has_color) {
+  try {
+    const vxf::Scan s = vxf::load_ply_points(path);
+    *n = s.points.size();
+    *has_color = s.has_colors() ? 1 : 0;
+    if (xyz)
+      for (size_t i = 0; i < s.points.size(); ++i)
+        for (int a = 0; a < 3; ++a) xyz[3 * i + a] = s.points[i][a];
+    if (rgb && s.has_colors())
+      for (size_t i = 0; i < s.colors.size(); ++i) {
+        rgb[3 * i] = s.colors[i].r;
+        rgb[3 * i + 1] = s.colors[i].g;
+        rgb[3 * i + 2] = s.colors[i].b;
+      }
+    return 0;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return 1;
+  }
+}
+
+// vxf::load_tum_trajectory: poses as row-major [R | t].
+int vxr_load_tum(const char* path, double* ts, float* poses, uint64_t* n) {
+  try {
+    const auto tr = vxf::load_tum_trajectory(path);
+    *n = tr.size();
+    for (size_t i = 0; i < tr.size(); ++i) {
+      if (ts) ts[i] = tr[i].timestamp;
+      if (poses)
+        for (int r = 0; r < 3; ++r) {
+          for (int c = 0; c < 3; ++c) poses[12 * i + 4 * r + c] = tr[i].pose.linear()(r, c);
+          poses[12 * i + 4 * r + 3] = tr[i].pose.translation()[r];
+        }
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return 1;
+  }
+}
+
+// vxf::save_ply_mesh of a mesh given as flat arrays.
+int vxr_save_ply_mesh(const char* path, const float* v, const float* nrm, const uint8_t* c, uint64_t nv,
+                      const uint32_t* tri, uint64_t nt) {
+  try {
+    vxf::Mesh m;
+    for (uint64_t i = 0; i < nv; ++i) {
+      m.vertices.emplace_back(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+      m.normals.emplace_back(nrm[3 * i], nrm[3 * i + 1], nrm[3 * i + 2]);
+      if (c) m.colors.push_back(vxf::Color{c[3 * i], c[3 * i + 1], c[3 * i + 2]});
+    }
+    for (uint64_t t = 0; t < nt; ++t) m.triangles.push_back({tri[3 * t], tri[3 * t + 1], tri[3 * t + 2]});
+    vxf::save_ply_mesh(m, path);
+    return 0;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return 1;
+  }
 }
 
 }  // extern "C"

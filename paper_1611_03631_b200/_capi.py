@@ -66,6 +66,10 @@ SIGNATURES = [
     ("vxg_mesh_extract", c_int,
      [c_void_p, POINTER(VxgMcTables), c_void_p, c_uint64, c_int, POINTER(c_uint64), POINTER(c_uint64)]),
     ("vxg_mesh_fetch", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("vxg_ply_load", c_int,
+     [c_char_p, c_int, c_void_p, c_void_p, c_uint64, c_int, POINTER(c_uint64), POINTER(c_int)]),
+    ("vxg_tum_load", c_int, [c_char_p, c_void_p, c_void_p, c_uint64, POINTER(c_uint64)]),
+    ("vxg_save_ply_mesh", c_int, [c_char_p, c_void_p, c_void_p, c_void_p, c_uint64, c_void_p, c_uint64]),
     ("vxg_block_count", c_int, [c_void_p, POINTER(c_uint64)]),
     ("vxg_export_blocks", c_int, [c_void_p, c_void_p, c_void_p, c_uint64, POINTER(c_uint64)]),
     ("vxg_import_blocks", c_int, [c_void_p, c_void_p, c_void_p, c_uint64]),

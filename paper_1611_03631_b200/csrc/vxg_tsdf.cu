@@ -47,6 +47,15 @@ namespace {
 
 thread_local std::string g_err;
 
+}  // namespace
+
+// vxg_last_error() for the other translation units of the library (scan I/O).
+namespace vxg {
+void set_last_error(const std::string& msg) { g_err = msg; }
+}  // namespace vxg
+
+namespace {
+
 struct Status {
   int code;
   std::string msg;

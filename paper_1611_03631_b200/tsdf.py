@@ -458,6 +458,65 @@ def extract_mesh(layer: TsdfLayer, tables, with_colors: bool = True) -> Mesh:
     ex.extract_all()
     return ex.combined()
 
+def _check_io(rc: int) -> None:
+    """Scan I/O errors are std::runtime_error in the reference (scan.cpp)."""
+    if rc in (1,):  # VXG_EINVAL: bad arguments on our side
+        check(rc)
+    if rc != 0:
+        raise RuntimeError(lib().vxg_last_error().decode())
+
+
+def load_ply_points(path: str, device: Optional[int] = None) -> Scan:
+    """vxf::load_ply_points (scan.cpp:70-180). A binary payload is decoded on the
+    GPU. device=None: a Scan with numpy arrays in host memory (identity pose);
+    device=k: (xyz, rgb-or-None) torch CUDA tensors on device k, ready for
+    integrate_packed(..., device_input=True)."""
+    n, hc = ctypes.c_uint64(), ctypes.c_int()
+    bp = path.encode()
+    _check_io(lib().vxg_ply_load(bp, 0 if device is None else device, None, None, 0, VXG_INPUT_HOST,
+                                 ctypes.byref(n), ctypes.byref(hc)))
+    N = n.value
+    if device is None:
+        xyz = np.zeros((N, 3), np.float32)
+        rgb = np.zeros((N, 3), np.uint8) if hc.value else None
+        _check_io(lib().vxg_ply_load(bp, 0, xyz.ctypes.data, None if rgb is None else rgb.ctypes.data, N,
+                                     VXG_INPUT_HOST, ctypes.byref(n), ctypes.byref(hc)))
+        return Scan(xyz, rgb)
+    import torch
+    xyz = torch.empty((N, 3), dtype=torch.float32, device=f"cuda:{device}")
+    rgb = torch.empty((N, 3), dtype=torch.uint8, device=f"cuda:{device}") if hc.value else None
+    _check_io(lib().vxg_ply_load(bp, device, xyz.data_ptr(), None if rgb is None else rgb.data_ptr(), N,
+                                 VXG_INPUT_DEVICE, ctypes.byref(n), ctypes.byref(hc)))
+    return xyz, rgb
+
+
+@dataclass
+class TimedPose:
+    """vxf::TimedPose (scan.h:22-25)."""
+    timestamp: float
+    pose: np.ndarray  # 3x4 [R | t]
+
+
+def load_tum_trajectory(path: str) -> list:
+    """vxf::load_tum_trajectory (scan.cpp:182-211)."""
+    n = ctypes.c_uint64()
+    bp = path.encode()
+    _check_io(lib().vxg_tum_load(bp, None, None, 0, ctypes.byref(n)))
+    ts = np.zeros(n.value, np.float64)
+    ps = np.zeros((n.value, 3, 4), np.float32)
+    _check_io(lib().vxg_tum_load(bp, ts.ctypes.data, ps.ctypes.data, n.value, ctypes.byref(n)))
+    return [TimedPose(float(ts[i]), ps[i]) for i in range(n.value)]
+
+
+def save_ply_mesh(mesh: "Mesh", path: str) -> None:
+    """vxf::save_ply_mesh (scan.cpp:213-240)."""
+    v = np.ascontiguousarray(mesh.vertices, np.float32)
+    nr = np.ascontiguousarray(mesh.normals, np.float32)
+    c = np.ascontiguousarray(mesh.colors, np.uint8) if mesh.has_colors() else None
+    t = np.ascontiguousarray(mesh.triangles, np.uint32)
+    _check_io(lib().vxg_save_ply_mesh(path.encode(), v.ctypes.data, nr.ctypes.data,
+                                      None if c is None else c.ctypes.data, len(v), t.ctypes.data, len(t)))
+
 def nccl_unique_id() -> bytes:
     """128-byte NCCL unique id for vxg_shard_init (rank 0 makes it, the caller broadcasts it)."""
     buf = (ctypes.c_uint8 * 128)()

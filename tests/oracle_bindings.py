@@ -98,6 +98,9 @@ def ref_lib():
         L.vxr_surface_error.argtypes = [c_void_p, c_void_p, c_size_t, c_float, c_void_p]
         L.vxr_set_block.argtypes = [c_void_p, c_void_p, c_void_p]
         L.vxr_mc_tables.argtypes = [POINTER(VxgMcTables)]
+        L.vxr_load_ply.argtypes = [c_char_p, c_void_p, c_void_p, POINTER(c_uint64), POINTER(c_int)]
+        L.vxr_load_tum.argtypes = [c_char_p, c_void_p, c_void_p, POINTER(c_uint64)]
+        L.vxr_save_ply_mesh.argtypes = [c_char_p, c_void_p, c_void_p, c_void_p, c_uint64, c_void_p, c_uint64]
         L.vxr_mesh_extract.restype = c_size_t
         L.vxr_mesh_extract.argtypes = [c_void_p, c_int, c_void_p, c_size_t] + [c_void_p] * 5 + \
             [c_size_t, c_size_t, POINTER(c_uint64)]
@@ -179,6 +182,37 @@ def mc_tables() -> VxgMcTables:
     t = VxgMcTables()
     ref_lib().vxr_mc_tables(ctypes.byref(t))
     return t
+
+
+def ref_load_ply(path):
+    """(xyz, rgb or None) from the reference's load_ply_points, or raises RuntimeError(text)."""
+    L = ref_lib()
+    n, hc = c_uint64(), c_int()
+    if L.vxr_load_ply(path.encode(), None, None, ctypes.byref(n), ctypes.byref(hc)):
+        raise RuntimeError(L.vxr_last_error().decode())
+    xyz = np.zeros((n.value, 3), np.float32)
+    rgb = np.zeros((n.value, 3), np.uint8) if hc.value else None
+    L.vxr_load_ply(path.encode(), _vp(xyz), _vp(rgb), ctypes.byref(n), ctypes.byref(hc))
+    return xyz, rgb
+
+
+def ref_load_tum(path):
+    L = ref_lib()
+    n = c_uint64()
+    if L.vxr_load_tum(path.encode(), None, None, ctypes.byref(n)):
+        raise RuntimeError(L.vxr_last_error().decode())
+    ts = np.zeros(n.value, np.float64)
+    ps = np.zeros((n.value, 3, 4), np.float32)
+    L.vxr_load_tum(path.encode(), _vp(ts), _vp(ps), ctypes.byref(n))
+    return ts, ps
+
+
+def ref_save_ply_mesh(path, v, n, c, tri):
+    L = ref_lib()
+    v, n, tri = (np.ascontiguousarray(a) for a in (v, n, tri))
+    c = None if c is None else np.ascontiguousarray(c)
+    if L.vxr_save_ply_mesh(path.encode(), _vp(v), _vp(n), _vp(c), len(v), _vp(tri), len(tri)):
+        raise RuntimeError(L.vxr_last_error().decode())
 
 
 def _mesh(call, with_colors):
