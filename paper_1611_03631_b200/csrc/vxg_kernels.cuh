@@ -1468,6 +1468,39 @@ __global__ void k_add_u64(uint32_t n, unsigned long long* __restrict__ dst, cons
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] += src[i];
 }
 
+// Pipeline chunk bounds: out[c] = first ray of chunk c (c <= n, out[n] = R),
+// out[n + 1 + c] = its first record; chunk c starts at the first ray whose
+// record offset reaches c * total / n.
+__global__ void k_chunk_bounds(uint32_t R, const unsigned long long* __restrict__ roff, unsigned long long total,
+                               uint32_t n, unsigned long long* __restrict__ out) {
+  for (uint32_t c = threadIdx.x; c <= n; c += blockDim.x) {
+    const unsigned long long target = total / n * c + (total % n) * c / n;
+    uint32_t lo = 0, hi = R;  // smallest r with roff(r) >= target, roff(R) = total
+    while (lo < hi) {
+      const uint32_t mid = lo + (hi - lo) / 2;
+      if (roff[mid] >= target) hi = mid; else lo = mid + 1;
+    }
+    if (c == n) lo = R;
+    out[c] = lo;
+    out[n + 1 + c] = lo < R ? roff[lo] : total;
+  }
+}
+
+// Emission order key of ray r: chunk first (descending sort puts chunk 0
+// first), then the record count (longest first inside a chunk).
+__global__ void k_chunk_keys(uint32_t R, const unsigned long long* __restrict__ rcount,
+                             const unsigned long long* __restrict__ bounds, uint32_t n,
+                             unsigned long long* __restrict__ keys) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < R; r += gridDim.x * blockDim.x) {
+    uint32_t lo = 0, hi = n - 1;  // largest c with bounds[c] <= r
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi + 1) / 2;
+      if (bounds[mid] <= r) lo = mid; else hi = mid - 1;
+    }
+    keys[r] = (static_cast<unsigned long long>(n - 1 - lo) << 16) | min(rcount[r], 65535ull);
+  }
+}
+
 __global__ void k_iota(uint32_t n, uint32_t* __restrict__ out) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = i;
 }

@@ -144,6 +144,19 @@ struct vxg_handle {
   cudaStream_t copy_st = nullptr;         // H2D staging of host inputs (overlaps compute)
   cudaStream_t fold_st = nullptr;         // short-run fold beside the long-run fold
   cudaEvent_t fold_fork = nullptr, fold_join = nullptr;
+  // ---- chunk pipeline: chunk c's fold (fold_long_st + fold_st) runs while
+  // chunk c+1 is emitted and sorted on st. Two buffer sets (records + runs)
+  // alternate between chunks; set_done[s] marks the end of the last fold that
+  // read set s. Folds of consecutive chunks are ordered (same voxels).
+  cudaStream_t fold_long_st = nullptr;
+  cudaEvent_t fold_long_done = nullptr, fold_origins = nullptr;
+  cudaEvent_t set_done[2] = {nullptr, nullptr};
+  bool set_busy[2] = {false, false};
+  int cur_set = 0;
+  bool fold_inflight = false;  // a fold was launched that st has not joined yet
+  uint32_t* top_pinned = nullptr;  // longest run per chunk (read back at the batch end)
+  uint32_t n_top = 0;
+  static constexpr uint32_t kTopCap = 256;
   std::vector<cudaEvent_t> copy_events;
   // ---- streaming ingestion: two staging slots (vxg_stage_packed / vxg_integrate_staged)
   struct StageSlot {
@@ -201,6 +214,11 @@ struct vxg_handle {
   DBuf<uint64_t> tbl_off, bcs;
   DBuf<uint32_t> rkeys, rkeys2, rvals, rvals2;
   DBuf<uint32_t> run_keys, run_len, run_start, run_len2, run_order, run_iota, work;
+  struct FoldSet {  // the other buffer set of the chunk pipeline (swapped with the members above)
+    DBuf<uint32_t> rkeys, rkeys2, rvals, rvals2, run_keys, run_len, run_start, run_len2, run_order, num_runs, work;
+  } alt;
+  DBuf<unsigned long long> ckeys;       // emission order keys: (chunk, ray length)
+  DBuf<unsigned long long> chunk_base;  // per chunk: first ray, first record
   DBuf<uint32_t> sort_counts, sort_offs, dense_start, dense_end, run_flag, run_pos;
   DBuf<FoldRay> fold_rays;
   DBuf<float4> pt_w;    // bundling: per sorted point (world point, weight)
@@ -261,16 +279,16 @@ struct vxg_handle {
   // Stage timer: begin() records on the stream; end() records and queues the pair.
   int cur_stage = -1;
   cudaEvent_t cur_begin = nullptr;
-  void begin(int s) {
+  void begin(int s, cudaStream_t on = nullptr) {
     if (!profile) return;
     cur_stage = s;
     cur_begin = ev();
-    CU(cudaEventRecord(cur_begin, st));
+    CU(cudaEventRecord(cur_begin, on ? on : st));
   }
-  void end(uint64_t units = 0, uint64_t n_launch = 0) {
+  void end(uint64_t units = 0, uint64_t n_launch = 0, cudaStream_t on = nullptr) {
     if (!profile || cur_stage < 0) return;
     cudaEvent_t e = ev();
-    CU(cudaEventRecord(e, st));
+    CU(cudaEventRecord(e, on ? on : st));
     pending.push_back({cur_stage, {cur_begin, e}});
     stage_units[cur_stage] += units;
     stage_launch[cur_stage] += n_launch;
@@ -397,6 +415,64 @@ struct vxg_handle {
     touched.release();
     touched.p = n;
     touched.cap = cap_blocks;
+  }
+
+  // ---------------------------------------------------------------- chunk pipeline
+  void ensure_fold_streams() {
+    if (fold_long_st != nullptr) return;
+    CU(cudaStreamCreateWithFlags(&fold_st, cudaStreamNonBlocking));
+    // the long-run CTAs must become resident before the short-run grid fills
+    // the SMs (the longest chain bounds the fold): highest priority
+    int lo_prio = 0, hi_prio = 0;
+    CU(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+    CU(cudaStreamCreateWithPriority(&fold_long_st, cudaStreamNonBlocking, hi_prio));
+    CU(cudaEventCreateWithFlags(&fold_fork, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&fold_join, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&fold_long_done, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&fold_origins, cudaEventDisableTiming));
+    for (auto& e : set_done) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CU(cudaHostAlloc(&top_pinned, kTopCap * sizeof(uint32_t), cudaHostAllocDefault));
+  }
+  // Switch to the other buffer set; st waits until the fold that last read it is done.
+  void swap_fold_set() {
+    rkeys.swap(alt.rkeys);
+    rkeys2.swap(alt.rkeys2);
+    rvals.swap(alt.rvals);
+    rvals2.swap(alt.rvals2);
+    run_keys.swap(alt.run_keys);
+    run_len.swap(alt.run_len);
+    run_start.swap(alt.run_start);
+    run_len2.swap(alt.run_len2);
+    run_order.swap(alt.run_order);
+    num_runs.swap(alt.num_runs);
+    work.swap(alt.work);
+    cur_set ^= 1;
+    if (set_busy[cur_set]) CU(cudaStreamWaitEvent(st, set_done[cur_set], 0));
+  }
+  // Host wait for every launched fold (before the slab moves or buffers are freed).
+  void sync_folds() {
+    if (fold_st != nullptr) CU(cudaStreamSynchronize(fold_st));
+    if (fold_long_st != nullptr) CU(cudaStreamSynchronize(fold_long_st));
+    set_busy[0] = set_busy[1] = false;
+  }
+  // Record buffers of the current set; reallocation waits for in-flight folds.
+  void ensure_records(uint64_t T) {
+    if (T > rkeys.cap || T > rkeys2.cap || T > rvals.cap || T > rvals2.cap) sync_folds();
+    rkeys.ensure(T);
+    rkeys2.ensure(T);
+    rvals.ensure(T);
+    rvals2.ensure(T);
+  }
+  // st waits for the last launched fold (end of a batch / before the slab is read).
+  void join_folds() {
+    if (!fold_inflight) return;
+    CU(cudaStreamWaitEvent(st, fold_join, 0));
+    fold_inflight = false;
+  }
+  // After a host sync of st that followed join_folds(): longest runs of the batch.
+  void drain_tops() {
+    for (uint32_t i = 0; i < n_top; ++i) info_max_run = std::max<uint64_t>(info_max_run, top_pinned[i]);
+    n_top = 0;
   }
 
   void read_counters(uint32_t* c) {
@@ -815,10 +891,12 @@ void vxg_handle::sort_fold(uint64_t T, uint64_t nslots, uint32_t F) {
   // compact the runs in key order
   run_flag.ensure(K);
   run_pos.ensure(K);
+  if (K > run_keys.cap || K > run_len.cap || K > run_start.cap || !num_runs.p || !work.p) sync_folds();
   run_keys.ensure(K);
   run_len.ensure(K);
   run_start.ensure(K);
   num_runs.ensure(1);
+  work.ensure(2);
   k_run_flags<<<grid_for(K), 256, 0, st>>>(static_cast<uint32_t>(K), dense_end.p, run_flag.p);
   ++launches;
   cub([&](void* t, size_t& b) {
@@ -831,6 +909,7 @@ void vxg_handle::sort_fold(uint64_t T, uint64_t nslots, uint32_t F) {
   uint32_t nruns = 0;
   CU(cudaMemcpyAsync(&nruns, num_runs.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
+  if (std::max<uint32_t>(nruns, 1) > std::min(run_len2.cap, run_order.cap)) sync_folds();
   run_len2.ensure(std::max<uint32_t>(nruns, 1));
   run_order.ensure(std::max<uint32_t>(nruns, 1));
   run_iota.ensure(std::max<uint32_t>(nruns, 1));
@@ -844,14 +923,23 @@ void vxg_handle::sort_fold(uint64_t T, uint64_t nslots, uint32_t F) {
     }, 2 + (lbits + 7) / 8);
   }
   end(T, 0);
-  begin(ST_APPLY);
+  ensure_fold_streams();
+  // longest run of this chunk, read back at the batch end
+  if (nruns) {
+    if (n_top == kTopCap) {
+      CU(cudaStreamSynchronize(st));
+      drain_tops();
+    }
+    CU(cudaMemcpyAsync(top_pinned + n_top++, run_len2.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  }
   uint8_t* tch = consumers.empty() ? nullptr : touched.p;
-  work.ensure(2);
   CU(cudaMemsetAsync(work.p, 0, 2 * sizeof(uint32_t), st));
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
-  // long runs: one CTA (4 producer/consumer pairs) per SM on st; short runs:
-  // k_fold_short on fold_st beside it (disjoint voxels), filling the rest
+  // long runs: one CTA (4 producer/consumer pairs) per SM on fold_long_st;
+  // short runs: k_fold_short on fold_st beside it (disjoint voxels). Both run
+  // after this chunk's runs are ready (fold_fork) and after the previous
+  // chunk's fold (fold_join); st goes on with the next chunk meanwhile.
   const unsigned long_grid = static_cast<unsigned>(std::max<uint64_t>(
       1, std::min<uint64_t>(static_cast<uint64_t>(dev_sms), (nruns + 3) / 4)));
   unsigned long long* dbg = nullptr;
@@ -863,16 +951,19 @@ void vxg_handle::sort_fold(uint64_t T, uint64_t nslots, uint32_t F) {
     fold_dbg_n = nruns;
   }
   if (nruns) {
-    if (fold_st == nullptr) {
-      CU(cudaStreamCreateWithFlags(&fold_st, cudaStreamNonBlocking));
-      CU(cudaEventCreateWithFlags(&fold_fork, cudaEventDisableTiming));
-      CU(cudaEventCreateWithFlags(&fold_join, cudaEventDisableTiming));
-    }
     d_org.ensure(3 * std::max<uint32_t>(F, 1));
-    k_origins<<<grid_for(3 * F), 256, 0, st>>>(F, d_poses.p, d_org.p);
-    ++launches;
     CU(cudaEventRecord(fold_fork, st));
-    CU(cudaStreamWaitEvent(fold_st, fold_fork, 0));
+    CU(cudaStreamWaitEvent(fold_long_st, fold_fork, 0));
+    if (fold_inflight) CU(cudaStreamWaitEvent(fold_long_st, fold_join, 0));  // previous chunk folded
+    // The long-run grid must be resident before the short-run grid (persistent
+    // CTAs) fills the SMs, or the longest chain starts only after every short
+    // run is done (measured 3.7 vs 2.6 ms on cfg1). It directly follows
+    // k_origins in its stream; the short grid waits for k_origins via an event,
+    // which the front end resolves after the in-stream successor is launched.
+    k_origins<<<grid_for(3 * F), 256, 0, fold_long_st>>>(F, d_poses.p, d_org.p);
+    ++launches;
+    CU(cudaEventRecord(fold_origins, fold_long_st));
+    CU(cudaStreamWaitEvent(fold_st, fold_origins, 0));
     static const int long_layout = [] {
       const char* e = getenv("VXG_LONG_LAYOUT");
       return e ? atoi(e) : 0;
@@ -887,49 +978,53 @@ void vxg_handle::sort_fold(uint64_t T, uint64_t nslots, uint32_t F) {
     }();
     const unsigned lg = long_ctas > 0 ? static_cast<unsigned>(long_ctas) : long_grid;
     const bool smem_org = F <= kOrgCache;
+    begin(ST_APPLY, fold_long_st);
 #define VXG_FOLD_LONG(P, SEP, THREADS)                                                                              \
   do {                                                                                                           \
     auto kern = smem_org ? k_fold_runs<P, SEP, true> : k_fold_runs<P, SEP, false>;                              \
     if (long_smem) CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, long_smem));      \
-    kern<<<lg, THREADS, long_smem, st>>>(num_runs.p, run_order.p, run_len2.p, run_keys.p, run_start.p, run_len.p, \
-                                         svals, fold_rays.p, d_org.p, F, view(), tp, tch, work.p, dbg);           \
+    kern<<<lg, THREADS, long_smem, fold_long_st>>>(num_runs.p, run_order.p, run_len2.p, run_keys.p, run_start.p,  \
+                                                   run_len.p, svals, fold_rays.p, d_org.p, F, view(), tp, tch,     \
+                                                   work.p, dbg);                                                 \
   } while (0)
     if (long_layout == 2)
       VXG_FOLD_LONG(2, true, 128);
     else
       VXG_FOLD_LONG(4, false, 256);
 #undef VXG_FOLD_LONG
+    CU(cudaEventRecord(fold_long_done, fold_long_st));
     static const int short_blocks = [] {
       const char* e = getenv("VXG_FOLD_SHORT_BLOCKS");
       return e ? atoi(e) : 5;
     }();
     static const bool serial = getenv("VXG_FOLD_SERIAL") != nullptr;  // dev: long runs uncontended
-    cudaStream_t sst = serial ? st : fold_st;
+    if (serial) CU(cudaStreamWaitEvent(fold_st, fold_long_done, 0));
     const unsigned short_grid = static_cast<unsigned>(std::max<uint64_t>(
         1, std::min<uint64_t>(static_cast<uint64_t>(dev_sms) * 4, (nruns + 255) / 256)));
 #define VXG_FOLD_SHORT(MB, C)                                                                                 \
   do {                                                                                                        \
     auto kern = smem_org ? k_fold_short<MB, C, true> : k_fold_short<MB, C, false>;                           \
-    kern<<<short_grid, 256, 0, sst>>>(num_runs.p, run_order.p, run_len2.p, run_keys.p, run_start.p, run_len.p, \
-                                      svals, fold_rays.p, d_org.p, F, view(), tp, tch, work.p);                \
+    kern<<<short_grid, 256, 0, fold_st>>>(num_runs.p, run_order.p, run_len2.p, run_keys.p, run_start.p,       \
+                                          run_len.p, svals, fold_rays.p, d_org.p, F, view(), tp, tch, work.p); \
   } while (0)
     if (short_blocks == 1)
       VXG_FOLD_SHORT(3, 4);
     else
       VXG_FOLD_SHORT(2, 4);
 #undef VXG_FOLD_SHORT
+    CU(cudaStreamWaitEvent(fold_st, fold_long_done, 0));
+    end(T, 2, fold_st);
     CU(cudaEventRecord(fold_join, fold_st));
-    CU(cudaStreamWaitEvent(st, fold_join, 0));
+    CU(cudaEventRecord(set_done[cur_set], fold_st));
+    set_busy[cur_set] = true;
+    fold_inflight = true;
     launches += 2;
   }
   CU(cudaGetLastError());
-  end(T, 1);
-  uint32_t top = 0;
-  if (nruns) CU(cudaMemcpyAsync(&top, run_len2.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
+  static const bool no_pipe = getenv("VXG_NO_PIPELINE") != nullptr;  // dev A/B: fold before the next chunk
+  if (no_pipe) join_folds();
   info_records += T;
   info_runs += nruns;
-  info_max_run = std::max<uint64_t>(info_max_run, top);
 }
 
 // After a produce+sort_fold attempt: true if the map had to grow (the caller
@@ -941,6 +1036,7 @@ bool vxg_handle::grew_after_attempt(int attempt) {
   if (c[1] & kErrKeyRange) throw VxgError(VXG_ERANGE, "voxel block index outside the supported range");
   if (c[1] & (kErrSlabFull | kErrHashFull)) {
     if (attempt > 64) throw VxgError(VXG_ENOMEM, "block allocation did not converge");
+    sync_folds();  // earlier chunks' folds still read/write the slab that is about to move
     if (c[1] & kErrHashFull) rehash(hcap * 2);
     grow_map(std::max<uint64_t>(c[0], cap_blocks + 1));
     ensure_touched();
@@ -949,63 +1045,64 @@ bool vxg_handle::grew_after_attempt(int attempt) {
   return false;
 }
 
+// Pipeline chunks: records are produced, sorted and folded in chunks of
+// consecutive rays (ray order), so every voxel still folds its updates in the
+// reference's order (chunk by chunk). Chunk c's fold overlaps chunk c+1's emit
+// and sort. Batches are chunked only when their records exceed kMaxRecords:
+// measured on cfg1 (2.4e8 records), 4 chunks cost 14.4 vs 12.6 ms/step — a
+// hot voxel's chain sits inside one chunk (its rays come from a few adjacent
+// frames), so every chunk's fold is still bound by a full-length chain and
+// the folds, which must run in chunk order, add up (VXG_CHUNK_RECORDS: A/B).
+uint32_t pipeline_chunks(uint64_t total) {
+  const uint64_t kMaxRecords = (1ull << 29) - (1ull << 20);  // keeps every chunk 32-bit addressable
+  static const uint64_t per = [kMaxRecords] {
+    const char* e = getenv("VXG_CHUNK_RECORDS");
+    return e ? std::max<uint64_t>(1, strtoull(e, nullptr, 10)) : kMaxRecords;
+  }();
+  uint64_t n = std::max<uint64_t>((total + per - 1) / per, (total + kMaxRecords - 1) / kMaxRecords);
+  return static_cast<uint32_t>(std::min<uint64_t>(std::max<uint64_t>(n, 1), 64));
+}
+
 void vxg_handle::emit_and_apply(uint32_t R, uint32_t F, const TermView& tv) {
   const TsdfParams tp = params();
   const uint64_t total = count_rays(R, F);
-  // chunk rays so one chunk's records stay addressable and within memory
-  const uint64_t kMaxRecords = 1ull << 29;
-  std::vector<unsigned long long> h_roff;
-  if (total > kMaxRecords) {
-    h_roff.resize(R);
-    CU(cudaMemcpyAsync(h_roff.data(), roff.p, R * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-  }
-  auto roff_at = [&](uint32_t r) -> uint64_t {
-    return r >= R ? total : (h_roff.empty() ? (r == 0 ? 0 : total) : h_roff[r]);
-  };
-  // emission order: rays by decreasing record count (balanced warps); the
-  // records still land at their ray-order offsets.
+  const uint32_t nch = pipeline_chunks(total);
+  // chunk bounds (first ray, first record) by record count, on the device
+  chunk_base.ensure(2 * (nch + 1));
+  std::vector<unsigned long long> hb(2 * (nch + 1));
+  k_chunk_bounds<<<1, 64, 0, st>>>(R, roff.p, total, nch, chunk_base.p);
+  ++launches;
+  CU(cudaMemcpyAsync(hb.data(), chunk_base.p, hb.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  // emission order: rays by decreasing record count inside each chunk (balanced
+  // warps); the records still land at their ray-order offsets.
   ray_perm.ensure(R);
   ray_iota.ensure(R);
   rcount2.ensure(R);
+  ckeys.ensure(R);
   k_iota<<<grid_for(R), 256, 0, st>>>(R, ray_iota.p);
-  ++launches;
+  k_chunk_keys<<<grid_for(R), 256, 0, st>>>(R, rcount.p, chunk_base.p, nch, ckeys.p);
+  launches += 2;
+  const int cbits = 16 + bits_for(nch - 1);
   cub([&](void* t, size_t& b) {
-    return cub::DeviceRadixSort::SortPairsDescending(t, b, rcount.p, rcount2.p, ray_iota.p, ray_perm.p,
-                                                     static_cast<int>(R), 0, 16, st);
-  }, 4);
+    return cub::DeviceRadixSort::SortPairsDescending(t, b, ckeys.p, rcount2.p, ray_iota.p, ray_perm.p,
+                                                     static_cast<int>(R), 0, cbits, st);
+  }, 2 + (cbits + 7) / 8);
   ensure_touched();
-  uint32_t r0 = 0;
-  while (r0 < R) {
-    uint32_t r1 = R;
-    if (!h_roff.empty()) {
-      // largest r1 with records(r0, r1) <= kMaxRecords (at least one ray)
-      uint32_t lo = r0 + 1, hi = R;
-      while (lo < hi) {
-        const uint32_t mid = lo + (hi - lo + 1) / 2;
-        if (roff_at(mid) - roff_at(r0) <= kMaxRecords) lo = mid; else hi = mid - 1;
-      }
-      r1 = lo;
-    }
-    const uint64_t base = roff_at(r0);
-    const uint64_t T = roff_at(r1) - base;
-    if (T == 0) {
-      r0 = r1;
-      continue;
-    }
-    rkeys.ensure(T);
-    rkeys2.ensure(T);
-    rvals.ensure(T);
-    rvals2.ensure(T);
-    d_upd.ensure(F);
+  CU(cudaStreamSynchronize(st));  // hb
+  d_upd.ensure(F);
+  for (uint32_t c = 0; c < nch; ++c) {
+    const uint32_t r0 = static_cast<uint32_t>(hb[c]), r1 = static_cast<uint32_t>(hb[c + 1]);
+    const uint64_t base = hb[nch + 1 + c];
+    const uint64_t T = hb[nch + 2 + c] - base;
+    if (T == 0 || r1 <= r0) continue;
+    swap_fold_set();
+    ensure_records(T);
     for (int attempt = 0;; ++attempt) {
       CU(cudaMemsetAsync(counters.p + 1, 0, sizeof(uint32_t), st));
       CU(cudaMemsetAsync(d_upd.p, 0, F * sizeof(unsigned long long), st));
       begin(ST_EMIT);
-      // single chunk: all rays in length order; multi-chunk: ray order
-      const uint32_t* perm = h_roff.empty() ? ray_perm.p : ray_iota.p;
-      k_emit<<<grid_for(r1 - r0, 128), 128, 0, st>>>(r0, r1, perm, rays.p, roff.p, base, d_poses.p, tp, view(), tv,
-                                                       rkeys.p, rvals.p, d_upd.p);
+      k_emit<<<grid_for(r1 - r0, 128), 128, 0, st>>>(r0, r1, ray_perm.p, rays.p, roff.p, base, d_poses.p, tp, view(),
+                                                       tv, rkeys.p, rvals.p, d_upd.p);
       ++launches;
       CU(cudaGetLastError());
       end(T, 1);
@@ -1017,8 +1114,8 @@ void vxg_handle::emit_and_apply(uint32_t R, uint32_t F, const TermView& tv) {
     k_add_u64<<<grid_for(F), 256, 0, st>>>(F, d_stats.p, d_upd.p);
     ++launches;
     CU(cudaGetLastError());
-    r0 = r1;
   }
+  join_folds();
 }
 
 // Stages the batch metadata and builds the rays (bundling + ray order).
@@ -1054,6 +1151,7 @@ void vxg_handle::begin_batch(const float* xyz, const uint8_t* rgb, const uint64_
 
 // Reads the per-frame stats back and feeds the updated-block consumers.
 void vxg_handle::end_batch(uint64_t F, vxg_stats* out) {
+  join_folds();
   begin(ST_D2H);
   std::vector<unsigned long long> s(3 * F);
   CU(cudaMemcpyAsync(s.data(), d_stats.p, 3 * F * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
@@ -1062,6 +1160,7 @@ void vxg_handle::end_batch(uint64_t F, vxg_stats* out) {
   end(0, 0);
   CU(cudaStreamSynchronize(st));
   collect();
+  drain_tops();
   if (out != nullptr) {
     for (uint64_t f = 0; f < F; ++f) {
       out[f].updates = s[f];
@@ -1182,10 +1281,7 @@ void vxg_handle::shard_back(const uint4* recv, uint64_t n, uint32_t F) {
   CU(cudaMemsetAsync(d_upd.p, 0, F * sizeof(unsigned long long), st));
   if (n > 0) {
     ensure_touched();
-    rkeys.ensure(n);
-    rkeys2.ensure(n);
-    rvals.ensure(n);
-    rvals2.ensure(n);
+    ensure_records(n);
     for (int attempt = 0;; ++attempt) {
       CU(cudaMemsetAsync(counters.p + 1, 0, sizeof(uint32_t), st));
       CU(cudaMemsetAsync(d_upd.p, 0, F * sizeof(unsigned long long), st));
@@ -1447,9 +1543,15 @@ int vxg_destroy(vxg_handle* h) {
     }
     if (h->fold_st) {
       cudaStreamSynchronize(h->fold_st);
+      cudaStreamSynchronize(h->fold_long_st);
       cudaStreamDestroy(h->fold_st);
+      cudaStreamDestroy(h->fold_long_st);
       cudaEventDestroy(h->fold_fork);
       cudaEventDestroy(h->fold_join);
+      cudaEventDestroy(h->fold_long_done);
+      cudaEventDestroy(h->fold_origins);
+      for (cudaEvent_t e : h->set_done) cudaEventDestroy(e);
+      cudaFreeHost(h->top_pinned);
     }
     if (h->nccl_comm) nccl()->CommDestroy(static_cast<ncclComm_t>(h->nccl_comm));
     if (h->own) cudaStreamDestroy(h->own);
