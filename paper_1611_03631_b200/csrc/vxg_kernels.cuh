@@ -1043,6 +1043,7 @@ __global__ void __launch_bounds__(64 * kP, 1) k_fold_runs(
   __shared__ uint32_t pair_run[kP];
   __shared__ float4 wscan[kP][8];
   __shared__ ChunkHdr ring_hdr[kP][kRingStages];  // the chunk's 32 weights, broadcast to the producer lanes
+  asm volatile("griddepcontrol.launch_dependents;");  // k_fold_short may start once every CTA is here
   if (map.counters[1] != 0u) return;  // emission failed (slab/hash full): host grows and replays
   if (threadIdx.x < kP * kRingStages) {
     mbar_init(&ring_full[threadIdx.x / kRingStages][threadIdx.x % kRingStages], 32);
@@ -1350,7 +1351,7 @@ __global__ void __launch_bounds__(64 * kP, 1) k_fold_runs(
 // stream next to k_fold_runs (disjoint voxels), with its own register budget
 // so more warps hide the ray-id -> ray gather latency.
 template <int kMinBlocks, int kC, bool kSmemOrg>
-__global__ void __launch_bounds__(256, kMinBlocks) k_fold_short(
+__device__ __forceinline__ void fold_short_body(
     const uint32_t* __restrict__ num_runs_p, const uint32_t* __restrict__ order,
     const uint32_t* __restrict__ sorted_len, const uint32_t* __restrict__ ukeys, const uint32_t* __restrict__ ustart,
     const uint32_t* __restrict__ ulen, const uint32_t* __restrict__ svals, const FoldRay* __restrict__ rays,
@@ -1388,20 +1389,26 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_fold_short(
       x.w = idx <= last ? x.w : 0.0f;
       return x;
     };
+    uint32_t idn[kC];  // ray ids one chunk ahead of the gathers: no id -> ray load chain in the loop
 #pragma unroll
     for (int u = 0; u < kC; ++u) rn[u] = rays[ids[min(static_cast<uint32_t>(u), last)]];
 #pragma unroll
     for (int u = 0; u < kC; ++u) xn[u] = weigh_at(u, rn[u]);
 #pragma unroll
     for (int u = 0; u < kC; ++u) rn[u] = rays[ids[min(static_cast<uint32_t>(kC + u), last)]];
+#pragma unroll
+    for (int u = 0; u < kC; ++u) idn[u] = ids[min(static_cast<uint32_t>(2 * kC + u), last)];
     for (uint32_t j = 0; j < c.len; j += kC) {
 #pragma unroll
       for (int u = 0; u < kC; ++u) xs[u] = xn[u];
-      // weigh chunk j+kC (gathered last iteration), gather chunk j+2kC
+      // weigh chunk j+kC (gathered last iteration), gather chunk j+2kC (ids
+      // loaded last iteration), load the ids of chunk j+3kC
 #pragma unroll
       for (int u = 0; u < kC; ++u) xn[u] = weigh_at(j + kC + u, rn[u]);
 #pragma unroll
-      for (int u = 0; u < kC; ++u) rn[u] = rays[ids[min(j + 2 * kC + u, last)]];
+      for (int u = 0; u < kC; ++u) rn[u] = rays[idn[u]];
+#pragma unroll
+      for (int u = 0; u < kC; ++u) idn[u] = ids[min(j + 3 * kC + u, last)];
       const VoxState s0 = st;
       bool ok = true;
 #pragma unroll
@@ -1416,6 +1423,22 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_fold_short(
     store_vox(vp, st);
     if (touched != nullptr) touched[c.key / static_cast<uint32_t>(map.nvox)] = 1u;
   }
+}
+
+// Short runs, launched behind k_fold_runs in the same stream as a programmatic
+// dependent (PDL): it starts once every long-run CTA is resident (each triggers
+// at entry), so the persistent short-run CTAs never delay the longest chains;
+// it completes only after k_fold_runs (griddepcontrol.wait on the way out).
+template <int kMinBlocks, int kC, bool kSmemOrg>
+__global__ void __launch_bounds__(256, kMinBlocks) k_fold_short(
+    const uint32_t* __restrict__ num_runs_p, const uint32_t* __restrict__ order,
+    const uint32_t* __restrict__ sorted_len, const uint32_t* __restrict__ ukeys, const uint32_t* __restrict__ ustart,
+    const uint32_t* __restrict__ ulen, const uint32_t* __restrict__ svals, const FoldRay* __restrict__ rays,
+    const float* __restrict__ g_org, uint32_t F, MapView map, TsdfParams tp, uint8_t* __restrict__ touched,
+    uint32_t* __restrict__ work) {
+  fold_short_body<kMinBlocks, kC, kSmemOrg>(num_runs_p, order, sorted_len, ukeys, ustart, ulen, svals, rays, g_org, F,
+                                            map, tp, touched, work);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // Self-tests of the fast fold arithmetic against the reference-order path.

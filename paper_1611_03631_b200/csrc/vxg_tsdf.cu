@@ -957,13 +957,10 @@ void vxg_handle::sort_fold(uint64_t T, uint64_t nslots, uint32_t F) {
     if (fold_inflight) CU(cudaStreamWaitEvent(fold_long_st, fold_join, 0));  // previous chunk folded
     // The long-run grid must be resident before the short-run grid (persistent
     // CTAs) fills the SMs, or the longest chain starts only after every short
-    // run is done (measured 3.7 vs 2.6 ms on cfg1). It directly follows
-    // k_origins in its stream; the short grid waits for k_origins via an event,
-    // which the front end resolves after the in-stream successor is launched.
+    // run is done (measured 3.7 vs 2.6 ms on cfg1): the short grid is its
+    // programmatic dependent in the same stream (see k_fold_short).
     k_origins<<<grid_for(3 * F), 256, 0, fold_long_st>>>(F, d_poses.p, d_org.p);
     ++launches;
-    CU(cudaEventRecord(fold_origins, fold_long_st));
-    CU(cudaStreamWaitEvent(fold_st, fold_origins, 0));
     static const int long_layout = [] {
       const char* e = getenv("VXG_LONG_LAYOUT");
       return e ? atoi(e) : 0;
@@ -992,30 +989,47 @@ void vxg_handle::sort_fold(uint64_t T, uint64_t nslots, uint32_t F) {
     else
       VXG_FOLD_LONG(4, false, 256);
 #undef VXG_FOLD_LONG
-    CU(cudaEventRecord(fold_long_done, fold_long_st));
     static const int short_blocks = [] {
       const char* e = getenv("VXG_FOLD_SHORT_BLOCKS");
       return e ? atoi(e) : 5;
     }();
     static const bool serial = getenv("VXG_FOLD_SERIAL") != nullptr;  // dev: long runs uncontended
-    if (serial) CU(cudaStreamWaitEvent(fold_st, fold_long_done, 0));
     const unsigned short_grid = static_cast<unsigned>(std::max<uint64_t>(
         1, std::min<uint64_t>(static_cast<uint64_t>(dev_sms) * 4, (nruns + 255) / 256)));
+    cudaLaunchAttribute pdl[1];
+    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl[0].val.programmaticStreamSerializationAllowed = serial ? 0 : 1;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(short_grid);
+    lc.blockDim = dim3(256);
+    lc.dynamicSmemBytes = 0;
+    lc.stream = fold_long_st;
+    lc.attrs = pdl;
+    lc.numAttrs = 1;
+    MapView mv = view();
+    const uint32_t* cnum = num_runs.p;
+    const uint32_t* cord = run_order.p;
+    const uint32_t* clen2 = run_len2.p;
+    const uint32_t* ckey = run_keys.p;
+    const uint32_t* cst = run_start.p;
+    const uint32_t* clen = run_len.p;
+    const uint32_t* csv = svals;
+    const FoldRay* crays = fold_rays.p;
+    const float* corg = d_org.p;
 #define VXG_FOLD_SHORT(MB, C)                                                                                 \
   do {                                                                                                        \
     auto kern = smem_org ? k_fold_short<MB, C, true> : k_fold_short<MB, C, false>;                           \
-    kern<<<short_grid, 256, 0, fold_st>>>(num_runs.p, run_order.p, run_len2.p, run_keys.p, run_start.p,       \
-                                          run_len.p, svals, fold_rays.p, d_org.p, F, view(), tp, tch, work.p); \
+    CU(cudaLaunchKernelEx(&lc, kern, cnum, cord, clen2, ckey, cst, clen, csv, crays, corg, F, mv, tp, tch,   \
+                          work.p));                                                                          \
   } while (0)
     if (short_blocks == 1)
       VXG_FOLD_SHORT(3, 4);
     else
       VXG_FOLD_SHORT(2, 4);
 #undef VXG_FOLD_SHORT
-    CU(cudaStreamWaitEvent(fold_st, fold_long_done, 0));
-    end(T, 2, fold_st);
-    CU(cudaEventRecord(fold_join, fold_st));
-    CU(cudaEventRecord(set_done[cur_set], fold_st));
+    end(T, 2, fold_long_st);
+    CU(cudaEventRecord(fold_join, fold_long_st));
+    CU(cudaEventRecord(set_done[cur_set], fold_long_st));
     set_busy[cur_set] = true;
     fold_inflight = true;
     launches += 2;
