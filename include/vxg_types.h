@@ -63,6 +63,32 @@ typedef struct vxg_mc_tables {
   int8_t tri_table[256][16];
 } vxg_mc_tables;
 
+/* vxf::FixedBandMode / DistanceMetric / QueueMode (esdf_integrator.h:12-26). */
+enum vxg_esdf_band { VXG_BAND_ONE_VOXEL = 0, VXG_BAND_HALF_TRUNCATION = 1 };
+enum vxg_esdf_metric { VXG_METRIC_QUASI_EUCLIDEAN = 0, VXG_METRIC_EUCLIDEAN = 1 };
+enum vxg_esdf_queue { VXG_QUEUE_FIFO = 0, VXG_QUEUE_PRIORITY_SINGLE = 1, VXG_QUEUE_PRIORITY_MULTI = 2 };
+
+/* vxf::EsdfConfig (esdf_integrator.h:28-41), same field meaning and defaults:
+ * d_max 4, one-voxel band, truncation 0.4, quasi-Euclidean, priority
+ * single-insert queue, bucket width 0 (= voxel size). */
+typedef struct vxg_esdf_config {
+  float d_max;
+  int32_t band_mode;    /* enum vxg_esdf_band */
+  float truncation;
+  int32_t metric;       /* enum vxg_esdf_metric */
+  int32_t queue_mode;   /* enum vxg_esdf_queue */
+  float bucket_width;
+} vxg_esdf_config;
+
+/* vxf::EsdfVoxel as laid out in HBM and in ESDF VXBLX payloads
+ * (serialization.cpp:116-122): f32 distance, u8 flags (1 observed, 2 fixed,
+ * 4 in raise, 8 in lower; voxel.h:24-27), 3x i8 parent. */
+typedef struct vxg_esdf_voxel {
+  float distance;
+  uint8_t flags;
+  int8_t parent[3];
+} vxg_esdf_voxel;
+
 /* Status codes (SURVEY.md §8b error convention). */
 enum vxg_status {
   VXG_OK = 0,

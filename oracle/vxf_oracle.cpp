@@ -177,12 +177,14 @@ struct vxo_layer {
   float voxel_size;
   int vps;
   std::unordered_map<Key3, std::vector<vxg_voxel>, BlockKeyHash> blocks;
+  std::vector<Key3> alloc_order;  // allocation sequence: rebuilds the reference's BlockMap iteration order
 
   // get_or_allocate_block (layer.h:79-87); default voxel all-zero (voxel.h:13-15).
   std::vector<vxg_voxel>& block(const Key3& b) {
     auto it = blocks.find(b);
     if (it == blocks.end()) {
       it = blocks.emplace(b, std::vector<vxg_voxel>(static_cast<size_t>(vps) * vps * vps, vxg_voxel{0.f, 0.f, 0, 0, 0, 0})).first;
+      alloc_order.push_back(b);
     }
     return it->second;
   }
@@ -797,4 +799,223 @@ extern "C" size_t vxo_mesh_extract(const vxo_layer* l, const vxg_mc_tables* t, i
     if (colors && with_colors && T) std::memcpy(colors, out.c.data(), 9 * T);
   }
   return order.size();
+}
+
+// ---------------------------------------------------------------- ESDF (occupancy-seeded baseline)
+// Restatement of EsdfIntegrator::build_from_occupancy (esdf_integrator.cpp:303-330)
+// with the reference's queue semantics, so parents (order-dependent under ties)
+// come out exactly as the reference's.
+namespace {
+
+constexpr uint8_t kEsdfObserved = 1, kEsdfFixed = 2, kEsdfInLower = 8;  // voxel.h:24-27
+
+struct EsdfVox {  // voxel.h:22-48 (parent kept as int16 like the reference)
+  float distance;
+  int16_t parent[3];
+  uint8_t flags;
+};
+
+struct EsdfWave {  // WavefrontQueue (esdf_integrator.cpp:20-52)
+  int mode;
+  float bucket_width;
+  std::vector<std::vector<Key3>> buckets;  // FIFO per bucket: vector + read head
+  std::vector<size_t> heads;
+  std::vector<Key3> fifo;
+  size_t fifo_head = 0;
+  size_t cursor = 0, size = 0;
+  EsdfWave(int m, float bw, float d_max) : mode(m), bucket_width(bw) {
+    if (mode != VXG_QUEUE_FIFO) {
+      const size_t n = static_cast<size_t>(std::ceil(d_max / bucket_width)) + 1;
+      buckets.resize(n);
+      heads.assign(n, 0);
+    }
+  }
+  void push(const Key3& g, float priority) {
+    if (mode == VXG_QUEUE_FIFO) {
+      fifo.push_back(g);
+    } else {
+      size_t b = static_cast<size_t>(std::fabs(priority) / bucket_width);
+      if (b >= buckets.size()) b = buckets.size() - 1;
+      buckets[b].push_back(g);
+      if (b < cursor) cursor = b;
+    }
+    ++size;
+  }
+  bool pop(Key3* g) {
+    if (size == 0) return false;
+    if (mode == VXG_QUEUE_FIFO) {
+      *g = fifo[fifo_head++];
+    } else {
+      while (heads[cursor] == buckets[cursor].size()) ++cursor;
+      *g = buckets[cursor][heads[cursor]++];
+    }
+    --size;
+    return true;
+  }
+};
+
+}  // namespace
+
+extern "C" size_t vxo_esdf_occupancy(const vxo_layer* l, const vxg_esdf_config* c, uint8_t* buf, size_t cap,
+                                     char* err, size_t err_len) {
+  auto fail = [&](const char* m) -> size_t {
+    if (err && err_len) {
+      std::strncpy(err, m, err_len - 1);
+      err[err_len - 1] = 0;
+    }
+    return 0;
+  };
+  const float v = l->voxel_size;
+  const int vps = l->vps;
+  // EsdfConfig::band_radius (esdf_integrator.h:36-38) + validate (:10-18)
+  const float gamma = c->band_mode == VXG_BAND_ONE_VOXEL ? v : 0.5f * c->truncation;
+  if (!(gamma > 0.0f) || !(gamma <= c->truncation)) return fail("esdf config requires 0 < band radius <= truncation");
+  if (!(c->d_max > gamma)) return fail("esdf config requires d_max > band radius");
+  // neighbours in the constructor's order (:69-79): dz, dy, dx in -1..1
+  struct Nb {
+    int dx, dy, dz;
+    float step;
+  };
+  std::vector<Nb> nbs;
+  for (int dz = -1; dz <= 1; ++dz)
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        if (dx == 0 && dy == 0 && dz == 0) continue;
+        nbs.push_back({dx, dy, dz, v * std::sqrt(static_cast<float>(dx * dx + dy * dy + dz * dz))});
+      }
+  const size_t nv = static_cast<size_t>(vps) * vps * vps;
+  std::unordered_map<Key3, std::vector<EsdfVox>, BlockKeyHash> esdf;
+  const EsdfVox def{c->d_max, {0, 0, 0}, 0};  // default voxel (:81-83)
+  auto vox = [&](const Key3& g) -> EsdfVox* {  // esdf_voxel (:86-97)
+    const Key3 b{floor_div(g[0], vps), floor_div(g[1], vps), floor_div(g[2], vps)};
+    auto it = esdf.find(b);
+    if (it == esdf.end()) return nullptr;
+    const int lx = g[0] - b[0] * vps, ly = g[1] - b[1] * vps, lz = g[2] - b[2] * vps;
+    return &it->second[static_cast<size_t>(lx + vps * (ly + vps * lz))];
+  };
+  const float bw = c->bucket_width > 0.0f ? c->bucket_width : v;
+  EsdfWave lower(c->queue_mode, bw, c->d_max);
+  auto push_lower = [&](const Key3& g, EsdfVox* e) {  // :99-105
+    if (c->queue_mode != VXG_QUEUE_PRIORITY_MULTI) {
+      if (e->flags & kEsdfInLower) return;
+      e->flags |= kEsdfInLower;
+    }
+    lower.push(g, std::fabs(e->distance));
+  };
+  // seeding (:310-326), in the reference TSDF layer's block iteration order:
+  // IndexMap = unordered_map with IndexHash (core.h:68-85) filled in allocation order
+  std::unordered_map<Key3, int, TeschnerHash> ref_order;
+  for (const Key3& b : l->alloc_order) ref_order.emplace(b, 0);
+  for (const auto& kv : ref_order) esdf.emplace(kv.first, std::vector<EsdfVox>(nv, def));
+  for (const auto& kr : ref_order) {
+    const auto& kv = *l->blocks.find(kr.first);
+    std::vector<EsdfVox>& eb = esdf.at(kv.first);
+    for (size_t lin = 0; lin < nv; ++lin) {
+      const vxg_voxel& tv = kv.second[lin];
+      if (!(tv.weight > 1e-4f)) continue;  // observed (core.h:32)
+      EsdfVox& ev = eb[lin];
+      ev.flags |= kEsdfObserved;
+      if (tv.distance < 0.0f) {
+        ev.distance = 0.0f;
+        ev.flags |= kEsdfFixed;
+        const int lx = static_cast<int>(lin % vps), ly = static_cast<int>((lin / vps) % vps),
+                  lz = static_cast<int>(lin / (static_cast<size_t>(vps) * vps));
+        push_lower(Key3{kv.first[0] * vps + lx, kv.first[1] * vps + ly, kv.first[2] * vps + lz}, &ev);
+      } else {
+        ev.distance = c->d_max;
+      }
+    }
+  }
+  // process_lower_queue (:220-230) + relax_neighbors (:232-294)
+  Key3 g;
+  while (lower.pop(&g)) {
+    EsdfVox* e = vox(g);
+    e->flags &= static_cast<uint8_t>(~kEsdfInLower);
+    if (!(e->flags & kEsdfObserved)) continue;
+    const EsdfVox cur = *e;
+    float seed_value = 0.0f;
+    const bool euclid = c->metric == VXG_METRIC_EUCLIDEAN;
+    if (euclid) {
+      const bool has_parent = cur.parent[0] != 0 || cur.parent[1] != 0 || cur.parent[2] != 0;
+      if (has_parent) {
+        const EsdfVox* seed = vox(Key3{g[0] + cur.parent[0], g[1] + cur.parent[1], g[2] + cur.parent[2]});
+        if (seed != nullptr && (seed->flags & kEsdfFixed)) {
+          seed_value = seed->distance;
+        } else {
+          const float len = v * std::sqrt(static_cast<float>(cur.parent[0] * cur.parent[0] +
+                                                             cur.parent[1] * cur.parent[1] +
+                                                             cur.parent[2] * cur.parent[2]));
+          seed_value = cur.distance > 0.0f ? cur.distance - len : cur.distance + len;
+        }
+      } else {
+        seed_value = cur.distance;
+      }
+    }
+    for (const Nb& n : nbs) {
+      const Key3 ng{g[0] + n.dx, g[1] + n.dy, g[2] + n.dz};
+      EsdfVox* nv_ = vox(ng);
+      if (nv_ == nullptr || !(nv_->flags & kEsdfObserved) || (nv_->flags & kEsdfFixed)) continue;
+      float cpos, cneg;
+      int16_t np[3];
+      if (!euclid) {
+        cpos = cur.distance + n.step;
+        cneg = cur.distance - n.step;
+        np[0] = static_cast<int16_t>(-n.dx);
+        np[1] = static_cast<int16_t>(-n.dy);
+        np[2] = static_cast<int16_t>(-n.dz);
+      } else {
+        np[0] = static_cast<int16_t>(cur.parent[0] - n.dx);
+        np[1] = static_cast<int16_t>(cur.parent[1] - n.dy);
+        np[2] = static_cast<int16_t>(cur.parent[2] - n.dz);
+        const float sd = v * std::sqrt(static_cast<float>(np[0] * np[0] + np[1] * np[1] + np[2] * np[2]));
+        cpos = seed_value + sd;
+        cneg = seed_value - sd;
+      }
+      if (nv_->distance > 0.0f && cpos < nv_->distance) {
+        nv_->distance = cpos;
+        std::memcpy(nv_->parent, np, sizeof(np));
+        push_lower(ng, nv_);
+      } else if (nv_->distance < 0.0f && cneg > nv_->distance) {
+        nv_->distance = cneg;
+        std::memcpy(nv_->parent, np, sizeof(np));
+        push_lower(ng, nv_);
+      }
+    }
+  }
+  // save_layer (serialization.cpp:141-168) with the ESDF payload (:116-122)
+  const size_t need = 6 + 4 + 8 + 4 + 1 + 8 + esdf.size() * (24 + nv * 8);
+  if (buf == nullptr || cap < need) return need;
+  uint8_t* o = buf;
+  auto put = [&](const void* src, size_t len) {
+    std::memcpy(o, src, len);
+    o += len;
+  };
+  const char magic[6] = {'V', 'X', 'B', 'L', 'X', '\0'};
+  const uint32_t version = 1;
+  const double vs = static_cast<double>(v);
+  const uint32_t vps32 = static_cast<uint32_t>(vps);
+  const uint8_t kind = 1;
+  const uint64_t count = esdf.size();
+  put(magic, 6);
+  put(&version, 4);
+  put(&vs, 8);
+  put(&vps32, 4);
+  put(&kind, 1);
+  put(&count, 8);
+  std::vector<Key3> order;
+  for (const auto& kv : esdf) order.push_back(kv.first);
+  std::sort(order.begin(), order.end());
+  for (const Key3& k : order) {
+    for (int i = 0; i < 3; ++i) {
+      const int64_t x = k[i];
+      put(&x, 8);
+    }
+    for (const EsdfVox& e : esdf.at(k)) {
+      put(&e.distance, 4);
+      uint8_t fp[4] = {e.flags, 0, 0, 0};
+      for (int i = 0; i < 3; ++i) fp[1 + i] = static_cast<uint8_t>(static_cast<int8_t>(std::clamp<int>(e.parent[i], -128, 127)));
+      put(fp, 4);
+    }
+  }
+  return need;
 }

@@ -103,6 +103,16 @@ size_t vxo_mesh_extract(const vxo_layer* l, const vxg_mc_tables* t, int with_col
                         size_t n_req, int32_t* bidx, uint64_t* frag_tri, float* verts, float* normals,
                         uint8_t* colors, size_t cap_frag, size_t cap_tri, uint64_t* n_tri);
 
+/* EsdfIntegrator::build_from_occupancy (esdf_integrator.cpp:303-330) over the
+ * oracle's TSDF layer, restated with the reference's wavefront queue
+ * (WavefrontQueue :20-52, push_lower :99-105, process_lower_queue :220-230,
+ * relax_neighbors :232-294, constructor :54-84, EsdfConfig::validate :10-18).
+ * Writes the ESDF VXBLX bytes (save_layer, serialization.cpp:116-122,141-168)
+ * into buf and returns the size needed (no write when cap is too small), or 0
+ * with err set when the config is invalid. */
+size_t vxo_esdf_occupancy(const vxo_layer* l, const vxg_esdf_config* c, uint8_t* buf, size_t cap, char* err,
+                          size_t err_len);
+
 #ifdef __cplusplus
 }
 #endif
