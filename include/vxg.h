@@ -163,6 +163,25 @@ int vxg_interpolate_distance(vxg_handle* h, const float* pts, uint64_t n, float*
  * reference's Accumulator. */
 int vxg_surface_error(vxg_handle* h, const float* pts, uint64_t n, float truncation, double* out);
 
+/* ---- ESDF on the device slab: vxf::EsdfIntegrator::build_from_occupancy
+ * (esdf_integrator.cpp:303-330), the occupancy-seeded baseline: every observed
+ * voxel with TSDF distance < 0 seeds at 0 (fixed), every other observed voxel
+ * starts at d_max and is lowered through observed 26-neighbours by the
+ * quasi-Euclidean steps v*sqrt(1|2|3) (relax_neighbors :258-292). One ESDF
+ * block per allocated TSDF block. Distances and flags are bit-exact with the
+ * reference for every queue mode (the quasi-Euclidean, only-lowering
+ * propagation has a unique fixed point); parents are the first minimising
+ * neighbour in the reference's neighbour order, which can differ from the
+ * reference's queue-order-dependent choice on ties. Errors: VXG_EINVAL with
+ * EsdfConfig::validate's text (:10-18), or for the Euclidean metric (its
+ * distances depend on the wavefront order; tools/esdf_order_probe). rounds
+ * (may be NULL) = relaxation launches until the fixed point. */
+int vxg_esdf_build_occupancy(vxg_handle* h, const vxg_esdf_config* config, uint64_t* rounds);
+/* save_layer(EsdfLayer) (serialization.cpp:141-168; payload f32 distance, u8
+ * flags, 3 x i8 parent, :116-122) of the last vxg_esdf_build_occupancy result;
+ * *need = byte size; writes only when cap >= *need. */
+int vxg_esdf_serialize_vxblx(vxg_handle* h, uint8_t* buf, uint64_t cap, uint64_t* need);
+
 /* Layer::voxel_ptr (layer.h:99-112) for n global voxel indices g[n*3]:
  * found[i] = 0 (block unallocated: absence, never a default voxel) or 1. */
 int vxg_query_voxels(vxg_handle* h, const int32_t* g, uint64_t n, vxg_voxel* out, uint8_t* found);

@@ -11,6 +11,7 @@
 #include <string>
 
 #include "vxf/analysis.h"
+#include "vxf/esdf_integrator.h"
 #include "vxf/interpolation.h"
 #include "vxf/layer.h"
 #include "vxf/marching_cubes_tables.h"
@@ -92,6 +93,30 @@ int vxr_integrate(void* hp, const float* xyz, const uint8_t* rgb, size_t n, cons
 }
 
 size_t vxr_block_count(void* hp) { return static_cast<RefHandle*>(hp)->layer.block_count(); }
+
+// vxf::EsdfIntegrator::build_from_occupancy (esdf_integrator.cpp:303-330) over
+// the handle's layer, saved with vxf::save_layer (ESDF payload) into a caller
+// buffer. Returns the byte size, or 0 with vxr_last_error() on an exception.
+size_t vxr_esdf_occupancy(void* hp, const vxg_esdf_config* c, uint8_t* buf, size_t cap) {
+  try {
+    vxf::EsdfConfig e;
+    e.d_max = c->d_max;
+    e.band_mode = static_cast<vxf::FixedBandMode>(c->band_mode);
+    e.truncation = c->truncation;
+    e.metric = static_cast<vxf::DistanceMetric>(c->metric);
+    e.queue_mode = static_cast<vxf::QueueMode>(c->queue_mode);
+    e.bucket_width = c->bucket_width;
+    const vxf::EsdfLayer esdf = vxf::EsdfIntegrator::build_from_occupancy(static_cast<RefHandle*>(hp)->layer, e);
+    std::ostringstream os(std::ios::binary);
+    vxf::save_layer(esdf, os);
+    const std::string s = os.str();
+    if (buf != nullptr && cap >= s.size()) std::memcpy(buf, s.data(), s.size());
+    return s.size();
+  } catch (const std::exception& ex) {
+    g_last_error = ex.what();
+    return 0;
+  }
+}
 
 // vxf::save_layer (serialization.cpp:141-168,216-218) into a caller buffer.
 size_t vxr_save_vxblx(void* hp, uint8_t* buf, size_t cap) {

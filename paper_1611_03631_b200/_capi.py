@@ -48,6 +48,11 @@ class VxgMcTables(ctypes.Structure):
                 ("edge_table", ctypes.c_uint16 * 256), ("tri_table", (ctypes.c_int8 * 16) * 256)]
 
 
+class VxgEsdfConfig(ctypes.Structure):
+    _fields_ = [("d_max", c_float), ("band_mode", c_int32), ("truncation", c_float), ("metric", c_int32),
+                ("queue_mode", c_int32), ("bucket_width", c_float)]
+
+
 # (name, restype, argtypes) for every symbol include/vxg.h declares.
 SIGNATURES = [
     ("vxg_last_error", c_char_p, []),
@@ -77,6 +82,8 @@ SIGNATURES = [
     ("vxg_interpolate_distance", c_int, [c_void_p, c_void_p, c_uint64, c_void_p, c_void_p, c_int]),
     ("vxg_surface_error", c_int, [c_void_p, c_void_p, c_uint64, c_float, c_void_p]),
     ("vxg_serialize_vxblx", c_int, [c_void_p, c_void_p, c_uint64, POINTER(c_uint64)]),
+    ("vxg_esdf_build_occupancy", c_int, [c_void_p, POINTER(VxgEsdfConfig), POINTER(c_uint64)]),
+    ("vxg_esdf_serialize_vxblx", c_int, [c_void_p, c_void_p, c_uint64, POINTER(c_uint64)]),
     ("vxg_save_vxblx", c_int, [c_void_p, c_char_p]),
     ("vxg_load_vxblx", c_int, [c_void_p, c_void_p, c_uint64]),
     ("vxg_reset", c_int, [c_void_p]),

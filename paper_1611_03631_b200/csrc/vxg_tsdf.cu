@@ -33,6 +33,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include "../../include/vxg.h"
+#include "vxg_esdf.cuh"
 #include "vxg_kernels.cuh"
 #include "vxg_sort.cuh"
 
@@ -190,6 +191,14 @@ struct vxg_handle {
   uint64_t hcap = 0;
   uint64_t n_blocks = 0;  // host mirror after each call
   std::vector<int32_t> host_idx;  // block index per slot (host mirror, grows with n_blocks)
+
+  // ---- ESDF (vxg_esdf_build_occupancy): one ESDF block per TSDF slot < esdf_blocks
+  DBuf<vxg_esdf_voxel> esdf;
+  DBuf<int32_t> esdf_nbr;
+  DBuf<uint8_t> esdf_act, esdf_act2;
+  DBuf<uint32_t> esdf_changed;
+  uint64_t esdf_blocks = 0;
+  bool esdf_ready = false;
 
   // ---- updated-block consumers (layer.h:124-148)
   std::map<std::string, std::set<uint32_t>> consumers;
@@ -2062,6 +2071,125 @@ int vxg_surface_error(vxg_handle* h, const float* pts, uint64_t n, float truncat
     out[2] = count ? max_abs : 0.0;
     out[3] = static_cast<double>(count);
     out[4] = n ? static_cast<double>(unknown) / static_cast<double>(n) : 0.0;
+  });
+}
+
+// EsdfConfig::band_radius + validate (esdf_integrator.h:36-40, .cpp:10-18).
+static std::string validate_esdf(const vxg_esdf_config* c, float voxel_size) {
+  const float gamma = c->band_mode == VXG_BAND_ONE_VOXEL ? voxel_size : 0.5f * c->truncation;
+  if (!(gamma > 0.0f) || !(gamma <= c->truncation)) return "esdf config requires 0 < band radius <= truncation";
+  if (!(c->d_max > gamma)) return "esdf config requires d_max > band radius";
+  return "";
+}
+
+int vxg_esdf_build_occupancy(vxg_handle* h, const vxg_esdf_config* config, uint64_t* rounds) {
+  return guarded([&] {
+    if (config == nullptr) throw VxgError(VXG_EINVAL, "null esdf config");
+    const std::string msg = validate_esdf(config, h->voxel_size);
+    if (!msg.empty()) throw VxgError(VXG_EINVAL, msg);
+    if (config->metric != VXG_METRIC_QUASI_EUCLIDEAN)
+      throw VxgError(VXG_EINVAL,
+                     "the device ESDF supports the quasi-Euclidean metric only (Euclidean results depend on the "
+                     "wavefront order)");
+    if (config->band_mode != VXG_BAND_ONE_VOXEL && config->band_mode != VXG_BAND_HALF_TRUNCATION)
+      throw VxgError(VXG_EINVAL, "esdf config has an unknown band mode");
+    set_device(h);
+    uint32_t c[2];
+    h->read_counters(c);
+    const uint64_t nb = std::min<uint64_t>(c[0], h->cap_blocks);
+    h->sync_block_mirror(nb);
+    h->esdf_ready = false;
+    h->esdf_blocks = nb;
+    uint64_t nr = 0;
+    if (nb > 0) {
+      const uint64_t nv = nb * static_cast<uint64_t>(h->nvox);
+      h->esdf.ensure(nv);
+      h->esdf_nbr.ensure(27 * nb);
+      h->esdf_act.ensure(nb);
+      h->esdf_act2.ensure(nb);
+      h->esdf_changed.ensure(1);
+      cudaStream_t st = h->st;
+      const MapView m = h->view();
+      k_esdf_neighbors<<<grid_for(27 * nb), 256, 0, st>>>(static_cast<uint32_t>(nb), h->block_idx.p, m,
+                                                          h->esdf_nbr.p);
+      k_esdf_init<<<grid_for(nv), 256, 0, st>>>(nv, h->slab.p, h->esdf.p, config->d_max);
+      h->launches += 2;
+      EsdfSteps steps;  // v * sqrt(|offset|^2) in fp32 (esdf_integrator.cpp:75)
+      steps.s[0] = 0.0f;
+      for (int k = 1; k <= 3; ++k) steps.s[k] = h->voxel_size * std::sqrt(static_cast<float>(k));
+      CU(cudaMemsetAsync(h->esdf_act.p, 1, nb, st));
+      const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(nb, 148ull * 8));
+      for (;;) {
+        CU(cudaMemsetAsync(h->esdf_act2.p, 0, nb, st));
+        CU(cudaMemsetAsync(h->esdf_changed.p, 0, sizeof(uint32_t), st));
+        k_esdf_relax<<<grid, 256, 0, st>>>(static_cast<uint32_t>(nb), h->esdf.p, h->esdf_nbr.p, h->vps, steps,
+                                           h->esdf_act.p, h->esdf_act2.p, h->esdf_changed.p);
+        ++h->launches;
+        ++nr;
+        uint32_t changed = 0;
+        CU(cudaMemcpyAsync(&changed, h->esdf_changed.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        h->esdf_act.swap(h->esdf_act2);
+        if (changed == 0) break;
+      }
+      k_esdf_parents<<<grid_for(nv), 256, 0, st>>>(static_cast<uint32_t>(nb), h->esdf.p, h->esdf_nbr.p, h->vps,
+                                                   steps, config->d_max);
+      ++h->launches;
+      CU(cudaGetLastError());
+      CU(cudaStreamSynchronize(st));
+    }
+    h->esdf_ready = true;
+    if (rounds) *rounds = nr;
+  });
+}
+
+// save_layer(EsdfLayer) (serialization.cpp:141-168, payload :116-122) of the
+// last vxg_esdf_build_occupancy result.
+int vxg_esdf_serialize_vxblx(vxg_handle* h, uint8_t* buf, uint64_t cap, uint64_t* need) {
+  return guarded([&] {
+    if (!h->esdf_ready) throw VxgError(VXG_EINVAL, "no ESDF layer: call vxg_esdf_build_occupancy first");
+    set_device(h);
+    const uint64_t nb = h->esdf_blocks;
+    std::vector<uint32_t> order(nb);
+    for (uint32_t i = 0; i < nb; ++i) order[i] = i;
+    const int32_t* idx = h->host_idx.data();
+    std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+      const int32_t* A = idx + 3 * a;
+      const int32_t* B = idx + 3 * b;
+      if (A[0] != B[0]) return A[0] < B[0];
+      if (A[1] != B[1]) return A[1] < B[1];
+      return A[2] < B[2];
+    });
+    const uint64_t total = 31 + nb * (24 + static_cast<uint64_t>(h->nvox) * 8);
+    if (need) *need = total;
+    if (buf == nullptr || cap < total) return;
+    uint8_t* o = buf;
+    auto put = [&](const void* src, size_t len) {
+      std::memcpy(o, src, len);
+      o += len;
+    };
+    const char magic[6] = {'V', 'X', 'B', 'L', 'X', '\0'};
+    const uint32_t version = 1;
+    const double vs = static_cast<double>(h->voxel_size);
+    const uint32_t vps = static_cast<uint32_t>(h->vps);
+    const uint8_t kind = 1;
+    put(magic, 6);
+    put(&version, 4);
+    put(&vs, 8);
+    put(&vps, 4);
+    put(&kind, 1);
+    put(&nb, 8);
+    const size_t bb = static_cast<size_t>(h->nvox) * sizeof(vxg_esdf_voxel);
+    std::vector<uint8_t> all(nb * bb);
+    if (nb) CU(cudaMemcpyAsync(all.data(), h->esdf.p, nb * bb, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaStreamSynchronize(h->st));
+    for (uint64_t k = 0; k < nb; ++k) {
+      for (int a = 0; a < 3; ++a) {
+        const int64_t v = h->host_idx[3 * order[k] + a];
+        put(&v, 8);
+      }
+      put(all.data() + static_cast<size_t>(order[k]) * bb, bb);  // payload layout == vxg_esdf_voxel
+    }
   });
 }
 

@@ -21,8 +21,8 @@ from typing import Dict, Optional, Sequence, Tuple
 
 import numpy as np
 
-from ._capi import (ParseError, VXG_INPUT_DEVICE, VXG_INPUT_HOST, VxgFrame, VxgMcTables, VxgStats, VxgTsdfConfig,
-                    VxgVoxel,
+from ._capi import (ParseError, VXG_INPUT_DEVICE, VXG_INPUT_HOST, VxgEsdfConfig, VxgFrame, VxgMcTables, VxgStats,
+                    VxgTsdfConfig, VxgVoxel,
                     check, lib)
 
 VOXEL_DTYPE = np.dtype([("distance", "<f4"), ("weight", "<f4"), ("r", "u1"), ("g", "u1"), ("b", "u1"),
@@ -374,6 +374,91 @@ class TsdfIntegrator:
             self._raycasts, self._skipped = int(out[-1, 1]), int(out[-1, 2])
         return out
 
+
+
+# ---------------------------------------------------------------- ESDF
+ESDF_VOXEL_DTYPE = np.dtype([("distance", "<f4"), ("flags", "u1"), ("parent", "i1", (3,))])  # serialization.cpp:116-122
+
+
+class FixedBandMode(enum.IntEnum):  # esdf_integrator.h:12-15
+    kOneVoxel = 0
+    kHalfTruncation = 1
+
+
+class DistanceMetric(enum.IntEnum):  # esdf_integrator.h:17-20
+    kQuasiEuclidean = 0
+    kEuclidean = 1
+
+
+class QueueMode(enum.IntEnum):  # esdf_integrator.h:22-26
+    kFifo = 0
+    kPrioritySingleInsert = 1
+    kPriorityMultiInsert = 2
+
+
+@dataclass
+class EsdfConfig:  # esdf_integrator.h:28-41 (same defaults)
+    d_max: float = 4.0
+    band_mode: FixedBandMode = FixedBandMode.kOneVoxel
+    truncation: float = 0.4
+    metric: DistanceMetric = DistanceMetric.kQuasiEuclidean
+    queue_mode: QueueMode = QueueMode.kPrioritySingleInsert
+    bucket_width: float = 0.0
+
+    def band_radius(self, voxel_size: float) -> float:
+        return float(np.float32(voxel_size) if self.band_mode == FixedBandMode.kOneVoxel
+                     else np.float32(0.5) * np.float32(self.truncation))
+
+    def to_c(self) -> VxgEsdfConfig:
+        return VxgEsdfConfig(self.d_max, int(self.band_mode), self.truncation, int(self.metric),
+                             int(self.queue_mode), self.bucket_width)
+
+
+class EsdfLayer:
+    """An ESDF layer produced on the device (vxf::EsdfLayer, layer.h:167): the
+    serialized VXBLX bytes (save_layer) plus a block view decoded from them."""
+
+    def __init__(self, data: bytes):
+        self._data = data
+        self.voxel_size = float(np.float32(np.frombuffer(data[10:18], dtype="<f8")[0]))
+        self.vps = int(np.frombuffer(data[18:22], dtype="<u4")[0])
+        self._count = int(np.frombuffer(data[23:31], dtype="<u8")[0])
+        self.rounds = 0
+
+    def voxels_per_side(self) -> int:
+        return self.vps
+
+    def block_count(self) -> int:
+        return self._count
+
+    def save_bytes(self) -> bytes:
+        return self._data
+
+    def blocks(self) -> Dict[Tuple[int, int, int], np.ndarray]:
+        nv = self.vps ** 3
+        rec = np.dtype([("idx", "<i8", (3,)), ("vox", ESDF_VOXEL_DTYPE, (nv,))])
+        arr = np.frombuffer(self._data, dtype=rec, count=self._count, offset=31)
+        return {tuple(int(x) for x in r["idx"]): r["vox"] for r in arr}
+
+
+class EsdfIntegrator:
+    """vxf::EsdfIntegrator's batch entry points that run on the device."""
+
+    @staticmethod
+    def build_from_occupancy(tsdf: "TsdfLayer", config: EsdfConfig) -> EsdfLayer:
+        """EsdfIntegrator::build_from_occupancy (esdf_integrator.cpp:303-330): every
+        observed voxel with negative TSDF distance seeds at 0; distances lower
+        outward (quasi-Euclidean). ValueError with the reference's validate()
+        text; ValueError for the Euclidean metric (order-dependent, not offered)."""
+        rounds = ctypes.c_uint64()
+        check(lib().vxg_esdf_build_occupancy(tsdf.handle, ctypes.byref(config.to_c()), ctypes.byref(rounds)))
+        need = ctypes.c_uint64()
+        check(lib().vxg_esdf_serialize_vxblx(tsdf.handle, None, 0, ctypes.byref(need)))
+        buf = np.zeros(need.value, dtype=np.uint8)
+        check(lib().vxg_esdf_serialize_vxblx(tsdf.handle, _ptr(buf), need.value, ctypes.byref(need)))
+        out = EsdfLayer(buf.tobytes())
+        out.rounds = int(rounds.value)
+        return out
 
 
 @dataclass

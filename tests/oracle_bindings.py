@@ -14,7 +14,7 @@ from ctypes import POINTER, c_char_p, c_float, c_int, c_int32, c_size_t, c_uint6
 
 import numpy as np
 
-from paper_1611_03631_b200._capi import VxgMcTables, VxgStats, VxgTsdfConfig, VxgVoxel
+from paper_1611_03631_b200._capi import VxgEsdfConfig, VxgMcTables, VxgStats, VxgTsdfConfig, VxgVoxel
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 ORACLE_SO = os.path.join(ROOT, "oracle", "liboracle.so")
@@ -61,6 +61,8 @@ def oracle_lib():
         L.vxo_mesh_extract.restype = c_size_t
         L.vxo_mesh_extract.argtypes = [c_void_p, POINTER(VxgMcTables), c_int, c_void_p, c_size_t] + [c_void_p] * 5 + \
             [c_size_t, c_size_t, POINTER(c_uint64)]
+        L.vxo_esdf_occupancy.restype = c_size_t
+        L.vxo_esdf_occupancy.argtypes = [c_void_p, POINTER(VxgEsdfConfig), c_void_p, c_size_t, c_char_p, c_size_t]
         L.vxo_bucket_schedule.restype = c_size_t
         L.vxo_bucket_schedule.argtypes = [c_size_t, c_size_t, c_void_p, c_size_t]
         _oracle = L
@@ -101,6 +103,8 @@ def ref_lib():
         L.vxr_load_ply.argtypes = [c_char_p, c_void_p, c_void_p, POINTER(c_uint64), POINTER(c_int)]
         L.vxr_load_tum.argtypes = [c_char_p, c_void_p, c_void_p, POINTER(c_uint64)]
         L.vxr_save_ply_mesh.argtypes = [c_char_p, c_void_p, c_void_p, c_void_p, c_uint64, c_void_p, c_uint64]
+        L.vxr_esdf_occupancy.restype = c_size_t
+        L.vxr_esdf_occupancy.argtypes = [c_void_p, POINTER(VxgEsdfConfig), c_void_p, c_size_t]
         L.vxr_mesh_extract.restype = c_size_t
         L.vxr_mesh_extract.argtypes = [c_void_p, c_int, c_void_p, c_size_t] + [c_void_p] * 5 + \
             [c_size_t, c_size_t, POINTER(c_uint64)]
@@ -145,6 +149,17 @@ class OracleLayer:
 
     def interpolate_distance(self, points):
         return _interp(self.L.vxo_interpolate, self.h, points)
+
+    def esdf_occupancy_bytes(self, esdf_config) -> bytes:
+        """build_from_occupancy (restated) -> ESDF VXBLX bytes; ValueError(text) if invalid."""
+        c = esdf_config.to_c() if hasattr(esdf_config, "to_c") else esdf_config
+        err = ctypes.create_string_buffer(256)
+        need = self.L.vxo_esdf_occupancy(self.h, ctypes.byref(c), None, 0, err, 256)
+        if need == 0:
+            raise ValueError(err.value.decode())
+        buf = np.zeros(need, dtype=np.uint8)
+        self.L.vxo_esdf_occupancy(self.h, ctypes.byref(c), _vp(buf), need, err, 256)
+        return buf.tobytes()
 
     def surface_error(self, points, truncation):
         return _surface_error(self.L.vxo_surface_error, self.h, points, truncation)
@@ -274,6 +289,16 @@ class RefLayer:
         if rc != 0:
             raise ValueError(self.L.vxr_last_error().decode())
         return int(st.updates), int(st.raycasts), int(st.skipped)
+
+    def esdf_occupancy_bytes(self, esdf_config) -> bytes:
+        """The reference's EsdfIntegrator::build_from_occupancy -> save_layer bytes."""
+        c = esdf_config.to_c() if hasattr(esdf_config, "to_c") else esdf_config
+        need = self.L.vxr_esdf_occupancy(self.h, ctypes.byref(c), None, 0)
+        if need == 0:
+            raise ValueError(self.L.vxr_last_error().decode())
+        buf = np.zeros(need, dtype=np.uint8)
+        self.L.vxr_esdf_occupancy(self.h, ctypes.byref(c), _vp(buf), need)
+        return buf.tobytes()
 
     def interpolate_distance(self, points):
         return _interp(self.L.vxr_interpolate, self.h, points)
