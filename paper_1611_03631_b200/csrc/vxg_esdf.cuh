@@ -65,6 +65,8 @@ __global__ void k_esdf_init(uint64_t n, const vxg_voxel* __restrict__ tsdf, vxg_
   }
 }
 
+constexpr int kEsdfThreads = 512;  // 8 voxels of a 16^3 block per thread: latency-bound sweeps want warps
+
 struct EsdfSteps {
   float s[4];  // v * sqrt(k) for k = |offset|^2 in 1..3 (constructor :75), s[0] unused
 };
@@ -92,7 +94,7 @@ __device__ __forceinline__ const vxg_esdf_voxel* esdf_neighbor(const vxg_esdf_vo
 // CTAs reading each other's blocks mid-update (possibly stale: L1 is not
 // coherent across SMs within a launch) converge to the same fixed point; the
 // barrier between sweeps makes the block's own updates visible.
-__global__ void __launch_bounds__(256) k_esdf_relax(uint32_t nb, vxg_esdf_voxel* __restrict__ esdf,
+__global__ void __launch_bounds__(kEsdfThreads) k_esdf_relax(uint32_t nb, vxg_esdf_voxel* __restrict__ esdf,
                                                     const int32_t* __restrict__ nbr, int vps, EsdfSteps steps,
                                                     const uint8_t* __restrict__ active_in,
                                                     uint8_t* __restrict__ active_out, uint32_t* __restrict__ changed) {
@@ -112,9 +114,9 @@ __global__ void __launch_bounds__(256) k_esdf_relax(uint32_t nb, vxg_esdf_voxel*
         if ((u.flags & (kEsdfObserved | kEsdfFixed)) != kEsdfObserved) continue;
         const int x = i % vps, y = (i / vps) % vps, z = i / (vps * vps);
         float best = u.distance;
-#pragma unroll 1
+#pragma unroll
         for (int dz = -1; dz <= 1; ++dz)
-#pragma unroll 1
+#pragma unroll
           for (int dy = -1; dy <= 1; ++dy)
 #pragma unroll
             for (int dx = -1; dx <= 1; ++dx) {

@@ -2122,7 +2122,7 @@ int vxg_esdf_build_occupancy(vxg_handle* h, const vxg_esdf_config* config, uint6
       for (;;) {
         CU(cudaMemsetAsync(h->esdf_act2.p, 0, nb, st));
         CU(cudaMemsetAsync(h->esdf_changed.p, 0, sizeof(uint32_t), st));
-        k_esdf_relax<<<grid, 256, 0, st>>>(static_cast<uint32_t>(nb), h->esdf.p, h->esdf_nbr.p, h->vps, steps,
+        k_esdf_relax<<<grid, kEsdfThreads, 0, st>>>(static_cast<uint32_t>(nb), h->esdf.p, h->esdf_nbr.p, h->vps, steps,
                                            h->esdf_act.p, h->esdf_act2.p, h->esdf_changed.p);
         ++h->launches;
         ++nr;
