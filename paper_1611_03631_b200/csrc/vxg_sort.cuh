@@ -80,11 +80,18 @@ __device__ __forceinline__ uint32_t digit_peers(uint32_t d) {
   return peers;
 }
 
-template <int kBits, int kIpt, int kMinBlocks, bool kPrefetch = false, bool kMatch = false>
+// kMarks (last pass only): instead of writing the sorted keys, mark each
+// voxel's run [dense_start, dense_end) of the final order. The pass input is
+// sorted by the other digits, so equal keys are contiguous inside a digit's
+// staged segment; a segment's first/last record may continue a run from the
+// previous / into the next sub-tile or CTA (atomicMin / atomicMax), a key
+// change inside a segment is the run's global start / end (plain store).
+template <int kBits, int kIpt, int kMinBlocks, bool kPrefetch = false, bool kMatch = false, bool kMarks = false>
 __global__ void __launch_bounds__(kSortThreads, kMinBlocks)
     k_sort_downsweep(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
                      uint32_t* __restrict__ vout, uint64_t n, int shift, uint32_t mask, uint32_t S,
-                     const uint32_t* __restrict__ offs) {
+                     const uint32_t* __restrict__ offs, uint32_t K = 0, uint32_t* __restrict__ dense_start = nullptr,
+                     uint32_t* __restrict__ dense_end = nullptr) {
   using C = SortCfg<kBits, kIpt>;
   extern __shared__ __align__(16) uint8_t sort_smem_raw[];
   typename C::Smem& sm = *reinterpret_cast<typename C::Smem*>(sort_smem_raw);
@@ -188,9 +195,21 @@ __global__ void __launch_bounds__(kSortThreads, kMinBlocks)
     __syncthreads();
     for (uint32_t i = tid; i < nv; i += kSortThreads) {
       const uint2 kv = sm.stage[i];
-      const uint32_t p = sm.gdelta[(kv.x >> shift) & mask] + i;
-      kout[p] = kv.x;
+      const uint32_t d = (kv.x >> shift) & mask;
+      const uint32_t p = sm.gdelta[d] + i;
+      if (!kMarks) kout[p] = kv.x;
       vout[p] = kv.y;
+      if (kMarks && kv.x < K) {
+        const uint32_t s0 = sm.tstart[d], s1 = s0 + sm.tcount[d];  // the digit's staged segment
+        if (i == s0)
+          atomicMin(&dense_start[kv.x], p);
+        else if (sm.stage[i - 1].x != kv.x)
+          dense_start[kv.x] = p;
+        if (i + 1 == s1)
+          atomicMax(&dense_end[kv.x], p + 1);
+        else if (sm.stage[i + 1].x != kv.x)
+          dense_end[kv.x] = p + 1;
+      }
     }
     __syncthreads();
     for (uint32_t d = tid; d < bins; d += kSortThreads) sm.gbase[d] += sm.tcount[d];

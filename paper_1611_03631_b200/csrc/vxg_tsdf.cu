@@ -518,10 +518,11 @@ struct vxg_handle {
   void emit_and_apply(uint32_t R, uint32_t F, const TermView& tv);
   uint64_t count_rays(uint32_t R, uint32_t F);
   void sort_fold(uint64_t T, uint64_t nslots, uint32_t F);
-  void sort_records(uint64_t T, int kbits, uint32_t** sk, uint32_t** sv);
+  void sort_records(uint64_t T, int kbits, uint32_t** sk, uint32_t** sv, uint32_t K);
   template <int kBits, int kIpt, int kMB>
   void lsd_sort(uint64_t T, int kbits, uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, uint32_t** sk,
-                uint32_t** sv, bool grouped);
+                uint32_t** sv, bool grouped, uint32_t K = 0);
+  bool marks_fused = false;  // the last sort pass wrote dense_start / dense_end (no sorted keys)
   int last_lsd_passes = 0;
   uint64_t last_blocks = 0;  // blocks allocated after the last produce attempt
   bool grew_after_attempt(int attempt);
@@ -804,13 +805,24 @@ uint64_t vxg_handle::count_rays(uint32_t R, uint32_t F) {
 // by a bit-permuted key (measured 3.57 vs 4.14 ms on cfg1).
 template <int kBits, int kIpt, int kMB>
 void vxg_handle::lsd_sort(uint64_t T, int kbits, uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
-                          uint32_t** sk, uint32_t** sv, bool grouped) {
+                          uint32_t** sk, uint32_t** sv, bool grouped, uint32_t K) {
   using C = SortCfg<kBits, kIpt>;
   static bool attr = false;
   if (!attr) {
     CU(cudaFuncSetAttribute(k_sort_downsweep<kBits, kIpt, kMB, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(sizeof(typename C::Smem))));
+    CU(cudaFuncSetAttribute(k_sort_downsweep<kBits, kIpt, kMB, true, true, true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(typename C::Smem))));
     attr = true;
+  }
+  // K > 0: the last pass marks the runs (dense_start / dense_end over K keys)
+  static const bool no_fuse = getenv("VXG_NO_FUSED_MARKS") != nullptr;  // dev A/B
+  marks_fused = K > 0 && !no_fuse;
+  if (marks_fused) {
+    dense_start.ensure(K);
+    dense_end.ensure(K);
+    CU(cudaMemsetAsync(dense_start.p, 0xFF, K * sizeof(uint32_t), st));
+    CU(cudaMemsetAsync(dense_end.p, 0, K * sizeof(uint32_t), st));
   }
   const int passes = std::max(1, (kbits + kBits - 1) / kBits);
   last_lsd_passes = passes;
@@ -833,8 +845,12 @@ void vxg_handle::lsd_sort(uint64_t T, int kbits, uint32_t* k0, uint32_t* v0, uin
     cub([&](void* t, size_t& b) {
       return cub::DeviceScan::ExclusiveSum(t, b, sort_counts.p, sort_offs.p, static_cast<int>(nc), st);
     }, 2);
-    k_sort_downsweep<kBits, kIpt, kMB, true, true><<<S, kSortThreads, sizeof(typename C::Smem), st>>>(
-        ki, vi, ko, vo, T, shift, mask, S, sort_offs.p);
+    if (marks_fused && q + 1 == passes)
+      k_sort_downsweep<kBits, kIpt, kMB, true, true, true><<<S, kSortThreads, sizeof(typename C::Smem), st>>>(
+          ki, vi, ko, vo, T, shift, mask, S, sort_offs.p, K, dense_start.p, dense_end.p);
+    else
+      k_sort_downsweep<kBits, kIpt, kMB, true, true><<<S, kSortThreads, sizeof(typename C::Smem), st>>>(
+          ki, vi, ko, vo, T, shift, mask, S, sort_offs.p);
     launches += 2;
     CU(cudaGetLastError());
     std::swap(ki, ko);
@@ -844,7 +860,7 @@ void vxg_handle::lsd_sort(uint64_t T, int kbits, uint32_t* k0, uint32_t* v0, uin
   *sv = vi;
 }
 
-void vxg_handle::sort_records(uint64_t T, int kbits, uint32_t** sk, uint32_t** sv) {
+void vxg_handle::sort_records(uint64_t T, int kbits, uint32_t** sk, uint32_t** sv, uint32_t K) {
   static const bool use_cub = [] {  // dev A/B: VXG_SORT=cub
     const char* e = getenv("VXG_SORT");
     return e && std::string(e) == "cub";
@@ -856,14 +872,15 @@ void vxg_handle::sort_records(uint64_t T, int kbits, uint32_t** sk, uint32_t** s
                                              st);
     }, 2 + (nb + 7) / 8);
     info_sort_passes = static_cast<uint64_t>((nb + 7) / 8);
+    marks_fused = false;
     *sk = rkeys2.p;
     *sv = rvals2.p;
     return;
   }
   if (kbits <= 21)
-    lsd_sort<7, 12, 4>(T, kbits, rkeys.p, rvals.p, rkeys2.p, rvals2.p, sk, sv, true);
+    lsd_sort<7, 12, 4>(T, kbits, rkeys.p, rvals.p, rkeys2.p, rvals2.p, sk, sv, true, K);
   else
-    lsd_sort<8, 12, 4>(T, kbits, rkeys.p, rvals.p, rkeys2.p, rvals2.p, sk, sv, true);
+    lsd_sort<8, 12, 4>(T, kbits, rkeys.p, rvals.p, rkeys2.p, rvals2.p, sk, sv, true, K);
   info_sort_passes = static_cast<uint64_t>(last_lsd_passes);
 }
 
@@ -888,15 +905,16 @@ void vxg_handle::sort_fold(uint64_t T, uint64_t nslots, uint32_t F) {
     }
   }
   uint32_t *skeys = nullptr, *svals = nullptr;
-  sort_records(T, kbits, &skeys, &svals);
+  sort_records(T, kbits, &skeys, &svals, static_cast<uint32_t>(K));
   end(T, 0);
   begin(ST_RUNS);
-  // mark each voxel's run [start, end) (dense by key)
-  dense_start.ensure(K);
-  dense_end.ensure(K);
-  CU(cudaMemsetAsync(dense_end.p, 0, K * sizeof(uint32_t), st));
-  k_run_marks<<<grid_for((T + 3) / 4), 256, 0, st>>>(T, skeys, dense_start.p, dense_end.p);
-  ++launches;
+  if (!marks_fused) {  // mark each voxel's run [start, end) (dense by key) from the sorted keys
+    dense_start.ensure(K);
+    dense_end.ensure(K);
+    CU(cudaMemsetAsync(dense_end.p, 0, K * sizeof(uint32_t), st));
+    k_run_marks<<<grid_for((T + 3) / 4), 256, 0, st>>>(T, skeys, dense_start.p, dense_end.p);
+    ++launches;
+  }
   // compact the runs in key order
   run_flag.ensure(K);
   run_pos.ensure(K);
