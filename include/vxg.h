@@ -195,8 +195,18 @@ int vxg_save_vxblx(vxg_handle* h, const char* path);
  * the stream's blocks; VXG_EPARSE with the reference's ParseError text. */
 int vxg_load_vxblx(vxg_handle* h, const uint8_t* buf, uint64_t len);
 
-/* Drops every block (fresh layer, same geometry and config). */
+/* Drops every block (fresh layer, same geometry and config). Deferred on the
+ * device: applied after the folds still in flight, before the next map access. */
 int vxg_reset(vxg_handle* h);
+
+/* A batch's ordered fold (the apply stage) may still be running on the device
+ * when vxg_integrate_* returns: its statistics do not depend on it, and the
+ * next batch's bundling overlaps it. Every entry point that reads or writes
+ * the map waits for it; vxg_flush orders the handle's stream (vxg_set_stream)
+ * after it without a host sync, so an event or copy queued afterwards sees the
+ * final map. (The reference's integrate() is synchronous,
+ * tsdf_integrator.cpp:111-127; results are identical.) */
+int vxg_flush(vxg_handle* h);
 
 /* Updated-block consumers (Layer::register_consumer / drain_updated,
  * layer.h:124-140): blocks allocated or updated since the consumer's last

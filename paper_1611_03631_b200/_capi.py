@@ -87,6 +87,7 @@ SIGNATURES = [
     ("vxg_save_vxblx", c_int, [c_void_p, c_char_p]),
     ("vxg_load_vxblx", c_int, [c_void_p, c_void_p, c_uint64]),
     ("vxg_reset", c_int, [c_void_p]),
+    ("vxg_flush", c_int, [c_void_p]),
     ("vxg_register_consumer", c_int, [c_void_p, c_char_p]),
     ("vxg_drain_updated", c_int, [c_void_p, c_char_p, c_void_p, c_uint64, POINTER(c_uint64)]),
     ("vxg_profile", c_int, [c_void_p, c_int]),

@@ -1025,41 +1025,46 @@ __global__ void k_run_marks(uint64_t T, const uint32_t* __restrict__ skeys, uint
   }
 }
 
-// kP producer/consumer pairs per CTA (64 kP threads). kSep: consumers only on
+// Shared state of kP long-run producer/consumer pairs.
+template <int kP>
+struct LongSmem {
+  PreRec ring[kP][kRingStages][32];
+  unsigned long long ring_full[kP][kRingStages];
+  unsigned long long ring_empty[kP][kRingStages];
+  uint32_t pair_run[kP];
+  float4 wscan[kP][8];  // the chunk's 32 weights, broadcast to the producer lanes
+  ChunkHdr ring_hdr[kP][kRingStages];
+};
+
+template <int kP>
+__device__ __forceinline__ void long_smem_init(LongSmem<kP>& S) {
+  if (threadIdx.x < kP * kRingStages) {
+    mbar_init(&S.ring_full[threadIdx.x / kRingStages][threadIdx.x % kRingStages], 32);
+    mbar_init(&S.ring_empty[threadIdx.x / kRingStages][threadIdx.x % kRingStages], 32);
+  }
+}
+
+// Long runs (>= kLongRun records), one producer/consumer warp pair per run,
+// handed out longest first through work[0]. wid: this warp's index among the
+// 2 kP pair warps (named barriers 1..kP). kSep: consumers only on
 // sub-partitions 0 and 1 (warp & 3 < 2), producers on 2 and 3, so no consumer
 // shares its scheduler with a producer.
-template <int kP, bool kSep, bool kSmemOrg>
-__global__ void __launch_bounds__(64 * kP, 1) k_fold_runs(
-    const uint32_t* __restrict__ num_runs_p, const uint32_t* __restrict__ order,
-    const uint32_t* __restrict__ sorted_len, const uint32_t* __restrict__ ukeys, const uint32_t* __restrict__ ustart,
+template <int kP, bool kSep>
+__device__ __forceinline__ void fold_long_pairs(
+    LongSmem<kP>& S, const int wid, const float* poses, const uint32_t nruns, const uint32_t n_long,
+    const uint32_t* __restrict__ order, const uint32_t* __restrict__ ukeys, const uint32_t* __restrict__ ustart,
     const uint32_t* __restrict__ ulen, const uint32_t* __restrict__ svals, const FoldRay* __restrict__ rays,
-    const float* __restrict__ g_org, uint32_t F, MapView map, TsdfParams tp, uint8_t* __restrict__ touched,
-    uint32_t* __restrict__ work, unsigned long long* __restrict__ dbg) {
-  __shared__ PreRec ring[kP][kRingStages][32];
-  __shared__ float s_org[3 * kOrgCache];
-  const float* poses = stage_origins<kSmemOrg>(s_org, g_org, F);
-  __shared__ unsigned long long ring_full[kP][kRingStages];
-  __shared__ unsigned long long ring_empty[kP][kRingStages];
-  __shared__ uint32_t pair_run[kP];
-  __shared__ float4 wscan[kP][8];
-  __shared__ ChunkHdr ring_hdr[kP][kRingStages];  // the chunk's 32 weights, broadcast to the producer lanes
-  asm volatile("griddepcontrol.launch_dependents;");  // k_fold_short may start once every CTA is here
-  if (map.counters[1] != 0u) return;  // emission failed (slab/hash full): host grows and replays
-  if (threadIdx.x < kP * kRingStages) {
-    mbar_init(&ring_full[threadIdx.x / kRingStages][threadIdx.x % kRingStages], 32);
-    mbar_init(&ring_empty[threadIdx.x / kRingStages][threadIdx.x % kRingStages], 32);
-  }
-  __syncthreads();
-  const uint32_t nruns = *num_runs_p;
+    const MapView& map, const TsdfParams& tp, uint8_t* __restrict__ touched, uint32_t* __restrict__ work,
+    unsigned long long* __restrict__ dbg) {
+  auto& ring = S.ring;
+  auto& ring_full = S.ring_full;
+  auto& ring_empty = S.ring_empty;
+  auto& pair_run = S.pair_run;
+  auto& wscan = S.wscan;
+  auto& ring_hdr = S.ring_hdr;
   const uint32_t n_all = nruns;
   const int lane = threadIdx.x & 31;
-  const int wid = threadIdx.x >> 5;
-  uint32_t n_long = 0;
-  if (lane == 0) n_long = count_long_runs(sorted_len, nruns);
-  n_long = __shfl_sync(0xffffffffu, n_long, 0);
   const float Wmax = tp.max_weight;
-
-  // ---- phase 1: long runs, one producer/consumer warp pair per run
   {
     // default (kP = 4): consumers are warps 4..7 (highest ids: the warp
     // arbiter favours them); pair p = consumer 4+p (sub-partition p) +
@@ -1347,24 +1352,42 @@ __global__ void __launch_bounds__(64 * kP, 1) k_fold_runs(
   }
 }
 
-// Short runs (< kLongRun records): one thread per run, launched on a second
-// stream next to k_fold_runs (disjoint voxels), with its own register budget
-// so more warps hide the ray-id -> ray gather latency.
-template <int kMinBlocks, int kC, bool kSmemOrg>
-__device__ __forceinline__ void fold_short_body(
+// Long runs alone: kP pairs per CTA (64 kP threads), one CTA per SM; the
+// short-run grid (k_fold_short) is its programmatic dependent.
+template <int kP, bool kSep, bool kSmemOrg>
+__global__ void __launch_bounds__(64 * kP, 1) k_fold_runs(
     const uint32_t* __restrict__ num_runs_p, const uint32_t* __restrict__ order,
     const uint32_t* __restrict__ sorted_len, const uint32_t* __restrict__ ukeys, const uint32_t* __restrict__ ustart,
     const uint32_t* __restrict__ ulen, const uint32_t* __restrict__ svals, const FoldRay* __restrict__ rays,
     const float* __restrict__ g_org, uint32_t F, MapView map, TsdfParams tp, uint8_t* __restrict__ touched,
-    uint32_t* __restrict__ work) {
+    uint32_t* __restrict__ work, unsigned long long* __restrict__ dbg) {
+  __shared__ LongSmem<kP> S;
   __shared__ float s_org[3 * kOrgCache];
   const float* poses = stage_origins<kSmemOrg>(s_org, g_org, F);
-  if (map.counters[1] != 0u) return;
+  asm volatile("griddepcontrol.launch_dependents;");  // k_fold_short may start once every CTA is here
+  // (no check of map.counters here: the host launches a fold only after its
+  // records' emission succeeded, and a later batch's emission may already be
+  // setting flags while this fold waits for its turn)
+  long_smem_init(S);
+  __syncthreads();
   const uint32_t nruns = *num_runs_p;
-  const int lane = threadIdx.x & 31;
   uint32_t n_long = 0;
-  if (lane == 0) n_long = count_long_runs(sorted_len, nruns);
+  if ((threadIdx.x & 31) == 0) n_long = count_long_runs(sorted_len, nruns);
   n_long = __shfl_sync(0xffffffffu, n_long, 0);
+  fold_long_pairs<kP, kSep>(S, static_cast<int>(threadIdx.x >> 5), poses, nruns, n_long, order, ukeys, ustart, ulen,
+                            svals, rays, map, tp, touched, work, dbg);
+}
+
+// Short runs (< kLongRun records): one thread per run, launched on a second
+// stream next to k_fold_runs (disjoint voxels), with its own register budget
+// so more warps hide the ray-id -> ray gather latency.
+template <int kC>
+__device__ __forceinline__ void fold_short_loop(
+    const float* poses, const uint32_t nruns, const uint32_t n_long, const uint32_t* __restrict__ order,
+    const uint32_t* __restrict__ ukeys, const uint32_t* __restrict__ ustart, const uint32_t* __restrict__ ulen,
+    const uint32_t* __restrict__ svals, const FoldRay* __restrict__ rays, const MapView& map, const TsdfParams& tp,
+    uint8_t* __restrict__ touched, uint32_t* __restrict__ work) {
+  const int lane = threadIdx.x & 31;
   while (true) {
     uint32_t base = 0;
     if (lane == 0) base = atomicAdd(&work[1], 32u);
@@ -1436,9 +1459,44 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_fold_short(
     const uint32_t* __restrict__ ulen, const uint32_t* __restrict__ svals, const FoldRay* __restrict__ rays,
     const float* __restrict__ g_org, uint32_t F, MapView map, TsdfParams tp, uint8_t* __restrict__ touched,
     uint32_t* __restrict__ work) {
-  fold_short_body<kMinBlocks, kC, kSmemOrg>(num_runs_p, order, sorted_len, ukeys, ustart, ulen, svals, rays, g_org, F,
-                                            map, tp, touched, work);
+  __shared__ float s_org[3 * kOrgCache];
+  const float* poses = stage_origins<kSmemOrg>(s_org, g_org, F);
+  {
+    const uint32_t nruns = *num_runs_p;
+    uint32_t n_long = 0;
+    if ((threadIdx.x & 31) == 0) n_long = count_long_runs(sorted_len, nruns);
+    n_long = __shfl_sync(0xffffffffu, n_long, 0);
+    fold_short_loop<kC>(poses, nruns, n_long, order, ukeys, ustart, ulen, svals, rays, map, tp, touched, work);
+  }
   asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+// Long and short runs in ONE persistent grid, one 512-thread CTA per SM: warps
+// 8..15 are the four long-run producer/consumer pairs (consumers = warps
+// 12..15, one per sub-partition, the highest warp ids so the arbiter favours
+// the serial chains), warps 0..7 fold short runs from the start; every pair
+// warp joins the short runs once the long runs are handed out.
+template <bool kSmemOrg>
+__global__ void __launch_bounds__(512, 1) k_fold_all(
+    const uint32_t* __restrict__ num_runs_p, const uint32_t* __restrict__ order,
+    const uint32_t* __restrict__ sorted_len, const uint32_t* __restrict__ ukeys, const uint32_t* __restrict__ ustart,
+    const uint32_t* __restrict__ ulen, const uint32_t* __restrict__ svals, const FoldRay* __restrict__ rays,
+    const float* __restrict__ g_org, uint32_t F, MapView map, TsdfParams tp, uint8_t* __restrict__ touched,
+    uint32_t* __restrict__ work, unsigned long long* __restrict__ dbg) {
+  __shared__ LongSmem<4> S;
+  __shared__ float s_org[3 * kOrgCache];
+  const float* poses = stage_origins<kSmemOrg>(s_org, g_org, F);
+  long_smem_init(S);
+  __syncthreads();
+  const uint32_t nruns = *num_runs_p;
+  uint32_t n_long = 0;
+  if ((threadIdx.x & 31) == 0) n_long = count_long_runs(sorted_len, nruns);
+  n_long = __shfl_sync(0xffffffffu, n_long, 0);
+  const int wid = static_cast<int>(threadIdx.x >> 5);
+  if (wid >= 8)
+    fold_long_pairs<4, false>(S, wid - 8, poses, nruns, n_long, order, ukeys, ustart, ulen, svals, rays, map, tp,
+                              touched, work, dbg);
+  fold_short_loop<4>(poses, nruns, n_long, order, ukeys, ustart, ulen, svals, rays, map, tp, touched, work);
 }
 
 // Self-tests of the fast fold arithmetic against the reference-order path.

@@ -155,6 +155,14 @@ struct vxg_handle {
   bool set_busy[2] = {false, false};
   int cur_set = 0;
   bool fold_inflight = false;  // a fold was launched that st has not joined yet
+  // ---- across calls: a batch's fold may still run when vxg_integrate_* returns
+  // (its stats do not depend on it); the next batch's bundling and ray order
+  // overlap it, and every entry point that reads or writes the map, or ends a
+  // timed region, joins it first (settle / vxg_flush). vxg_reset is deferred
+  // the same way: applied (after the fold) just before the next batch's first
+  // map access, or by settle().
+  bool async_fold = true;
+  bool pending_reset = false;
   uint32_t* top_pinned = nullptr;  // longest run per chunk (read back at the batch end)
   uint32_t n_top = 0;
   static constexpr uint32_t kTopCap = 256;
@@ -225,6 +233,7 @@ struct vxg_handle {
   DBuf<uint32_t> run_keys, run_len, run_start, run_len2, run_order, run_iota, work;
   struct FoldSet {  // the other buffer set of the chunk pipeline (swapped with the members above)
     DBuf<uint32_t> rkeys, rkeys2, rvals, rvals2, run_keys, run_len, run_start, run_len2, run_order, num_runs, work;
+    DBuf<float> d_org;
   } alt;
   DBuf<unsigned long long> ckeys;       // emission order keys: (chunk, ray length)
   DBuf<unsigned long long> chunk_base;  // per chunk: first ray, first record
@@ -303,15 +312,23 @@ struct vxg_handle {
     stage_launch[cur_stage] += n_launch;
     cur_stage = -1;
   }
-  void collect() {  // after a stream sync
+  void collect() {  // after a stream sync; stages still running (a fold that outlives the call) stay queued
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> keep;
     for (auto& pe : pending) {
+      const cudaError_t q = cudaEventQuery(pe.second.second);
+      if (q == cudaErrorNotReady) {
+        (void)cudaGetLastError();
+        keep.push_back(pe);
+        continue;
+      }
+      CU(q);
       float ms = 0.f;
       CU(cudaEventElapsedTime(&ms, pe.second.first, pe.second.second));
       stage_ms[pe.first] += ms;
       event_pool.push_back(pe.second.first);
       event_pool.push_back(pe.second.second);
     }
-    pending.clear();
+    pending.swap(keep);
   }
 
   // CUB device algorithm; n_kernels = kernels it launches (for the launch count).
@@ -455,6 +472,7 @@ struct vxg_handle {
     run_order.swap(alt.run_order);
     num_runs.swap(alt.num_runs);
     work.swap(alt.work);
+    d_org.swap(alt.d_org);
     cur_set ^= 1;
     if (set_busy[cur_set]) CU(cudaStreamWaitEvent(st, set_done[cur_set], 0));
   }
@@ -478,6 +496,33 @@ struct vxg_handle {
     CU(cudaStreamWaitEvent(st, fold_join, 0));
     fold_inflight = false;
   }
+  // A deferred vxg_reset: clear the slab's used blocks, the hash and the
+  // counters once every fold that writes them is done.
+  void apply_pending_reset() {
+    if (!pending_reset) return;
+    join_folds();
+    uint32_t c[2];
+    read_counters(c);
+    const uint64_t used = std::min<uint64_t>(std::max<uint64_t>(std::max<uint64_t>(c[0], reset_used), last_blocks),
+                                             cap_blocks);
+    CU(cudaMemsetAsync(slab.p, 0, used * nvox * sizeof(vxg_voxel), st));
+    CU(cudaMemsetAsync(hkeys.p, 0xFF, hcap * sizeof(unsigned long long), st));
+    CU(cudaMemsetAsync(hvals.p, 0xFF, hcap * sizeof(int32_t), st));
+    CU(cudaMemsetAsync(counters.p, 0, 2 * sizeof(uint32_t), st));
+    last_blocks = 0;
+    reset_used = 0;
+    pending_reset = false;
+  }
+  // Before any entry point that reads or writes the map: st ordered after
+  // every launched fold, deferred reset applied.
+  void settle() {
+    apply_pending_reset();
+    join_folds();
+  }
+  // Folds may outlive the call only on a plain single-GPU handle without
+  // updated-block consumers (the fold marks the touched blocks they drain).
+  bool fold_may_outlive_call() const { return async_fold && consumers.empty() && shard_world <= 1 && !debug_fold; }
+  uint64_t reset_used = 0;  // blocks in use when vxg_reset was called (deferred)
   // After a host sync of st that followed join_folds(): longest runs of the batch.
   void drain_tops() {
     for (uint32_t i = 0; i < n_top; ++i) info_max_run = std::max<uint64_t>(info_max_run, top_pinned[i]);
@@ -779,6 +824,7 @@ uint64_t vxg_handle::count_rays(uint32_t R, uint32_t F) {
   begin(ST_RAYS);
   rcount.ensure(R);
   roff.ensure(R);
+  join_folds();  // the previous batch's fold reads fold_rays
   fold_rays.ensure(R);
   k_ray_count<<<grid_for(R), 256, 0, st>>>(R, rays.p, d_poses.p, tp, rcount.p, d_stats.p + F, fold_rays.p);
   ++launches;
@@ -978,16 +1024,17 @@ void vxg_handle::sort_fold(uint64_t T, uint64_t nslots, uint32_t F) {
     fold_dbg_n = nruns;
   }
   if (nruns) {
+    // origins of this set on st (d_poses is rewritten by the next batch
+    // while this fold may still wait for the previous one)
     d_org.ensure(3 * std::max<uint32_t>(F, 1));
+    k_origins<<<grid_for(3 * F), 256, 0, st>>>(F, d_poses.p, d_org.p);
+    ++launches;
     CU(cudaEventRecord(fold_fork, st));
-    CU(cudaStreamWaitEvent(fold_long_st, fold_fork, 0));
-    if (fold_inflight) CU(cudaStreamWaitEvent(fold_long_st, fold_join, 0));  // previous chunk folded
+    CU(cudaStreamWaitEvent(fold_long_st, fold_fork, 0));  // after the previous chunk's fold: same stream
     // The long-run grid must be resident before the short-run grid (persistent
     // CTAs) fills the SMs, or the longest chain starts only after every short
     // run is done (measured 3.7 vs 2.6 ms on cfg1): the short grid is its
     // programmatic dependent in the same stream (see k_fold_short).
-    k_origins<<<grid_for(3 * F), 256, 0, fold_long_st>>>(F, d_poses.p, d_org.p);
-    ++launches;
     static const int long_layout = [] {
       const char* e = getenv("VXG_LONG_LAYOUT");
       return e ? atoi(e) : 0;
@@ -1002,7 +1049,29 @@ void vxg_handle::sort_fold(uint64_t T, uint64_t nslots, uint32_t F) {
     }();
     const unsigned lg = long_ctas > 0 ? static_cast<unsigned>(long_ctas) : long_grid;
     const bool smem_org = F <= kOrgCache;
+    static const int fold_merged = [] {  // dev A/B: VXG_FOLD_MERGED=0 -> two grids (long + PDL short)
+      const char* e = getenv("VXG_FOLD_MERGED");
+      return e ? atoi(e) : 1;
+    }();
     begin(ST_APPLY, fold_long_st);
+    if (fold_merged) {
+      auto kern = smem_org ? k_fold_all<true> : k_fold_all<false>;
+      kern<<<static_cast<unsigned>(dev_sms), 512, 0, fold_long_st>>>(num_runs.p, run_order.p, run_len2.p, run_keys.p,
+                                                                     run_start.p, run_len.p, svals, fold_rays.p,
+                                                                     d_org.p, F, view(), tp, tch, work.p, dbg);
+      CU(cudaGetLastError());
+      end(T, 2, fold_long_st);
+      CU(cudaEventRecord(fold_join, fold_long_st));
+      CU(cudaEventRecord(set_done[cur_set], fold_long_st));
+      set_busy[cur_set] = true;
+      fold_inflight = true;
+      launches += 1;
+      info_records += T;
+      info_runs += nruns;
+      static const bool no_pipe_m = getenv("VXG_NO_PIPELINE") != nullptr;
+      if (no_pipe_m) join_folds();
+      return;
+    }
 #define VXG_FOLD_LONG(P, SEP, THREADS)                                                                              \
   do {                                                                                                           \
     auto kern = smem_org ? k_fold_runs<P, SEP, true> : k_fold_runs<P, SEP, false>;                              \
@@ -1106,6 +1175,7 @@ uint32_t pipeline_chunks(uint64_t total) {
 
 void vxg_handle::emit_and_apply(uint32_t R, uint32_t F, const TermView& tv) {
   const TsdfParams tp = params();
+  apply_pending_reset();
   const uint64_t total = count_rays(R, F);
   const uint32_t nch = pipeline_chunks(total);
   // chunk bounds (first ray, first record) by record count, on the device
@@ -1156,7 +1226,7 @@ void vxg_handle::emit_and_apply(uint32_t R, uint32_t F, const TermView& tv) {
     ++launches;
     CU(cudaGetLastError());
   }
-  join_folds();
+  if (!fold_may_outlive_call()) join_folds();
 }
 
 // Stages the batch metadata and builds the rays (bundling + ray order).
@@ -1192,7 +1262,7 @@ void vxg_handle::begin_batch(const float* xyz, const uint8_t* rgb, const uint64_
 
 // Reads the per-frame stats back and feeds the updated-block consumers.
 void vxg_handle::end_batch(uint64_t F, vxg_stats* out) {
-  join_folds();
+  if (!fold_may_outlive_call()) join_folds();
   begin(ST_D2H);
   std::vector<unsigned long long> s(3 * F);
   CU(cudaMemcpyAsync(s.data(), d_stats.p, 3 * F * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
@@ -1231,6 +1301,7 @@ void vxg_handle::run_sub(const float* xyz, const uint8_t* rgb, const uint64_t* o
   begin_batch(xyz, rgb, offsets, poses, F, &R, &tv);
   if (shard_world > 1) {
     if (nccl_comm == nullptr) throw VxgError(VXG_EINVAL, "sharded handle without a communicator (vxg_shard_init)");
+    settle();
     shard_front(R, static_cast<uint32_t>(F), tv);
     if (!shard_replicated) nccl_exchange();
     shard_back(owned_records(), owned_count(), static_cast<uint32_t>(F));
@@ -1553,6 +1624,7 @@ int vxg_create(const vxg_tsdf_config* config, float voxel_size, int vps, int dev
       CU(cudaSetDevice(device));
       CU(cudaStreamCreateWithFlags(&h->own, cudaStreamNonBlocking));
       h->st = h->own;
+      h->async_fold = getenv("VXG_SYNC_FOLD") == nullptr;  // dev A/B: every call joins its fold
       h->alloc_map(block_capacity ? block_capacity : 4096);
     } catch (...) {
       delete h;
@@ -1566,6 +1638,7 @@ int vxg_destroy(vxg_handle* h) {
   if (h == nullptr) return VXG_OK;
   return guarded([&] {
     cudaSetDevice(h->device);
+    h->sync_folds();
     if (h->st != nullptr && h->st == h->own) cudaStreamSynchronize(h->st);
     if (h->own) cudaStreamSynchronize(h->own);
     for (auto& pe : h->pending) {
@@ -1606,6 +1679,17 @@ int vxg_get_config(const vxg_handle* h, vxg_tsdf_config* out) {
   return VXG_OK;
 }
 
+// Orders the handle's stream after every fold launched so far (a batch's fold
+// may outlive vxg_integrate_*), and applies a deferred reset. No host sync:
+// work queued on the stream afterwards (an event, a copy) sees the final map.
+int vxg_flush(vxg_handle* h) {
+  return guarded([&] {
+    if (h == nullptr) throw VxgError(VXG_EINVAL, "null argument");
+    set_device(h);
+    h->settle();
+  });
+}
+
 int vxg_set_config(vxg_handle* h, const vxg_tsdf_config* config) {
   return guarded([&] {
     const std::string msg = validate_config(config);
@@ -1617,6 +1701,7 @@ int vxg_set_config(vxg_handle* h, const vxg_tsdf_config* config) {
 int vxg_set_stream(vxg_handle* h, void* stream) {
   return guarded([&] {
     set_device(h);
+    h->settle();
     CU(cudaStreamSynchronize(h->st));
     h->st = stream != nullptr ? static_cast<cudaStream_t>(stream) : h->own;
   });
@@ -1852,6 +1937,7 @@ int vxg_integrate(vxg_handle* h, const float* xyz, const uint8_t* rgb, uint64_t 
 int vxg_block_count(vxg_handle* h, uint64_t* out) {
   return guarded([&] {
     set_device(h);
+    h->settle();
     uint32_t c[2];
     h->read_counters(c);
     *out = std::min<uint64_t>(c[0], h->cap_blocks);
@@ -1861,6 +1947,7 @@ int vxg_block_count(vxg_handle* h, uint64_t* out) {
 int vxg_export_blocks(vxg_handle* h, int32_t* idx, vxg_voxel* voxels, uint64_t cap, uint64_t* n_out) {
   return guarded([&] {
     set_device(h);
+    h->settle();
     std::vector<uint32_t> order;
     export_sorted(h, &order);
     const uint64_t n = std::min<uint64_t>(cap, order.size());
@@ -1884,6 +1971,7 @@ int vxg_export_blocks(vxg_handle* h, int32_t* idx, vxg_voxel* voxels, uint64_t c
 int vxg_import_blocks(vxg_handle* h, const int32_t* idx, const vxg_voxel* voxels, uint64_t n) {
   return guarded([&] {
     set_device(h);
+    h->settle();
     if (n == 0) return;
     DBuf<int32_t> didx, slots;
     DBuf<vxg_voxel> dv;
@@ -1918,6 +2006,7 @@ int vxg_import_blocks(vxg_handle* h, const int32_t* idx, const vxg_voxel* voxels
 int vxg_query_voxels(vxg_handle* h, const int32_t* g, uint64_t n, vxg_voxel* out, uint8_t* found) {
   return guarded([&] {
     set_device(h);
+    h->settle();
     if (n == 0) return;
     DBuf<int32_t> dg;
     DBuf<vxg_voxel> dout;
@@ -1937,6 +2026,7 @@ int vxg_query_voxels(vxg_handle* h, const int32_t* g, uint64_t n, vxg_voxel* out
 int vxg_interpolate_distance(vxg_handle* h, const float* pts, uint64_t n, float* d, uint8_t* found, int flags) {
   return guarded([&] {
     set_device(h);
+    h->settle();
     if (n == 0) return;
     if (pts == nullptr || d == nullptr || found == nullptr) throw VxgError(VXG_EINVAL, "null argument");
     if (flags & VXG_INPUT_DEVICE) {
@@ -1968,6 +2058,7 @@ int vxg_mesh_extract(vxg_handle* h, const vxg_mc_tables* tables, const int32_t* 
       throw VxgError(VXG_EINVAL, "null argument");
     if (blocks == nullptr && n_req > 0) throw VxgError(VXG_EINVAL, "null block list");
     set_device(h);
+    h->settle();
     h->mesh_ready = false;
     std::vector<uint32_t> order;
     export_sorted(h, &order);  // every allocated block, sorted by (x, y, z)
@@ -2047,6 +2138,7 @@ int vxg_mesh_fetch(vxg_handle* h, int32_t* block_idx, uint64_t* frag_tri, float*
     if (h == nullptr) throw VxgError(VXG_EINVAL, "null argument");
     if (!h->mesh_ready) throw VxgError(VXG_EINVAL, "no extracted mesh (call vxg_mesh_extract first)");
     set_device(h);
+    h->settle();
     const uint64_t B = h->mesh_bidx.size() / 3, T = h->mesh_T;
     if (block_idx) std::memcpy(block_idx, h->mesh_bidx.data(), 3 * B * sizeof(int32_t));
     if (frag_tri) std::memcpy(frag_tri, h->mesh_frag.data(), (B + 1) * sizeof(uint64_t));
@@ -2112,6 +2204,7 @@ int vxg_esdf_build_occupancy(vxg_handle* h, const vxg_esdf_config* config, uint6
     if (config->band_mode != VXG_BAND_ONE_VOXEL && config->band_mode != VXG_BAND_HALF_TRUNCATION)
       throw VxgError(VXG_EINVAL, "esdf config has an unknown band mode");
     set_device(h);
+    h->settle();
     uint32_t c[2];
     h->read_counters(c);
     const uint64_t nb = std::min<uint64_t>(c[0], h->cap_blocks);
@@ -2167,6 +2260,7 @@ int vxg_esdf_serialize_vxblx(vxg_handle* h, uint8_t* buf, uint64_t cap, uint64_t
   return guarded([&] {
     if (!h->esdf_ready) throw VxgError(VXG_EINVAL, "no ESDF layer: call vxg_esdf_build_occupancy first");
     set_device(h);
+    h->settle();
     const uint64_t nb = h->esdf_blocks;
     std::vector<uint32_t> order(nb);
     for (uint32_t i = 0; i < nb; ++i) order[i] = i;
@@ -2214,6 +2308,7 @@ int vxg_esdf_serialize_vxblx(vxg_handle* h, uint8_t* buf, uint64_t cap, uint64_t
 int vxg_serialize_vxblx(vxg_handle* h, uint8_t* buf, uint64_t cap, uint64_t* need) {
   return guarded([&] {
     set_device(h);
+    h->settle();
     std::vector<uint32_t> order;
     export_sorted(h, &order);
     const uint64_t nb = order.size();
@@ -2272,18 +2367,15 @@ int vxg_save_vxblx(vxg_handle* h, const char* path) {
   return VXG_OK;
 }
 
+// Deferred: the slab, hash and counters are cleared once the folds still in
+// flight are done, before the next batch's first map access (or by any entry
+// point that reads the map). The host mirror is empty from here on.
 int vxg_reset(vxg_handle* h) {
   return guarded([&] {
     set_device(h);
-    const uint64_t used = std::min<uint64_t>(h->n_blocks, h->cap_blocks);
-    uint32_t c[2];
-    h->read_counters(c);
-    const uint64_t used2 = std::min<uint64_t>(std::max<uint64_t>(c[0], used), h->cap_blocks);
-    CU(cudaMemsetAsync(h->slab.p, 0, used2 * h->nvox * sizeof(vxg_voxel), h->st));
-    CU(cudaMemsetAsync(h->hkeys.p, 0xFF, h->hcap * sizeof(unsigned long long), h->st));
-    CU(cudaMemsetAsync(h->hvals.p, 0xFF, h->hcap * sizeof(int32_t), h->st));
-    CU(cudaMemsetAsync(h->counters.p, 0, 2 * sizeof(uint32_t), h->st));
-    CU(cudaStreamSynchronize(h->st));
+    h->reset_used = std::max<uint64_t>(h->reset_used, std::min<uint64_t>(h->n_blocks, h->cap_blocks));
+    h->pending_reset = true;
+    if (!h->async_fold) h->settle();
     h->n_blocks = 0;
     h->host_idx.clear();
     for (auto& kv : h->consumers) kv.second.clear();
@@ -2340,6 +2432,7 @@ int vxg_load_vxblx(vxg_handle* h, const uint8_t* buf, uint64_t len) {
       }
     }
     set_device(h);
+    h->settle();
     h->voxel_size = static_cast<float>(vs);
     if (static_cast<int>(vps) != h->vps) {
       h->vps = static_cast<int>(vps);
@@ -2358,6 +2451,7 @@ int vxg_register_consumer(vxg_handle* h, const char* name) {
   return guarded([&] {
     if (name == nullptr) throw VxgError(VXG_EINVAL, "null consumer name");
     set_device(h);
+    h->settle();
     h->consumers[name];
     h->ensure_touched();
   });
@@ -2389,6 +2483,14 @@ int vxg_stage_count(void) { return kStages; }
 const char* vxg_stage_name(int s) { return (s >= 0 && s < kStages) ? kStageNames[s] : ""; }
 
 int vxg_stage_times(vxg_handle* h, double* ms, uint64_t* launches, uint64_t* units, int reset) {
+  if (h == nullptr) return VXG_EINVAL;
+  const int rc = guarded([&] {  // every stage of the calls so far, including a fold still running
+    set_device(h);
+    h->join_folds();
+    CU(cudaStreamSynchronize(h->st));
+    h->collect();
+  });
+  if (rc != VXG_OK) return rc;
   for (int s = 0; s < kStages; ++s) {
     if (ms) ms[s] = h->stage_ms[s];
     if (launches) launches[s] = h->stage_launch[s];
@@ -2453,6 +2555,7 @@ extern "C" int vxg_debug_fold(vxg_handle* h, int enable, unsigned long long* out
 extern "C" int vxg_debug_top_runs(vxg_handle* h, uint32_t* len, uint32_t* keys, uint32_t n) {
   return guarded([&] {
     set_device(h);
+    h->settle();
     std::vector<uint32_t> ord(n);
     CU(cudaMemcpy(len, h->run_len2.p, n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
     CU(cudaMemcpy(ord.data(), h->run_order.p, n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
@@ -2490,6 +2593,7 @@ int vxg_shard_init(vxg_handle* h, int rank, int world, const uint8_t* id_bytes) 
   return guarded([&] {
     if (world < 1 || rank < 0 || rank >= world) throw VxgError(VXG_EINVAL, "invalid shard rank / world");
     set_device(h);
+    h->settle();
     if (world > 1) {
       ncclUniqueId id;
       std::memcpy(id.internal, id_bytes, NCCL_UNIQUE_ID_BYTES);

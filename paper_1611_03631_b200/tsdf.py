@@ -227,6 +227,11 @@ class TsdfLayer:
     def reset(self) -> None:
         check(lib().vxg_reset(self._h))
 
+    def flush(self) -> None:
+        """Order the handle's stream after the last batch's fold (no host sync):
+        an event recorded afterwards covers the whole integration."""
+        check(lib().vxg_flush(self._h))
+
     # ---- updated-block consumers (layer.h:124-148)
     def register_consumer(self, name: str) -> None:
         check(lib().vxg_register_consumer(self._h, name.encode()))
