@@ -324,7 +324,7 @@ def main():
     roof_sort = roof("record_sort", "k_sort_upsweep + k_sort_downsweep (x passes)", 20.0 * n_rec * passes,
                      f"LSD radix sort of 8-byte (voxel key, ray id) records, {passes} passes x (4 B upsweep read "
                      f"+ 8 B read + 8 B write) per record")
-    roof_apply = roof("apply", "k_fold_runs + k_fold_short", 16.0 * n_upd + 24.0 * n_vox,
+    roof_apply = roof("apply", "k_fold_all (long-run producer/consumer pairs + short runs, one grid)", 16.0 * n_upd + 24.0 * n_vox,
                       "16 B/update + 24 B/distinct voxel (SURVEY.md 8d); bound in practice by the longest "
                       "per-voxel chain (work.longest_fold_chain sequential steps)")
     roofline = roof_sort if stages["record_sort"][0] >= stages["apply"][0] else roof_apply

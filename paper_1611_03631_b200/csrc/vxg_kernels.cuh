@@ -483,63 +483,91 @@ __device__ __forceinline__ void walk_axis_init(float st, float en, float v, int*
   *span += static_cast<uint32_t>(dd < 0 ? -dd : dd);
 }
 
-__global__ void __launch_bounds__(128) k_emit(uint32_t R0, uint32_t R1, const uint32_t* __restrict__ perm,
+// kAnti: MergeMode::kGroupedAntiGraze probe; kPow2: vps = 2^lg (block/local
+// split by shift and mask, the floor division of core.h:34-40 for a power of
+// two), else the incremental carry of the stepped axis.
+// A warp walks its 32 rays in lockstep (step k of every lane, inactive past a
+// ray's end); each lane stages its keys in a shared-memory row of 32, and every
+// 32 steps the warp writes row after row as 128-byte runs (a ray's records are
+// contiguous at offset[ray]): coalesced stores instead of 32 scattered ones.
+constexpr int kEmitThreads = 128;
+template <bool kAnti, bool kPow2>
+__global__ void __launch_bounds__(kEmitThreads) k_emit(uint32_t R0, uint32_t R1, const uint32_t* __restrict__ perm,
                        const RayInfo* __restrict__ rays, const unsigned long long* __restrict__ roff, uint64_t base,
                        const float* __restrict__ poses, TsdfParams tp, MapView map, TermView tv,
                        uint32_t* __restrict__ rkeys, uint32_t* __restrict__ rvals,
                        unsigned long long* __restrict__ updates) {
+  constexpr int kWarps = kEmitThreads / 32;
   __shared__ unsigned long long bcache[kBlockCacheSize];
+  __shared__ uint32_t kstage[kWarps][32 * 33];  // one padded row per lane: conflict-free both ways
+  __shared__ uint4 kmeta[kWarps][32];           // per lane: (count, first record, ray id)
   for (int i = threadIdx.x; i < kBlockCacheSize; i += blockDim.x) bcache[i] = ~0ull;
   __syncthreads();
+  const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
+  uint32_t* row = &kstage[wib][lane * 33];
+  const uint32_t* wrows = kstage[wib];
+  const uint4* wmeta = kmeta[wib];
   const int vps = map.vps;
+  const int lg = kPow2 ? __ffs(vps) - 1 : 0;
   const float v = tp.voxel_size;
-  const bool anti = tp.merge_mode == VXG_MERGE_GROUPED_ANTI_GRAZE;
-  for (uint32_t t = R0 + blockIdx.x * blockDim.x + threadIdx.x; t < R1; t += gridDim.x * blockDim.x) {
-    const uint32_t j = perm[t];
-    const RayInfo r = rays[j];
+  const uint32_t wstride = gridDim.x * kWarps * 32u;
+  for (uint32_t t0 = R0 + (blockIdx.x * kWarps + wib) * 32u; t0 < R1; t0 += wstride) {
+    const uint32_t t = t0 + lane;
+    const bool has = t < R1;
+    const uint32_t j = has ? perm[t] : 0u;
+    RayInfo r;
+    if (has) {
+      r = rays[j];
+    } else {
+      r = RayInfo{};
+      r.valid = 0u;
+      r.frame = 0u;
+    }
     const float* Pm = poses + 12 * r.frame;
     const float o0 = Pm[3], o1 = Pm[7], o2 = Pm[11];
     const float depth = r.depth;
-    uint32_t valid = 0;
-    if (r.valid == 1u && !(depth <= 0.0f)) {
-      const float ray0 = fsub(r.p[0], o0), ray1 = fsub(r.p[1], o1), ray2 = fsub(r.p[2], o2);
+    uint32_t valid = 0, count = 0, out0 = 0;
+    const bool live = has && r.valid == 1u && !(depth <= 0.0f);
+    float ray0 = 0.0f, ray1 = 0.0f, ray2 = 0.0f, w_front = 0.0f;
+    Walk wk{};
+    if (live) {
+      ray0 = fsub(r.p[0], o0), ray1 = fsub(r.p[1], o1), ray2 = fsub(r.p[2], o2);
       const float s = fdiv(tp.truncation, depth);
       // mweight_base for any d >= 0 (d > -eps in the drop-off mode), times the ray weight
-      const float w_front = fmul(mweight_base(tp.weight_mode, r.base, 0.0f, tp.truncation, tp.dropoff_epsilon), r.weight);
-      Walk wk;
+      w_front = fmul(mweight_base(tp.weight_mode, r.base, 0.0f, tp.truncation, tp.dropoff_epsilon), r.weight);
       uint32_t span = 0;
       walk_axis_init(o0, fadd(r.p[0], fmul(ray0, s)), v, &wk.c0, &wk.e0, &wk.s0, &wk.m0, &wk.d0, &span);
       walk_axis_init(o1, fadd(r.p[1], fmul(ray1, s)), v, &wk.c1, &wk.e1, &wk.s1, &wk.m1, &wk.d1, &span);
       walk_axis_init(o2, fadd(r.p[2], fmul(ray2, s)), v, &wk.c2, &wk.e2, &wk.s2, &wk.m2, &wk.d2, &span);
-      const uint32_t count = span + 1u;
-      const uint64_t out0 = roff[j] - base;
-      int og0 = 0, og1 = 0, og2 = 0;
-      if (anti) {
-        og0 = gidx(o0, v);
-        og1 = gidx(o1, v);
-        og2 = gidx(o2, v);
-      }
-      float x0 = vcenter(wk.c0, v), x1 = vcenter(wk.c1, v), x2 = vcenter(wk.c2, v);
-      int b0 = floor_div(wk.c0, vps), b1 = floor_div(wk.c1, vps), b2 = floor_div(wk.c2, vps);
-      int l0 = wk.c0 - b0 * vps, l1 = wk.c1 - b1 * vps, l2 = wk.c2 - b2 * vps;
-      int cb0 = 0x7fffffff, cb1 = 0, cb2 = 0;
-      int32_t cslot = -1;
-      const uint64_t al_lo = (out0 + 3ull) & ~3ull, al_hi = (out0 + count) & ~3ull;
-      uint32_t q0 = 0, q1 = 0, q2 = 0, q3 = 0;
-      // the ray index is every record's sort value: vector fill
-      for (uint64_t o = out0; o < out0 + count;) {
-        if ((o & 3ull) == 0 && o + 4 <= out0 + count) {
-          *reinterpret_cast<uint4*>(rvals + o) = make_uint4(j, j, j, j);
-          o += 4;
-        } else {
-          rvals[o] = j;
-          ++o;
-        }
-      }
-      for (uint32_t k = 0; k < count; ++k) {
+      count = span + 1u;
+      // record offsets inside one chunk are 32-bit (chunks stay below 2^29 records)
+      out0 = static_cast<uint32_t>(roff[j] - base);
+    }
+    kmeta[wib][lane] = make_uint4(count, out0, j, 0u);
+    int og0 = 0, og1 = 0, og2 = 0;
+    if (kAnti) {
+      og0 = gidx(o0, v);
+      og1 = gidx(o1, v);
+      og2 = gidx(o2, v);
+    }
+    float x0 = vcenter(wk.c0, v), x1 = vcenter(wk.c1, v), x2 = vcenter(wk.c2, v);
+    int b0, b1, b2, l0, l1, l2;
+    if (kPow2) {
+      b0 = wk.c0 >> lg, b1 = wk.c1 >> lg, b2 = wk.c2 >> lg;
+      l0 = wk.c0 & (vps - 1), l1 = wk.c1 & (vps - 1), l2 = wk.c2 & (vps - 1);
+    } else {
+      b0 = floor_div(wk.c0, vps), b1 = floor_div(wk.c1, vps), b2 = floor_div(wk.c2, vps);
+      l0 = wk.c0 - b0 * vps, l1 = wk.c1 - b1 * vps, l2 = wk.c2 - b2 * vps;
+    }
+    int cb0 = 0x7fffffff, cb1 = 0, cb2 = 0;
+    int32_t cslot = -1;
+    const uint32_t maxc = __reduce_max_sync(0xffffffffu, count);
+    __syncwarp();  // kmeta visible to the warp
+    for (uint32_t k = 0; k < maxc; ++k) {
+      if (k < count) {
         uint32_t key = kInvalidRecord;
         bool skip = false;
-        if (anti) {
+        if (kAnti) {
           const int g[3] = {wk.c0, wk.c1, wk.c2};
           const int og[3] = {og0, og1, og2};
           skip = !(wk.c0 == r.term[0] && wk.c1 == r.term[1] && wk.c2 == r.term[2]) && is_terminal(tv, r.frame, og, g);
@@ -548,11 +576,11 @@ __global__ void __launch_bounds__(128) k_emit(uint32_t R0, uint32_t R1, const ui
           // projective_distance(x, p, s) (tsdf_integrator.cpp:22-27); p - s == ray.
           // In front of the point (along >= 0) d = +|t| >= 0, where every weight
           // mode gives the ray's constant w_front: the norm is needed only behind it.
-          const float t0 = fsub(r.p[0], x0), t1 = fsub(r.p[1], x1), t2 = fsub(r.p[2], x2);
-          const float along = dot3(t0, t1, t2, ray0, ray1, ray2);
+          const float t0f = fsub(r.p[0], x0), t1f = fsub(r.p[1], x1), t2f = fsub(r.p[2], x2);
+          const float along = dot3(t0f, t1f, t2f, ray0, ray1, ray2);
           float w = w_front;
           if (!(along >= 0.0f)) {
-            const float magnitude = norm3(t0, t1, t2);
+            const float magnitude = norm3(t0f, t1f, t2f);
             const float d = along < 0.0f ? -magnitude : magnitude;
             w = fmul(mweight_base(tp.weight_mode, r.base, d, tp.truncation, tp.dropoff_epsilon), r.weight);
           }
@@ -569,48 +597,61 @@ __global__ void __launch_bounds__(128) k_emit(uint32_t R0, uint32_t R1, const ui
               }
             }
             if (cslot >= 0) {
-              key = static_cast<uint32_t>(cslot) * static_cast<uint32_t>(map.nvox) +
-                    static_cast<uint32_t>(l0 + vps * (l1 + vps * l2));
+              const uint32_t lin = kPow2 ? static_cast<uint32_t>(l0 | (l1 << lg) | (l2 << (2 * lg)))
+                                         : static_cast<uint32_t>(l0 + vps * (l1 + vps * l2));
+              key = static_cast<uint32_t>(cslot) * static_cast<uint32_t>(map.nvox) + lin;
             }
             ++valid;
           }
         }
-        // 16-byte vector stores on the 4-aligned interior of the ray's range
-        const uint64_t o_idx = out0 + k;
-        if (o_idx < al_lo || o_idx >= al_hi) {
-          rkeys[o_idx] = key;
+        row[k & 31u] = key;
+        // RayCaster::next tail (the walk stops after count voxels, which is
+        // where the reference's end-voxel test stops it): axis = argmin t_max,
+        // ties to the lowest axis. Straight-line selects: the lanes of a warp
+        // step different axes.
+        const bool a1 = wk.m1 < wk.m0;
+        const float mlo = a1 ? wk.m1 : wk.m0;
+        const bool a2 = wk.m2 < mlo;
+        const bool st2 = a2, st1 = !a2 & a1, st0 = !a2 & !a1;
+        wk.c0 += st0 ? wk.s0 : 0;
+        wk.c1 += st1 ? wk.s1 : 0;
+        wk.c2 += st2 ? wk.s2 : 0;
+        wk.m0 = st0 ? fadd(wk.m0, wk.d0) : wk.m0;
+        wk.m1 = st1 ? fadd(wk.m1, wk.d1) : wk.m1;
+        wk.m2 = st2 ? fadd(wk.m2, wk.d2) : wk.m2;
+        x0 = vcenter(wk.c0, v);
+        x1 = vcenter(wk.c1, v);
+        x2 = vcenter(wk.c2, v);
+        if (kPow2) {
+          b0 = wk.c0 >> lg, b1 = wk.c1 >> lg, b2 = wk.c2 >> lg;
+          l0 = wk.c0 & (vps - 1), l1 = wk.c1 & (vps - 1), l2 = wk.c2 & (vps - 1);
         } else {
-          q0 = q1;
-          q1 = q2;
-          q2 = q3;
-          q3 = key;
-          if ((o_idx & 3ull) == 3ull) *reinterpret_cast<uint4*>(rkeys + (o_idx - 3)) = make_uint4(q0, q1, q2, q3);
+          l0 += st0 ? wk.s0 : 0;
+          l1 += st1 ? wk.s1 : 0;
+          l2 += st2 ? wk.s2 : 0;
+          b0 += (l0 == vps) - (l0 < 0);
+          b1 += (l1 == vps) - (l1 < 0);
+          b2 += (l2 == vps) - (l2 < 0);
+          l0 = l0 == vps ? 0 : (l0 < 0 ? vps - 1 : l0);
+          l1 = l1 == vps ? 0 : (l1 < 0 ? vps - 1 : l1);
+          l2 = l2 == vps ? 0 : (l2 < 0 ? vps - 1 : l2);
         }
-        if (k + 1 < count && !(wk.c0 == wk.e0 && wk.c1 == wk.e1 && wk.c2 == wk.e2)) {
-          // RayCaster::next tail: axis = argmin t_max, ties to the lowest axis
-          const bool a1 = wk.m1 < wk.m0;
-          const float mlo = a1 ? wk.m1 : wk.m0;
-          const bool a2 = wk.m2 < mlo;
-          if (a2) {
-            wk.c2 += wk.s2;
-            wk.m2 = fadd(wk.m2, wk.d2);
-            x2 = vcenter(wk.c2, v);
-            l2 += wk.s2;
-            if (l2 == vps) { l2 = 0; ++b2; } else if (l2 < 0) { l2 = vps - 1; --b2; }
-          } else if (a1) {
-            wk.c1 += wk.s1;
-            wk.m1 = fadd(wk.m1, wk.d1);
-            x1 = vcenter(wk.c1, v);
-            l1 += wk.s1;
-            if (l1 == vps) { l1 = 0; ++b1; } else if (l1 < 0) { l1 = vps - 1; --b1; }
-          } else {
-            wk.c0 += wk.s0;
-            wk.m0 = fadd(wk.m0, wk.d0);
-            x0 = vcenter(wk.c0, v);
-            l0 += wk.s0;
-            if (l0 == vps) { l0 = 0; ++b0; } else if (l0 < 0) { l0 = vps - 1; --b0; }
+      }
+      if ((k & 31u) == 31u || k + 1u == maxc) {  // warp-uniform: write the staged rows
+        __syncwarp();
+        const uint32_t k0 = k & ~31u, nrow = (k & 31u) + 1u;
+        for (uint32_t l = 0; l < 32u; ++l) {
+          const uint4 ml = wmeta[l];  // broadcast
+          if (ml.x > k0) {
+            const uint32_t m = min(nrow, ml.x - k0);
+            if (lane < m) {
+              const uint32_t o = ml.y + k0 + lane;
+              rkeys[o] = wrows[l * 33u + lane];
+              rvals[o] = ml.z;  // the ray index is every record's sort value
+            }
           }
         }
+        __syncwarp();
       }
     }
     warp_add_by_key(updates, r.frame, valid);

@@ -1212,8 +1212,14 @@ void vxg_handle::emit_and_apply(uint32_t R, uint32_t F, const TermView& tv) {
       CU(cudaMemsetAsync(counters.p + 1, 0, sizeof(uint32_t), st));
       CU(cudaMemsetAsync(d_upd.p, 0, F * sizeof(unsigned long long), st));
       begin(ST_EMIT);
-      k_emit<<<grid_for(r1 - r0, 128), 128, 0, st>>>(r0, r1, ray_perm.p, rays.p, roff.p, base, d_poses.p, tp, view(),
-                                                       tv, rkeys.p, rvals.p, d_upd.p);
+      {
+        const bool anti = tp.merge_mode == VXG_MERGE_GROUPED_ANTI_GRAZE;
+        const bool pow2 = (vps & (vps - 1)) == 0;
+        auto kern = anti ? (pow2 ? k_emit<true, true> : k_emit<true, false>)
+                         : (pow2 ? k_emit<false, true> : k_emit<false, false>);
+        kern<<<grid_for(r1 - r0, 128), 128, 0, st>>>(r0, r1, ray_perm.p, rays.p, roff.p, base, d_poses.p, tp, view(),
+                                                     tv, rkeys.p, rvals.p, d_upd.p);
+      }
       ++launches;
       CU(cudaGetLastError());
       end(T, 1);

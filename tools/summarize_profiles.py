@@ -72,7 +72,7 @@ def main():
     total = sum(per.values())
     lines = [f"# {tag}: ncu launch list (gpu__time_duration.sum, --clock-control none)", "",
              "Cold-cache, serialised per-launch times of `python tools/bench_once.py 100 2` (two cfg1 steps of "
-             "100 frames; the two fold kernels, concurrent in the bench, run one after the other under ncu). "
+             "100 frames; the fold is one grid, k_fold_all, long and short runs together). "
              "Compare SHARES, not absolutes.", "",
              "| kernel | launches | total ms | share |", "|---|---|---|---|"]
     for k, v in sorted(per.items(), key=lambda x: -x[1]):
@@ -100,7 +100,7 @@ def main():
     n_sort_launches = max(1, len([m for m in sort_caps if "downsweep" in m["kernel"]]))
     sort_step = sum(m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
                     for m in sort_caps) * passes / n_sort_launches
-    apply_step = dram(["k_fold_runs", "k_fold_short"])
+    apply_step = dram(["k_fold_all", "k_fold_runs", "k_fold_short"])
     inputs = {"record_sort_dram_bytes_per_step": sort_step, "apply_dram_bytes_per_step": apply_step,
               "source": f"profiles/{tag}_summary.json", "sort_passes": passes}
     lines += ["", f"DRAM bytes per step: record_sort {sort_step:.3e} ({passes} passes), apply {apply_step:.3e}."]
