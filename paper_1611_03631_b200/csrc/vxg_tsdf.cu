@@ -848,7 +848,11 @@ uint64_t vxg_handle::count_rays(uint32_t R, uint32_t F) {
 // first — in emission (ray) order the top digit (block slot bits) is the most
 // clustered, so that pass scatters long coalesced segments and ranks few
 // distinct values — then the others from the bottom: groups come out ordered
-// by a bit-permuted key (measured 3.57 vs 4.14 ms on cfg1).
+// by a bit-permuted key (measured 3.57 vs 4.14 ms on cfg1). Other plans
+// (VXG_DIGITS, B200, cfg1): 14:7,7:7,0:7 3.81; 12:9,0:6,6:6 3.97; 14:7,0:6,6:8
+// 3.88; 12:9,0:4,4:8 4.15; plain LSD 4.29 vs 3.77 ms for the default.
+std::vector<std::pair<int, int>> grouped_digit_plan(int kbits);
+
 template <int kBits, int kIpt, int kMB>
 void vxg_handle::lsd_sort(uint64_t T, int kbits, uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
                           uint32_t** sk, uint32_t** sv, bool grouped, uint32_t K) {
@@ -870,19 +874,26 @@ void vxg_handle::lsd_sort(uint64_t T, int kbits, uint32_t* k0, uint32_t* v0, uin
     CU(cudaMemsetAsync(dense_start.p, 0xFF, K * sizeof(uint32_t), st));
     CU(cudaMemsetAsync(dense_end.p, 0, K * sizeof(uint32_t), st));
   }
-  const int passes = std::max(1, (kbits + kBits - 1) / kBits);
+  std::vector<std::pair<int, int>> plan = grouped ? grouped_digit_plan(kbits) : std::vector<std::pair<int, int>>{};
+  if (plan.empty()) {
+    const int np = std::max(1, (kbits + kBits - 1) / kBits);
+    int dshift[8], dbits[8];  // natural digits, least significant first
+    for (int p = 0, sh = 0; p < np; ++p) {
+      dbits[p] = (kbits - sh + (np - p) - 1) / (np - p);
+      dshift[p] = sh;
+      sh += dbits[p];
+    }
+    for (int q = 0; q < np; ++q) {
+      const int p = !grouped ? q : (q == 0 ? np - 1 : q - 1);
+      plan.emplace_back(dshift[p], dbits[p]);
+    }
+  }
+  const int passes = static_cast<int>(plan.size());
   last_lsd_passes = passes;
   const uint32_t S = static_cast<uint32_t>((T + C::kSuper - 1) / C::kSuper);
   uint32_t *ki = k0, *vi = v0, *ko = k1, *vo = v1;
-  int dshift[8], dbits[8];  // natural digits, least significant first
-  for (int p = 0, sh = 0; p < passes; ++p) {
-    dbits[p] = (kbits - sh + (passes - p) - 1) / (passes - p);
-    dshift[p] = sh;
-    sh += dbits[p];
-  }
   for (int q = 0; q < passes; ++q) {
-    const int p = !grouped ? q : (q == 0 ? passes - 1 : q - 1);
-    const int shift = dshift[p], bits = dbits[p];
+    const int shift = plan[q].first, bits = plan[q].second;
     const uint32_t mask = bits ? (1u << bits) - 1u : 0u;
     const uint64_t nc = static_cast<uint64_t>(mask + 1u) * S;
     sort_counts.ensure(nc);
@@ -906,6 +917,26 @@ void vxg_handle::lsd_sort(uint64_t T, int kbits, uint32_t* k0, uint32_t* v0, uin
   *sv = vi;
 }
 
+// Digit plan of the grouped record sort, (shift, bits) per pass in pass order
+// (dev A/B: VXG_DIGITS="14:7,0:7,7:7"; the fields must tile [0, kbits)).
+// Empty: the default (top digit first, then the others from the bottom).
+std::vector<std::pair<int, int>> grouped_digit_plan(int kbits) {
+  std::vector<std::pair<int, int>> plan;
+  const char* e = getenv("VXG_DIGITS");
+  if (e == nullptr) return plan;
+  uint64_t cover = 0;
+  for (const char* c = e; *c;) {
+    int sh = 0, b = 0, n = 0;
+    if (sscanf(c, "%d:%d%n", &sh, &b, &n) != 2) return {};
+    plan.emplace_back(sh, b);
+    cover |= ((1ull << b) - 1ull) << sh;
+    c += n;
+    if (*c == ',') ++c;
+  }
+  if (cover != (1ull << kbits) - 1ull) return {};
+  return plan;
+}
+
 void vxg_handle::sort_records(uint64_t T, int kbits, uint32_t** sk, uint32_t** sv, uint32_t K) {
   static const bool use_cub = [] {  // dev A/B: VXG_SORT=cub
     const char* e = getenv("VXG_SORT");
@@ -923,10 +954,14 @@ void vxg_handle::sort_records(uint64_t T, int kbits, uint32_t** sk, uint32_t** s
     *sv = rvals2.p;
     return;
   }
-  if (kbits <= 21)
-    lsd_sort<7, 12, 4>(T, kbits, rkeys.p, rvals.p, rkeys2.p, rvals2.p, sk, sv, true, K);
-  else
+  int maxb = 0;
+  for (const auto& d : grouped_digit_plan(kbits)) maxb = std::max(maxb, d.second);
+  if (maxb > 8)
+    lsd_sort<9, 12, 4>(T, kbits, rkeys.p, rvals.p, rkeys2.p, rvals2.p, sk, sv, true, K);
+  else if (maxb == 8 || (maxb == 0 && kbits > 21))
     lsd_sort<8, 12, 4>(T, kbits, rkeys.p, rvals.p, rkeys2.p, rvals2.p, sk, sv, true, K);
+  else
+    lsd_sort<7, 12, 4>(T, kbits, rkeys.p, rvals.p, rkeys2.p, rvals2.p, sk, sv, true, K);
   info_sort_passes = static_cast<uint64_t>(last_lsd_passes);
 }
 
