@@ -1517,7 +1517,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_fold_short(
 // 12..15, one per sub-partition, the highest warp ids so the arbiter favours
 // the serial chains), warps 0..7 fold short runs from the start; every pair
 // warp joins the short runs once the long runs are handed out.
-template <bool kSmemOrg>
+template <bool kSmemOrg, int kC = 2>
 __global__ void __launch_bounds__(512, 1) k_fold_all(
     const uint32_t* __restrict__ num_runs_p, const uint32_t* __restrict__ order,
     const uint32_t* __restrict__ sorted_len, const uint32_t* __restrict__ ukeys, const uint32_t* __restrict__ ustart,
@@ -1537,7 +1537,7 @@ __global__ void __launch_bounds__(512, 1) k_fold_all(
   if (wid >= 8)
     fold_long_pairs<4, false>(S, wid - 8, poses, nruns, n_long, order, ukeys, ustart, ulen, svals, rays, map, tp,
                               touched, work, dbg);
-  fold_short_loop<4>(poses, nruns, n_long, order, ukeys, ustart, ulen, svals, rays, map, tp, touched, work);
+  fold_short_loop<kC>(poses, nruns, n_long, order, ukeys, ustart, ulen, svals, rays, map, tp, touched, work);
 }
 
 // Self-tests of the fast fold arithmetic against the reference-order path.

@@ -1090,7 +1090,15 @@ void vxg_handle::sort_fold(uint64_t T, uint64_t nslots, uint32_t F) {
     }();
     begin(ST_APPLY, fold_long_st);
     if (fold_merged) {
-      auto kern = smem_org ? k_fold_all<true> : k_fold_all<false>;
+      static const int fold_kc = [] {  // dev A/B: records per short-run chunk (VXG_FOLD_KC = 1 | 2 | 3 | 4)
+        const char* e = getenv("VXG_FOLD_KC");
+        return e ? atoi(e) : 2;  // measured apply 2.74 / 2.34 / 2.38 / 2.57 ms for 1 / 2 / 3 / 4 (cfg1)
+      }();
+      auto kern = !smem_org ? k_fold_all<false, 2>
+                            : (fold_kc == 2 ? k_fold_all<true, 2>
+                                : (fold_kc == 1 ? k_fold_all<true, 1>
+                                                : (fold_kc == 3 ? k_fold_all<true, 3>
+                                                                : (fold_kc == 4 ? k_fold_all<true, 4> : k_fold_all<true, 2>))));
       kern<<<static_cast<unsigned>(dev_sms), 512, 0, fold_long_st>>>(num_runs.p, run_order.p, run_len2.p, run_keys.p,
                                                                      run_start.p, run_len.p, svals, fold_rays.p,
                                                                      d_org.p, F, view(), tp, tch, work.p, dbg);
@@ -1155,6 +1163,12 @@ void vxg_handle::sort_fold(uint64_t T, uint64_t nslots, uint32_t F) {
   } while (0)
     if (short_blocks == 1)
       VXG_FOLD_SHORT(3, 4);
+    else if (short_blocks == 3)
+      VXG_FOLD_SHORT(2, 2);
+    else if (short_blocks == 4)
+      VXG_FOLD_SHORT(3, 2);
+    else if (short_blocks == 6)
+      VXG_FOLD_SHORT(4, 2);
     else
       VXG_FOLD_SHORT(2, 4);
 #undef VXG_FOLD_SHORT
