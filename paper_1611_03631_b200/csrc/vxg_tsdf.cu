@@ -239,6 +239,7 @@ struct vxg_handle {
   DBuf<unsigned long long> chunk_base;  // per chunk: first ray, first record
   DBuf<uint32_t> sort_counts, sort_offs, dense_start, dense_end, run_flag, run_pos;
   DBuf<FoldRay> fold_rays;
+  DBuf<uint32_t> num_segs;  // bundling: bucket count (RLE output)
   DBuf<float4> pt_w;    // bundling: per sorted point (world point, weight)
   DBuf<uint32_t> pt_c;  // bundling: per sorted point colour
   DBuf<float> d_org;  // sensor origins, 3 floats per frame
@@ -687,7 +688,7 @@ void vxg_handle::build_rays_grouped(const float* dxyz, const uint8_t* drgb, uint
   const int end_bit = 3 * kb + fb;
   ukeys.ensure(P);
   ucounts.ensure(P);
-  num_runs.ensure(1);
+  num_segs.ensure(1);  // its own count: num_runs belongs to the fold sets (a fold may still read it)
   if (end_bit <= 32) {  // 32-bit keys: half the sort traffic
     uint32_t* k32 = reinterpret_cast<uint32_t*>(pkeys.ensure((P + 1) / 2));
     uint32_t* k32b = reinterpret_cast<uint32_t*>(pkeys2.ensure((P + 1) / 2));
@@ -706,9 +707,9 @@ void vxg_handle::build_rays_grouped(const float* dxyz, const uint8_t* drgb, uint
       k32b = reinterpret_cast<uint32_t*>(pkeys2.p);
     }
     cub([&](void* t, size_t& b) {
-      return cub::DeviceRunLengthEncode::Encode(t, b, k32b, u32, ucounts.p, num_runs.p, static_cast<int>(P), st);
+      return cub::DeviceRunLengthEncode::Encode(t, b, k32b, u32, ucounts.p, num_segs.p, static_cast<int>(P), st);
     }, 2);
-    k_widen_keys<<<grid_for(P), 256, 0, st>>>(num_runs.p, u32, ukeys.p);
+    k_widen_keys<<<grid_for(P), 256, 0, st>>>(num_segs.p, u32, ukeys.p);
     ++launches;
     pt_w.ensure(P);
     pt_c.ensure(P);
@@ -728,7 +729,7 @@ void vxg_handle::build_rays_grouped(const float* dxyz, const uint8_t* drgb, uint
                                              end_bit, st);
     }, 2 + (end_bit + 7) / 8);
     cub([&](void* t, size_t& b) {
-      return cub::DeviceRunLengthEncode::Encode(t, b, pkeys2.p, ukeys.p, ucounts.p, num_runs.p, static_cast<int>(P),
+      return cub::DeviceRunLengthEncode::Encode(t, b, pkeys2.p, ukeys.p, ucounts.p, num_segs.p, static_cast<int>(P),
                                                 st);
     }, 2);
     pt_w.ensure(P);
@@ -739,7 +740,7 @@ void vxg_handle::build_rays_grouped(const float* dxyz, const uint8_t* drgb, uint
     CU(cudaGetLastError());
   }
   uint32_t S = 0;
-  CU(cudaMemcpyAsync(&S, num_runs.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(&S, num_segs.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
   uoffs.ensure(std::max<uint32_t>(S, 1));
   cub([&](void* t, size_t& b) {
@@ -750,7 +751,7 @@ void vxg_handle::build_rays_grouped(const float* dxyz, const uint8_t* drgb, uint
   seg_start.ensure(F);
   CU(cudaMemsetAsync(seg_count.p, 0, F * sizeof(uint32_t), st));
   CU(cudaMemsetAsync(seg_start.p, 0xFF, F * sizeof(uint32_t), st));
-  k_seg_reduce<<<grid_for(S), 256, 0, st>>>(num_runs.p, ukeys.p, uoffs.p, ucounts.p, pvals2.p, pt_w.p, pt_c.p, drgb,
+  k_seg_reduce<<<grid_for(S), 256, 0, st>>>(num_segs.p, ukeys.p, uoffs.p, ucounts.p, pvals2.p, pt_w.p, pt_c.p, drgb,
                                             d_off.p,
                                             d_poses.p, tp, rb, kb, segs.p, seg_count.p, seg_start.p, d_stats.p + 2 * F);
   ++launches;
