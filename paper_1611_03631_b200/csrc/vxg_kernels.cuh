@@ -229,19 +229,32 @@ __global__ void k_seg_reduce(const uint32_t* __restrict__ num_segs_p, const unsi
     const float o[3] = {Pm[3], Pm[7], Pm[11]};
     double wp[3] = {0.0, 0.0, 0.0}, wc[3] = {0.0, 0.0, 0.0}, W = 0.0;
     const uint32_t first = svals[start];
-    for (uint32_t j = 0; j < cnt; ++j) {  // point order within the bucket (stable sort)
-      const float4 q = pw[start + j];
+    // point order within the bucket (stable sort); the terms of kSegChunk
+    // points are loaded before their (sequential) sums, so the loads overlap
+    auto add_point = [&](const float4& q, uint32_t c) {
       const double wd = static_cast<double>(q.w);
       wp[0] = __dadd_rn(wp[0], __dmul_rn(wd, static_cast<double>(q.x)));
       wp[1] = __dadd_rn(wp[1], __dmul_rn(wd, static_cast<double>(q.y)));
       wp[2] = __dadd_rn(wp[2], __dmul_rn(wd, static_cast<double>(q.z)));
       if (rgb != nullptr) {
-        const uint32_t c = cc[start + j];
 #pragma unroll
         for (int k = 0; k < 3; ++k) wc[k] = __dadd_rn(wc[k], __dmul_rn(wd, static_cast<double>((c >> (8 * k)) & 0xffu)));
       }
       W = __dadd_rn(W, wd);
+    };
+    uint32_t j = 0;
+    for (; j + kSegChunk <= cnt; j += kSegChunk) {
+      float4 q[kSegChunk];
+      uint32_t c[kSegChunk];
+#pragma unroll
+      for (int u = 0; u < kSegChunk; ++u) {
+        q[u] = pw[start + j + u];
+        c[u] = rgb != nullptr ? cc[start + j + u] : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < kSegChunk; ++u) add_point(q[u], c[u]);
     }
+    for (; j < cnt; ++j) add_point(pw[start + j], rgb != nullptr ? cc[start + j] : 0u);
 #pragma unroll
     for (int k = 0; k < 3; ++k) out.mean[k] = __double2float_rn(__ddiv_rn(wp[k], W));
     uint32_t col = 0u;
