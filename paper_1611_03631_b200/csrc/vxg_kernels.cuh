@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(uint32_t R0, uint32_t R1,
     const float depth = r.depth;
     uint32_t valid = 0, count = 0, out0 = 0;
     const bool live = has && r.valid == 1u && !(depth <= 0.0f);
-    float ray0 = 0.0f, ray1 = 0.0f, ray2 = 0.0f, w_front = 0.0f;
+    float ray0 = 0.0f, ray1 = 0.0f, ray2 = 0.0f, w_front = 0.0f, t_safe = -1.0f;
     Walk wk{};
     if (live) {
       ray0 = fsub(r.p[0], o0), ray1 = fsub(r.p[1], o1), ray2 = fsub(r.p[2], o2);
@@ -553,6 +553,13 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(uint32_t R0, uint32_t R1,
       walk_axis_init(o1, fadd(r.p[1], fmul(ray1, s)), v, &wk.c1, &wk.e1, &wk.s1, &wk.m1, &wk.d1, &span);
       walk_axis_init(o2, fadd(r.p[2], fmul(ray2, s)), v, &wk.c2, &wk.e2, &wk.s2, &wk.m2, &wk.d2, &span);
       count = span + 1u;
+      // walk parameter (0 at the origin, 1 at the end point p + ray * s) below
+      // which every voxel centre is provably in front of the point: a voxel
+      // left at t_exit * |end - o| < depth - 3 v has its centre at least
+      // 1.1 v before the point along the ray (half diagonal 0.87 v, plus one
+      // voxel for the DDA's rounded axis choices), where the reference's
+      // rounded `along` cannot be negative, so d >= 0 and w = w_front
+      t_safe = (depth - 3.0f * v) / (fadd(depth, tp.truncation) + v);
       // record offsets inside one chunk are 32-bit (chunks stay below 2^29 records)
       out0 = static_cast<uint32_t>(roff[j] - base);
     }
@@ -563,7 +570,6 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(uint32_t R0, uint32_t R1,
       og1 = gidx(o1, v);
       og2 = gidx(o2, v);
     }
-    float x0 = vcenter(wk.c0, v), x1 = vcenter(wk.c1, v), x2 = vcenter(wk.c2, v);
     int b0, b1, b2, l0, l1, l2;
     if (kPow2) {
       b0 = wk.c0 >> lg, b1 = wk.c1 >> lg, b2 = wk.c2 >> lg;
@@ -589,13 +595,17 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(uint32_t R0, uint32_t R1,
           // projective_distance(x, p, s) (tsdf_integrator.cpp:22-27); p - s == ray.
           // In front of the point (along >= 0) d = +|t| >= 0, where every weight
           // mode gives the ray's constant w_front: the norm is needed only behind it.
-          const float t0f = fsub(r.p[0], x0), t1f = fsub(r.p[1], x1), t2f = fsub(r.p[2], x2);
-          const float along = dot3(t0f, t1f, t2f, ray0, ray1, ray2);
           float w = w_front;
-          if (!(along >= 0.0f)) {
-            const float magnitude = norm3(t0f, t1f, t2f);
-            const float d = along < 0.0f ? -magnitude : magnitude;
-            w = fmul(mweight_base(tp.weight_mode, r.base, d, tp.truncation, tp.dropoff_epsilon), r.weight);
+          const float t_exit = fminf(fminf(wk.m0, wk.m1), wk.m2);
+          if (!(t_exit < t_safe)) {  // the last voxels of the walk: evaluate along (and d behind the point)
+            const float x0 = vcenter(wk.c0, v), x1 = vcenter(wk.c1, v), x2 = vcenter(wk.c2, v);
+            const float t0f = fsub(r.p[0], x0), t1f = fsub(r.p[1], x1), t2f = fsub(r.p[2], x2);
+            const float along = dot3(t0f, t1f, t2f, ray0, ray1, ray2);
+            if (!(along >= 0.0f)) {
+              const float magnitude = norm3(t0f, t1f, t2f);
+              const float d = along < 0.0f ? -magnitude : magnitude;
+              w = fmul(mweight_base(tp.weight_mode, r.base, d, tp.truncation, tp.dropoff_epsilon), r.weight);
+            }
           }
           if (!(w <= 0.0f)) {
             if (b0 != cb0 || b1 != cb1 || b2 != cb2) {
@@ -632,9 +642,6 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(uint32_t R0, uint32_t R1,
         wk.m0 = st0 ? fadd(wk.m0, wk.d0) : wk.m0;
         wk.m1 = st1 ? fadd(wk.m1, wk.d1) : wk.m1;
         wk.m2 = st2 ? fadd(wk.m2, wk.d2) : wk.m2;
-        x0 = vcenter(wk.c0, v);
-        x1 = vcenter(wk.c1, v);
-        x2 = vcenter(wk.c2, v);
         if (kPow2) {
           b0 = wk.c0 >> lg, b1 = wk.c1 >> lg, b2 = wk.c2 >> lg;
           l0 = wk.c0 & (vps - 1), l1 = wk.c1 & (vps - 1), l2 = wk.c2 & (vps - 1);
