@@ -881,7 +881,10 @@ __global__ void k_localize(uint64_t n, const uint4* __restrict__ recv, MapView m
 //    kFoldChunk records evaluated ahead of each folded chunk.
 // The fold step itself is update_voxel_fast (shared reciprocal, stationary
 // colour skip), bit-identical to update_tsdf_voxel.
-constexpr uint32_t kLongRun = 4096;
+#ifndef VXG_LONG_RUN
+#define VXG_LONG_RUN 4096
+#endif
+constexpr uint32_t kLongRun = VXG_LONG_RUN;
 constexpr int kFoldChunk = 8;
 
 struct alignas(16) Upd {
