@@ -193,22 +193,43 @@ __global__ void __launch_bounds__(kSortThreads, kMinBlocks)
       if (t + 1 < C::kNsub && nb < n) load_sub(nb, static_cast<uint32_t>(min(static_cast<uint64_t>(C::kSub), n - nb)));
     }
     __syncthreads();
-    for (uint32_t i = tid; i < nv; i += kSortThreads) {
-      const uint2 kv = sm.stage[i];
-      const uint32_t d = (kv.x >> shift) & mask;
-      const uint32_t p = sm.gdelta[d] + i;
-      if (!kMarks) kout[p] = kv.x;
-      vout[p] = kv.y;
-      if (kMarks && kv.x < K) {
-        const uint32_t s0 = sm.tstart[d], s1 = s0 + sm.tcount[d];  // the digit's staged segment
-        if (i == s0)
-          atomicMin(&dense_start[kv.x], p);
-        else if (sm.stage[i - 1].x != kv.x)
-          dense_start[kv.x] = p;
-        if (i + 1 == s1)
-          atomicMax(&dense_end[kv.x], p + 1);
-        else if (sm.stage[i + 1].x != kv.x)
-          dense_end[kv.x] = p + 1;
+    if (!kMarks) {
+      for (uint32_t i = tid; i < nv; i += kSortThreads) {
+        const uint2 kv = sm.stage[i];
+        const uint32_t d = (kv.x >> shift) & mask;
+        const uint32_t p = sm.gdelta[d] + i;
+        kout[p] = kv.x;
+        vout[p] = kv.y;
+      }
+    } else {
+      // consecutive staged records sit in consecutive lanes: the neighbours'
+      // keys come by shuffle; a digit change between neighbours is the digit
+      // segment's edge (the staged records are in digit order)
+      for (uint32_t b = static_cast<uint32_t>(tid) & ~31u; b < nv; b += kSortThreads) {  // warp-uniform
+        const uint32_t i = b + lane;
+        const bool in = i < nv;
+        const uint2 kv = in ? sm.stage[i] : make_uint2(0xFFFFFFFFu, 0u);
+        uint32_t prev = __shfl_up_sync(0xffffffffu, kv.x, 1);
+        uint32_t next = __shfl_down_sync(0xffffffffu, kv.x, 1);
+        if (lane == 0u) prev = (in && i > 0) ? sm.stage[i - 1].x : 0xFFFFFFFFu;
+        if (lane == 31u || i + 1 >= nv) next = (i + 1 < nv) ? sm.stage[i + 1].x : 0xFFFFFFFFu;
+        if (in) {
+          const uint32_t d = (kv.x >> shift) & mask;
+          const uint32_t p = sm.gdelta[d] + i;
+          vout[p] = kv.y;
+          if (kv.x < K) {
+            const bool seg_first = i == 0 || ((prev >> shift) & mask) != d;
+            const bool seg_last = i + 1 == nv || ((next >> shift) & mask) != d;
+            if (seg_first)
+              atomicMin(&dense_start[kv.x], p);
+            else if (prev != kv.x)
+              dense_start[kv.x] = p;
+            if (seg_last)
+              atomicMax(&dense_end[kv.x], p + 1);
+            else if (next != kv.x)
+              dense_end[kv.x] = p + 1;
+          }
+        }
       }
     }
     __syncthreads();
