@@ -1318,6 +1318,7 @@ void vxg_handle::begin_batch(const float* xyz, const uint8_t* rgb, const uint64_
 
 // Reads the per-frame stats back and feeds the updated-block consumers.
 void vxg_handle::end_batch(uint64_t F, vxg_stats* out) {
+  apply_pending_reset();  // a batch without rays never reached the map: the reset still applies
   if (!fold_may_outlive_call()) join_folds();
   begin(ST_D2H);
   std::vector<unsigned long long> s(3 * F);

@@ -103,3 +103,19 @@ def test_flush_then_stream_sync(gpu):
     st = layer.stage_times(reset=True)
     assert st["apply"][0] > 0.0
     layer.profile(False)
+
+
+def test_reset_then_empty_batch(gpu):
+    """A batch without rays after a deferred reset still leaves an empty layer."""
+    wc = W.CONFIGS[1]
+    cfg = W.tsdf_config(wc)
+    layer = TsdfLayer(wc.voxel_size, wc.vps)
+    integ = TsdfIntegrator(cfg, layer)
+    _gpu_batch(integ, _frames(0, 2))
+    layer.reset()
+    empty_pts = np.zeros((0, 3), np.float32)
+    pose = np.eye(4, dtype=np.float32)[:3]
+    stats = integ.integrate_batch([Scan(empty_pts, None, pose)])
+    assert int(stats[0, 0]) == 0
+    assert layer.block_count() == 0
+    assert layer.save_bytes() == OracleLayer(cfg, wc.voxel_size, wc.vps).save_bytes()
