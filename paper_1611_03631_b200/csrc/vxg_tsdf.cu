@@ -826,6 +826,7 @@ uint64_t vxg_handle::count_rays(uint32_t R, uint32_t F) {
   rcount.ensure(R);
   roff.ensure(R);
   join_folds();  // the previous batch's fold reads fold_rays
+  if (R > fold_rays.cap) sync_folds();  // (and the host may free it only after that fold)
   fold_rays.ensure(R);
   k_ray_count<<<grid_for(R), 256, 0, st>>>(R, rays.p, d_poses.p, tp, rcount.p, d_stats.p + F, fold_rays.p);
   ++launches;
@@ -1062,6 +1063,7 @@ void vxg_handle::sort_fold(uint64_t T, uint64_t nslots, uint32_t F) {
   if (nruns) {
     // origins of this set on st (d_poses is rewritten by the next batch
     // while this fold may still wait for the previous one)
+    if (3ull * std::max<uint32_t>(F, 1) > d_org.cap) sync_folds();  // the set's old table may still be read
     d_org.ensure(3 * std::max<uint32_t>(F, 1));
     k_origins<<<grid_for(3 * F), 256, 0, st>>>(F, d_poses.p, d_org.p);
     ++launches;
