@@ -344,6 +344,7 @@ struct vxg_handle {
 
   // ---------------------------------------------------------------- map
   void alloc_map(uint64_t cap) {
+    sync_folds();  // the slab about to be freed may still be folded into
     cap_blocks = cap;
     slab.release();
     block_idx.release();
