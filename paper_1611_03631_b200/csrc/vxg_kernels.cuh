@@ -4,8 +4,9 @@
 //   slab       : cap_blocks x vps^3 vxg_voxel (12 B AoS, x-fastest = the VXBLX
 //                voxel payload, serialization.cpp:107-114), zero = default voxel
 //   block hash : open addressing, linear probing, 2^k x (u64 packed key, i32 slot)
-//   records    : per voxel update u32 sort key (slot*vps^3 + local) + u32 seq
-//                + 16 B payload {d, w, rgb|has_color<<31, 0}
+//   records    : per candidate voxel update, u32 key (slot*vps^3 + local, or
+//                0xFFFFFFFF for a skipped candidate) + u32 ray id (8 B); the fold
+//                re-derives (d, w, colour) from the ray (FoldRay, one 32-B sector)
 #pragma once
 
 #include <cstdint>
