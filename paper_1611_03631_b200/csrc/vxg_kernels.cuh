@@ -504,7 +504,10 @@ __device__ __forceinline__ void walk_axis_init(float st, float en, float v, int*
 // ray's end); each lane stages its keys in a shared-memory row of 32, and every
 // 32 steps the warp writes row after row as 128-byte runs (a ray's records are
 // contiguous at offset[ray]): coalesced stores instead of 32 scattered ones.
-constexpr int kEmitThreads = 128;
+#ifndef VXG_EMIT_THREADS
+#define VXG_EMIT_THREADS 256
+#endif
+constexpr int kEmitThreads = VXG_EMIT_THREADS;
 template <bool kAnti, bool kPow2>
 __global__ void __launch_bounds__(kEmitThreads) k_emit(uint32_t R0, uint32_t R1, const uint32_t* __restrict__ perm,
                        const RayInfo* __restrict__ rays, const unsigned long long* __restrict__ roff, uint64_t base,

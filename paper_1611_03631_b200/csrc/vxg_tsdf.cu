@@ -1270,7 +1270,7 @@ void vxg_handle::emit_and_apply(uint32_t R, uint32_t F, const TermView& tv) {
         const bool pow2 = (vps & (vps - 1)) == 0;
         auto kern = anti ? (pow2 ? k_emit<true, true> : k_emit<true, false>)
                          : (pow2 ? k_emit<false, true> : k_emit<false, false>);
-        kern<<<grid_for(r1 - r0, 128), 128, 0, st>>>(r0, r1, ray_perm.p, rays.p, roff.p, base, d_poses.p, tp, view(),
+        kern<<<grid_for(r1 - r0, kEmitThreads), kEmitThreads, 0, st>>>(r0, r1, ray_perm.p, rays.p, roff.p, base, d_poses.p, tp, view(),
                                                      tv, rkeys.p, rvals.p, d_upd.p);
       }
       ++launches;
