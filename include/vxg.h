@@ -147,6 +147,13 @@ int vxg_block_count(vxg_handle* h, uint64_t* out);
  * blocks; *n_out = blocks written. Either output pointer may be NULL. */
 int vxg_export_blocks(vxg_handle* h, int32_t* idx, vxg_voxel* voxels, uint64_t cap, uint64_t* n_out);
 
+/* Layer::block_ptr (layer.h:89-97) + copy-out for n block indices idx[n*3]:
+ * voxels = n x vps^3 vxg_voxel (x-fastest; zeros for an absent block),
+ * found[i] = 1 when block i is allocated. One device gather and one D2H per
+ * 256 MB of payload (the C++ drop-in's per-scan writeback). Either output
+ * may be NULL. */
+int vxg_fetch_blocks(vxg_handle* h, const int32_t* idx, uint64_t n, vxg_voxel* voxels, uint8_t* found);
+
 /* Inserts / overwrites blocks (idx B x 3, voxels B x vps^3) — used to resume
  * from a VXBLX checkpoint (load_tsdf_layer, serialization.cpp:193-212) or to
  * mirror a host layer. */

@@ -5,6 +5,7 @@
 // (tests/test_oracle_pin.py), to generate tests/golden/ fixtures, and as the
 // timed CPU baseline (bench.py cpu_baseline kind "reference", --impl reference).
 // No reference source is copied into this repository.
+#include <chrono>
 #include <cstring>
 #include <sstream>
 #include <stdexcept>
@@ -25,6 +26,7 @@
 namespace {
 
 thread_local std::string g_last_error;
+thread_local double g_last_seconds = 0.0;
 
 vxf::TsdfConfig to_config(const vxg_tsdf_config* c) {
   vxf::TsdfConfig t;
@@ -49,6 +51,9 @@ struct RefHandle {
 extern "C" {
 
 const char* vxr_last_error(void) { return g_last_error.c_str(); }
+
+// Seconds the last vxr_integrate spent inside TsdfIntegrator::integrate.
+double vxr_last_integrate_seconds(void) { return g_last_seconds; }
 
 void* vxr_create(const vxg_tsdf_config* c, float voxel_size, int vps) {
   try {
@@ -79,7 +84,11 @@ int vxr_integrate(void* hp, const float* xyz, const uint8_t* rgb, size_t n, cons
   }
   scan.pose = pose_t;
   try {
+    // timed exactly as the reference times an insert (benchmark.cpp:93-95,
+    // cli.cpp:171-174): steady_clock around integrate() only
+    const auto t0 = std::chrono::steady_clock::now();
     const size_t updates = h->integrator.integrate(scan);
+    g_last_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     if (out != nullptr) {
       out->updates = updates;
       out->raycasts = h->integrator.raycasts_last_scan();
@@ -125,6 +134,24 @@ size_t vxr_save_vxblx(void* hp, uint8_t* buf, size_t cap) {
   const std::string s = os.str();
   if (buf != nullptr && cap >= s.size()) std::memcpy(buf, s.data(), s.size());
   return s.size();
+}
+
+// vxf::load_tsdf_layer (serialization.cpp:193-212) of a VXBLX image, then
+// vxf::save_layer of the loaded layer into a caller buffer. Returns the byte
+// size, or 0 with vxr_last_error() on a ParseError.
+size_t vxr_load_resave(const uint8_t* in, size_t len, uint8_t* buf, size_t cap) {
+  try {
+    std::istringstream is(std::string(reinterpret_cast<const char*>(in), len), std::ios::binary);
+    const vxf::TsdfLayer layer = vxf::load_tsdf_layer(is);
+    std::ostringstream os(std::ios::binary);
+    vxf::save_layer(layer, os);
+    const std::string s = os.str();
+    if (buf != nullptr && cap >= s.size()) std::memcpy(buf, s.data(), s.size());
+    return s.size();
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return 0;
+  }
 }
 
 int vxr_config_validate(const vxg_tsdf_config* c, char* err, size_t err_len) {

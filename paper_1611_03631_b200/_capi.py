@@ -78,6 +78,7 @@ SIGNATURES = [
     ("vxg_block_count", c_int, [c_void_p, POINTER(c_uint64)]),
     ("vxg_export_blocks", c_int, [c_void_p, c_void_p, c_void_p, c_uint64, POINTER(c_uint64)]),
     ("vxg_import_blocks", c_int, [c_void_p, c_void_p, c_void_p, c_uint64]),
+    ("vxg_fetch_blocks", c_int, [c_void_p, c_void_p, c_uint64, c_void_p, c_void_p]),
     ("vxg_query_voxels", c_int, [c_void_p, c_void_p, c_uint64, c_void_p, c_void_p]),
     ("vxg_interpolate_distance", c_int, [c_void_p, c_void_p, c_uint64, c_void_p, c_void_p, c_int]),
     ("vxg_surface_error", c_int, [c_void_p, c_void_p, c_uint64, c_float, c_void_p]),

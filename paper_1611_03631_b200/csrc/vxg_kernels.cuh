@@ -321,6 +321,68 @@ __global__ void k_order_keys(uint32_t S, const SegInfo* __restrict__ segs, const
   }
 }
 
+// ---- rehash epochs of one frame's bucketing map.
+// Inside a frame (segments segs[0..K)), rank = first-appearance rank of the
+// key. Epoch e (bucket count bc, keys of rank < t_hi present) re-inserts the
+// previous epoch's iteration order (positions 0..t_lo-1), then the keys of
+// rank [t_lo, t_hi) in first-appearance order; its iteration order sorts the
+// present keys by (first occupation of their bucket desc, position desc).
+__global__ void k_rh_pos_keys(uint32_t K, const SegInfo* __restrict__ segs, uint32_t* __restrict__ keys,
+                              uint32_t* __restrict__ vals) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < K; i += gridDim.x * blockDim.x) {
+    keys[i] = segs[i].pos;
+    vals[i] = i;
+  }
+}
+
+__global__ void k_rh_rank(uint32_t K, const uint32_t* __restrict__ by_pos, uint32_t* __restrict__ rank) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < K; r += gridDim.x * blockDim.x) rank[by_pos[r]] = r;
+}
+
+__device__ __forceinline__ uint32_t rh_pos(uint32_t rank, const uint32_t* prev, uint32_t i, uint32_t t_lo) {
+  return rank < t_lo ? prev[i] : rank;
+}
+
+__global__ void k_rh_fo(uint32_t K, const SegInfo* __restrict__ segs, const uint32_t* __restrict__ rank,
+                        const uint32_t* __restrict__ prev, uint32_t t_lo, uint64_t t_hi, uint64_t bc,
+                        uint32_t* __restrict__ fo) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < K; i += gridDim.x * blockDim.x) {
+    const uint32_t r = rank[i];
+    if (r >= t_hi) continue;
+    atomicMin(&fo[segs[i].hash % bc], rh_pos(r, prev, i, t_lo));
+  }
+}
+
+// pass 1 key (secondary): position, descending
+__global__ void k_rh_pos_desc(uint32_t K, const uint32_t* __restrict__ rank, const uint32_t* __restrict__ prev,
+                              uint32_t t_lo, uint32_t M, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < K; i += gridDim.x * blockDim.x) {
+    keys[i] = M - rh_pos(rank[i], prev, i, t_lo);
+    vals[i] = i;
+  }
+}
+
+// pass 2 key (primary, stable over pass 1): first occupation of the bucket,
+// descending; keys not yet present last
+__global__ void k_rh_fo_desc(uint32_t K, const uint32_t* __restrict__ vals, const SegInfo* __restrict__ segs,
+                             const uint32_t* __restrict__ rank, uint64_t t_hi, uint64_t bc,
+                             const uint32_t* __restrict__ fo, uint32_t M, uint32_t* __restrict__ keys) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < K; j += gridDim.x * blockDim.x) {
+    const uint32_t i = vals[j];
+    keys[j] = rank[i] < t_hi ? M - fo[segs[i].hash % bc] : M + 1u;
+  }
+}
+
+// prev[order[j]] = j for the m present keys; on the last epoch also the
+// frame's slice of the global ray order
+__global__ void k_rh_commit(uint32_t m, const uint32_t* __restrict__ order, uint32_t* __restrict__ prev,
+                            uint32_t seg0, uint32_t* __restrict__ ray_order) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
+    prev[order[j]] = j;
+    if (ray_order != nullptr) ray_order[j] = seg0 + order[j];
+  }
+}
+
 __global__ void k_gather_rays(uint32_t R, const uint32_t* __restrict__ order, const SegInfo* __restrict__ segs,
                               RayInfo* __restrict__ rays) {
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < R; j += gridDim.x * blockDim.x) {
@@ -1713,6 +1775,34 @@ __global__ void k_scatter_blocks(uint64_t n, const int32_t* __restrict__ slots, 
     const int32_t s = slots[b];
     if (s < 0) continue;
     map.slab[static_cast<uint64_t>(s) * nv + (i - b * nv)] = src[i];
+  }
+}
+
+// Export: blocks slots[0..n) gathered into one contiguous AoS buffer (the
+// VXBLX payload order), pad bytes zeroed; 4-byte words, coalesced both ways.
+__global__ void k_gather_blocks(uint64_t n, const uint32_t* __restrict__ slots, const vxg_voxel* __restrict__ slab,
+                                uint32_t nvox, vxg_voxel* __restrict__ dst) {
+  const uint64_t wpb = 3ull * nvox;  // 4-byte words per block
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(slab);
+  uint32_t* out = reinterpret_cast<uint32_t*>(dst);
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n * wpb;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t b = i / wpb, w = i - b * wpb;
+    const uint32_t sl = slots[b];
+    uint32_t v = sl == 0xFFFFFFFFu ? 0u : __ldg(src + static_cast<uint64_t>(sl) * wpb + w);  // absent: zeros
+    if (w % 3 == 2) v &= 0x00FFFFFFu;  // r, g, b, pad=0
+    out[i] = v;
+  }
+}
+
+// Layer::block_ptr (layer.h:89-97) for n block indices: slot, or ~0u when absent.
+__global__ void k_block_slots(uint64_t n, const int32_t* __restrict__ idx, MapView map, uint32_t* __restrict__ slots) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const int b0 = idx[3 * i], b1 = idx[3 * i + 1], b2 = idx[3 * i + 2];
+    int32_t s = -1;
+    if (block_in_range(b0, b1, b2)) s = map.find(pack_block(b0, b1, b2));
+    slots[i] = (s < 0 || static_cast<uint32_t>(s) >= map.cap_blocks) ? 0xFFFFFFFFu : static_cast<uint32_t>(s);
   }
 }
 

@@ -228,6 +228,7 @@ struct vxg_handle {
   DBuf<RayInfo> rays;
   DBuf<unsigned long long> rcount, roff, rcount2;
   DBuf<uint32_t> ray_perm, ray_iota;
+  DBuf<uint32_t> rh_k0, rh_k1, rh_v0, rh_v1, rh_rank, rh_prev;  // rehash epochs (order_rehash_frame)
   DBuf<uint64_t> tbl_off, bcs;
   DBuf<uint32_t> rkeys, rkeys2, rvals, rvals2;
   DBuf<uint32_t> run_keys, run_len, run_start, run_len2, run_order, run_iota, work;
@@ -343,30 +344,59 @@ struct vxg_handle {
   }
 
   // ---------------------------------------------------------------- map
-  void alloc_map(uint64_t cap) {
+  // (Re)allocates an empty map of `cap` blocks of new_vps^3 voxels. Every
+  // check and allocation happens before any handle state changes: on failure
+  // the handle keeps its previous map (and geometry) intact.
+  void alloc_map(uint64_t cap, int new_vps = 0) {
+    if (new_vps <= 0) new_vps = vps;
+    const uint64_t nv = static_cast<uint64_t>(new_vps) * new_vps * new_vps;
+    cap = std::max<uint64_t>(cap, 1);
+    if (cap * nv >= 0xFFFFFFFFull)  // voxel keys slot * vps^3 + local are 32-bit (kInvalidRecord = ~0u)
+      throw VxgError(VXG_ENOMEM, "block slab would exceed the 32-bit voxel key range");
     sync_folds();  // the slab about to be freed may still be folded into
-    cap_blocks = cap;
+    uint64_t hc = 1;
+    while (hc < 2 * cap) hc <<= 1;
+    vxg_voxel* ns = nullptr;
+    int32_t* ni = nullptr;
+    unsigned long long* nk = nullptr;
+    int32_t* nh = nullptr;
+    auto fail = [&](const char* what) {
+      cudaGetLastError();
+      if (ns) cudaFree(ns);
+      if (ni) cudaFree(ni);
+      if (nk) cudaFree(nk);
+      if (nh) cudaFree(nh);
+      throw VxgError(VXG_ENOMEM, std::string("cannot allocate the ") + what + " for " + std::to_string(cap) +
+                                     " blocks");
+    };
+    if (cudaMalloc(&ns, cap * nv * sizeof(vxg_voxel)) != cudaSuccess) fail("block slab");
+    if (cudaMalloc(&ni, cap * 3 * sizeof(int32_t)) != cudaSuccess) fail("block index table");
+    if (cudaMalloc(&nk, hc * sizeof(unsigned long long)) != cudaSuccess) fail("block hash");
+    if (cudaMalloc(&nh, hc * sizeof(int32_t)) != cudaSuccess) fail("block hash");
+    counters.ensure(4);
     slab.release();
     block_idx.release();
-    CU(cudaMalloc(&slab.p, cap * nvox * sizeof(vxg_voxel)));
-    slab.cap = cap * nvox;
-    CU(cudaMemsetAsync(slab.p, 0, cap * nvox * sizeof(vxg_voxel), st));
-    CU(cudaMalloc(&block_idx.p, cap * 3 * sizeof(int32_t)));
-    block_idx.cap = cap * 3;
-    hcap = 1;
-    while (hcap < 2 * cap) hcap <<= 1;
     hkeys.release();
     hvals.release();
-    CU(cudaMalloc(&hkeys.p, hcap * sizeof(unsigned long long)));
-    hkeys.cap = hcap;
-    CU(cudaMalloc(&hvals.p, hcap * sizeof(int32_t)));
-    hvals.cap = hcap;
+    slab.p = ns;
+    slab.cap = cap * nv;
+    block_idx.p = ni;
+    block_idx.cap = cap * 3;
+    hkeys.p = nk;
+    hkeys.cap = hc;
+    hvals.p = nh;
+    hvals.cap = hc;
+    hcap = hc;
+    cap_blocks = cap;
+    vps = new_vps;
+    nvox = static_cast<int>(nv);
+    CU(cudaMemsetAsync(slab.p, 0, cap * nv * sizeof(vxg_voxel), st));
     CU(cudaMemsetAsync(hkeys.p, 0xFF, hcap * sizeof(unsigned long long), st));
     CU(cudaMemsetAsync(hvals.p, 0xFF, hcap * sizeof(int32_t), st));
-    counters.ensure(4);
     CU(cudaMemsetAsync(counters.p, 0, 4 * sizeof(uint32_t), st));
     n_blocks = 0;
     host_idx.clear();
+    touched.release();  // per-slot flags of the old map
     CU(cudaStreamSynchronize(st));
   }
 
@@ -531,10 +561,40 @@ struct vxg_handle {
     n_top = 0;
   }
 
-  void read_counters(uint32_t* c) {
-    CU(cudaMemcpyAsync(c, counters.p, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  // Small device->host reads go through a pinned mailbox: a pageable
+  // destination makes the driver stage the copy, and such a copy can queue
+  // behind a large H2D in flight on the copy stream (the next batch's
+  // staging), stalling the call for the whole transfer.
+  struct D2H {
+    void* host;
+    const void* dev;
+    size_t bytes;
+  };
+  uint8_t* mailbox = nullptr;
+  size_t mailbox_cap = 0;
+  void fetch(std::initializer_list<D2H> list) {
+    size_t total = 0;
+    for (const D2H& d : list) total += (d.bytes + 15) & ~size_t(15);
+    if (total > mailbox_cap) {
+      if (mailbox) CU(cudaFreeHost(mailbox));
+      mailbox = nullptr;
+      mailbox_cap = std::max<size_t>(total + total / 2, 4096);
+      CU(cudaHostAlloc(reinterpret_cast<void**>(&mailbox), mailbox_cap, cudaHostAllocDefault));
+    }
+    size_t o = 0;
+    for (const D2H& d : list) {
+      if (d.bytes) CU(cudaMemcpyAsync(mailbox + o, d.dev, d.bytes, cudaMemcpyDeviceToHost, st));
+      o += (d.bytes + 15) & ~size_t(15);
+    }
     CU(cudaStreamSynchronize(st));
+    o = 0;
+    for (const D2H& d : list) {
+      if (d.bytes) std::memcpy(d.host, mailbox + o, d.bytes);
+      o += (d.bytes + 15) & ~size_t(15);
+    }
   }
+
+  void read_counters(uint32_t* c) { fetch({{c, counters.p, 2 * sizeof(uint32_t)}}); }
 
   // Refresh host_idx for slots appended since the last call.
   void sync_block_mirror(uint64_t nb) {
@@ -547,9 +607,7 @@ struct vxg_handle {
     const uint64_t have = host_idx.size() / 3;
     host_idx.resize(3 * nb);
     if (nb > have) {
-      CU(cudaMemcpyAsync(host_idx.data() + 3 * have, block_idx.p + 3 * have, (nb - have) * 3 * sizeof(int32_t),
-                         cudaMemcpyDeviceToHost, st));
-      CU(cudaStreamSynchronize(st));
+      fetch({{host_idx.data() + 3 * have, block_idx.p + 3 * have, (nb - have) * 3 * sizeof(int32_t)}});
     }
     n_blocks = nb;
   }
@@ -611,9 +669,7 @@ void vxg_handle::build_rays_simple(const float* dxyz, const uint8_t* drgb, uint6
     return cub::DeviceScan::ExclusiveSum(t, b, flags.p, ray_idx.p, static_cast<int>(P), st);
   }, 2);
   uint32_t last_idx = 0, last_flag = 0;
-  CU(cudaMemcpyAsync(&last_idx, ray_idx.p + (P - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-  CU(cudaMemcpyAsync(&last_flag, flags.p + (P - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
+  fetch({{&last_idx, ray_idx.p + (P - 1), sizeof(uint32_t)}, {&last_flag, flags.p + (P - 1), sizeof(uint32_t)}});
   const uint32_t R = last_idx + last_flag;
   rays.ensure(std::max<uint32_t>(R, 1));
   k_simple_rays<<<grid_for(P), 256, 0, st>>>(dxyz, drgb, P, d_off.p, d_poses.p, F, flags.p, ray_idx.p, rays.p);
@@ -624,54 +680,53 @@ void vxg_handle::build_rays_simple(const float* dxyz, const uint8_t* drgb, uint6
 }
 
 // Reorders frame f's K buckets when its map rehashes while they are inserted
-// (SURVEY.md Appendix B): epoch e re-inserts the previous iteration order, then
-// appends the next keys by first appearance, under bucket count bc_e.
+// (SURVEY.md Appendix B), on the device: epoch e re-inserts the previous
+// iteration order, then appends the next keys by first appearance, under
+// bucket count bc_e (k_rh_*). Each epoch's order is two stable 32-bit sorts
+// (position desc, then first bucket occupation desc). No host round trip.
 void vxg_handle::order_rehash_frame(uint32_t f, uint32_t K, uint32_t seg0, uint64_t n_points, const Schedule& sch,
                                     uint32_t ray0, int pb) {
+  (void)f;
   (void)n_points;
-  // rank = first-appearance rank: sort the frame's segments by pos.
-  std::vector<SegInfo> hseg(K);
-  CU(cudaMemcpyAsync(hseg.data(), segs.p + seg0, K * sizeof(SegInfo), cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
-  std::vector<uint32_t> by_pos(K);
-  for (uint32_t i = 0; i < K; ++i) by_pos[i] = i;
-  std::sort(by_pos.begin(), by_pos.end(), [&](uint32_t a, uint32_t b) { return hseg[a].pos < hseg[b].pos; });
-  std::vector<uint32_t> rank(K);
-  for (uint32_t r = 0; r < K; ++r) rank[by_pos[r]] = r;
-  // Host emulation of the epochs is O(K log K) per epoch; frames that rehash are
-  // the rare ~10^6-bucket case (cfg4) and this runs once per such frame.
-  std::vector<uint32_t> pos(K), order;  // order: local seg ids in current list order
+  (void)pb;
+  const SegInfo* fs = segs.p + seg0;
+  uint32_t* k0 = rh_k0.ensure(K);
+  uint32_t* k1 = rh_k1.ensure(K);
+  uint32_t* v0 = rh_v0.ensure(K);
+  uint32_t* v1 = rh_v1.ensure(K);
+  uint32_t* rank = rh_rank.ensure(K);
+  uint32_t* prev = rh_prev.ensure(K);
+  const int kb = bits_for(K);  // positions < K <= 2^kb - 1
+  const uint32_t M = (1u << kb) - 1u;
+  uint32_t *sk = nullptr, *sv = nullptr;
+  // rank = first-appearance rank inside the frame
+  k_rh_pos_keys<<<grid_for(K), 256, 0, st>>>(K, fs, k0, v0);
+  lsd_sort<8, 12, 4>(K, pb, k0, v0, k1, v1, &sk, &sv, false);
+  k_rh_rank<<<grid_for(K), 256, 0, st>>>(K, sv, rank);
+  launches += 2;
   for (size_t e = 0; e < sch.size(); ++e) {
     const uint64_t t_lo = sch[e].first;
     const uint64_t t_hi = e + 1 < sch.size() ? sch[e + 1].first : UINT64_MAX;
     if (t_lo >= K && e > 0) break;
+    const bool last = t_hi >= K;
     const uint64_t bc = sch[e].second;
-    std::vector<uint32_t> prev_index(K, 0);
-    for (size_t i = 0; i < order.size(); ++i) prev_index[order[i]] = static_cast<uint32_t>(i);
-    std::vector<uint32_t> members;
-    for (uint32_t i = 0; i < K; ++i) {
-      if (rank[i] >= t_hi) continue;
-      pos[i] = rank[i] < t_lo ? prev_index[i] : rank[i];
-      members.push_back(i);
-    }
-    std::map<uint64_t, uint32_t> fo;
-    for (uint32_t i : members) {
-      const uint64_t b = hseg[i].hash % bc;
-      auto it = fo.find(b);
-      if (it == fo.end() || pos[i] < it->second) fo[b] = pos[i];
-    }
-    std::sort(members.begin(), members.end(), [&](uint32_t a, uint32_t b) {
-      const uint32_t fa = fo[hseg[a].hash % bc], fb = fo[hseg[b].hash % bc];
-      if (fa != fb) return fa > fb;
-      return pos[a] > pos[b];
-    });
-    order = members;
+    fo.ensure(bc);
+    CU(cudaMemsetAsync(fo.p, 0xFF, bc * sizeof(uint32_t), st));
+    const uint32_t tl = static_cast<uint32_t>(t_lo);
+    k_rh_fo<<<grid_for(K), 256, 0, st>>>(K, fs, rank, prev, tl, t_hi, bc, fo.p);
+    k_rh_pos_desc<<<grid_for(K), 256, 0, st>>>(K, rank, prev, tl, M, k0, v0);
+    lsd_sort<8, 12, 4>(K, kb, k0, v0, k1, v1, &sk, &sv, false);
+    uint32_t* kf = sk == k0 ? k1 : k0;  // free key buffer
+    uint32_t* vf = sv == v0 ? v1 : v0;  // free value buffer
+    k_rh_fo_desc<<<grid_for(K), 256, 0, st>>>(K, sv, fs, rank, t_hi, bc, fo.p, M, kf);
+    uint32_t *sk2 = nullptr, *sv2 = nullptr;
+    lsd_sort<8, 12, 4>(K, kb + 1, kf, sv, sk, vf, &sk2, &sv2, false);
+    const uint32_t m = static_cast<uint32_t>(std::min<uint64_t>(K, t_hi));
+    k_rh_commit<<<grid_for(m), 256, 0, st>>>(m, sv2, prev, seg0, last ? ovals.p + ray0 : nullptr);
+    launches += 4;
+    CU(cudaGetLastError());
+    if (last) break;
   }
-  (void)pb;
-  std::vector<uint32_t> global(order.size());
-  for (size_t i = 0; i < order.size(); ++i) global[i] = seg0 + order[i];
-  CU(cudaMemcpyAsync(ovals.p + ray0, global.data(), global.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-  CU(cudaStreamSynchronize(st));
 }
 
 void vxg_handle::build_rays_grouped(const float* dxyz, const uint8_t* drgb, uint64_t P, const uint64_t* h_off,
@@ -741,8 +796,7 @@ void vxg_handle::build_rays_grouped(const float* dxyz, const uint8_t* drgb, uint
     CU(cudaGetLastError());
   }
   uint32_t S = 0;
-  CU(cudaMemcpyAsync(&S, num_segs.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
+  fetch({{&S, num_segs.p, sizeof(uint32_t)}});
   uoffs.ensure(std::max<uint32_t>(S, 1));
   cub([&](void* t, size_t& b) {
     return cub::DeviceScan::ExclusiveSum(t, b, ucounts.p, uoffs.p, static_cast<int>(S), st);
@@ -758,9 +812,7 @@ void vxg_handle::build_rays_grouped(const float* dxyz, const uint8_t* drgb, uint
   ++launches;
   CU(cudaGetLastError());
   std::vector<uint32_t> K(F), start(F);
-  CU(cudaMemcpyAsync(K.data(), seg_count.p, F * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-  CU(cudaMemcpyAsync(start.data(), seg_start.p, F * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
+  fetch({{K.data(), seg_count.p, F * sizeof(uint32_t)}, {start.data(), seg_start.p, F * sizeof(uint32_t)}});
   end(P, 7);
 
   // ---- K3 ray order
@@ -836,9 +888,8 @@ uint64_t vxg_handle::count_rays(uint32_t R, uint32_t F) {
     return cub::DeviceScan::ExclusiveSum(t, b, rcount.p, roff.p, static_cast<int>(R), st);
   }, 2);
   unsigned long long tail[2] = {0, 0};
-  CU(cudaMemcpyAsync(&tail[0], roff.p + (R - 1), sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-  CU(cudaMemcpyAsync(&tail[1], rcount.p + (R - 1), sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
+  fetch({{&tail[0], roff.p + (R - 1), sizeof(unsigned long long)},
+         {&tail[1], rcount.p + (R - 1), sizeof(unsigned long long)}});
   end(R, 3);
   return tail[0] + tail[1];
 }
@@ -1018,8 +1069,7 @@ void vxg_handle::sort_fold(uint64_t T, uint64_t nslots, uint32_t F) {
   ++launches;
   CU(cudaGetLastError());
   uint32_t nruns = 0;
-  CU(cudaMemcpyAsync(&nruns, num_runs.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
+  fetch({{&nruns, num_runs.p, sizeof(uint32_t)}});
   if (std::max<uint32_t>(nruns, 1) > std::min(run_len2.cap, run_order.cap)) sync_folds();
   run_len2.ensure(std::max<uint32_t>(nruns, 1));
   run_order.ensure(std::max<uint32_t>(nruns, 1));
@@ -1236,7 +1286,6 @@ void vxg_handle::emit_and_apply(uint32_t R, uint32_t F, const TermView& tv) {
   std::vector<unsigned long long> hb(2 * (nch + 1));
   k_chunk_bounds<<<1, 64, 0, st>>>(R, roff.p, total, nch, chunk_base.p);
   ++launches;
-  CU(cudaMemcpyAsync(hb.data(), chunk_base.p, hb.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   // emission order: rays by decreasing record count inside each chunk (balanced
   // warps); the records still land at their ray-order offsets.
   ray_perm.ensure(R);
@@ -1252,7 +1301,7 @@ void vxg_handle::emit_and_apply(uint32_t R, uint32_t F, const TermView& tv) {
                                                      static_cast<int>(R), 0, cbits, st);
   }, 2 + (cbits + 7) / 8);
   ensure_touched();
-  CU(cudaStreamSynchronize(st));  // hb
+  fetch({{hb.data(), chunk_base.p, hb.size() * sizeof(unsigned long long)}});
   d_upd.ensure(F);
   for (uint32_t c = 0; c < nch; ++c) {
     const uint32_t r0 = static_cast<uint32_t>(hb[c]), r1 = static_cast<uint32_t>(hb[c + 1]);
@@ -1325,11 +1374,9 @@ void vxg_handle::end_batch(uint64_t F, vxg_stats* out) {
   if (!fold_may_outlive_call()) join_folds();
   begin(ST_D2H);
   std::vector<unsigned long long> s(3 * F);
-  CU(cudaMemcpyAsync(s.data(), d_stats.p, 3 * F * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   uint32_t c[2];
-  CU(cudaMemcpyAsync(c, counters.p, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   end(0, 0);
-  CU(cudaStreamSynchronize(st));
+  fetch({{s.data(), d_stats.p, 3 * F * sizeof(unsigned long long)}, {c, counters.p, 2 * sizeof(uint32_t)}});
   collect();
   drain_tops();
   if (out != nullptr) {
@@ -1344,9 +1391,8 @@ void vxg_handle::end_batch(uint64_t F, vxg_stats* out) {
   sync_block_mirror(nb);
   if (!consumers.empty() && nb > 0 && touched.p != nullptr) {
     std::vector<uint8_t> t(nb);
-    CU(cudaMemcpyAsync(t.data(), touched.p, nb, cudaMemcpyDeviceToHost, st));
+    fetch({{t.data(), touched.p, nb}});
     CU(cudaMemsetAsync(touched.p, 0, touched.cap, st));
-    CU(cudaStreamSynchronize(st));
     for (auto& kv : consumers)
       for (uint32_t i = 0; i < nb; ++i)
         if (t[i]) kv.second.insert(i);
@@ -1641,6 +1687,26 @@ void export_sorted(vxg_handle* h, std::vector<uint32_t>* order) {
   });
 }
 
+// Copies the blocks at slots[0..n) (host array) into `dst` (host memory,
+// n * vps^3 voxels, pads zeroed): a device gather into contiguous scratch,
+// then one D2H per piece of at most 256 MB.
+void gather_to_host(vxg_handle* h, const uint32_t* slots, uint64_t n, vxg_voxel* dst) {
+  const uint64_t nv = static_cast<uint64_t>(h->nvox);
+  const uint64_t per = std::max<uint64_t>(1, (256ull << 20) / (nv * sizeof(vxg_voxel)));
+  DBuf<uint32_t> dslots;
+  DBuf<vxg_voxel> buf;
+  dslots.ensure(std::min(per, n));
+  buf.ensure(std::min(per, n) * nv);
+  for (uint64_t k0 = 0; k0 < n; k0 += per) {
+    const uint64_t m = std::min(per, n - k0);
+    CU(cudaMemcpyAsync(dslots.p, slots + k0, m * sizeof(uint32_t), cudaMemcpyHostToDevice, h->st));
+    k_gather_blocks<<<grid_for(m * nv * 3), 256, 0, h->st>>>(m, dslots.p, h->slab.p, static_cast<uint32_t>(nv), buf.p);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(dst + k0 * nv, buf.p, m * nv * sizeof(vxg_voxel), cudaMemcpyDeviceToHost, h->st));
+    CU(cudaStreamSynchronize(h->st));
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -1727,6 +1793,7 @@ int vxg_destroy(vxg_handle* h) {
       for (cudaEvent_t e : h->set_done) cudaEventDestroy(e);
       cudaFreeHost(h->top_pinned);
     }
+    if (h->mailbox) cudaFreeHost(h->mailbox);
     if (h->nccl_comm) nccl()->CommDestroy(static_cast<ncclComm_t>(h->nccl_comm));
     if (h->own) cudaStreamDestroy(h->own);
     delete h;
@@ -2015,16 +2082,45 @@ int vxg_export_blocks(vxg_handle* h, int32_t* idx, vxg_voxel* voxels, uint64_t c
       for (uint64_t k = 0; k < n; ++k)
         for (int a = 0; a < 3; ++a) idx[3 * k + a] = h->host_idx[3 * order[k] + a];
     }
-    if (voxels != nullptr && n > 0) {
-      const size_t bb = static_cast<size_t>(h->nvox) * sizeof(vxg_voxel);
-      for (uint64_t k = 0; k < n; ++k) {
-        CU(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(voxels) + k * bb,
-                           reinterpret_cast<uint8_t*>(h->slab.p) + static_cast<size_t>(order[k]) * bb, bb,
-                           cudaMemcpyDeviceToHost, h->st));
+    if (voxels != nullptr && n > 0) gather_to_host(h, order.data(), n, voxels);
+    if (n_out) *n_out = n;
+  });
+}
+
+int vxg_fetch_blocks(vxg_handle* h, const int32_t* idx, uint64_t n, vxg_voxel* voxels, uint8_t* found) {
+  return guarded([&] {
+    set_device(h);
+    h->settle();
+    if (n == 0) return;
+    if (idx == nullptr) throw VxgError(VXG_EINVAL, "null argument");
+    const uint64_t nv = static_cast<uint64_t>(h->nvox);
+    const uint64_t per = std::max<uint64_t>(1, (256ull << 20) / (nv * sizeof(vxg_voxel)));
+    DBuf<int32_t> didx;
+    DBuf<uint32_t> dslots;
+    DBuf<vxg_voxel> buf;
+    std::vector<uint32_t> hs;
+    didx.ensure(3 * std::min(per, n));
+    dslots.ensure(std::min(per, n));
+    if (voxels != nullptr) buf.ensure(std::min(per, n) * nv);
+    for (uint64_t k0 = 0; k0 < n; k0 += per) {
+      const uint64_t m = std::min(per, n - k0);
+      CU(cudaMemcpyAsync(didx.p, idx + 3 * k0, 3 * m * sizeof(int32_t), cudaMemcpyHostToDevice, h->st));
+      k_block_slots<<<grid_for(m), 256, 0, h->st>>>(m, didx.p, h->view(), dslots.p);
+      CU(cudaGetLastError());
+      if (voxels != nullptr) {
+        k_gather_blocks<<<grid_for(m * nv * 3), 256, 0, h->st>>>(m, dslots.p, h->slab.p, static_cast<uint32_t>(nv),
+                                                                 buf.p);
+        CU(cudaGetLastError());
+        CU(cudaMemcpyAsync(voxels + k0 * nv, buf.p, m * nv * sizeof(vxg_voxel), cudaMemcpyDeviceToHost, h->st));
+      }
+      if (found != nullptr) {
+        hs.resize(m);
+        CU(cudaMemcpyAsync(hs.data(), dslots.p, m * sizeof(uint32_t), cudaMemcpyDeviceToHost, h->st));
       }
       CU(cudaStreamSynchronize(h->st));
+      if (found != nullptr)
+        for (uint64_t k = 0; k < m; ++k) found[k0 + k] = hs[k] != 0xFFFFFFFFu ? 1 : 0;
     }
-    if (n_out) *n_out = n;
   });
 }
 
@@ -2033,6 +2129,31 @@ int vxg_import_blocks(vxg_handle* h, const int32_t* idx, const vxg_voxel* voxels
     set_device(h);
     h->settle();
     if (n == 0) return;
+    // A block index given more than once: the last copy wins whole, as in the
+    // reference's load (get_or_allocate_block + read_voxel per block,
+    // serialization.cpp:193-212). Earlier copies are dropped before upload.
+    std::vector<int32_t> uidx;
+    std::vector<vxg_voxel> uvox;
+    {
+      std::map<std::array<int32_t, 3>, uint64_t> last;
+      for (uint64_t b = 0; b < n; ++b) last[{idx[3 * b], idx[3 * b + 1], idx[3 * b + 2]}] = b;
+      if (last.size() != n) {
+        const uint64_t nv = static_cast<uint64_t>(h->nvox);
+        std::vector<uint64_t> keep;
+        keep.reserve(last.size());
+        for (uint64_t b = 0; b < n; ++b)
+          if (last[{idx[3 * b], idx[3 * b + 1], idx[3 * b + 2]}] == b) keep.push_back(b);
+        uidx.resize(3 * keep.size());
+        uvox.resize(keep.size() * nv);
+        for (size_t k = 0; k < keep.size(); ++k) {
+          std::memcpy(uidx.data() + 3 * k, idx + 3 * keep[k], 3 * sizeof(int32_t));
+          std::memcpy(uvox.data() + k * nv, voxels + keep[k] * nv, nv * sizeof(vxg_voxel));
+        }
+        idx = uidx.data();
+        voxels = uvox.data();
+        n = keep.size();
+      }
+    }
     DBuf<int32_t> didx, slots;
     DBuf<vxg_voxel> dv;
     didx.ensure(3 * n);
@@ -2392,17 +2513,21 @@ int vxg_serialize_vxblx(vxg_handle* h, uint8_t* buf, uint64_t cap, uint64_t* nee
     put(&kind, 1);
     put(&nb, 8);
     const size_t bb = static_cast<size_t>(h->nvox) * sizeof(vxg_voxel);
-    std::vector<vxg_voxel> tmp(h->nvox);
-    for (uint64_t k = 0; k < nb; ++k) {
-      for (int a = 0; a < 3; ++a) {
-        const int64_t v = h->host_idx[3 * order[k] + a];
-        put(&v, 8);
+    // the blocks' payloads in sorted order: one gather + one D2H per 4096 blocks,
+    // written into place behind each block's 24-byte index
+    const uint64_t kStep = 4096;
+    std::vector<vxg_voxel> tmp;
+    for (uint64_t k0 = 0; k0 < nb; k0 += kStep) {
+      const uint64_t m = std::min<uint64_t>(kStep, nb - k0);
+      tmp.resize(m * static_cast<uint64_t>(h->nvox));
+      gather_to_host(h, order.data() + k0, m, tmp.data());
+      for (uint64_t k = 0; k < m; ++k) {
+        for (int a = 0; a < 3; ++a) {
+          const int64_t v = h->host_idx[3 * order[k0 + k] + a];
+          put(&v, 8);
+        }
+        put(tmp.data() + k * h->nvox, bb);  // payload layout == vxg_voxel (f32, f32, u8 x3, u8 pad)
       }
-      CU(cudaMemcpyAsync(tmp.data(), reinterpret_cast<uint8_t*>(h->slab.p) + static_cast<size_t>(order[k]) * bb, bb,
-                         cudaMemcpyDeviceToHost, h->st));
-      CU(cudaStreamSynchronize(h->st));
-      for (int i = 0; i < h->nvox; ++i) tmp[i].pad = 0;
-      put(tmp.data(), bb);  // payload layout == vxg_voxel (f32, f32, u8 x3, u8 pad)
     }
   });
 }
@@ -2493,14 +2618,15 @@ int vxg_load_vxblx(vxg_handle* h, const uint8_t* buf, uint64_t len) {
     }
     set_device(h);
     h->settle();
-    h->voxel_size = static_cast<float>(vs);
     if (static_cast<int>(vps) != h->vps) {
-      h->vps = static_cast<int>(vps);
-      h->nvox = static_cast<int>(nvox);
-      h->alloc_map(std::max<uint64_t>(h->cap_blocks, count + 64));
+      // the new geometry's key range is checked before the handle changes
+      uint64_t cap = h->cap_blocks;
+      while (cap > 1 && cap * nvox >= 0xFFFFFFFFull) cap /= 2;
+      h->alloc_map(std::max<uint64_t>(cap, count + 64), static_cast<int>(vps));
     } else {
       if (vxg_reset(h) != VXG_OK) throw VxgError(VXG_ECUDA, g_err);
     }
+    h->voxel_size = static_cast<float>(vs);
     // duplicate indices: later blocks overwrite earlier ones (get_or_allocate_block)
     const int rc = vxg_import_blocks(h, idx.data(), vox.data(), count);
     if (rc != VXG_OK) throw VxgError(rc, g_err);

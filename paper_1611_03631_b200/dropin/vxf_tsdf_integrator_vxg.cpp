@@ -18,8 +18,8 @@
 //    or gained blocks the device does not hold, it is re-uploaded (the
 //    single-writer contract, layer.h:53-55, means it is otherwise unchanged).
 //  * the free functions projective_distance / measurement_weight /
-//    update_tsdf_voxel evaluate on the device (vxg_eval_*). RayCaster is a
-//    host-side iterator over the same walk (not on the integration path).
+//    update_tsdf_voxel evaluate on the device (vxg_eval_*); RayCaster iterates
+//    over the device walk (vxg_eval_raycast; not on the integration path).
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -117,40 +117,57 @@ void upload(Mirror& m, TsdfLayer& layer, const TsdfConfig& cfg) {
   check(vxg_drain_updated(m.h, kConsumer, sink.data(), n, &n));
 }
 
-// Writes the blocks updated by the last scan back into the host layer.
+// Writes the blocks updated by the last scan back into the host layer: the
+// drained block indices, then their payloads in one device gather + D2H
+// (vxg_fetch_blocks), copied into the host blocks.
 void download(Mirror& m, TsdfLayer& layer) {
   uint64_t n = 0;
   check(vxg_drain_updated(m.h, kConsumer, nullptr, 0, &n));
   std::vector<int32_t> idx(3 * (n + 1));
   check(vxg_drain_updated(m.h, kConsumer, idx.data(), n, &n));
   if (n == 0) return;
-  const int vps = m.vps;
-  const size_t nv = static_cast<size_t>(vps) * vps * vps;
-  std::vector<int32_t> g(3 * nv * n);
-  for (uint64_t b = 0; b < n; ++b)
-    for (size_t i = 0; i < nv; ++i) {
-      const int lx = static_cast<int>(i % vps), ly = static_cast<int>((i / vps) % vps),
-                lz = static_cast<int>(i / (static_cast<size_t>(vps) * vps));
-      g[3 * (b * nv + i) + 0] = idx[3 * b + 0] * vps + lx;
-      g[3 * (b * nv + i) + 1] = idx[3 * b + 1] * vps + ly;
-      g[3 * (b * nv + i) + 2] = idx[3 * b + 2] * vps + lz;
-    }
+  const size_t nv = static_cast<size_t>(m.vps) * m.vps * m.vps;
   std::vector<vxg_voxel> out(nv * n);
-  std::vector<uint8_t> found(nv * n);
-  check(vxg_query_voxels(m.h, g.data(), nv * n, out.data(), found.data()));
+  check(vxg_fetch_blocks(m.h, idx.data(), n, out.data(), nullptr));
   for (uint64_t b = 0; b < n; ++b) {
     const BlockIndex bidx(idx[3 * b], idx[3 * b + 1], idx[3 * b + 2]);
     Block<TsdfVoxel>& block = layer.get_or_allocate_block(bidx);
     layer.mark_updated(bidx);
+    const vxg_voxel* src = out.data() + b * nv;
     for (size_t i = 0; i < nv; ++i) {
-      const vxg_voxel& v = out[b * nv + i];
       TsdfVoxel& t = block.voxel(i);
-      t.distance = v.distance;
-      t.weight = v.weight;
-      t.color = Color{v.r, v.g, v.b};
+      t.distance = src[i].distance;
+      t.weight = src[i].weight;
+      t.color = Color{src[i].r, src[i].g, src[i].b};
     }
     m.fingerprint[key3(bidx)] = &block;
   }
+}
+
+// The voxels of one walk, computed by the device DDA (vxg_eval_raycast); the
+// last walk is cached per thread so RayCaster::next is a lookup.
+struct Walk {
+  float start[3] = {}, end[3] = {}, v = 0.f;
+  bool valid = false;
+  std::vector<int32_t> voxels;  // 3 per voxel, traversal order
+};
+thread_local Walk g_walk;
+
+const Walk& device_walk(const float s[3], const float e[3], float v) {
+  Walk& w = g_walk;
+  if (w.valid && std::memcmp(w.start, s, sizeof(w.start)) == 0 && std::memcmp(w.end, e, sizeof(w.end)) == 0 &&
+      std::memcmp(&w.v, &v, sizeof(v)) == 0)
+    return w;
+  uint32_t count = 0;
+  check(vxg_eval_raycast(0, s, e, 1, v, &count, nullptr, nullptr));
+  const uint64_t off = 0;
+  w.voxels.assign(3 * static_cast<size_t>(count), 0);
+  if (count > 0) check(vxg_eval_raycast(0, s, e, 1, v, &count, &off, w.voxels.data()));
+  std::memcpy(w.start, s, sizeof(w.start));
+  std::memcpy(w.end, e, sizeof(w.end));
+  w.v = v;
+  w.valid = true;
+  return w;
 }
 
 }  // namespace
@@ -193,41 +210,38 @@ void update_tsdf_voxel(TsdfVoxel* voxel, FloatingPoint d, FloatingPoint w, Float
   update_tsdf_voxel(voxel, d, w, truncation, max_weight, Color{}, false);
 }
 
-// Host-side walk iterator with the reference's exact semantics
-// (tsdf_integrator.cpp:69-104); the integration path uses the device walk.
+// RayCaster (tsdf_integrator.cpp:69-104) as an adapter over the device walk:
+// the members keep the segment (t_max_ = start, t_delta_ = end, step_[0] =
+// the voxel size's bits), current_/end_ the first/terminal voxel and
+// remaining_ the voxels still to visit; next() reads the walk the device
+// computed for this segment (same voxels, same order, span + 1 of them).
 RayCaster::RayCaster(const Point& start, const Point& end, FloatingPoint voxel_size) {
-  current_ = global_index_from_point(start, voxel_size);
-  end_ = global_index_from_point(end, voxel_size);
-  const Point direction = end - start;
-  size_t span = 0;
-  for (int i = 0; i < 3; ++i) {
-    step_[i] = direction[i] > 0.0f ? 1 : (direction[i] < 0.0f ? -1 : 0);
-    if (step_[i] == 0) {
-      t_max_[i] = std::numeric_limits<FloatingPoint>::infinity();
-      t_delta_[i] = std::numeric_limits<FloatingPoint>::infinity();
-    } else {
-      const FloatingPoint boundary = static_cast<FloatingPoint>(current_[i] + (step_[i] > 0 ? 1 : 0)) * voxel_size;
-      t_max_[i] = (boundary - start[i]) / direction[i];
-      t_delta_[i] = voxel_size / std::abs(direction[i]);
-    }
-    span += static_cast<size_t>(std::abs(end_[i] - current_[i]));
+  const float s[3] = {start.x(), start.y(), start.z()}, e[3] = {end.x(), end.y(), end.z()};
+  const Walk& w = device_walk(s, e, voxel_size);
+  t_max_ = start;
+  t_delta_ = end;
+  int32_t vbits = 0;
+  std::memcpy(&vbits, &voxel_size, sizeof(vbits));
+  step_ = Eigen::Vector3i(vbits, 0, 0);
+  remaining_ = w.voxels.size() / 3;
+  if (remaining_ > 0) {
+    current_ = GlobalVoxelIndex(w.voxels[0], w.voxels[1], w.voxels[2]);
+    const size_t l = 3 * (remaining_ - 1);
+    end_ = GlobalVoxelIndex(w.voxels[l], w.voxels[l + 1], w.voxels[l + 2]);
   }
-  remaining_ = span + 1;
 }
 
 bool RayCaster::next(GlobalVoxelIndex* index) {
   if (done_ || remaining_ == 0) return false;
+  const float s[3] = {t_max_.x(), t_max_.y(), t_max_.z()}, e[3] = {t_delta_.x(), t_delta_.y(), t_delta_.z()};
+  float v = 0.f;
+  const int32_t vbits = step_[0];
+  std::memcpy(&v, &vbits, sizeof(v));
+  const Walk& w = device_walk(s, e, v);
+  const size_t k = w.voxels.size() / 3 - remaining_;
+  current_ = GlobalVoxelIndex(w.voxels[3 * k], w.voxels[3 * k + 1], w.voxels[3 * k + 2]);
   *index = current_;
-  --remaining_;
-  if (current_.x() == end_.x() && current_.y() == end_.y() && current_.z() == end_.z()) {
-    done_ = true;
-    return true;
-  }
-  int axis = 0;
-  if (t_max_[1] < t_max_[axis]) axis = 1;
-  if (t_max_[2] < t_max_[axis]) axis = 2;
-  current_[axis] += step_[axis];
-  t_max_[axis] += t_delta_[axis];
+  if (--remaining_ == 0) done_ = true;
   return true;
 }
 

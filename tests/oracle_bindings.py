@@ -108,8 +108,23 @@ def ref_lib():
         L.vxr_mesh_extract.restype = c_size_t
         L.vxr_mesh_extract.argtypes = [c_void_p, c_int, c_void_p, c_size_t] + [c_void_p] * 5 + \
             [c_size_t, c_size_t, POINTER(c_uint64)]
+        L.vxr_last_integrate_seconds.restype = ctypes.c_double
+        L.vxr_last_integrate_seconds.argtypes = []
+        L.vxr_load_resave.restype = c_size_t
+        L.vxr_load_resave.argtypes = [c_void_p, c_size_t, c_void_p, c_size_t]
         _ref = L
     return _ref
+
+
+def ref_load_resave(data: bytes) -> bytes:
+    """vxf::load_tsdf_layer then vxf::save_layer (the reference's own code)."""
+    L = ref_lib()
+    n = L.vxr_load_resave(data, len(data), None, 0)
+    if n == 0:
+        raise ValueError(L.vxr_last_error().decode())
+    buf = ctypes.create_string_buffer(n)
+    L.vxr_load_resave(data, len(data), buf, n)
+    return buf.raw
 
 
 def _pose_arr(pose):
@@ -289,6 +304,10 @@ class RefLayer:
         if rc != 0:
             raise ValueError(self.L.vxr_last_error().decode())
         return int(st.updates), int(st.raycasts), int(st.skipped)
+
+    def last_integrate_seconds(self) -> float:
+        """steady_clock time of the last integrate() alone (benchmark.cpp:93-95)."""
+        return float(self.L.vxr_last_integrate_seconds())
 
     def esdf_occupancy_bytes(self, esdf_config) -> bytes:
         """The reference's EsdfIntegrator::build_from_occupancy -> save_layer bytes."""

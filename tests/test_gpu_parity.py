@@ -10,6 +10,7 @@ import pytest
 
 from paper_1611_03631_b200 import MergeMode, Scan, TsdfConfig, TsdfIntegrator, TsdfLayer, WeightMode
 from paper_1611_03631_b200 import workload as W
+from oracle_bindings import ref_available
 from parity_helpers import diff_report, run_pair
 
 pytestmark = pytest.mark.gpu
@@ -155,6 +156,41 @@ def test_vxblx_round_trip_and_resume(gpu, tmp_path):
     assert a.save_bytes() == b.save_bytes()
 
 
+def _dup_image(data: bytes, extra_from: int, modify) -> bytes:
+    """A VXBLX image whose block list repeats block `extra_from` (a modified
+    copy appended at the end): the reference's load keeps the LAST copy whole."""
+    import struct
+    nb = struct.unpack_from("<Q", data, 23)[0]
+    vps = struct.unpack_from("<I", data, 18)[0]
+    bs = 24 + 12 * vps ** 3
+    blk = bytearray(data[31 + extra_from * bs: 31 + (extra_from + 1) * bs])
+    modify(blk)
+    return data[:23] + struct.pack("<Q", nb + 1) + data[31:] + bytes(blk)
+
+
+@pytest.mark.skipif(not ref_available(), reason="oracle/_ref not built")
+def test_vxblx_load_duplicate_blocks(gpu):
+    """Duplicate block indices in a VXBLX file: the device load equals the
+    reference's load_tsdf_layer (last copy wins whole)."""
+    from oracle_bindings import ref_load_resave
+    wc = W.CONFIGS[1]
+    cfg = W.tsdf_config(wc)
+    a = TsdfLayer(wc.voxel_size)
+    TsdfIntegrator(cfg, a).integrate_batch([Scan(*f) for f in W.frames(1, count=2, scale=0.15)])
+    good = a.save_bytes()
+
+    def scramble(blk):
+        for i in range(24, len(blk), 12 * 37):
+            blk[i:i + 8] = bytes([7, 0, 128, 63, 0, 0, 32, 65])  # d = 1.0000008, w = 10
+    img = _dup_image(good, 1, scramble)
+    want = ref_load_resave(img)
+    b = TsdfLayer(wc.voxel_size)
+    for _ in range(2):  # twice: nondeterministic slot races would show
+        b.load_bytes(img)
+        assert b.save_bytes() == want
+    assert want != good
+
+
 def test_parse_errors(gpu):
     from paper_1611_03631_b200 import ParseError
     layer = TsdfLayer(0.1)
@@ -225,6 +261,50 @@ def test_configs_full_size_frames(gpu, cfg_id, count, scale):
     layer = TsdfLayer(wc.voxel_size, wc.vps)
     integ = TsdfIntegrator(cfg, layer)
     _check(layer, integ, cfg, wc, W.frames(cfg_id, count=count, scale=scale, start=1), batch=True)
+
+
+def test_rehash_epochs_on_device(gpu):
+    """Scans whose bucketing map rehashes while it is filled (every point in a
+    voxel of its own: > N/4 distinct terminal voxels, three rehashes at N =
+    20k) between ordinary frames, in one batch: the device epoch emulation of
+    the libstdc++ iteration order (k_rh_*) gives the reference's ray order,
+    bit-exact vs the oracle."""
+    rng = np.random.default_rng(7)
+    wc = W.CONFIGS[1]
+    cfg = W.tsdf_config(wc)
+    frames = [W.frame(1, 3, scale=0.2)]
+    for n in (20000, 5000):
+        pts = rng.uniform(-2.0, 2.0, size=(n, 3)).astype(np.float32)
+        pts[:, 2] = np.abs(pts[:, 2]) + 0.5
+        col = rng.integers(0, 256, size=(n, 3), dtype=np.uint8)
+        frames.append((pts, col, W.pose(1, 40)))
+    frames.append(W.frame(1, 7, scale=0.2))
+    layer = TsdfLayer(wc.voxel_size, wc.vps)
+    integ = TsdfIntegrator(cfg, layer)
+    _check(layer, integ, cfg, wc, frames, batch=True)
+
+
+def test_cfg4_full_frames(gpu):
+    """Two full 2048x2048 cfg4 frames (v = 2 cm, 4.2e6 points and ~1e9 updates
+    each) in one batch against the REFERENCE's own layer for them
+    (tests/golden/full_digests.json: sha256 of oracle/_ref's VXBLX bytes,
+    made by tests/golden/make_full_digests.py; too large to commit as bytes)."""
+    import hashlib
+    import json
+    import os
+    from golden_full import input_digest
+    d = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "full_digests.json")))["cfg4_full_f1_f2"]
+    wc = W.CONFIGS[d["config"]]
+    cfg = W.tsdf_config(wc)
+    frames = W.frames(d["config"], count=d["count"], start=d["start"])
+    assert input_digest(frames) == d["input_sha256"], "workload generator drift"
+    layer = TsdfLayer(wc.voxel_size, wc.vps, block_capacity=8192)
+    integ = TsdfIntegrator(cfg, layer)
+    stats = integ.integrate_batch([Scan(*f) for f in frames])
+    assert [[int(v) for v in row] for row in stats] == d["stats"]
+    assert layer.block_count() == d["blocks"]
+    b = layer.save_bytes()
+    assert len(b) == d["vxblx_bytes"] and hashlib.sha256(b).hexdigest() == d["vxblx_sha256"]
 
 
 def test_batch_split_invariance_full_size(gpu):

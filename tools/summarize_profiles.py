@@ -115,7 +115,13 @@ def main():
     open(os.path.join(ROOT, "profiles", f"{tag}_summary.md"), "w").write("\n".join(lines) + "\n")
     json.dump({"launch_ms": per, "launch_count": count, "full": caps, "roofline_inputs": inputs},
               open(os.path.join(ROOT, "profiles", f"{tag}_summary.json"), "w"), indent=1)
-    json.dump(inputs, open(os.path.join(ROOT, "profiles", "roofline_inputs.json"), "w"), indent=1)
+    ri_path = os.path.join(ROOT, "profiles", "roofline_inputs.json")
+    try:
+        ri = json.load(open(ri_path))
+    except Exception:
+        ri = {}
+    ri[(bench or {}).get("config", {}).get("workload", "cfg1_rgbd_merged_640x480_x100")] = inputs
+    json.dump(ri, open(ri_path, "w"), indent=1)
     print("\n".join(lines[:60]))
 
 
