@@ -228,6 +228,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=CPU_BUDGET_S)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-latency", action="store_true")
+    ap.add_argument("--sharded-nccl", action="store_true",
+                    help="run the sharded NCCL path even at N=1 (1-rank communicator, NCCL self send/recv)")
     ap.add_argument("--replicated", action="store_true",
                     help="N>1: replicated traversal (every rank walks all rays, no record exchange)")
     args = ap.parse_args()
@@ -280,6 +282,9 @@ def run_vxg_arm(args):
         obj = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         layer.shard_init(rank, world, obj[0], replicated=args.replicated)
+    elif args.sharded_nccl:
+        from paper_1611_03631_b200 import nccl_unique_id
+        layer.shard_init(0, 1, nccl_unique_id(), replicated=args.replicated)
     integ = TsdfIntegrator(cfg, layer)
 
     d_xyz = torch.from_numpy(xyz).cuda()
@@ -471,7 +476,8 @@ def run_vxg_arm(args):
             "parallelism": ((f"map sharded by block owner over {world} ranks, replicated traversal (no record "
                              f"exchange)" if args.replicated else
                              f"map sharded by block owner over {world} ranks, NCCL all-to-all of update records")
-                            if world > 1 else "1 GPU"),
+                            if world > 1 else ("1 GPU, sharded path over a 1-rank NCCL communicator"
+                                               if args.sharded_nccl else "1 GPU")),
             "work": {"points_per_step": P, "updates_per_step": n_upd, "frames_per_call": FC,
                      "records_per_step": n_rec, "n_vox_per_step": n_vox, "longest_fold_chain": info["max_chain"],
                      "blocks": info["blocks"], "sort_passes": passes},

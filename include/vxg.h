@@ -233,7 +233,9 @@ int vxg_drain_updated(vxg_handle* h, const char* name, int32_t* idx, uint64_t ca
 int vxg_nccl_unique_id(uint8_t* out);
 /* Makes h the shard `rank` of `world` (one process per GPU); world > 1 creates
  * an NCCL communicator from id_bytes. vxg_integrate_* then run sharded and
- * return the global per-frame counters on every rank. */
+ * return the global per-frame counters on every rank. world == 1 with a
+ * non-NULL id_bytes runs the same sharded path over a 1-rank communicator
+ * (NCCL self send/recv): the exchange on one GPU, for tests and bench. */
 int vxg_shard_init(vxg_handle* h, int rank, int world, const uint8_t* id_bytes);
 /* Sharding mode (SURVEY.md 8e fallback): on = replicated traversal — every
  * rank walks ALL rays and keeps only the records of the blocks it owns, so no

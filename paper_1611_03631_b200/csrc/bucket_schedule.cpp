@@ -47,15 +47,28 @@ Schedule probe(uint64_t n_points, uint64_t max_keys) {
 
 }  // namespace
 
+// Bucket count right after reserve(n_points / 4 + 1) on an empty map.
+uint64_t initial_buckets(uint64_t n_points) {
+  static std::map<uint64_t, uint64_t> memo;  // under g_mu
+  auto it = memo.find(n_points);
+  if (it != memo.end()) return it->second;
+  std::unordered_map<uint64_t, char> m;
+  m.reserve(n_points / 4 + 1);
+  return memo[n_points] = m.bucket_count();
+}
+
 // Schedule valid for any scan of n_points points with at most max_keys
-// distinct terminal voxels.
+// distinct terminal voxels. The growth after reserve depends only on the
+// bucket count reserve picked (the rehash policy's next-resize threshold is a
+// function of the bucket count), so the probe is cached per initial bucket
+// count: scans whose point counts differ (LiDAR) share it.
 Schedule bucket_schedule(uint64_t n_points, uint64_t max_keys) {
   std::lock_guard<std::mutex> lock(g_mu);
-  Cached& c = g_cache[n_points];
+  const uint64_t bc0 = initial_buckets(n_points);
+  Cached& c = g_cache[bc0];
   if (c.schedule.empty() || c.covered < max_keys) {
     uint64_t want = max_keys;
     if (c.covered > 0 && want < 2 * c.covered) want = 2 * c.covered;
-    if (want > n_points) want = n_points;
     if (want < max_keys) want = max_keys;
     c.schedule = probe(n_points, want);
     c.covered = want;

@@ -321,65 +321,111 @@ __global__ void k_order_keys(uint32_t S, const SegInfo* __restrict__ segs, const
   }
 }
 
-// ---- rehash epochs of one frame's bucketing map.
-// Inside a frame (segments segs[0..K)), rank = first-appearance rank of the
-// key. Epoch e (bucket count bc, keys of rank < t_hi present) re-inserts the
-// previous epoch's iteration order (positions 0..t_lo-1), then the keys of
-// rank [t_lo, t_hi) in first-appearance order; its iteration order sorts the
-// present keys by (first occupation of their bucket desc, position desc).
-__global__ void k_rh_pos_keys(uint32_t K, const SegInfo* __restrict__ segs, uint32_t* __restrict__ keys,
-                              uint32_t* __restrict__ vals) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < K; i += gridDim.x * blockDim.x) {
-    keys[i] = segs[i].pos;
+// ---- rehash epochs of the frames whose bucketing map rehashes (SURVEY.md
+// Appendix B), all such frames of a batch at once. The frames' segments are
+// concatenated (frame g owns [base, base + K)); every sort key carries g in its
+// high bits, so one stable sort orders every frame's segments independently.
+// Inside a frame, rank = first-appearance rank of the key. Epoch e (bucket
+// count bc, keys of rank < t_hi present) re-inserts the previous epoch's
+// iteration order (positions 0..t_lo-1), then the keys of rank [t_lo, t_hi) in
+// first-appearance order; its iteration order sorts the present keys by (first
+// occupation of their bucket desc, position desc). Frames with fewer epochs sit
+// out the later ones (active = 0: key 0, no writes).
+struct RhFrame {
+  uint32_t seg0;    // first segment of the frame in segs
+  uint32_t base;    // first index in the concatenated arrays
+  uint32_t K;       // segments (distinct terminal keys) of the frame
+  uint32_t ray0;    // first slot of the frame in the global ray order
+  uint32_t t_lo;    // keys re-inserted from the previous epoch's order
+  uint32_t t_hi;    // keys present in this epoch (clamped to K)
+  uint32_t active;  // this epoch exists for the frame
+  uint32_t last;    // this epoch is the frame's final one
+  uint64_t bc;      // bucket count
+  uint64_t fo_off;  // the frame's first-occupation table in fo
+};
+
+__global__ void k_rhb_init(uint32_t n, uint32_t G, const RhFrame* __restrict__ fr, const SegInfo* __restrict__ segs,
+                           int pb, uint32_t* __restrict__ rh_g, uint32_t* __restrict__ keys,
+                           uint32_t* __restrict__ vals) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    uint32_t lo = 0, hi = G;  // last frame with base <= i
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (fr[mid].base <= i) lo = mid; else hi = mid;
+    }
+    rh_g[i] = lo;
+    keys[i] = (lo << pb) | segs[fr[lo].seg0 + (i - fr[lo].base)].pos;
     vals[i] = i;
   }
 }
 
-__global__ void k_rh_rank(uint32_t K, const uint32_t* __restrict__ by_pos, uint32_t* __restrict__ rank) {
-  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < K; r += gridDim.x * blockDim.x) rank[by_pos[r]] = r;
+__global__ void k_rhb_rank(uint32_t n, const RhFrame* __restrict__ fr, const uint32_t* __restrict__ rh_g,
+                           const uint32_t* __restrict__ by_pos, uint32_t* __restrict__ rank) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const uint32_t i = by_pos[j];
+    rank[i] = j - fr[rh_g[i]].base;
+  }
 }
 
 __device__ __forceinline__ uint32_t rh_pos(uint32_t rank, const uint32_t* prev, uint32_t i, uint32_t t_lo) {
   return rank < t_lo ? prev[i] : rank;
 }
 
-__global__ void k_rh_fo(uint32_t K, const SegInfo* __restrict__ segs, const uint32_t* __restrict__ rank,
-                        const uint32_t* __restrict__ prev, uint32_t t_lo, uint64_t t_hi, uint64_t bc,
-                        uint32_t* __restrict__ fo) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < K; i += gridDim.x * blockDim.x) {
+__global__ void k_rhb_fo(uint32_t n, const RhFrame* __restrict__ fr, const uint32_t* __restrict__ rh_g,
+                         const SegInfo* __restrict__ segs, const uint32_t* __restrict__ rank,
+                         const uint32_t* __restrict__ prev, uint32_t* __restrict__ fo) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const RhFrame p = fr[rh_g[i]];
     const uint32_t r = rank[i];
-    if (r >= t_hi) continue;
-    atomicMin(&fo[segs[i].hash % bc], rh_pos(r, prev, i, t_lo));
+    if (!p.active || r >= p.t_hi) continue;
+    atomicMin(&fo[p.fo_off + segs[p.seg0 + (i - p.base)].hash % p.bc], rh_pos(r, prev, i, p.t_lo));
   }
 }
 
 // pass 1 key (secondary): position, descending
-__global__ void k_rh_pos_desc(uint32_t K, const uint32_t* __restrict__ rank, const uint32_t* __restrict__ prev,
-                              uint32_t t_lo, uint32_t M, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < K; i += gridDim.x * blockDim.x) {
-    keys[i] = M - rh_pos(rank[i], prev, i, t_lo);
+__global__ void k_rhb_pos_desc(uint32_t n, const RhFrame* __restrict__ fr, const uint32_t* __restrict__ rh_g,
+                               const uint32_t* __restrict__ rank, const uint32_t* __restrict__ prev, int kb,
+                               uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  const uint32_t M = (1u << kb) - 1u;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t g = rh_g[i];
+    const RhFrame& p = fr[g];
+    keys[i] = (g << (kb + 1)) | (p.active ? M - rh_pos(rank[i], prev, i, p.t_lo) : 0u);
     vals[i] = i;
   }
 }
 
 // pass 2 key (primary, stable over pass 1): first occupation of the bucket,
 // descending; keys not yet present last
-__global__ void k_rh_fo_desc(uint32_t K, const uint32_t* __restrict__ vals, const SegInfo* __restrict__ segs,
-                             const uint32_t* __restrict__ rank, uint64_t t_hi, uint64_t bc,
-                             const uint32_t* __restrict__ fo, uint32_t M, uint32_t* __restrict__ keys) {
-  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < K; j += gridDim.x * blockDim.x) {
+__global__ void k_rhb_fo_desc(uint32_t n, const RhFrame* __restrict__ fr, const uint32_t* __restrict__ rh_g,
+                              const uint32_t* __restrict__ vals, const SegInfo* __restrict__ segs,
+                              const uint32_t* __restrict__ rank, const uint32_t* __restrict__ fo, int kb,
+                              uint32_t* __restrict__ keys) {
+  const uint32_t M = (1u << kb) - 1u;
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     const uint32_t i = vals[j];
-    keys[j] = rank[i] < t_hi ? M - fo[segs[i].hash % bc] : M + 1u;
+    const uint32_t g = rh_g[i];
+    const RhFrame p = fr[g];
+    uint32_t k = 0u;
+    if (p.active)
+      k = rank[i] < p.t_hi ? M - fo[p.fo_off + segs[p.seg0 + (i - p.base)].hash % p.bc] : M + 1u;
+    keys[j] = (g << (kb + 1)) | k;
   }
 }
 
-// prev[order[j]] = j for the m present keys; on the last epoch also the
-// frame's slice of the global ray order
-__global__ void k_rh_commit(uint32_t m, const uint32_t* __restrict__ order, uint32_t* __restrict__ prev,
-                            uint32_t seg0, uint32_t* __restrict__ ray_order) {
-  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
-    prev[order[j]] = j;
-    if (ray_order != nullptr) ray_order[j] = seg0 + order[j];
+// prev[order[j]] = local position for the present keys; on a frame's last
+// epoch also its slice of the global ray order
+__global__ void k_rhb_commit(uint32_t n, const RhFrame* __restrict__ fr, const uint32_t* __restrict__ rh_g,
+                             const uint32_t* __restrict__ order, uint32_t* __restrict__ prev,
+                             uint32_t* __restrict__ ray_order) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const uint32_t i = order[j];
+    const RhFrame p = fr[rh_g[i]];
+    if (!p.active) continue;
+    const uint32_t jl = j - p.base;
+    if (jl >= p.t_hi) continue;  // t_hi <= K
+    prev[i] = jl;
+    if (p.last) ray_order[p.ray0 + jl] = p.seg0 + (i - p.base);
   }
 }
 

@@ -228,7 +228,8 @@ struct vxg_handle {
   DBuf<RayInfo> rays;
   DBuf<unsigned long long> rcount, roff, rcount2;
   DBuf<uint32_t> ray_perm, ray_iota;
-  DBuf<uint32_t> rh_k0, rh_k1, rh_v0, rh_v1, rh_rank, rh_prev;  // rehash epochs (order_rehash_frame)
+  DBuf<uint32_t> rh_k0, rh_k1, rh_v0, rh_v1, rh_rank, rh_prev, rh_g;  // rehash epochs (order_rehash_frames)
+  DBuf<RhFrame> rh_frames;
   DBuf<uint64_t> tbl_off, bcs;
   DBuf<uint32_t> rkeys, rkeys2, rvals, rvals2;
   DBuf<uint32_t> run_keys, run_len, run_start, run_len2, run_order, run_iota, work;
@@ -553,7 +554,8 @@ struct vxg_handle {
   }
   // Folds may outlive the call only on a plain single-GPU handle without
   // updated-block consumers (the fold marks the touched blocks they drain).
-  bool fold_may_outlive_call() const { return async_fold && consumers.empty() && shard_world <= 1 && !debug_fold; }
+  bool sharded() const { return shard_world > 1 || nccl_comm != nullptr; }
+  bool fold_may_outlive_call() const { return async_fold && consumers.empty() && !sharded() && !debug_fold; }
   uint64_t reset_used = 0;  // blocks in use when vxg_reset was called (deferred)
   // After a host sync of st that followed join_folds(): longest runs of the batch.
   void drain_tops() {
@@ -618,8 +620,9 @@ struct vxg_handle {
   void build_rays_simple(const float* dxyz, const uint8_t* drgb, uint64_t P, uint32_t F, uint32_t* R_out);
   void build_rays_grouped(const float* dxyz, const uint8_t* drgb, uint64_t P, const uint64_t* h_off, uint32_t F,
                           uint32_t* R_out, TermView* tv);
-  void order_rehash_frame(uint32_t f, uint32_t K, uint32_t seg0, uint64_t n_points, const Schedule& sch,
-                          uint32_t ray0, int pb);
+  void order_rehash_frames(const std::vector<uint32_t>& frames, const std::vector<uint32_t>& K,
+                           const std::vector<uint32_t>& start, const std::vector<Schedule>& sched,
+                           const std::vector<uint32_t>& ray0, int pb);
   void emit_and_apply(uint32_t R, uint32_t F, const TermView& tv);
   uint64_t count_rays(uint32_t R, uint32_t F);
   void sort_fold(uint64_t T, uint64_t nslots, uint32_t F);
@@ -679,53 +682,100 @@ void vxg_handle::build_rays_simple(const float* dxyz, const uint8_t* drgb, uint6
   *R_out = R;
 }
 
-// Reorders frame f's K buckets when its map rehashes while they are inserted
-// (SURVEY.md Appendix B), on the device: epoch e re-inserts the previous
-// iteration order, then appends the next keys by first appearance, under
-// bucket count bc_e (k_rh_*). Each epoch's order is two stable 32-bit sorts
-// (position desc, then first bucket occupation desc). No host round trip.
-void vxg_handle::order_rehash_frame(uint32_t f, uint32_t K, uint32_t seg0, uint64_t n_points, const Schedule& sch,
-                                    uint32_t ray0, int pb) {
-  (void)f;
-  (void)n_points;
-  (void)pb;
-  const SegInfo* fs = segs.p + seg0;
-  uint32_t* k0 = rh_k0.ensure(K);
-  uint32_t* k1 = rh_k1.ensure(K);
-  uint32_t* v0 = rh_v0.ensure(K);
-  uint32_t* v1 = rh_v1.ensure(K);
-  uint32_t* rank = rh_rank.ensure(K);
-  uint32_t* prev = rh_prev.ensure(K);
-  const int kb = bits_for(K);  // positions < K <= 2^kb - 1
-  const uint32_t M = (1u << kb) - 1u;
-  uint32_t *sk = nullptr, *sv = nullptr;
-  // rank = first-appearance rank inside the frame
-  k_rh_pos_keys<<<grid_for(K), 256, 0, st>>>(K, fs, k0, v0);
-  lsd_sort<8, 12, 4>(K, pb, k0, v0, k1, v1, &sk, &sv, false);
-  k_rh_rank<<<grid_for(K), 256, 0, st>>>(K, sv, rank);
-  launches += 2;
-  for (size_t e = 0; e < sch.size(); ++e) {
-    const uint64_t t_lo = sch[e].first;
-    const uint64_t t_hi = e + 1 < sch.size() ? sch[e + 1].first : UINT64_MAX;
-    if (t_lo >= K && e > 0) break;
-    const bool last = t_hi >= K;
-    const uint64_t bc = sch[e].second;
-    fo.ensure(bc);
-    CU(cudaMemsetAsync(fo.p, 0xFF, bc * sizeof(uint32_t), st));
-    const uint32_t tl = static_cast<uint32_t>(t_lo);
-    k_rh_fo<<<grid_for(K), 256, 0, st>>>(K, fs, rank, prev, tl, t_hi, bc, fo.p);
-    k_rh_pos_desc<<<grid_for(K), 256, 0, st>>>(K, rank, prev, tl, M, k0, v0);
-    lsd_sort<8, 12, 4>(K, kb, k0, v0, k1, v1, &sk, &sv, false);
-    uint32_t* kf = sk == k0 ? k1 : k0;  // free key buffer
-    uint32_t* vf = sv == v0 ? v1 : v0;  // free value buffer
-    k_rh_fo_desc<<<grid_for(K), 256, 0, st>>>(K, sv, fs, rank, t_hi, bc, fo.p, M, kf);
-    uint32_t *sk2 = nullptr, *sv2 = nullptr;
-    lsd_sort<8, 12, 4>(K, kb + 1, kf, sv, sk, vf, &sk2, &sv2, false);
-    const uint32_t m = static_cast<uint32_t>(std::min<uint64_t>(K, t_hi));
-    k_rh_commit<<<grid_for(m), 256, 0, st>>>(m, sv2, prev, seg0, last ? ovals.p + ray0 : nullptr);
-    launches += 4;
-    CU(cudaGetLastError());
-    if (last) break;
+// Reorders the buckets of every frame whose map rehashes while they are
+// inserted, on the device and for all such frames at
+// once: epoch e re-inserts the previous iteration order, then appends the next
+// keys by first appearance, under bucket count bc_e (k_rhb_*). Each epoch
+// level is two stable 32-bit sorts over the concatenated frames (frame in the
+// high key bits; position desc, then first bucket occupation desc), so the
+// launch count grows with the epoch count, not with the frame count. Frames
+// are processed in groups whose index fits the key.
+void vxg_handle::order_rehash_frames(const std::vector<uint32_t>& frames, const std::vector<uint32_t>& K,
+                                     const std::vector<uint32_t>& start, const std::vector<Schedule>& sched,
+                                     const std::vector<uint32_t>& ray0, int pb) {
+  uint32_t maxK = 1;
+  for (uint32_t f : frames) maxK = std::max(maxK, K[f]);
+  const int kb = bits_for(maxK);  // positions < K <= 2^kb - 1
+  const int key_bits = std::max(pb, kb + 1);
+  if (key_bits >= 32) throw VxgError(VXG_EINVAL, "scan too large for the rehash ray-order key");
+  const size_t group = size_t(1) << std::min(16, 32 - key_bits);  // frames per group: g < 2^(32 - key_bits)
+  for (size_t g0 = 0; g0 < frames.size(); g0 += group) {
+    const size_t G = std::min(group, frames.size() - g0);
+    const int gb = bits_for(G - 1);
+    // epochs per frame and the per-(epoch, frame) parameters
+    std::vector<uint32_t> n_ep(G);
+    uint32_t E = 0, n = 0;
+    for (size_t g = 0; g < G; ++g) {
+      const uint32_t f = frames[g0 + g];
+      const Schedule& sch = sched[f];
+      uint32_t e = 0;
+      while (e < sch.size()) {
+        if (e > 0 && sch[e].first >= K[f]) break;
+        ++e;
+        const uint64_t t_hi = e < sch.size() ? sch[e].first : UINT64_MAX;
+        if (t_hi >= K[f]) break;
+      }
+      n_ep[g] = e;
+      E = std::max(E, e);
+      n += K[f];
+    }
+    std::vector<RhFrame> P(static_cast<size_t>(E) * G);
+    std::vector<uint64_t> fo_total(E, 0);
+    uint32_t base = 0;
+    for (size_t g = 0; g < G; ++g) {
+      const uint32_t f = frames[g0 + g];
+      const Schedule& sch = sched[f];
+      for (uint32_t e = 0; e < E; ++e) {
+        RhFrame& q = P[e * G + g];
+        q = RhFrame{};
+        q.seg0 = start[f];
+        q.base = base;
+        q.K = K[f];
+        q.ray0 = ray0[f];
+        if (e < n_ep[g]) {
+          const uint64_t t_hi = e + 1 < sch.size() ? sch[e + 1].first : UINT64_MAX;
+          q.t_lo = static_cast<uint32_t>(sch[e].first);
+          q.t_hi = static_cast<uint32_t>(std::min<uint64_t>(t_hi, K[f]));
+          q.active = 1u;
+          q.last = e + 1 == n_ep[g] ? 1u : 0u;
+          q.bc = sch[e].second;
+          q.fo_off = fo_total[e];
+          fo_total[e] += q.bc;
+        }
+      }
+      base += K[f];
+    }
+    RhFrame* dP = rh_frames.ensure(P.size());
+    CU(cudaMemcpyAsync(dP, P.data(), P.size() * sizeof(RhFrame), cudaMemcpyHostToDevice, st));
+    uint32_t* k0 = rh_k0.ensure(n);
+    uint32_t* k1 = rh_k1.ensure(n);
+    uint32_t* v0 = rh_v0.ensure(n);
+    uint32_t* v1 = rh_v1.ensure(n);
+    uint32_t* rank = rh_rank.ensure(n);
+    uint32_t* prev = rh_prev.ensure(n);
+    uint32_t* rg = rh_g.ensure(n);
+    uint32_t *sk = nullptr, *sv = nullptr;
+    // rank = first-appearance rank inside the frame
+    k_rhb_init<<<grid_for(n), 256, 0, st>>>(n, static_cast<uint32_t>(G), dP, segs.p, pb, rg, k0, v0);
+    lsd_sort<8, 12, 4>(n, gb + pb, k0, v0, k1, v1, &sk, &sv, false);
+    k_rhb_rank<<<grid_for(n), 256, 0, st>>>(n, dP, rg, sv, rank);
+    launches += 2;
+    for (uint32_t e = 0; e < E; ++e) {
+      const RhFrame* dPe = dP + static_cast<size_t>(e) * G;
+      fo.ensure(std::max<uint64_t>(fo_total[e], 1));
+      CU(cudaMemsetAsync(fo.p, 0xFF, fo_total[e] * sizeof(uint32_t), st));
+      k_rhb_fo<<<grid_for(n), 256, 0, st>>>(n, dPe, rg, segs.p, rank, prev, fo.p);
+      k_rhb_pos_desc<<<grid_for(n), 256, 0, st>>>(n, dPe, rg, rank, prev, kb, k0, v0);
+      lsd_sort<8, 12, 4>(n, gb + kb + 1, k0, v0, k1, v1, &sk, &sv, false);
+      uint32_t* kf = sk == k0 ? k1 : k0;  // free key buffer
+      uint32_t* vf = sv == v0 ? v1 : v0;  // free value buffer
+      k_rhb_fo_desc<<<grid_for(n), 256, 0, st>>>(n, dPe, rg, sv, segs.p, rank, fo.p, kb, kf);
+      uint32_t *sk2 = nullptr, *sv2 = nullptr;
+      lsd_sort<8, 12, 4>(n, gb + kb + 1, kf, sv, sk, vf, &sk2, &sv2, false);
+      k_rhb_commit<<<grid_for(n), 256, 0, st>>>(n, dPe, rg, sv2, prev, ovals.p);
+      launches += 4;
+      CU(cudaGetLastError());
+    }
   }
 }
 
@@ -855,11 +905,10 @@ void vxg_handle::build_rays_grouped(const float* dxyz, const uint8_t* drgb, uint
   }, 2 + (obits + 7) / 8);
   std::swap(ovals.p, ovals2.p);
   std::swap(ovals.cap, ovals2.cap);
-  for (uint32_t f = 0; f < F; ++f) {
-    if (sched[f].size() > 1 && K[f] > sched[f][1].first) {
-      order_rehash_frame(f, K[f], start[f], h_off[f + 1] - h_off[f], sched[f], ray0[f], pb);
-    }
-  }
+  std::vector<uint32_t> rehashing;
+  for (uint32_t f = 0; f < F; ++f)
+    if (sched[f].size() > 1 && K[f] > sched[f][1].first) rehashing.push_back(f);
+  if (!rehashing.empty()) order_rehash_frames(rehashing, K, start, sched, ray0, pb);
   rays.ensure(std::max<uint32_t>(R, 1));
   k_gather_rays<<<grid_for(R), 256, 0, st>>>(R, ovals.p, segs.p, rays.p);
   ++launches;
@@ -1405,7 +1454,7 @@ void vxg_handle::run_sub(const float* xyz, const uint8_t* rgb, const uint64_t* o
   uint32_t R = 0;
   TermView tv;
   begin_batch(xyz, rgb, offsets, poses, F, &R, &tv);
-  if (shard_world > 1) {
+  if (sharded()) {
     if (nccl_comm == nullptr) throw VxgError(VXG_EINVAL, "sharded handle without a communicator (vxg_shard_init)");
     settle();
     shard_front(R, static_cast<uint32_t>(F), tv);
@@ -2780,7 +2829,7 @@ int vxg_shard_init(vxg_handle* h, int rank, int world, const uint8_t* id_bytes) 
     if (world < 1 || rank < 0 || rank >= world) throw VxgError(VXG_EINVAL, "invalid shard rank / world");
     set_device(h);
     h->settle();
-    if (world > 1) {
+    if (world > 1 || id_bytes != nullptr) {  // world 1 with an id: the NCCL path over a 1-rank communicator
       ncclUniqueId id;
       std::memcpy(id.internal, id_bytes, NCCL_UNIQUE_ID_BYTES);
       ncclComm_t comm;

@@ -271,8 +271,11 @@ class TsdfLayer:
         """Makes this layer shard `rank` of `world` (one process per GPU, NCCL
         all-to-all of update records between shards).
         replicated=True: every rank walks all rays and keeps its own blocks'
-        records (no record exchange)."""
-        buf = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id.ljust(128, b"\0")[:128])
+        records (no record exchange). world=1 with an id runs the sharded path
+        through a 1-rank NCCL communicator (self send/recv)."""
+        if nccl_id:
+            _nccl_preload()
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id.ljust(128, b"\0")[:128]) if nccl_id else None
         check(lib().vxg_shard_init(self._h, int(rank), int(world), buf))
         check(lib().vxg_shard_set_replicated(self._h, 1 if replicated else 0))
 
@@ -607,8 +610,20 @@ def save_ply_mesh(mesh: "Mesh", path: str) -> None:
     _check_io(lib().vxg_save_ply_mesh(path.encode(), v.ctypes.data, nr.ctypes.data,
                                       None if c is None else c.ctypes.data, len(v), t.ctypes.data, len(t)))
 
+def _nccl_preload() -> None:
+    """libvxg dlopens libnccl.so.2 by soname. Import torch first when it is
+    installed, so that the soname resolves to torch's bundled NCCL (the one
+    torch.distributed uses) instead of pinning an older system copy that
+    libtorch_cuda could not load against afterwards."""
+    try:
+        import torch  # noqa: F401
+    except ImportError:
+        pass
+
+
 def nccl_unique_id() -> bytes:
     """128-byte NCCL unique id for vxg_shard_init (rank 0 makes it, the caller broadcasts it)."""
+    _nccl_preload()
     buf = (ctypes.c_uint8 * 128)()
     check(lib().vxg_nccl_unique_id(buf))
     return bytes(buf)

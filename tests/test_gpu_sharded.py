@@ -74,3 +74,29 @@ def test_replicated_traversal_equals_oracle(gpu, world, cfg_id):
     got, exp = g.save_bytes(), ora.save_bytes()
     assert got == exp, diff_report(got, exp)
     assert sum(1 for c in g.shard_block_counts() if c > 0) > 1
+
+
+@pytest.mark.parametrize("cfg_id", [1, 3])
+def test_nccl_one_rank_exchange(gpu, cfg_id):
+    """The real NCCL path (ncclSend/ncclRecv of the counts and records in a
+    group, ncclAllReduce of the per-frame counters, vxg_tsdf.cu nccl_exchange /
+    nccl_reduce_updates) over a 1-rank communicator: one GPU exchanges with
+    itself, so the same protocol a multi-GPU run uses executes on hardware.
+    The layer equals the single-GPU one and the oracle."""
+    from paper_1611_03631_b200 import nccl_unique_id
+    wc = W.CONFIGS[cfg_id]
+    cfg = W.tsdf_config(wc)
+    frames = W.frames(cfg_id, count=3, scale=0.3, start=5)
+    ora = OracleLayer(cfg, wc.voxel_size, wc.vps)
+    o_stats = [list(ora.integrate(*f)) for f in frames]
+    layer = TsdfLayer(wc.voxel_size, wc.vps)
+    layer.shard_init(0, 1, nccl_unique_id())
+    integ = TsdfIntegrator(cfg, layer)
+    stats = [[int(v) for v in r] for r in integ.integrate_batch([Scan(*f) for f in frames])]
+    assert stats == o_stats
+    # a second call through the same communicator, frame by frame
+    for f in W.frames(cfg_id, count=2, scale=0.3, start=9):
+        o = list(ora.integrate(*f))
+        assert [integ.integrate(Scan(*f)), integ.raycasts_last_scan(), integ.skipped_points_last_scan()] == o
+    got, exp = layer.save_bytes(), ora.save_bytes()
+    assert got == exp, diff_report(got, exp)
