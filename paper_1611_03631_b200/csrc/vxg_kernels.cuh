@@ -48,6 +48,15 @@ struct alignas(32) FoldRay {
   float pad;
 };
 
+// Record values: the ray index, with kFarRecord set when the emit proved the
+// voxel centre more than truncation + v in front of the point along the ray
+// (d >= truncation in the reference's rounded arithmetic): clamp(d) is then
+// exactly +truncation and w the ray's w_front = mweight_base(d > -eps) *
+// weight, so the fold reads only the ray's 8-byte FarRay {w_front, colour}
+// (4 per sector, a quarter of the FoldRay table) instead of its FoldRay.
+constexpr uint32_t kFarRecord = 0x80000000u;
+constexpr uint32_t kRayMask = 0x7fffffffu;
+
 struct alignas(16) Record {
   float d;
   float w;
@@ -477,7 +486,8 @@ __device__ __forceinline__ float mweight_base(int mode, float base, float d, flo
 // the ray's depth and hoisted 1/depth^2.
 __global__ void k_ray_count(uint32_t R, RayInfo* __restrict__ rays, const float* __restrict__ poses,
                             TsdfParams tp, unsigned long long* __restrict__ counts,
-                            unsigned long long* __restrict__ raycasts, FoldRay* __restrict__ fray) {
+                            unsigned long long* __restrict__ raycasts, FoldRay* __restrict__ fray,
+                            uint2* __restrict__ far) {
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < R; j += gridDim.x * blockDim.x) {
     const RayInfo r = rays[j];
     uint64_t c = 0;
@@ -499,6 +509,9 @@ __global__ void k_ray_count(uint32_t R, RayInfo* __restrict__ rays, const float*
       fr.base = base;
       fr.pad = depth;
       fray[j] = fr;
+      far[j] = make_uint2(
+          __float_as_uint(fmul(mweight_base(tp.weight_mode, base, 0.0f, tp.truncation, tp.dropoff_epsilon), r.weight)),
+          r.color);
       if (!(depth <= 0.0f)) {
         cast = 1u;
         const float s = fdiv(tp.truncation, depth);
@@ -653,7 +666,7 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(uint32_t R0, uint32_t R1,
     const float depth = r.depth;
     uint32_t valid = 0, count = 0, out0 = 0;
     const bool live = has && r.valid == 1u && !(depth <= 0.0f);
-    float ray0 = 0.0f, ray1 = 0.0f, ray2 = 0.0f, w_front = 0.0f, t_safe = -1.0f;
+    float ray0 = 0.0f, ray1 = 0.0f, ray2 = 0.0f, w_front = 0.0f, t_safe = -1.0f, t_far = -1.0f;
     Walk wk{};
     if (live) {
       ray0 = fsub(r.p[0], o0), ray1 = fsub(r.p[1], o1), ray2 = fsub(r.p[2], o2);
@@ -672,6 +685,10 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(uint32_t R0, uint32_t R1,
       // voxel for the DDA's rounded axis choices), where the reference's
       // rounded `along` cannot be negative, so d >= 0 and w = w_front
       t_safe = (depth - 3.0f * v) / (fadd(depth, tp.truncation) + v);
+      // likewise a voxel left before t_far has its centre more than
+      // truncation + 1.1 v before the point: d >= truncation (kFarRecord).
+      // t_exit grows along the walk, so the far records are a prefix of the ray's.
+      t_far = (depth - tp.truncation - 3.0f * v) / (fadd(depth, tp.truncation) + v);
       // record offsets inside one chunk are 32-bit (chunks stay below 2^29 records)
       out0 = static_cast<uint32_t>(roff[j] - base);
     }
@@ -694,8 +711,10 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(uint32_t R0, uint32_t R1,
     int32_t cslot = -1;
     const uint32_t maxc = __reduce_max_sync(0xffffffffu, count);
     __syncwarp();  // kmeta visible to the warp
+    uint32_t nfar = 0;  // leading records of this ray proven far (kFarRecord)
     for (uint32_t k = 0; k < maxc; ++k) {
       if (k < count) {
+        nfar += fminf(fminf(wk.m0, wk.m1), wk.m2) < t_far ? 1u : 0u;
         uint32_t key = kInvalidRecord;
         bool skip = false;
         if (kAnti) {
@@ -770,6 +789,7 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(uint32_t R0, uint32_t R1,
         }
       }
       if ((k & 31u) == 31u || k + 1u == maxc) {  // warp-uniform: write the staged rows
+        kmeta[wib][lane].w = nfar;  // far records are a prefix: those below nfar so far
         __syncwarp();
         const uint32_t k0 = k & ~31u, nrow = (k & 31u) + 1u;
         for (uint32_t l = 0; l < 32u; ++l) {
@@ -779,7 +799,7 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(uint32_t R0, uint32_t R1,
             if (lane < m) {
               const uint32_t o = ml.y + k0 + lane;
               rkeys[o] = wrows[l * 33u + lane];
-              rvals[o] = ml.z;  // the ray index is every record's sort value
+              rvals[o] = ml.z | (k0 + lane < ml.w ? kFarRecord : 0u);  // ray index (+ far flag): the sort value
             }
           }
         }
@@ -1035,6 +1055,52 @@ __device__ __forceinline__ Upd weigh(const FoldRay& ry, const float* org, float 
   return u;
 }
 
+// A record's ray for the fold: far records (kFarRecord) read only the
+// FarRay (no FoldRay load); the weighing then runs branch-free on a zero ray
+// and weigh_far selects the far values, so a warp whose lanes mix far and near
+// records does not diverge.
+struct FoldIn {
+  FoldRay ry;
+  uint2 fr;  // {w_front bits, colour}; .x = 0xFFFFFFFF marks a near record
+};
+__device__ __forceinline__ FoldIn load_fold_in(const FoldRay* __restrict__ rays, const uint2* __restrict__ far,
+                                               uint32_t v) {
+  FoldIn in;
+  const uint32_t r = v & kRayMask;
+  if (v & kFarRecord) {
+    in.ry = FoldRay{};
+    in.fr = far[r];
+  } else {
+    in.ry = rays[r];
+    in.fr = make_uint2(0xFFFFFFFFu, 0u);
+  }
+  return in;
+}
+__device__ __forceinline__ Upd weigh_in(const FoldIn& in, const float* org, float x0, float x1, float x2,
+                                        const TsdfParams& tp) {
+  Upd u = weigh(in.ry, org, x0, x1, x2, tp);
+  const bool far = in.fr.x != 0xFFFFFFFFu;
+  u.d = far ? tp.truncation : u.d;
+  u.w = far ? __uint_as_float(in.fr.x) : u.w;
+  u.c = far ? in.fr.y : u.c;
+  return u;
+}
+// Warp-cooperative form (every lane weighs its own record, all lanes call):
+// when no lane holds a near record the projective distance is skipped.
+__device__ __forceinline__ Upd weigh_in_warp(const FoldIn& in, bool live, const float* org, float x0, float x1,
+                                             float x2, const TsdfParams& tp) {
+  const bool far = in.fr.x != 0xFFFFFFFFu;
+  if (__all_sync(0xffffffffu, far || !live)) {
+    Upd u;
+    u.d = tp.truncation;
+    u.w = __uint_as_float(in.fr.x);
+    u.c = in.fr.y;
+    u.pad = 0u;
+    return u;
+  }
+  return weigh_in(in, org, x0, x1, x2, tp);
+}
+
 constexpr uint32_t kOrgCache = 1024;  // frames whose origins fit the fold kernels' smem table
 
 __global__ void k_origins(uint32_t F, const float* __restrict__ poses, float* __restrict__ org) {
@@ -1229,7 +1295,7 @@ template <int kP, bool kSep>
 __device__ __forceinline__ void fold_long_pairs(
     LongSmem<kP>& S, const int wid, const float* poses, const uint32_t nruns, const uint32_t n_long,
     const uint32_t* __restrict__ order, const uint32_t* __restrict__ ukeys, const uint32_t* __restrict__ ustart,
-    const uint32_t* __restrict__ ulen, const uint32_t* __restrict__ svals, const FoldRay* __restrict__ rays,
+    const uint32_t* __restrict__ ulen, const uint32_t* __restrict__ svals, const FoldRay* __restrict__ rays, const uint2* __restrict__ far,
     const MapView& map, const TsdfParams& tp, uint8_t* __restrict__ touched, uint32_t* __restrict__ work,
     unsigned long long* __restrict__ dbg) {
   auto& ring = S.ring;
@@ -1266,15 +1332,13 @@ __device__ __forceinline__ void fold_long_pairs(
         float W = vp->weight;
         // pipeline (gather latency ~ a whole chunk of the consumer's chain):
         // rays three chunks ahead, their ids five chunks ahead
-        const FoldRay zr{};
+        const FoldIn zr{FoldRay{}, make_uint2(0xFFFFFFFFu, 0u)};
         const uint32_t* ids = svals + c.start;
         auto id_at = [&](uint32_t jj) { return jj < c.len ? ids[jj] : 0u; };
-        auto ray_at = [&](uint32_t jj, uint32_t v) { return jj < c.len ? rays[v] : zr; };
-        auto weigh_at = [&](uint32_t jj, const FoldRay& r) {
-          Upd x;
-          if (jj < c.len) {
-            x = weigh(r, poses, c.x0, c.x1, c.x2, tp);
-          } else {
+        auto ray_at = [&](uint32_t jj, uint32_t v) { return jj < c.len ? load_fold_in(rays, far, v) : zr; };
+        auto weigh_at = [&](uint32_t jj, const FoldIn& r) {
+          Upd x = weigh_in_warp(r, jj < c.len, poses, c.x0, c.x1, c.x2, tp);
+          if (jj >= c.len) {
             x.d = 0.0f;
             x.w = 0.0f;
             x.c = 0u;
@@ -1282,14 +1346,14 @@ __device__ __forceinline__ void fold_long_pairs(
           }
           return x;
         };
-        FoldRay ry1 = ray_at(32 + lane, id_at(32 + lane));
-        FoldRay ry2 = ray_at(64 + lane, id_at(64 + lane));
+        FoldIn ry1 = ray_at(32 + lane, id_at(32 + lane));
+        FoldIn ry2 = ray_at(64 + lane, id_at(64 + lane));
         uint32_t v3 = id_at(96 + lane), v4 = id_at(128 + lane);
         // records are weighed one chunk ahead of their hand-over
         Upd u_next = weigh_at(lane, ray_at(lane, id_at(lane)));
         for (uint32_t k = 0; k < nchunks; ++k, ++kk) {
           const uint32_t j = k * 32 + lane;
-          const FoldRay ry3 = ray_at(j + 96, v3);
+          const FoldIn ry3 = ray_at(j + 96, v3);
           v3 = v4;
           v4 = id_at(j + 160);
           const uint32_t cnt = min(32u, c.len - k * 32);
@@ -1423,7 +1487,9 @@ __device__ __forceinline__ void fold_long_pairs(
           bool done = false;
           if (stationary) {  // distance chain only: FMUL, FADD, 3-FMA quotient per step
             float D = st.D;
-            QuotRange qr;  // range checks accumulate off the chain (no predicate chain)
+            // range of |a| off the chain (two FMNMX per step): every a in
+            // [2^-60, 2^60] is quot_ok; a = +-0 fails conservatively (exact re-run)
+            float amin = 0x1p100f, amax = 0.0f;
             const float4* rq = reinterpret_cast<const float4*>(rb);
             constexpr int kStride = sizeof(PreRec) / sizeof(float4);
             if (cnt == 32) {
@@ -1436,18 +1502,20 @@ __device__ __forceinline__ void fold_long_pairs(
                 const float4 x = buf[u % kAhead];
                 if (u + kAhead < 32) buf[u % kAhead] = rq[(u + kAhead) * kStride];
                 const float a = __fadd_rn(__fmul_rn(x.x, D), x.w);
-                qr_add(qr, a);
+                amin = fminf(amin, fabsf(a));
+                amax = fmaxf(amax, fabsf(a));
                 D = fast_quot0(a, Recip{x.y, x.z, true});
               }
             } else {
               for (uint32_t u = 0; u < cnt; ++u) {
                 const float4 x = rq[u * kStride];
                 const float a = __fadd_rn(__fmul_rn(x.x, D), x.w);
-                qr_add(qr, a);
+                amin = fminf(amin, fabsf(a));
+                amax = fmaxf(amax, fabsf(a));
                 D = fast_quot0(a, Recip{x.y, x.z, true});
               }
             }
-            if (qr_ok(qr)) {
+            if (amin >= 0x1p-60f && amax <= 0x1p60f && D == D) {  // (FMNMX drops NaN: test D itself)
               st.D = D;
               st.W = W_end;
               done = true;
@@ -1534,7 +1602,7 @@ template <int kP, bool kSep, bool kSmemOrg>
 __global__ void __launch_bounds__(64 * kP, 1) k_fold_runs(
     const uint32_t* __restrict__ num_runs_p, const uint32_t* __restrict__ order,
     const uint32_t* __restrict__ sorted_len, const uint32_t* __restrict__ ukeys, const uint32_t* __restrict__ ustart,
-    const uint32_t* __restrict__ ulen, const uint32_t* __restrict__ svals, const FoldRay* __restrict__ rays,
+    const uint32_t* __restrict__ ulen, const uint32_t* __restrict__ svals, const FoldRay* __restrict__ rays, const uint2* __restrict__ far,
     const float* __restrict__ g_org, uint32_t F, MapView map, TsdfParams tp, uint8_t* __restrict__ touched,
     uint32_t* __restrict__ work, unsigned long long* __restrict__ dbg) {
   __shared__ LongSmem<kP> S;
@@ -1551,7 +1619,7 @@ __global__ void __launch_bounds__(64 * kP, 1) k_fold_runs(
   if ((threadIdx.x & 31) == 0) n_long = count_long_runs(sorted_len, nruns);
   n_long = __shfl_sync(0xffffffffu, n_long, 0);
   fold_long_pairs<kP, kSep>(S, static_cast<int>(threadIdx.x >> 5), poses, nruns, n_long, order, ukeys, ustart, ulen,
-                            svals, rays, map, tp, touched, work, dbg);
+                            svals, rays, far, map, tp, touched, work, dbg);
 }
 
 // Short runs (< kLongRun records): one thread per run, launched on a second
@@ -1561,7 +1629,7 @@ template <int kC>
 __device__ __forceinline__ void fold_short_loop(
     const float* poses, const uint32_t nruns, const uint32_t n_long, const uint32_t* __restrict__ order,
     const uint32_t* __restrict__ ukeys, const uint32_t* __restrict__ ustart, const uint32_t* __restrict__ ulen,
-    const uint32_t* __restrict__ svals, const FoldRay* __restrict__ rays, const MapView& map, const TsdfParams& tp,
+    const uint32_t* __restrict__ svals, const FoldRay* __restrict__ rays, const uint2* __restrict__ far, const MapView& map, const TsdfParams& tp,
     uint8_t* __restrict__ touched, uint32_t* __restrict__ work) {
   const int lane = threadIdx.x & 31;
   while (true) {
@@ -1581,20 +1649,20 @@ __device__ __forceinline__ void fold_short_loop(
     // loop body has no per-record guards.
     const uint32_t* ids = svals + c.start;
     const uint32_t last = c.len - 1;
-    FoldRay rn[kC];
+    FoldIn rn[kC];
     Upd xn[kC], xs[kC];
-    auto weigh_at = [&](uint32_t idx, const FoldRay& ry) {
-      Upd x = weigh(ry, poses, c.x0, c.x1, c.x2, tp);
+    auto weigh_at = [&](uint32_t idx, const FoldIn& ry) {
+      Upd x = weigh_in(ry, poses, c.x0, c.x1, c.x2, tp);
       x.w = idx <= last ? x.w : 0.0f;
       return x;
     };
     uint32_t idn[kC];  // ray ids one chunk ahead of the gathers: no id -> ray load chain in the loop
 #pragma unroll
-    for (int u = 0; u < kC; ++u) rn[u] = rays[ids[min(static_cast<uint32_t>(u), last)]];
+    for (int u = 0; u < kC; ++u) rn[u] = load_fold_in(rays, far, ids[min(static_cast<uint32_t>(u), last)]);
 #pragma unroll
     for (int u = 0; u < kC; ++u) xn[u] = weigh_at(u, rn[u]);
 #pragma unroll
-    for (int u = 0; u < kC; ++u) rn[u] = rays[ids[min(static_cast<uint32_t>(kC + u), last)]];
+    for (int u = 0; u < kC; ++u) rn[u] = load_fold_in(rays, far, ids[min(static_cast<uint32_t>(kC + u), last)]);
 #pragma unroll
     for (int u = 0; u < kC; ++u) idn[u] = ids[min(static_cast<uint32_t>(2 * kC + u), last)];
     for (uint32_t j = 0; j < c.len; j += kC) {
@@ -1605,7 +1673,7 @@ __device__ __forceinline__ void fold_short_loop(
 #pragma unroll
       for (int u = 0; u < kC; ++u) xn[u] = weigh_at(j + kC + u, rn[u]);
 #pragma unroll
-      for (int u = 0; u < kC; ++u) rn[u] = rays[idn[u]];
+      for (int u = 0; u < kC; ++u) rn[u] = load_fold_in(rays, far, idn[u]);
 #pragma unroll
       for (int u = 0; u < kC; ++u) idn[u] = ids[min(j + 3 * kC + u, last)];
       const VoxState s0 = st;
@@ -1632,7 +1700,7 @@ template <int kMinBlocks, int kC, bool kSmemOrg>
 __global__ void __launch_bounds__(256, kMinBlocks) k_fold_short(
     const uint32_t* __restrict__ num_runs_p, const uint32_t* __restrict__ order,
     const uint32_t* __restrict__ sorted_len, const uint32_t* __restrict__ ukeys, const uint32_t* __restrict__ ustart,
-    const uint32_t* __restrict__ ulen, const uint32_t* __restrict__ svals, const FoldRay* __restrict__ rays,
+    const uint32_t* __restrict__ ulen, const uint32_t* __restrict__ svals, const FoldRay* __restrict__ rays, const uint2* __restrict__ far,
     const float* __restrict__ g_org, uint32_t F, MapView map, TsdfParams tp, uint8_t* __restrict__ touched,
     uint32_t* __restrict__ work) {
   __shared__ float s_org[3 * kOrgCache];
@@ -1642,7 +1710,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_fold_short(
     uint32_t n_long = 0;
     if ((threadIdx.x & 31) == 0) n_long = count_long_runs(sorted_len, nruns);
     n_long = __shfl_sync(0xffffffffu, n_long, 0);
-    fold_short_loop<kC>(poses, nruns, n_long, order, ukeys, ustart, ulen, svals, rays, map, tp, touched, work);
+    fold_short_loop<kC>(poses, nruns, n_long, order, ukeys, ustart, ulen, svals, rays, far, map, tp, touched, work);
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
@@ -1656,7 +1724,7 @@ template <bool kSmemOrg, int kC = 2>
 __global__ void __launch_bounds__(512, 1) k_fold_all(
     const uint32_t* __restrict__ num_runs_p, const uint32_t* __restrict__ order,
     const uint32_t* __restrict__ sorted_len, const uint32_t* __restrict__ ukeys, const uint32_t* __restrict__ ustart,
-    const uint32_t* __restrict__ ulen, const uint32_t* __restrict__ svals, const FoldRay* __restrict__ rays,
+    const uint32_t* __restrict__ ulen, const uint32_t* __restrict__ svals, const FoldRay* __restrict__ rays, const uint2* __restrict__ far,
     const float* __restrict__ g_org, uint32_t F, MapView map, TsdfParams tp, uint8_t* __restrict__ touched,
     uint32_t* __restrict__ work, unsigned long long* __restrict__ dbg) {
   __shared__ LongSmem<4> S;
@@ -1670,9 +1738,9 @@ __global__ void __launch_bounds__(512, 1) k_fold_all(
   n_long = __shfl_sync(0xffffffffu, n_long, 0);
   const int wid = static_cast<int>(threadIdx.x >> 5);
   if (wid >= 8)
-    fold_long_pairs<4, false>(S, wid - 8, poses, nruns, n_long, order, ukeys, ustart, ulen, svals, rays, map, tp,
-                              touched, work, dbg);
-  fold_short_loop<kC>(poses, nruns, n_long, order, ukeys, ustart, ulen, svals, rays, map, tp, touched, work);
+    fold_long_pairs<4, false>(S, wid - 8, poses, nruns, n_long, order, ukeys, ustart, ulen, svals, rays, far, map,
+                              tp, touched, work, dbg);
+  fold_short_loop<kC>(poses, nruns, n_long, order, ukeys, ustart, ulen, svals, rays, far, map, tp, touched, work);
 }
 
 // Self-tests of the fast fold arithmetic against the reference-order path.

@@ -241,6 +241,7 @@ struct vxg_handle {
   DBuf<unsigned long long> chunk_base;  // per chunk: first ray, first record
   DBuf<uint32_t> sort_counts, sort_offs, dense_start, dense_end, run_flag, run_pos;
   DBuf<FoldRay> fold_rays;
+  DBuf<uint2> far_rays;  // {w_front, colour} per ray: what a far record's fold step reads
   DBuf<uint32_t> num_segs;  // bundling: bucket count (RLE output)
   DBuf<float4> pt_w;    // bundling: per sorted point (world point, weight)
   DBuf<uint32_t> pt_c;  // bundling: per sorted point colour
@@ -928,9 +929,11 @@ uint64_t vxg_handle::count_rays(uint32_t R, uint32_t F) {
   rcount.ensure(R);
   roff.ensure(R);
   join_folds();  // the previous batch's fold reads fold_rays
-  if (R > fold_rays.cap) sync_folds();  // (and the host may free it only after that fold)
+  if (R > fold_rays.cap || R > far_rays.cap) sync_folds();  // (and the host may free them only after that fold)
   fold_rays.ensure(R);
-  k_ray_count<<<grid_for(R), 256, 0, st>>>(R, rays.p, d_poses.p, tp, rcount.p, d_stats.p + F, fold_rays.p);
+  far_rays.ensure(R);
+  k_ray_count<<<grid_for(R), 256, 0, st>>>(R, rays.p, d_poses.p, tp, rcount.p, d_stats.p + F, fold_rays.p,
+                                           far_rays.p);
   ++launches;
   CU(cudaGetLastError());
   cub([&](void* t, size_t& b) {
@@ -1204,7 +1207,8 @@ void vxg_handle::sort_fold(uint64_t T, uint64_t nslots, uint32_t F) {
                                                                 : (fold_kc == 4 ? k_fold_all<true, 4> : k_fold_all<true, 2>))));
       kern<<<static_cast<unsigned>(dev_sms), 512, 0, fold_long_st>>>(num_runs.p, run_order.p, run_len2.p, run_keys.p,
                                                                      run_start.p, run_len.p, svals, fold_rays.p,
-                                                                     d_org.p, F, view(), tp, tch, work.p, dbg);
+                                                                     far_rays.p, d_org.p, F, view(), tp, tch, work.p,
+                                                                     dbg);
       CU(cudaGetLastError());
       end(T, 2, fold_long_st);
       CU(cudaEventRecord(fold_join, fold_long_st));
@@ -1223,7 +1227,7 @@ void vxg_handle::sort_fold(uint64_t T, uint64_t nslots, uint32_t F) {
     auto kern = smem_org ? k_fold_runs<P, SEP, true> : k_fold_runs<P, SEP, false>;                              \
     if (long_smem) CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, long_smem));      \
     kern<<<lg, THREADS, long_smem, fold_long_st>>>(num_runs.p, run_order.p, run_len2.p, run_keys.p, run_start.p,  \
-                                                   run_len.p, svals, fold_rays.p, d_org.p, F, view(), tp, tch,     \
+                                                   run_len.p, svals, fold_rays.p, far_rays.p, d_org.p, F, view(), tp, tch, \
                                                    work.p, dbg);                                                 \
   } while (0)
     if (long_layout == 2)
@@ -1257,11 +1261,12 @@ void vxg_handle::sort_fold(uint64_t T, uint64_t nslots, uint32_t F) {
     const uint32_t* clen = run_len.p;
     const uint32_t* csv = svals;
     const FoldRay* crays = fold_rays.p;
+    const uint2* cfar = far_rays.p;
     const float* corg = d_org.p;
 #define VXG_FOLD_SHORT(MB, C)                                                                                 \
   do {                                                                                                        \
     auto kern = smem_org ? k_fold_short<MB, C, true> : k_fold_short<MB, C, false>;                           \
-    CU(cudaLaunchKernelEx(&lc, kern, cnum, cord, clen2, ckey, cst, clen, csv, crays, corg, F, mv, tp, tch,   \
+    CU(cudaLaunchKernelEx(&lc, kern, cnum, cord, clen2, ckey, cst, clen, csv, crays, cfar, corg, F, mv, tp, tch, \
                           work.p));                                                                          \
   } while (0)
     if (short_blocks == 1)
@@ -1327,6 +1332,7 @@ uint32_t pipeline_chunks(uint64_t total) {
 
 void vxg_handle::emit_and_apply(uint32_t R, uint32_t F, const TermView& tv) {
   const TsdfParams tp = params();
+  if (R > kRayMask) throw VxgError(VXG_EINVAL, "too many rays in one batch (record values hold 31-bit ray ids)");
   apply_pending_reset();
   const uint64_t total = count_rays(R, F);
   const uint32_t nch = pipeline_chunks(total);
