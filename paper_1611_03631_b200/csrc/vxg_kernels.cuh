@@ -1181,15 +1181,14 @@ __device__ __forceinline__ uint32_t count_long_runs(const uint32_t* __restrict__
 // waits on global memory or on the weighing arithmetic.
 constexpr int kRingStages = 4;
 
-struct alignas(16) PreRec {  // one record as handed to the long-run consumer
+struct alignas(32) PreRec {  // one record as handed to the long-run consumer (one 32-byte sector)
   float W;   // weight before this update (the producer's W scan)
   float T;   // RN(W + w)
   float r1;  // refined reciprocal of T
   float wc;  // RN(w * clamp(d))
-  float wn0, wn1, wn2;  // RN(w * new colour channel)
-  uint32_t c;           // colour word (has_color << 31)
-  float w, d;           // raw (for the stationarity vote and the exact fallback)
-  uint32_t ok, pad;     // w in (0, 2^100) and T in the fast-division range
+  uint32_t c;   // colour word (has_color << 31); the consumer forms RN(w * channel) itself when it needs it
+  float w, d;   // raw (for the colour chains and the exact fallback)
+  uint32_t ok;  // w in (0, 2^100) and T in the fast-division range
 };
 
 // Per-chunk summary the producer publishes with the chunk: the weight after
@@ -1204,13 +1203,14 @@ struct alignas(16) ChunkHdr {
   int hi[3];
 };
 
-// k = max{k in [0, 255] : RN(k w) < thr}, for w > 0 and thr > 0 (k = 0 always qualifies).
+// Some k in [0, 255] with RN(k w) < thr, for w > 0 and thr > 0 (RN(k w) is
+// monotone in k, so every smaller k qualifies too): the estimate thr / w,
+// shaved by 1e-4 and verified by the one multiplication that defines it. It
+// is the maximal k except within 1e-4 of an integer quotient; a smaller
+// radius only sends a few more chunks down the colour chains (same results).
 __device__ __forceinline__ int stationary_radius(float w, float thr) {
-  int k = static_cast<int>(fminf(floorf(__fdividef(thr, w)), 255.0f));
-  k = k < 0 ? 0 : k;
-  while (k > 0 && !(__fmul_rn(static_cast<float>(k), w) < thr)) --k;
-  while (k < 255 && __fmul_rn(static_cast<float>(k + 1), w) < thr) ++k;
-  return k;
+  const int k = static_cast<int>(fminf(__fdividef(thr, w) * 0.9999f, 255.0f));
+  return (k > 0 && __fmul_rn(static_cast<float>(k), w) < thr) ? k : 0;
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -1276,13 +1276,15 @@ struct LongSmem {
   uint32_t pair_run[kP];
   float4 wscan[kP][8];  // the chunk's 32 weights, broadcast to the producer lanes
   ChunkHdr ring_hdr[kP][kRingStages];
+  uint2 spec_tab[kP][2][32];  // per record: its step as a map over 7 candidate distances (+ dead), one byte each
 };
 
 template <int kP>
 __device__ __forceinline__ void long_smem_init(LongSmem<kP>& S) {
   if (threadIdx.x < kP * kRingStages) {
-    mbar_init(&S.ring_full[threadIdx.x / kRingStages][threadIdx.x % kRingStages], 32);
-    mbar_init(&S.ring_empty[threadIdx.x / kRingStages][threadIdx.x % kRingStages], 32);
+    // one arrival per hand-over: lane 0, after a __syncwarp that orders the warp's ring accesses before it
+    mbar_init(&S.ring_full[threadIdx.x / kRingStages][threadIdx.x % kRingStages], 1);
+    mbar_init(&S.ring_empty[threadIdx.x / kRingStages][threadIdx.x % kRingStages], 1);
   }
 }
 
@@ -1416,14 +1418,10 @@ __device__ __forceinline__ void fold_long_pairs(
           const Recip rt = make_recip(pr.T);
           pr.r1 = rt.r1;
           pr.wc = __fmul_rn(w, clamped);
-          pr.wn0 = __fmul_rn(w, __uint2float_rn(u.c & 0xffu));
-          pr.wn1 = __fmul_rn(w, __uint2float_rn((u.c >> 8) & 0xffu));
-          pr.wn2 = __fmul_rn(w, __uint2float_rn((u.c >> 16) & 0xffu));
           pr.c = u.c;
           pr.w = w;
           pr.d = u.d;
           pr.ok = ((w > 0.0f) & (w < 0x1p100f) & rt.ok) ? 1u : 0u;
-          pr.pad = 0u;
           // chunk summary (records >= cnt do not constrain it)
           int lo0 = -1024, lo1 = -1024, lo2 = -1024, hi0 = 1024, hi1 = 1024, hi2 = 1024;
           const bool in_chunk = static_cast<uint32_t>(lane) < cnt;
@@ -1441,6 +1439,10 @@ __device__ __forceinline__ void fold_long_pairs(
           ChunkHdr hd;
           hd.W_end = W;
           hd.ok = __all_sync(0xffffffffu, !in_chunk || pr.ok) ? 1u : 0u;
+          // bit 1: every record pulls towards +truncation (clamped d = truncation:
+          // free space in front of the surface) — the consumer's cue to try the
+          // speculative walk
+          hd.ok |= __all_sync(0xffffffffu, !in_chunk || clamped == tp.truncation) ? 2u : 0u;
           hd.lo[0] = __reduce_max_sync(0xffffffffu, lo0);
           hd.lo[1] = __reduce_max_sync(0xffffffffu, lo1);
           hd.lo[2] = __reduce_max_sync(0xffffffffu, lo2);
@@ -1453,7 +1455,8 @@ __device__ __forceinline__ void fold_long_pairs(
           if (dbg != nullptr) pwait += clock64() - tw0;
           ring[pair][s][lane] = pr;
           if (lane == 0) ring_hdr[pair][s] = hd;
-          mbar_arrive(&ring_full[pair][s]);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&ring_full[pair][s]);
           ry1 = ry2;
           ry2 = ry3;
         }
@@ -1465,8 +1468,10 @@ __device__ __forceinline__ void fold_long_pairs(
         }
       } else {
         VoxState st = load_vox(vp);
-        unsigned long long t_start = 0, n_sat = 0;
-        long long cwait = 0, cbusy0 = dbg != nullptr ? clock64() : 0, ct_vote = 0, ct_chain = 0;
+        unsigned long long t_start = 0, n_sat = 0, n_spec = 0, n_fail = 0, n_skip = 0;
+        uint32_t spec_skip = 0u, spec_back = 0u;  // back-off after a walk left its window
+        long long cwait = 0, cbusy0 = dbg != nullptr ? clock64() : 0, ct_vote = 0, ct_chain = 0, ct_spec = 0, nc_spec = 0,
+                  ct_serial = 0, nc_serial = 0;
         if (dbg != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
         for (uint32_t k = 0; k < nchunks; ++k, ++kk) {
           const int s = static_cast<int>(kk % kRingStages);
@@ -1480,12 +1485,74 @@ __device__ __forceinline__ void fold_long_pairs(
           const float W_end = hd.W_end;
           // colours provably unchanged over the whole chunk? (intervals from the producer)
           const int o0 = static_cast<int>(st.cr), o1 = static_cast<int>(st.cg), o2 = static_cast<int>(st.cb);
-          const bool vote = hd.ok != 0u && hd.lo[0] <= o0 && o0 <= hd.hi[0] && hd.lo[1] <= o1 && o1 <= hd.hi[1] &&
+          const bool vote = (hd.ok & 1u) != 0u && hd.lo[0] <= o0 && o0 <= hd.hi[0] && hd.lo[1] <= o1 && o1 <= hd.hi[1] &&
                             hd.lo[2] <= o2 && o2 <= hd.hi[2];
           const bool stationary = vote;  // warp-uniform
           const long long tc1 = dbg != nullptr ? clock64() : 0;
-          bool done = false;
-          if (stationary) {  // distance chain only: FMUL, FADD, 3-FMA quotient per step
+          bool done = false, spec_done = false;
+          // Speculative walk. In free space every record pulls D towards
+          // +truncation, where D already sits: a step moves it by 0 or +-1 ulp
+          // (rounding), so over a chunk D stays within a few ulps of where it
+          // started. Each lane evaluates ITS record's step — the same
+          // instructions as the serial chain below — on the 7 floats D0-3ulp ..
+          // D0+3ulp and publishes the results as a byte map over candidate
+          // indices (7 = left the window, absorbing); the chain is then one PRMT
+          // per record, composing the 32 maps in order from index 3. Exact by
+          // construction; a walk that leaves the window (or a failed range
+          // check) re-runs the chunk serially and backs off.
+          if (stationary && cnt == 32 && (hd.ok & 2u) != 0u) {
+            const uint32_t b0 = __float_as_uint(st.D);
+            if (spec_skip != 0u) {
+              --spec_skip;
+              ++n_skip;
+            } else if (b0 - 0x00800004u < 0x7e000000u) {  // D0 and its neighbours positive, normal, finite
+              const float4 x = reinterpret_cast<const float4*>(rb + lane)[0];  // W, T, r1, wc
+              const Recip rt{x.y, x.z, true};
+              const uint32_t base = b0 - 3u;
+              uint32_t tlo = 0u, thi = 0x07000000u;
+              bool rng = true;
+#pragma unroll
+              for (int cnd = 0; cnd < 7; ++cnd) {
+                const float a = __fadd_rn(__fmul_rn(x.x, __uint_as_float(base + cnd)), x.w);
+                const float q = fast_quot0(a, rt);
+                rng &= fast_range(a);
+                const uint32_t code = min(__float_as_uint(q) - base, 7u);
+                if (cnd < 4) tlo |= code << (8 * cnd); else thi |= code << (8 * (cnd - 4));
+              }
+              if (!rng) tlo = thi = 0x07070707u;
+              uint2* tb = S.spec_tab[pair][kk & 1u];
+              tb[lane] = make_uint2(tlo, thi);
+              __syncwarp();
+              const uint4* t4 = reinterpret_cast<const uint4*>(tb);
+              uint32_t sel = 3u;
+#pragma unroll
+              for (int u = 0; u < 16; ++u) {
+                const uint4 t = t4[u];
+                // prmt's own selector semantics (bit 3 of a nibble = sign
+                // replication) never trigger: every table byte is <= 7
+                asm("prmt.b32 %0, %1, %2, %0;" : "+r"(sel) : "r"(t.x), "r"(t.y));
+                asm("prmt.b32 %0, %1, %2, %0;" : "+r"(sel) : "r"(t.z), "r"(t.w));
+              }
+              sel &= 7u;
+              if (sel != 7u) {
+                st.D = __uint_as_float(base + sel);
+                st.W = W_end;
+                done = true;
+                spec_done = true;
+                n_sat += cnt;
+                n_spec += cnt;
+                spec_back = 0u;
+              } else {
+                ++n_fail;
+                // a failed walk costs about a third of the serial chunk it falls
+                // back to: only a streak of failures (D is on the move) backs off
+                spec_back = min(spec_back + 1u, 8u);
+                spec_skip = spec_back >= 3u ? 1u << (spec_back - 3u) : 0u;
+              }
+            }
+          }
+          if (done) {
+          } else if (stationary) {  // distance chain only: FMUL, FADD, 3-FMA quotient per step
             float D = st.D;
             // range of |a| off the chain (two FMNMX per step): every a in
             // [2^-60, 2^60] is quot_ok; a = +-0 fails conservatively (exact re-run)
@@ -1532,7 +1599,7 @@ __device__ __forceinline__ void fold_long_pairs(
               const PreRec& x = rb[u];
               const bool live = x.w > 0.0f;
               const bool active = !colour || (x.c >> 31) != 0u;
-              const float add = ch == 0 ? x.wc : (ch == 1 ? x.wn0 : (ch == 2 ? x.wn1 : x.wn2));
+              const float add = ch == 0 ? x.wc : __fmul_rn(x.w, __uint2float_rn((x.c >> (colour ? 8 * ch - 8 : 0)) & 0xffu));
               const float a = __fadd_rn(__fmul_rn(x.W, qs), add);
               const float q = fast_quot0(a, Recip{x.T, x.r1, true});
               if (live & active) {
@@ -1560,17 +1627,29 @@ __device__ __forceinline__ void fold_long_pairs(
           }
           if (dbg != nullptr) {
             asm volatile("" ::"f"(st.D));
-            ct_chain += clock64() - tc1;
+            const long long tc2 = clock64();
+            ct_chain += tc2 - tc1;
             ct_vote += tc1 - tc0;
+            if (spec_done) {
+              ct_spec += tc2 - tc1;
+              ++nc_spec;
+            } else {
+              ct_serial += tc2 - tc1;
+              ++nc_serial;
+            }
           }
           __syncwarp();
-          mbar_arrive(&ring_empty[pair][s]);
+          if (lane == 0) mbar_arrive(&ring_empty[pair][s]);
         }
         if (dbg != nullptr && lane == 0) {
           atomicAdd(&dbg[4 * n_all + 2], static_cast<unsigned long long>(cwait));
           atomicAdd(&dbg[4 * n_all + 3], static_cast<unsigned long long>(clock64() - cbusy0));
           atomicAdd(&dbg[4 * n_all + 8], static_cast<unsigned long long>(ct_vote));
           atomicAdd(&dbg[4 * n_all + 9], static_cast<unsigned long long>(ct_chain));
+          atomicAdd(&dbg[4 * n_all + 10], static_cast<unsigned long long>(ct_spec));
+          atomicAdd(&dbg[4 * n_all + 11], static_cast<unsigned long long>(nc_spec));
+          atomicAdd(&dbg[4 * n_all + 12], static_cast<unsigned long long>(ct_serial));
+          atomicAdd(&dbg[4 * n_all + 13], static_cast<unsigned long long>(nc_serial));
         }
         if (lane == 0) {
           store_vox(vp, st);
@@ -1580,8 +1659,8 @@ __device__ __forceinline__ void fold_long_pairs(
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
             dbg[4 * r + 0] = t_start;
             dbg[4 * r + 1] = t_end;
-            dbg[4 * r + 2] = c.len;
-            dbg[4 * r + 3] = n_sat;
+            dbg[4 * r + 2] = c.len | (min(n_fail, 0xFFFFull) << 32) | (min(n_skip, 0xFFFFull) << 48);
+            dbg[4 * r + 3] = n_sat | (n_spec << 32);
           }
         }
       }
