@@ -23,7 +23,7 @@ workload: $(PKG)/workload/libworkload.so
 oracle:
 	$(MAKE) -C oracle
 
-$(OBJDIR)/vxg_tsdf.o: $(CSRC)/vxg_tsdf.cu $(CSRC)/vxg_kernels.cuh $(CSRC)/vxg_device.cuh include/vxg.h include/vxg_types.h
+$(OBJDIR)/vxg_tsdf.o: $(CSRC)/vxg_tsdf.cu $(CSRC)/vxg_kernels.cuh $(CSRC)/vxg_device.cuh $(CSRC)/vxg_sort.cuh $(CSRC)/vxg_esdf.cuh include/vxg.h include/vxg_types.h
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -c -o $@ $<
 

@@ -12,6 +12,7 @@
 #include <cstdint>
 
 #include "vxg_device.cuh"
+#include "vxg_sort.cuh"
 
 namespace vxg {
 
@@ -161,12 +162,6 @@ __global__ void k_group_keys(const float* __restrict__ xyz, uint64_t P, const ui
     keys[i] = static_cast<KeyT>(key);
     vals[i] = static_cast<uint32_t>(i);
   }
-}
-
-__global__ void k_widen_keys(const uint32_t* __restrict__ num_p, const uint32_t* __restrict__ in,
-                             unsigned long long* __restrict__ out) {
-  const uint32_t n = *num_p;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = in[i];
 }
 
 // Per bucket: sequential fp64 sums in scan order (tsdf_integrator.cpp:213-219),
@@ -1164,11 +1159,19 @@ __device__ __forceinline__ void store_vox(vxg_voxel* vp, const VoxState& s) {
   vp->b = static_cast<uint8_t>(s.cb);
 }
 
-__device__ __forceinline__ uint32_t count_long_runs(const uint32_t* __restrict__ sorted_len, uint32_t nruns) {
-  uint32_t lo = 0, hi = nruns;  // first index with len < kLongRun (lengths sorted descending)
+constexpr int floor_log2_c(uint32_t x) { return x <= 1u ? 0 : 1 + floor_log2_c(x >> 1); }
+static_assert(kLongRun >= 16u && (kLongRun & ((1u << (floor_log2_c(kLongRun) - 3)) - 1u)) == 0u,
+              "kLongRun must be the first length of its run-length code (run_len_code)");
+
+// Long runs come first in the fold order: sorted_code holds kRunCodeMax -
+// run_len_code(length) in ascending order, and len >= kLongRun <=> code(len)
+// >= code(kLongRun) because kLongRun starts a code.
+__device__ __forceinline__ uint32_t count_long_runs(const uint32_t* __restrict__ sorted_code, uint32_t nruns) {
+  const uint32_t thr = kRunCodeMax - run_len_code(kLongRun);
+  uint32_t lo = 0, hi = nruns;  // first index whose run is shorter than kLongRun
   while (lo < hi) {
     const uint32_t mid = (lo + hi) >> 1;
-    if (sorted_len[mid] >= kLongRun) lo = mid + 1; else hi = mid;
+    if (sorted_code[mid] <= thr) lo = mid + 1; else hi = mid;
   }
   return lo;
 }

@@ -24,11 +24,11 @@ constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
 
 // kBits: largest digit of a pass; kIpt: records per thread per sub-tile.
-template <int kBits, int kIpt>
+template <int kBits, int kIpt, int kNs = 8>
 struct SortCfg {
   static constexpr int kBins = 1 << kBits;
   static constexpr int kSub = kSortThreads * kIpt;                  // records per sub-tile
-  static constexpr int kNsub = 8;                                   // sub-tiles per super-tile (one CTA)
+  static constexpr int kNsub = kNs;                                 // sub-tiles per super-tile (one CTA); 1 for small inputs (more CTAs)
   static constexpr uint32_t kSuper = static_cast<uint32_t>(kSub) * kNsub;
   static constexpr int kWcStride = kBins + 2;                       // + overflow bin for the tail, even
   static constexpr int kScanPer = (kBins + 1 + kSortThreads - 1) / kSortThreads;
@@ -43,11 +43,11 @@ struct SortCfg {
   };
 };
 
-template <int kBits, int kIpt>
+template <int kBits, int kIpt, int kNs = 8>
 __global__ void __launch_bounds__(kSortThreads) k_sort_upsweep(const uint32_t* __restrict__ keys, uint64_t n,
                                                                int shift, uint32_t mask, uint32_t S,
                                                                uint32_t* __restrict__ counts) {
-  using C = SortCfg<kBits, kIpt>;
+  using C = SortCfg<kBits, kIpt, kNs>;
   __shared__ uint32_t h[C::kBins];
   const uint32_t bins = mask + 1u;
   for (uint32_t d = threadIdx.x; d < bins; d += kSortThreads) h[d] = 0u;
@@ -86,13 +86,14 @@ __device__ __forceinline__ uint32_t digit_peers(uint32_t d) {
 // staged segment; a segment's first/last record may continue a run from the
 // previous / into the next sub-tile or CTA (atomicMin / atomicMax), a key
 // change inside a segment is the run's global start / end (plain store).
-template <int kBits, int kIpt, int kMinBlocks, bool kPrefetch = false, bool kMatch = false, bool kMarks = false>
+template <int kBits, int kIpt, int kMinBlocks, bool kPrefetch = false, bool kMatch = false, bool kMarks = false,
+          int kNs = 8>
 __global__ void __launch_bounds__(kSortThreads, kMinBlocks)
     k_sort_downsweep(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
                      uint32_t* __restrict__ vout, uint64_t n, int shift, uint32_t mask, uint32_t S,
                      const uint32_t* __restrict__ offs, uint32_t K = 0, uint32_t* __restrict__ dense_start = nullptr,
                      uint32_t* __restrict__ dense_end = nullptr) {
-  using C = SortCfg<kBits, kIpt>;
+  using C = SortCfg<kBits, kIpt, kNs>;
   extern __shared__ __align__(16) uint8_t sort_smem_raw[];
   typename C::Smem& sm = *reinterpret_cast<typename C::Smem*>(sort_smem_raw);
   const uint32_t bins = mask + 1u;
@@ -237,26 +238,205 @@ __global__ void __launch_bounds__(kSortThreads, kMinBlocks)
   }
 }
 
-// Runs of the sorted records, one per voxel, from the dense per-key head/tail
-// marks the weigh pass wrote (dense_end[k] == 0: voxel k has no record).
-__global__ void k_run_flags(uint32_t K, const uint32_t* __restrict__ dense_end, uint32_t* __restrict__ flag) {
-  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x)
-    flag[k] = dense_end[k] != 0u ? 1u : 0u;
-}
-
-__global__ void k_run_scatter(uint32_t K, const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos,
-                              const uint32_t* __restrict__ dense_start, const uint32_t* __restrict__ dense_end,
-                              uint32_t* __restrict__ run_keys, uint32_t* __restrict__ run_start,
-                              uint32_t* __restrict__ run_len, uint32_t* __restrict__ nruns) {
-  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x) {
-    if (flag[k]) {
-      const uint32_t j = pos[k];
-      run_keys[j] = k;
+// Runs of the sorted records, one per voxel with records (dense_end[k] != 0),
+// compacted in key order through the scan below.
+struct RunIn {
+  const uint32_t* dense_end;
+  __device__ __forceinline__ uint32_t operator()(uint64_t k) const { return dense_end[k] != 0u ? 1u : 0u; }
+};
+struct RunOut {
+  uint64_t K;
+  const uint32_t* dense_start;
+  const uint32_t* dense_end;
+  uint32_t* run_keys;
+  uint32_t* run_start;
+  uint32_t* run_len;
+  uint32_t* nruns;
+  __device__ __forceinline__ void operator()(uint64_t k, uint32_t has, uint32_t j) const {
+    if (has) {
+      run_keys[j] = static_cast<uint32_t>(k);
       run_start[j] = dense_start[k];
       run_len[j] = dense_end[k] - dense_start[k];
     }
-    if (k == K - 1) *nruns = pos[k] + flag[k];
+    if (k == K - 1) *nruns = j + has;
   }
+};
+
+// ---- exclusive prefix sums: reduce-then-scan over tiles of kScanTile items
+// (k_scan_reduce -> the tile sums scanned by the same routine -> k_scan_apply).
+// in == out is allowed (every item is read before it is written, by the same
+// thread).
+constexpr int kScanThreads = 256;
+constexpr int kScanIpt = 16;
+constexpr uint32_t kScanTile = kScanThreads * kScanIpt;
+
+// In: value of item i (uint64_t -> T). Out: (i, value, exclusive prefix) -> side effects.
+template <typename T>
+struct ScanLoad {
+  const T* p;
+  __device__ __forceinline__ T operator()(uint64_t i) const { return p[i]; }
+};
+template <typename T>
+struct ScanStore {
+  T* p;
+  __device__ __forceinline__ void operator()(uint64_t i, T, T pre) const { p[i] = pre; }
+};
+
+__device__ __forceinline__ void scan_pin(uint32_t& x) { asm volatile("" : "+r"(x)); }
+__device__ __forceinline__ void scan_pin(unsigned long long& x) { asm volatile("" : "+l"(x)); }
+
+template <typename T, typename In>
+__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(In in, uint64_t n, T* __restrict__ tile_sums) {
+  __shared__ T s_warp[kScanThreads / 32];
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kScanTile;
+  T x = 0;
+#pragma unroll
+  for (int j = 0; j < kScanIpt; ++j) {
+    const uint64_t i = base + static_cast<uint64_t>(j) * kScanThreads + threadIdx.x;
+    if (i < n) x += in(i);
+  }
+  const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+  if (lane == 0u) s_warp[w] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    T tot = 0;
+#pragma unroll
+    for (int q = 0; q < kScanThreads / 32; ++q) tot += s_warp[q];
+    tile_sums[blockIdx.x] = tot;
+  }
+}
+
+// out(i, in(i), tile_offs[tile] + sum of the tile's items before i). A warp
+// owns kScanIpt * 32 consecutive items, item (j, lane) = j * 32 + lane of its
+// span: coalesced accesses, one shuffle scan per j, one barrier per tile.
+// tile_offs == nullptr: one CTA walks `tiles` consecutive tiles alone with a
+// running carry (small inputs: one launch instead of three).
+template <typename T, typename In, typename Out>
+__global__ void __launch_bounds__(kScanThreads) k_scan_apply(In in, uint64_t n, const T* __restrict__ tile_offs,
+                                                             Out out, int tiles = 1) {
+  __shared__ T s_warp[2][kScanThreads / 32];
+  const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+  T carry = tile_offs != nullptr ? tile_offs[blockIdx.x] : T(0);
+  for (int t = 0; t < tiles; ++t) {
+    const uint64_t i0 = (static_cast<uint64_t>(blockIdx.x) + t) * kScanTile + static_cast<uint64_t>(w) * (32 * kScanIpt) + lane;
+    T v[kScanIpt], e[kScanIpt], run = 0;  // e: exclusive prefix inside the warp's span
+#pragma unroll
+    for (int j = 0; j < kScanIpt; ++j) v[j] = i0 + j * 32 < n ? in(i0 + j * 32) : T(0);
+    // all loads in flight before the first scan (otherwise the compiler
+    // re-reads in(i) per use and exposes one memory round trip per j)
+#pragma unroll
+    for (int j = 0; j < kScanIpt; ++j) scan_pin(v[j]);
+#pragma unroll
+    for (int j = 0; j < kScanIpt; ++j) {
+      T x = v[j];
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const T y = __shfl_up_sync(0xffffffffu, x, off);
+        if (lane >= static_cast<uint32_t>(off)) x += y;
+      }
+      e[j] = run + x - v[j];
+      run += __shfl_sync(0xffffffffu, x, 31);
+    }
+    T* sw = s_warp[t & 1];  // double-buffered: one barrier per tile
+    if (lane == 0u) sw[w] = run;
+    __syncthreads();
+    T pre = carry, tot = 0;
+#pragma unroll
+    for (int q = 0; q < kScanThreads / 32; ++q) {
+      const T c = sw[q];
+      if (q < static_cast<int>(w)) pre += c;
+      tot += c;
+    }
+#pragma unroll
+    for (int j = 0; j < kScanIpt; ++j)
+      if (i0 + j * 32 < n) out(i0 + j * 32, v[j], pre + e[j]);
+    carry += tot;
+  }
+}
+
+// ---- bundling: one bucket per run of equal sorted keys (a compaction of the
+// run heads through the scan above: the keys are read twice, nothing else)
+template <typename KeyT>
+struct SegHeadIn {
+  const KeyT* k;
+  __device__ __forceinline__ uint32_t operator()(uint64_t i) const { return (i == 0 || k[i] != k[i - 1]) ? 1u : 0u; }
+};
+template <typename KeyT>
+struct SegHeadOut {
+  const KeyT* k;
+  uint64_t n;
+  unsigned long long* ukeys;
+  uint32_t* ustart;
+  uint32_t* num_segs;
+  __device__ __forceinline__ void operator()(uint64_t i, uint32_t head, uint32_t pre) const {
+    if (head) {
+      ukeys[pre] = static_cast<unsigned long long>(k[i]);
+      ustart[pre] = static_cast<uint32_t>(i);
+    }
+    if (i == n - 1) *num_segs = pre + head;
+  }
+};
+
+__global__ void k_seg_counts(uint32_t S, uint64_t P, const uint32_t* __restrict__ ustart, uint32_t* __restrict__ ucount) {
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x)
+    ucount[s] = (s + 1 < S ? ustart[s + 1] : static_cast<uint32_t>(P)) - ustart[s];
+}
+
+// ---- 64-bit keys through the 32-bit pair sort: positions sorted by the low
+// word, then (stable) by the high word
+__global__ void k_key_word(uint64_t n, const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ perm,
+                           int shift, uint32_t mask, bool complement, uint32_t* __restrict__ out_k,
+                           uint32_t* __restrict__ out_v) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t src = perm != nullptr ? perm[i] : static_cast<uint32_t>(i);
+    const uint32_t wv = static_cast<uint32_t>(keys[src] >> shift) & mask;
+    out_k[i] = complement ? mask - wv : wv;
+    if (out_v != nullptr) out_v[i] = src;
+  }
+}
+
+__global__ void k_gather_sorted(uint64_t n, const uint32_t* __restrict__ perm, const unsigned long long* __restrict__ keys,
+                                const uint32_t* __restrict__ vals, unsigned long long* __restrict__ out_keys,
+                                uint32_t* __restrict__ out_vals) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t src = perm[i];
+    if (out_keys != nullptr) out_keys[i] = keys[src];
+    if (out_vals != nullptr) out_vals[i] = vals[src];
+  }
+}
+
+// ---- fold order: runs by a coarse length code, longest first, key order inside a code
+// Codes are monotone in the length: exact below 16, then 8 steps per octave
+// (lengths within 12.5 % share a code), so a warp's 32 short runs are
+// balanced while runs of one code keep their key order (neighbouring voxels
+// share rays: the fold's gathers stay local). kLongRun must be a code boundary.
+__device__ __host__ __forceinline__ uint32_t run_len_code(uint32_t len) {
+  if (len < 16u) return len;
+#ifdef __CUDA_ARCH__
+  const int e = 31 - __clz(len);
+#else
+  int e = 31;
+  while (!(len >> e)) --e;
+#endif
+  return 16u + static_cast<uint32_t>(e - 4) * 8u + ((len >> (e - 3)) & 7u);
+}
+constexpr uint32_t kRunCodeMax = 255u;
+
+__global__ void k_run_codes(uint32_t nruns, const uint32_t* __restrict__ run_len, uint32_t* __restrict__ dcode,
+                            uint32_t* __restrict__ iota, uint32_t* __restrict__ max_len) {
+  uint32_t m = 0;
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nruns; r += gridDim.x * blockDim.x) {
+    const uint32_t len = run_len[r];
+    dcode[r] = kRunCodeMax - run_len_code(len);
+    iota[r] = r;
+    m = max(m, len);
+  }
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31u) == 0u && m) atomicMax(max_len, m);
 }
 
 }  // namespace vxg

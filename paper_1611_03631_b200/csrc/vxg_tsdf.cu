@@ -28,9 +28,6 @@
 #include <utility>
 #include <vector>
 
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_run_length_encode.cuh>
-#include <cub/device/device_scan.cuh>
 
 #include "../../include/vxg.h"
 #include "vxg_esdf.cuh"
@@ -213,7 +210,6 @@ struct vxg_handle {
   DBuf<uint8_t> touched;
 
   // ---- scratch
-  DBuf<uint8_t> cub_tmp;
   DBuf<float> in_xyz;
   DBuf<uint8_t> in_rgb;
   DBuf<uint64_t> d_off;
@@ -232,7 +228,7 @@ struct vxg_handle {
   DBuf<RhFrame> rh_frames;
   DBuf<uint64_t> tbl_off, bcs;
   DBuf<uint32_t> rkeys, rkeys2, rvals, rvals2;
-  DBuf<uint32_t> run_keys, run_len, run_start, run_len2, run_order, run_iota, work;
+  DBuf<uint32_t> run_keys, run_len, run_start, run_len2, run_order, run_iota, run_code, run_max, work;
   struct FoldSet {  // the other buffer set of the chunk pipeline (swapped with the members above)
     DBuf<uint32_t> rkeys, rkeys2, rvals, rvals2, run_keys, run_len, run_start, run_len2, run_order, num_runs, work;
     DBuf<float> d_org;
@@ -335,15 +331,53 @@ struct vxg_handle {
     pending.swap(keep);
   }
 
-  // CUB device algorithm; n_kernels = kernels it launches (for the launch count).
-  template <typename Fn>
-  void cub(Fn fn, int n_kernels = 1) {
-    size_t bytes = 0;
-    CU(fn(nullptr, bytes));
-    if (bytes == 0) bytes = 1;
-    CU(fn(cub_tmp.ensure(bytes), bytes));
-    launches += static_cast<uint64_t>(n_kernels);
+  // Exclusive prefix sums on st (vxg_sort.cuh); in == out is allowed.
+  DBuf<unsigned long long> scan_tmp[3];
+  static constexpr uint64_t kScanSoloTiles = 2;  // up to 8 K items: one CTA, one launch
+  template <typename T, typename In, typename Out>
+  void scan_with(In in, Out out, uint64_t n) {
+    if (n == 0) return;
+    const uint64_t tiles = (n + kScanTile - 1) / kScanTile;
+    if (tiles <= kScanSoloTiles) {
+      k_scan_apply<T, In, Out><<<1, kScanThreads, 0, st>>>(in, n, nullptr, out, static_cast<int>(tiles));
+      ++launches;
+      CU(cudaGetLastError());
+      return;
+    }
+    T* sums = reinterpret_cast<T*>(scan_tmp[0].ensure(tiles));
+    k_scan_reduce<T, In><<<static_cast<unsigned>(tiles), kScanThreads, 0, st>>>(in, n, sums);
+    scan_level<T>(sums, tiles, 1);
+    k_scan_apply<T, In, Out><<<static_cast<unsigned>(tiles), kScanThreads, 0, st>>>(in, n, sums, out);
+    launches += 2;
+    CU(cudaGetLastError());
   }
+  template <typename T>
+  void scan_level(T* sums, uint64_t n, int level) {  // in place
+    const uint64_t tiles = (n + kScanTile - 1) / kScanTile;
+    using L = ScanLoad<T>;
+    using S = ScanStore<T>;
+    if (tiles <= kScanSoloTiles) {
+      k_scan_apply<T, L, S><<<1, kScanThreads, 0, st>>>(L{sums}, n, nullptr, S{sums}, static_cast<int>(tiles));
+      ++launches;
+      return;
+    }
+    if (level > 2) throw VxgError(VXG_EINVAL, "prefix sum too large");
+    T* up = reinterpret_cast<T*>(scan_tmp[level].ensure(tiles));
+    k_scan_reduce<T, L><<<static_cast<unsigned>(tiles), kScanThreads, 0, st>>>(L{sums}, n, up);
+    scan_level<T>(up, tiles, level + 1);
+    k_scan_apply<T, L, S><<<static_cast<unsigned>(tiles), kScanThreads, 0, st>>>(L{sums}, n, up, S{sums});
+    launches += 2;
+  }
+  template <typename T>
+  void scan_exclusive(const T* in, T* out, uint64_t n) {
+    scan_with<T>(ScanLoad<T>{in}, ScanStore<T>{out}, n);
+  }
+  // Stable sort of n (64-bit key, value) pairs by the low `bits` key bits
+  // through the 32-bit pair sort: positions by the low word, then by the high
+  // word; out_keys / out_vals (either may be null) receive the sorted pairs.
+  DBuf<uint32_t> s64_k0, s64_k1, s64_v0, s64_v1;
+  void sort_pairs64(const unsigned long long* keys, const uint32_t* vals, uint64_t n, int bits, bool descending,
+                    unsigned long long* out_keys, uint32_t* out_vals);
 
   // ---------------------------------------------------------------- map
   // (Re)allocates an empty map of `cap` blocks of new_vps^3 voxels. Every
@@ -628,9 +662,17 @@ struct vxg_handle {
   uint64_t count_rays(uint32_t R, uint32_t F);
   void sort_fold(uint64_t T, uint64_t nslots, uint32_t F);
   void sort_records(uint64_t T, int kbits, uint32_t** sk, uint32_t** sv, uint32_t K);
-  template <int kBits, int kIpt, int kMB>
+  template <int kBits, int kIpt, int kMB, int kNs = 8>
   void lsd_sort(uint64_t T, int kbits, uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, uint32_t** sk,
                 uint32_t** sv, bool grouped, uint32_t K = 0);
+  // the plain pair sort: small inputs take one sub-tile per CTA (8x the CTAs)
+  void sort_pairs32(uint64_t n, int kbits, uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, uint32_t** sk,
+                    uint32_t** sv) {
+    if (n < (16u << 20))
+      lsd_sort<8, 12, 4, 1>(n, kbits, k0, v0, k1, v1, sk, sv, false);
+    else
+      lsd_sort<8, 12, 4>(n, kbits, k0, v0, k1, v1, sk, sv, false);
+  }
   bool marks_fused = false;  // the last sort pass wrote dense_start / dense_end (no sorted keys)
   int last_lsd_passes = 0;
   uint64_t last_blocks = 0;  // blocks allocated after the last produce attempt
@@ -661,6 +703,35 @@ struct vxg_handle {
   void nccl_reduce_updates(uint32_t F);
 };
 
+void vxg_handle::sort_pairs64(const unsigned long long* keys, const uint32_t* vals, uint64_t n, int bits,
+                              bool descending, unsigned long long* out_keys, uint32_t* out_vals) {
+  if (n == 0) return;
+  if (n > 0xFFFFFFFFull) throw VxgError(VXG_EINVAL, "sort too large (32-bit positions)");
+  bits = std::max(bits, 1);
+  s64_k0.ensure(n);
+  s64_k1.ensure(n);
+  s64_v0.ensure(n);
+  s64_v1.ensure(n);
+  const int lo_bits = std::min(bits, 32), hi_bits = bits - lo_bits;
+  const uint32_t lo_mask = lo_bits == 32 ? 0xFFFFFFFFu : (1u << lo_bits) - 1u;
+  uint32_t *sk = nullptr, *sv = nullptr;
+  k_key_word<<<grid_for(n), 256, 0, st>>>(n, keys, nullptr, 0, lo_mask, descending, s64_k0.p, s64_v0.p);
+  ++launches;
+  sort_pairs32(n, lo_bits, s64_k0.p, s64_v0.p, s64_k1.p, s64_v1.p, &sk, &sv);
+  if (hi_bits > 0) {
+    uint32_t* kf = sk == s64_k0.p ? s64_k1.p : s64_k0.p;  // free key buffer
+    uint32_t* vf = sv == s64_v0.p ? s64_v1.p : s64_v0.p;  // free value buffer
+    k_key_word<<<grid_for(n), 256, 0, st>>>(n, keys, sv, 32, (1u << hi_bits) - 1u, descending, kf, nullptr);
+    ++launches;
+    uint32_t *sk2 = nullptr, *sv2 = nullptr;
+    sort_pairs32(n, hi_bits, kf, sv, sk, vf, &sk2, &sv2);
+    sv = sv2;
+  }
+  k_gather_sorted<<<grid_for(n), 256, 0, st>>>(n, sv, keys, vals, out_keys, out_vals);
+  ++launches;
+  CU(cudaGetLastError());
+}
+
 void vxg_handle::build_rays_simple(const float* dxyz, const uint8_t* drgb, uint64_t P, uint32_t F, uint32_t* R_out) {
   const TsdfParams tp = params();
   begin(ST_BUNDLE);
@@ -669,9 +740,7 @@ void vxg_handle::build_rays_simple(const float* dxyz, const uint8_t* drgb, uint6
   k_simple_inrange<<<grid_for(P), 256, 0, st>>>(dxyz, P, d_off.p, d_poses.p, F, tp, flags.p, d_stats.p + 2 * F);
   ++launches;
   CU(cudaGetLastError());
-  cub([&](void* t, size_t& b) {
-    return cub::DeviceScan::ExclusiveSum(t, b, flags.p, ray_idx.p, static_cast<int>(P), st);
-  }, 2);
+  scan_exclusive<uint32_t>(flags.p, ray_idx.p, P);
   uint32_t last_idx = 0, last_flag = 0;
   fetch({{&last_idx, ray_idx.p + (P - 1), sizeof(uint32_t)}, {&last_flag, flags.p + (P - 1), sizeof(uint32_t)}});
   const uint32_t R = last_idx + last_flag;
@@ -758,7 +827,7 @@ void vxg_handle::order_rehash_frames(const std::vector<uint32_t>& frames, const 
     uint32_t *sk = nullptr, *sv = nullptr;
     // rank = first-appearance rank inside the frame
     k_rhb_init<<<grid_for(n), 256, 0, st>>>(n, static_cast<uint32_t>(G), dP, segs.p, pb, rg, k0, v0);
-    lsd_sort<8, 12, 4>(n, gb + pb, k0, v0, k1, v1, &sk, &sv, false);
+    sort_pairs32(n, gb + pb, k0, v0, k1, v1, &sk, &sv);
     k_rhb_rank<<<grid_for(n), 256, 0, st>>>(n, dP, rg, sv, rank);
     launches += 2;
     for (uint32_t e = 0; e < E; ++e) {
@@ -767,12 +836,12 @@ void vxg_handle::order_rehash_frames(const std::vector<uint32_t>& frames, const 
       CU(cudaMemsetAsync(fo.p, 0xFF, fo_total[e] * sizeof(uint32_t), st));
       k_rhb_fo<<<grid_for(n), 256, 0, st>>>(n, dPe, rg, segs.p, rank, prev, fo.p);
       k_rhb_pos_desc<<<grid_for(n), 256, 0, st>>>(n, dPe, rg, rank, prev, kb, k0, v0);
-      lsd_sort<8, 12, 4>(n, gb + kb + 1, k0, v0, k1, v1, &sk, &sv, false);
+      sort_pairs32(n, gb + kb + 1, k0, v0, k1, v1, &sk, &sv);
       uint32_t* kf = sk == k0 ? k1 : k0;  // free key buffer
       uint32_t* vf = sv == v0 ? v1 : v0;  // free value buffer
       k_rhb_fo_desc<<<grid_for(n), 256, 0, st>>>(n, dPe, rg, sv, segs.p, rank, fo.p, kb, kf);
       uint32_t *sk2 = nullptr, *sv2 = nullptr;
-      lsd_sort<8, 12, 4>(n, gb + kb + 1, kf, sv, sk, vf, &sk2, &sv2, false);
+      sort_pairs32(n, gb + kb + 1, kf, sv, sk, vf, &sk2, &sv2);
       k_rhb_commit<<<grid_for(n), 256, 0, st>>>(n, dPe, rg, sv2, prev, ovals.p);
       launches += 4;
       CU(cudaGetLastError());
@@ -799,25 +868,22 @@ void vxg_handle::build_rays_grouped(const float* dxyz, const uint8_t* drgb, uint
   if (end_bit <= 32) {  // 32-bit keys: half the sort traffic
     uint32_t* k32 = reinterpret_cast<uint32_t*>(pkeys.ensure((P + 1) / 2));
     uint32_t* k32b = reinterpret_cast<uint32_t*>(pkeys2.ensure((P + 1) / 2));
-    uint32_t* u32 = reinterpret_cast<uint32_t*>(okeys.ensure((P + 1) / 2));
     k_group_keys<uint32_t><<<grid_for(P), 256, 0, st>>>(dxyz, P, d_off.p, d_poses.p, F, tp, rb, kb, k32, pvals.p,
                                                         counters.p);
     ++launches;
     CU(cudaGetLastError());
     // stable sort by (frame, terminal voxel): the custom LSD sort, 8-bit digits
     uint32_t *sk = nullptr, *sv = nullptr;
-    lsd_sort<8, 12, 4>(P, end_bit, k32, pvals.p, k32b, pvals2.p, &sk, &sv, false);  // frames stay contiguous
+    sort_pairs32(P, end_bit, k32, pvals.p, k32b, pvals2.p, &sk, &sv);  // frames stay contiguous
     if (sk != k32b) {  // even pass count: the result is in the first buffers
       pkeys.swap(pkeys2);
       pvals.swap(pvals2);
       k32 = reinterpret_cast<uint32_t*>(pkeys.p);
       k32b = reinterpret_cast<uint32_t*>(pkeys2.p);
     }
-    cub([&](void* t, size_t& b) {
-      return cub::DeviceRunLengthEncode::Encode(t, b, k32b, u32, ucounts.p, num_segs.p, static_cast<int>(P), st);
-    }, 2);
-    k_widen_keys<<<grid_for(P), 256, 0, st>>>(num_segs.p, u32, ukeys.p);
-    ++launches;
+    // one bucket per run of equal keys: heads, their ranks, (key, start) per bucket
+    uoffs.ensure(P);
+    scan_with<uint32_t>(SegHeadIn<uint32_t>{k32b}, SegHeadOut<uint32_t>{k32b, P, ukeys.p, uoffs.p, num_segs.p}, P);
     pt_w.ensure(P);
     pt_c.ensure(P);
     k_point_prep<uint32_t><<<grid_for(P), 256, 0, st>>>(P, k32b, pvals2.p, dxyz, drgb, d_poses.p, tp, kb, pt_w.p,
@@ -831,14 +897,10 @@ void vxg_handle::build_rays_grouped(const float* dxyz, const uint8_t* drgb, uint
                                                                   pkeys.p, pvals.p, counters.p);
     ++launches;
     CU(cudaGetLastError());
-    cub([&](void* t, size_t& b) {
-      return cub::DeviceRadixSort::SortPairs(t, b, pkeys.p, pkeys2.p, pvals.p, pvals2.p, static_cast<int>(P), 0,
-                                             end_bit, st);
-    }, 2 + (end_bit + 7) / 8);
-    cub([&](void* t, size_t& b) {
-      return cub::DeviceRunLengthEncode::Encode(t, b, pkeys2.p, ukeys.p, ucounts.p, num_segs.p, static_cast<int>(P),
-                                                st);
-    }, 2);
+    sort_pairs64(pkeys.p, pvals.p, P, end_bit, false, pkeys2.p, pvals2.p);
+    uoffs.ensure(P);
+    scan_with<uint32_t>(SegHeadIn<unsigned long long>{pkeys2.p},
+                        SegHeadOut<unsigned long long>{pkeys2.p, P, ukeys.p, uoffs.p, num_segs.p}, P);
     pt_w.ensure(P);
     pt_c.ensure(P);
     k_point_prep<unsigned long long><<<grid_for(P), 256, 0, st>>>(P, pkeys2.p, pvals2.p, dxyz, drgb, d_poses.p, tp, kb,
@@ -848,10 +910,10 @@ void vxg_handle::build_rays_grouped(const float* dxyz, const uint8_t* drgb, uint
   }
   uint32_t S = 0;
   fetch({{&S, num_segs.p, sizeof(uint32_t)}});
-  uoffs.ensure(std::max<uint32_t>(S, 1));
-  cub([&](void* t, size_t& b) {
-    return cub::DeviceScan::ExclusiveSum(t, b, ucounts.p, uoffs.p, static_cast<int>(S), st);
-  }, 2);
+  if (S) {
+    k_seg_counts<<<grid_for(S), 256, 0, st>>>(S, P, uoffs.p, ucounts.p);
+    ++launches;
+  }
   segs.ensure(std::max<uint32_t>(S, 1));
   seg_count.ensure(F);
   seg_start.ensure(F);
@@ -901,9 +963,7 @@ void vxg_handle::build_rays_grouped(const float* dxyz, const uint8_t* drgb, uint
   launches += 2;
   CU(cudaGetLastError());
   const int obits = std::min(64, fb + 2 * pb + 1);
-  cub([&](void* t, size_t& b) {
-    return cub::DeviceRadixSort::SortPairs(t, b, okeys.p, okeys2.p, ovals.p, ovals2.p, static_cast<int>(S), 0, obits, st);
-  }, 2 + (obits + 7) / 8);
+  sort_pairs64(okeys.p, ovals.p, S, obits, false, nullptr, ovals2.p);
   std::swap(ovals.p, ovals2.p);
   std::swap(ovals.cap, ovals2.cap);
   std::vector<uint32_t> rehashing;
@@ -936,9 +996,7 @@ uint64_t vxg_handle::count_rays(uint32_t R, uint32_t F) {
                                            far_rays.p);
   ++launches;
   CU(cudaGetLastError());
-  cub([&](void* t, size_t& b) {
-    return cub::DeviceScan::ExclusiveSum(t, b, rcount.p, roff.p, static_cast<int>(R), st);
-  }, 2);
+  scan_exclusive<unsigned long long>(rcount.p, roff.p, R);
   unsigned long long tail[2] = {0, 0};
   fetch({{&tail[0], roff.p + (R - 1), sizeof(unsigned long long)},
          {&tail[1], rcount.p + (R - 1), sizeof(unsigned long long)}});
@@ -959,15 +1017,15 @@ uint64_t vxg_handle::count_rays(uint32_t R, uint32_t F) {
 // 3.88; 12:9,0:4,4:8 4.15; plain LSD 4.29 vs 3.77 ms for the default.
 std::vector<std::pair<int, int>> grouped_digit_plan(int kbits);
 
-template <int kBits, int kIpt, int kMB>
+template <int kBits, int kIpt, int kMB, int kNs>
 void vxg_handle::lsd_sort(uint64_t T, int kbits, uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1,
                           uint32_t** sk, uint32_t** sv, bool grouped, uint32_t K) {
-  using C = SortCfg<kBits, kIpt>;
+  using C = SortCfg<kBits, kIpt, kNs>;
   static bool attr = false;
   if (!attr) {
-    CU(cudaFuncSetAttribute(k_sort_downsweep<kBits, kIpt, kMB, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(sizeof(typename C::Smem))));
-    CU(cudaFuncSetAttribute(k_sort_downsweep<kBits, kIpt, kMB, true, true, true>,
+    CU(cudaFuncSetAttribute(k_sort_downsweep<kBits, kIpt, kMB, true, true, false, kNs>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(typename C::Smem))));
+    CU(cudaFuncSetAttribute(k_sort_downsweep<kBits, kIpt, kMB, true, true, true, kNs>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(typename C::Smem))));
     attr = true;
   }
@@ -1004,17 +1062,15 @@ void vxg_handle::lsd_sort(uint64_t T, int kbits, uint32_t* k0, uint32_t* v0, uin
     const uint64_t nc = static_cast<uint64_t>(mask + 1u) * S;
     sort_counts.ensure(nc);
     sort_offs.ensure(nc);
-    k_sort_upsweep<kBits, kIpt><<<S, kSortThreads, 0, st>>>(ki, T, shift, mask, S, sort_counts.p);
-    cub([&](void* t, size_t& b) {
-      return cub::DeviceScan::ExclusiveSum(t, b, sort_counts.p, sort_offs.p, static_cast<int>(nc), st);
-    }, 2);
+    k_sort_upsweep<kBits, kIpt, kNs><<<S, kSortThreads, 0, st>>>(ki, T, shift, mask, S, sort_counts.p);
+    scan_exclusive<uint32_t>(sort_counts.p, sort_offs.p, nc);
     if (marks_fused && q + 1 == passes)
-      k_sort_downsweep<kBits, kIpt, kMB, true, true, true><<<S, kSortThreads, sizeof(typename C::Smem), st>>>(
+      k_sort_downsweep<kBits, kIpt, kMB, true, true, true, kNs><<<S, kSortThreads, sizeof(typename C::Smem), st>>>(
           ki, vi, ko, vo, T, shift, mask, S, sort_offs.p, K, dense_start.p, dense_end.p);
     else
-      k_sort_downsweep<kBits, kIpt, kMB, true, true><<<S, kSortThreads, sizeof(typename C::Smem), st>>>(
+      k_sort_downsweep<kBits, kIpt, kMB, true, true, false, kNs><<<S, kSortThreads, sizeof(typename C::Smem), st>>>(
           ki, vi, ko, vo, T, shift, mask, S, sort_offs.p);
-    launches += 2;
+    launches += 2;  // (+ the prefix-sum kernels, counted by scan_exclusive)
     CU(cudaGetLastError());
     std::swap(ki, ko);
     std::swap(vi, vo);
@@ -1044,22 +1100,6 @@ std::vector<std::pair<int, int>> grouped_digit_plan(int kbits) {
 }
 
 void vxg_handle::sort_records(uint64_t T, int kbits, uint32_t** sk, uint32_t** sv, uint32_t K) {
-  static const bool use_cub = [] {  // dev A/B: VXG_SORT=cub
-    const char* e = getenv("VXG_SORT");
-    return e && std::string(e) == "cub";
-  }();
-  if (use_cub) {
-    const int nb = std::max(kbits, 1);
-    cub([&](void* t, size_t& b) {
-      return cub::DeviceRadixSort::SortPairs(t, b, rkeys.p, rkeys2.p, rvals.p, rvals2.p, static_cast<int>(T), 0, nb,
-                                             st);
-    }, 2 + (nb + 7) / 8);
-    info_sort_passes = static_cast<uint64_t>((nb + 7) / 8);
-    marks_fused = false;
-    *sk = rkeys2.p;
-    *sv = rvals2.p;
-    return;
-  }
   int maxb = 0;
   for (const auto& d : grouped_digit_plan(kbits)) maxb = std::max(maxb, d.second);
   if (maxb > 8)
@@ -1103,37 +1143,36 @@ void vxg_handle::sort_fold(uint64_t T, uint64_t nslots, uint32_t F) {
     ++launches;
   }
   // compact the runs in key order
-  run_flag.ensure(K);
-  run_pos.ensure(K);
   if (K > run_keys.cap || K > run_len.cap || K > run_start.cap || !num_runs.p || !work.p) sync_folds();
   run_keys.ensure(K);
   run_len.ensure(K);
   run_start.ensure(K);
   num_runs.ensure(1);
   work.ensure(2);
-  k_run_flags<<<grid_for(K), 256, 0, st>>>(static_cast<uint32_t>(K), dense_end.p, run_flag.p);
-  ++launches;
-  cub([&](void* t, size_t& b) {
-    return cub::DeviceScan::ExclusiveSum(t, b, run_flag.p, run_pos.p, static_cast<int>(K), st);
-  }, 2);
-  k_run_scatter<<<grid_for(K), 256, 0, st>>>(static_cast<uint32_t>(K), run_flag.p, run_pos.p, dense_start.p,
-                                              dense_end.p, run_keys.p, run_start.p, run_len.p, num_runs.p);
-  ++launches;
-  CU(cudaGetLastError());
+  scan_with<uint32_t>(RunIn{dense_end.p},
+                      RunOut{K, dense_start.p, dense_end.p, run_keys.p, run_start.p, run_len.p, num_runs.p}, K);
   uint32_t nruns = 0;
   fetch({{&nruns, num_runs.p, sizeof(uint32_t)}});
   if (std::max<uint32_t>(nruns, 1) > std::min(run_len2.cap, run_order.cap)) sync_folds();
   run_len2.ensure(std::max<uint32_t>(nruns, 1));
   run_order.ensure(std::max<uint32_t>(nruns, 1));
   run_iota.ensure(std::max<uint32_t>(nruns, 1));
+  run_code.ensure(std::max<uint32_t>(nruns, 1));
+  run_max.ensure(1);
   if (nruns) {
-    k_iota<<<grid_for(nruns), 256, 0, st>>>(nruns, run_iota.p);
+    // fold order: one stable counting pass over a coarse length code, longest
+    // runs first (they bound the fold's critical path), key order inside a
+    // code (run_len_code); run_len2 receives the sorted codes
+    CU(cudaMemsetAsync(run_max.p, 0, sizeof(uint32_t), st));
+    k_run_codes<<<grid_for(nruns), 256, 0, st>>>(nruns, run_len.p, run_code.p, run_iota.p, run_max.p);
     ++launches;
-    const int lbits = bits_for(T);
-    cub([&](void* t, size_t& b) {  // longest runs first: they bound the fold's critical path
-      return cub::DeviceRadixSort::SortPairsDescending(t, b, run_len.p, run_len2.p, run_iota.p, run_order.p,
-                                                       static_cast<int>(nruns), 0, lbits, st);
-    }, 2 + (lbits + 7) / 8);
+    uint32_t *sk = nullptr, *sv = nullptr;
+    const bool mf = marks_fused;
+    const int lp = last_lsd_passes;
+    sort_pairs32(nruns, 8, run_code.p, run_iota.p, run_len2.p, run_order.p, &sk, &sv);
+    marks_fused = mf;
+    last_lsd_passes = lp;
+    if (sk != run_len2.p) throw VxgError(VXG_ECUDA, "run order sort: unexpected pass count");
   }
   end(T, 0);
   ensure_fold_streams();
@@ -1143,7 +1182,7 @@ void vxg_handle::sort_fold(uint64_t T, uint64_t nslots, uint32_t F) {
       CU(cudaStreamSynchronize(st));
       drain_tops();
     }
-    CU(cudaMemcpyAsync(top_pinned + n_top++, run_len2.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(top_pinned + n_top++, run_max.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   }
   uint8_t* tch = consumers.empty() ? nullptr : touched.p;
   CU(cudaMemsetAsync(work.p, 0, 2 * sizeof(uint32_t), st));
@@ -1345,16 +1384,12 @@ void vxg_handle::emit_and_apply(uint32_t R, uint32_t F, const TermView& tv) {
   // warps); the records still land at their ray-order offsets.
   ray_perm.ensure(R);
   ray_iota.ensure(R);
-  rcount2.ensure(R);
   ckeys.ensure(R);
   k_iota<<<grid_for(R), 256, 0, st>>>(R, ray_iota.p);
   k_chunk_keys<<<grid_for(R), 256, 0, st>>>(R, rcount.p, chunk_base.p, nch, ckeys.p);
   launches += 2;
   const int cbits = 16 + bits_for(nch - 1);
-  cub([&](void* t, size_t& b) {
-    return cub::DeviceRadixSort::SortPairsDescending(t, b, ckeys.p, rcount2.p, ray_iota.p, ray_perm.p,
-                                                     static_cast<int>(R), 0, cbits, st);
-  }, 2 + (cbits + 7) / 8);
+  sort_pairs64(ckeys.p, ray_iota.p, R, cbits, true, nullptr, ray_perm.p);
   ensure_touched();
   fetch({{hb.data(), chunk_base.p, hb.size() * sizeof(unsigned long long)}});
   d_upd.ensure(F);
@@ -1519,12 +1554,10 @@ void vxg_handle::shard_front(uint32_t R, uint32_t F, const TermView& tv) {
   launches += 2;
   CU(cudaGetLastError());
   const int obits = bits_for(static_cast<uint64_t>(shard_world));
-  cub([&](void* t, size_t& b) {  // stable partition by owner (invalid records: owner == world, last)
-    return cub::DeviceRadixSort::SortPairs(t, b, gowner.p, gowner2.p, giota.p, gperm.p, static_cast<int>(T), 0, obits,
-                                           st);
-  }, 3);
+  uint32_t *so = nullptr, *sp = nullptr;  // stable partition by owner (invalid records: owner == world, last)
+  sort_pairs32(T, obits, gowner.p, giota.p, gowner2.p, gperm.p, &so, &sp);
   obounds.ensure(shard_world + 1);
-  k_owner_bounds<<<1, 64, 0, st>>>(T, gowner2.p, static_cast<uint32_t>(shard_world), obounds.p);
+  k_owner_bounds<<<1, 64, 0, st>>>(T, so, static_cast<uint32_t>(shard_world), obounds.p);
   ++launches;
   std::vector<unsigned long long> bnd(shard_world + 1);
   CU(cudaMemcpyAsync(bnd.data(), obounds.p, (shard_world + 1) * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
@@ -1536,7 +1569,7 @@ void vxg_handle::shard_front(uint32_t R, uint32_t F, const TermView& tv) {
   const uint64_t n_valid = bnd[shard_world];
   send_buf.ensure(std::max<uint64_t>(n_valid, 1));
   if (n_valid) {
-    k_gather_send<<<grid_for(n_valid), 256, 0, st>>>(n_valid, gperm.p, gkeys.p, gvals.p, send_buf.p);
+    k_gather_send<<<grid_for(n_valid), 256, 0, st>>>(n_valid, sp, gkeys.p, gvals.p, send_buf.p);
     ++launches;
     CU(cudaGetLastError());
   }
@@ -2337,9 +2370,7 @@ int vxg_mesh_extract(vxg_handle* h, const vxg_mc_tables* tables, const int32_t* 
       k_mc_count<<<grid, 256, 0, h->st>>>(nc, h->mesh_slots.p, h->view(), h->mesh_tab.p, h->mesh_ntri.p);
       CU(cudaMemsetAsync(h->mesh_ntri.p + nc, 0, sizeof(uint32_t), h->st));
       ++h->launches;
-      h->cub([&](void* t, size_t& b) {
-        return cub::DeviceScan::ExclusiveSum(t, b, h->mesh_ntri.p, h->mesh_off.p, static_cast<int>(nc + 1), h->st);
-      }, 2);
+      h->scan_exclusive<uint32_t>(h->mesh_ntri.p, h->mesh_off.p, nc + 1);
       // fragment boundaries: the scan at every block's first cube (+ the total)
       h->mesh_frag_dev.ensure(B + 1);
       k_gather_stride<<<grid_for(B + 1), 256, 0, h->st>>>(B + 1, h->mesh_off.p, static_cast<uint64_t>(h->nvox),
@@ -2797,10 +2828,19 @@ extern "C" int vxg_debug_top_runs(vxg_handle* h, uint32_t* len, uint32_t* keys, 
   return guarded([&] {
     set_device(h);
     h->settle();
-    std::vector<uint32_t> ord(n);
-    CU(cudaMemcpy(len, h->run_len2.p, n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
-    CU(cudaMemcpy(ord.data(), h->run_order.p, n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
-    for (uint32_t i = 0; i < n; ++i) CU(cudaMemcpy(&keys[i], h->run_keys.p + ord[i], 4, cudaMemcpyDeviceToHost));
+    // (the fold order is by length code, key order inside a code: the first n
+    // runs are among the longest, not exactly the n longest)
+    uint32_t nruns = 0;
+    CU(cudaMemcpy(&nruns, h->num_runs.p, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    const uint32_t m = std::min(n, nruns);
+    std::vector<uint32_t> ord(m), rl(nruns), rk(nruns);
+    CU(cudaMemcpy(ord.data(), h->run_order.p, m * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(rl.data(), h->run_len.p, nruns * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(rk.data(), h->run_keys.p, nruns * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    for (uint32_t i = 0; i < n; ++i) {
+      keys[i] = i < m ? rk[ord[i]] : 0xFFFFFFFFu;
+      len[i] = i < m ? rl[ord[i]] : 0u;
+    }
   });
 }
 
