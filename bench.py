@@ -466,6 +466,9 @@ def run_vxg_arm(args):
                               + ("" if nf == F else "; the remaining frames are not timed (rate extrapolated)")),
                    "median_insert_ms": 1e3 * statistics.median(per_f), "frames": nf, "nproc": os.cpu_count()}
 
+    api_streamed = ("vxg_stage_packed + vxg_integrate_staged (pinned host input, the next batch staged before this "
+                    "one is integrated)")
+    api_sync = "vxg_integrate_packed (pinned host input, H2D then compute)"
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -481,13 +484,15 @@ def run_vxg_arm(args):
             "work": {"points_per_step": P, "updates_per_step": n_upd, "frames_per_call": FC,
                      "records_per_step": n_rec, "n_vox_per_step": n_vox, "longest_fold_chain": info["max_chain"],
                      "blocks": info["blocks"], "sort_passes": passes},
-            "e2e": {"value": total_updates / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
-                    "api": "vxg_stage_packed + vxg_integrate_staged (pinned host input, the next batch staged "
-                           "before this one is integrated)",
+            # both host-input entry points are timed with their H2D copies inside the region; the headline is
+            # the faster one ON THIS BOX (the streamed path depends on how well the box overlaps DMA with compute)
+            "e2e": {"value": total_updates / (min(e2e_ms, e2e_sync_ms) / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": min(e2e_ms, e2e_sync_ms),
+                    "api": api_streamed if e2e_ms <= e2e_sync_ms else api_sync,
                     "h2d_gbs_in_run": h2d_gbs,
+                    "streamed": {"value": total_updates / (e2e_ms / 1e3), "ms_per_step": e2e_ms, "api": api_streamed},
                     "sync_one_call": {"value": total_updates / (e2e_sync_ms / 1e3), "ms_per_step": e2e_sync_ms,
-                                      "api": "vxg_integrate_packed (pinned host input, H2D then compute)"}},
+                                      "api": api_sync}},
             "latency_f1": lat,
             "ms_per_frame_f1": lat["median_ms"] if lat else None,
             "roofline": roofline,

@@ -1182,7 +1182,10 @@ __device__ __forceinline__ uint32_t count_long_runs(const uint32_t* __restrict__
 // into a kRingStages-deep shared-memory ring; the consumer only folds. mbarrier
 // full/empty per stage hand chunks over, so the consumer's serial chain never
 // waits on global memory or on the weighing arithmetic.
-constexpr int kRingStages = 4;
+#ifndef VXG_RING_STAGES
+#define VXG_RING_STAGES 4
+#endif
+constexpr int kRingStages = VXG_RING_STAGES;
 
 struct alignas(32) PreRec {  // one record as handed to the long-run consumer (one 32-byte sector)
   float W;   // weight before this update (the producer's W scan)
@@ -1333,7 +1336,8 @@ __device__ __forceinline__ void fold_long_pairs(
         // The weight chain W_{i+1} = min(W_i + w_i, Wmax) does not depend on
         // the distance or the colours: run it here and hand each record its
         // W_i, T_i = RN(W_i + w_i), reciprocal, RN(w clamp(d)), RN(w n_c).
-        long long pwait = 0, pbusy0 = dbg != nullptr ? clock64() : 0, pt_weigh = 0, pt_scan = 0;
+        long long pwait = 0, pbusy0 = dbg != nullptr ? clock64() : 0, pt_weigh = 0, pt_scan = 0, pt_top = 0, pt_pre = 0,
+                  pt_store = 0;
         float W = vp->weight;
         // pipeline (gather latency ~ a whole chunk of the consumer's chain):
         // rays three chunks ahead, their ids five chunks ahead
@@ -1357,6 +1361,7 @@ __device__ __forceinline__ void fold_long_pairs(
         // records are weighed one chunk ahead of their hand-over
         Upd u_next = weigh_at(lane, ray_at(lane, id_at(lane)));
         for (uint32_t k = 0; k < nchunks; ++k, ++kk) {
+          const long long tt0 = dbg != nullptr ? clock64() : 0;
           const uint32_t j = k * 32 + lane;
           const FoldIn ry3 = ray_at(j + 96, v3);
           v3 = v4;
@@ -1364,6 +1369,7 @@ __device__ __forceinline__ void fold_long_pairs(
           const uint32_t cnt = min(32u, c.len - k * 32);
           const Upd u = u_next;
           const long long tp0 = dbg != nullptr ? clock64() : 0;
+          pt_top += tp0 - tt0;
           u_next = weigh_at(j + 32, ry1);
           if (dbg != nullptr) {  // force the weighing to complete before the timestamp
             asm volatile("" ::"f"(u_next.d), "f"(u_next.w));
@@ -1414,6 +1420,7 @@ __device__ __forceinline__ void fold_long_pairs(
             asm volatile("" ::"f"(W), "f"(Wmine));
             pt_scan += clock64() - tp1;
           }
+          const long long tp2 = dbg != nullptr ? clock64() : 0;
           PreRec pr;
           const float clamped = u.d < -tp.truncation ? -tp.truncation : (tp.truncation < u.d ? tp.truncation : u.d);
           pr.W = Wmine;
@@ -1453,21 +1460,28 @@ __device__ __forceinline__ void fold_long_pairs(
           hd.hi[1] = __reduce_min_sync(0xffffffffu, hi1);
           hd.hi[2] = __reduce_min_sync(0xffffffffu, hi2);
           const int s = static_cast<int>(kk % kRingStages);
+          if (dbg != nullptr) asm volatile("" ::"r"(hd.hi[2]), "r"(hd.lo[0]), "f"(pr.r1));
           const long long tw0 = dbg != nullptr ? clock64() : 0;
+          pt_pre += tw0 - tp2;
           if (kk >= kRingStages) mbar_wait(&ring_empty[pair][s], ((kk / kRingStages) - 1) & 1u);
-          if (dbg != nullptr) pwait += clock64() - tw0;
+          const long long tw1 = dbg != nullptr ? clock64() : 0;
+          pwait += tw1 - tw0;
           ring[pair][s][lane] = pr;
           if (lane == 0) ring_hdr[pair][s] = hd;
           __syncwarp();
           if (lane == 0) mbar_arrive(&ring_full[pair][s]);
           ry1 = ry2;
           ry2 = ry3;
+          if (dbg != nullptr) pt_store += clock64() - tw1;
         }
         if (dbg != nullptr && lane == 0) {
           atomicAdd(&dbg[4 * n_all + 4], static_cast<unsigned long long>(pwait));
           atomicAdd(&dbg[4 * n_all + 5], static_cast<unsigned long long>(clock64() - pbusy0));
           atomicAdd(&dbg[4 * n_all + 6], static_cast<unsigned long long>(pt_weigh));
           atomicAdd(&dbg[4 * n_all + 7], static_cast<unsigned long long>(pt_scan));
+          atomicAdd(&dbg[4 * n_all + 14], static_cast<unsigned long long>(pt_top));
+          atomicAdd(&dbg[4 * n_all + 15], static_cast<unsigned long long>(pt_pre));
+          atomicAdd(&dbg[4 * n_all + 16], static_cast<unsigned long long>(pt_store));
         }
       } else {
         VoxState st = load_vox(vp);

@@ -1196,8 +1196,8 @@ void vxg_handle::sort_fold(uint64_t T, uint64_t nslots, uint32_t F) {
       1, std::min<uint64_t>(static_cast<uint64_t>(dev_sms), (nruns + 3) / 4)));
   unsigned long long* dbg = nullptr;
   if (debug_fold) {
-    fold_dbg.ensure(4 * nruns + 16);
-    CU(cudaMemsetAsync(fold_dbg.p, 0, (4 * nruns + 16) * sizeof(unsigned long long), st));
+    fold_dbg.ensure(4 * nruns + 20);
+    CU(cudaMemsetAsync(fold_dbg.p, 0, (4 * nruns + 20) * sizeof(unsigned long long), st));
     CU(cudaMemsetAsync(fold_dbg.p + 4 * nruns + 1, 0xFF, sizeof(unsigned long long), st));
     dbg = fold_dbg.p;
     fold_dbg_n = nruns;
@@ -2817,7 +2817,7 @@ extern "C" int vxg_debug_fold(vxg_handle* h, int enable, unsigned long long* out
     h->debug_fold = enable != 0;
     if (n) *n = h->fold_dbg_n;
     if (out && h->fold_dbg.p) {
-      const uint64_t m = std::min<uint64_t>(cap, 4ull * h->fold_dbg_n + 16);
+      const uint64_t m = std::min<uint64_t>(cap, 4ull * h->fold_dbg_n + 20);
       CU(cudaMemcpy(out, h->fold_dbg.p, m * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     }
   });

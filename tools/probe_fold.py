@@ -21,7 +21,7 @@ integ.integrate_packed(dx.data_ptr(), dc.data_ptr(), off, poses, True)
 print('apply ms', layer.stage_times(True)['apply'][0])
 n = ctypes.c_uint64()
 L.vxg_debug_fold(layer.handle, 0, None, 0, ctypes.byref(n))
-buf = np.zeros(4 * n.value + 16, np.uint64)
+buf = np.zeros(4 * n.value + 20, np.uint64)
 L.vxg_debug_fold(layer.handle, 0, buf.ctypes.data, len(buf), ctypes.byref(n))
 d = buf[:4 * n.value].reshape(-1, 4).astype(np.int64)
 spec = d[:, 3] >> 32
@@ -33,6 +33,8 @@ cw, cb, pw, pb, pwe, psc, cvo, cch = [int(x) for x in buf[4 * n.value + 2:4 * n.
 csp, nsp, cse, nse = [int(x) for x in buf[4 * n.value + 10:4 * n.value + 14]]
 print(f'spec chunks {nsp} at {csp/max(nsp,1):.0f} cycles; other chunks {nse} at {cse/max(nse,1):.0f} cycles')
 nrec = int(d[d[:, 1] > 0][:, 2].sum())
+ptop, ppre, pstore = [int(x) for x in buf[4 * n.value + 14:4 * n.value + 17]]
+print(f'producer per record: top {ptop/nrec:.1f} prerec {ppre/nrec:.1f} store {pstore/nrec:.1f}')
 print(f'per record (cycles, summed over pairs): consumer busy {cb/nrec:.1f} wait {cw/nrec:.1f} vote {cvo/nrec:.1f} chain {cch/nrec:.1f}; producer busy {pb/nrec:.1f} wait {pw/nrec:.1f} weigh {pwe/nrec:.1f} scan {psc/nrec:.1f}')
 print(f'consumer wait {cw / max(cb, 1):.3f} of busy; producer wait {pw / max(pb, 1):.3f} of busy')
 long_ = d[d[:, 1] > 0]
