@@ -408,12 +408,14 @@ def run_vxg_arm(args):
             t_a = time.perf_counter()
             integ.integrate_packed(hx, hc, o, poses[f:f + 1], False)
             layer.flush()
+            torch.cuda.synchronize()  # vxg_flush only orders the handle's stream behind the fold: wait on the host
             per.append(time.perf_counter() - t_a)
         per_ms = sorted(1e3 * x for x in per)
         lat = {"frames": nl, "median_ms": statistics.median(per_ms),
                "p90_ms": per_ms[min(len(per_ms) - 1, int(0.9 * len(per_ms)))], "mean_ms": statistics.mean(per_ms),
-               "api": "vxg_integrate_packed with F=1 from pinned host memory + vxg_flush (the layer is final "
-                      "when the call returns); host steady clock per call, like cli.cpp:171-174"}
+               "api": "vxg_integrate_packed with F=1 from pinned host memory + vxg_flush + a host wait for the "
+                      "device (the layer is final in HBM when the clock stops); host steady clock per call, like "
+                      "cli.cpp:171-174"}
 
     # ---- rooflines (SURVEY.md 8d accounting): HBM-bound stages,
     # achieved = algorithmic bytes / the stage's CUDA-event time on the launching stream

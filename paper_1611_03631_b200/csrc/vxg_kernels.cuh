@@ -74,6 +74,7 @@ struct TsdfParams {
   float max_ray;
   int weight_mode;
   int merge_mode;
+  uint32_t long_code;  // fold: runs whose length code (run_len_code) is >= this go to the warp pairs
 };
 
 __device__ __forceinline__ uint32_t frame_of(const uint64_t* off, uint32_t F, uint64_t i) {
@@ -1164,11 +1165,15 @@ static_assert(kLongRun >= 16u && (kLongRun & ((1u << (floor_log2_c(kLongRun) - 3
               "kLongRun must be the first length of its run-length code (run_len_code)");
 
 // Long runs come first in the fold order: sorted_code holds kRunCodeMax -
-// run_len_code(length) in ascending order, and len >= kLongRun <=> code(len)
-// >= code(kLongRun) because kLongRun starts a code.
-__device__ __forceinline__ uint32_t count_long_runs(const uint32_t* __restrict__ sorted_code, uint32_t nruns) {
-  const uint32_t thr = kRunCodeMax - run_len_code(kLongRun);
-  uint32_t lo = 0, hi = nruns;  // first index whose run is shorter than kLongRun
+// run_len_code(length) in ascending order; a run is long when its code is >=
+// long_code. The host picks long_code per fold (vxg_handle::long_code_for):
+// code(kLongRun) for full batches (kLongRun starts a code, so that is len >=
+// kLongRun), lower for small ones, where the thread-per-run path would leave
+// one thread folding a thousand-record run while the GPU idles.
+__device__ __forceinline__ uint32_t count_long_runs(const uint32_t* __restrict__ sorted_code, uint32_t nruns,
+                                                    uint32_t long_code) {
+  const uint32_t thr = kRunCodeMax - long_code;
+  uint32_t lo = 0, hi = nruns;  // first index whose run is short
   while (lo < hi) {
     const uint32_t mid = (lo + hi) >> 1;
     if (sorted_code[mid] <= thr) lo = mid + 1; else hi = mid;
@@ -1712,7 +1717,7 @@ __global__ void __launch_bounds__(64 * kP, 1) k_fold_runs(
   __syncthreads();
   const uint32_t nruns = *num_runs_p;
   uint32_t n_long = 0;
-  if ((threadIdx.x & 31) == 0) n_long = count_long_runs(sorted_len, nruns);
+  if ((threadIdx.x & 31) == 0) n_long = count_long_runs(sorted_len, nruns, tp.long_code);
   n_long = __shfl_sync(0xffffffffu, n_long, 0);
   fold_long_pairs<kP, kSep>(S, static_cast<int>(threadIdx.x >> 5), poses, nruns, n_long, order, ukeys, ustart, ulen,
                             svals, rays, far, map, tp, touched, work, dbg);
@@ -1804,7 +1809,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_fold_short(
   {
     const uint32_t nruns = *num_runs_p;
     uint32_t n_long = 0;
-    if ((threadIdx.x & 31) == 0) n_long = count_long_runs(sorted_len, nruns);
+    if ((threadIdx.x & 31) == 0) n_long = count_long_runs(sorted_len, nruns, tp.long_code);
     n_long = __shfl_sync(0xffffffffu, n_long, 0);
     fold_short_loop<kC>(poses, nruns, n_long, order, ukeys, ustart, ulen, svals, rays, far, map, tp, touched, work);
   }
@@ -1830,7 +1835,7 @@ __global__ void __launch_bounds__(512, 1) k_fold_all(
   __syncthreads();
   const uint32_t nruns = *num_runs_p;
   uint32_t n_long = 0;
-  if ((threadIdx.x & 31) == 0) n_long = count_long_runs(sorted_len, nruns);
+  if ((threadIdx.x & 31) == 0) n_long = count_long_runs(sorted_len, nruns, tp.long_code);
   n_long = __shfl_sync(0xffffffffu, n_long, 0);
   const int wid = static_cast<int>(threadIdx.x >> 5);
   if (wid >= 8)

@@ -281,7 +281,23 @@ struct vxg_handle {
     t.max_ray = cfg.max_ray_length;
     t.weight_mode = cfg.weight_mode;
     t.merge_mode = cfg.merge_mode;
+    t.long_code = run_len_code(kLongRun);
     return t;
+  }
+  // Length code from which a run of a fold over T records goes to the warp
+  // pairs (21 ns per record, one run per pair) instead of one thread (~250 ns
+  // per record, 32 runs per warp). The thread path has ~3x the throughput, the
+  // pair path 12x less latency per run: a run should take the pair path when
+  // folding it in one thread would outlast the rest of the fold, i.e. when
+  // its length exceeds a fixed fraction of T (kLongRun / 2.4e8 on the cfg1
+  // batch the threshold was tuned on). Full batches keep kLongRun; a single
+  // 640x480 frame (2 M records) sends runs >= 64 to the pairs.
+  static uint32_t long_code_for(uint64_t T) {
+    static const bool fixed = getenv("VXG_FIXED_LONG_RUN") != nullptr;  // dev A/B
+    if (fixed) return run_len_code(kLongRun);
+    const double want = static_cast<double>(T) * (static_cast<double>(kLongRun) / 2.4e8);
+    const uint32_t len = static_cast<uint32_t>(std::min<double>(kLongRun, std::max(64.0, want)));
+    return run_len_code(len);
   }
 
   cudaEvent_t ev() {
@@ -1114,7 +1130,8 @@ void vxg_handle::sort_records(uint64_t T, int kbits, uint32_t** sk, uint32_t** s
 // Sorts the T records of one attempt (keys < nslots * vps^3, or invalid) and
 // folds every voxel's run in ray order.
 void vxg_handle::sort_fold(uint64_t T, uint64_t nslots, uint32_t F) {
-  const TsdfParams tp = params();
+  TsdfParams tp = params();
+  tp.long_code = long_code_for(T);
   begin(ST_SORT);
   const uint64_t K = std::max<uint64_t>(1, std::min<uint64_t>(nslots, cap_blocks) * static_cast<uint64_t>(nvox));
   const int kbits = bits_for(K);  // every valid key < K <= 2^kbits - 1: the invalid key sorts last
