@@ -1288,6 +1288,10 @@ struct LongSmem {
   float4 wscan[kP][8];  // the chunk's 32 weights, broadcast to the producer lanes
   ChunkHdr ring_hdr[kP][kRingStages];
   uint2 spec_tab[kP][2][32];  // per record: its step as a map over 7 candidate distances (+ dead), one byte each
+  // two producers per run (kProd = 2) alternate chunks: chunk c's producer hands the weight after it to
+  // chunk c+1's through wbox[c & 1] / wfull[c & 1]
+  float wbox[kP][2];
+  unsigned long long wfull[kP][2];
 };
 
 template <int kP>
@@ -1297,6 +1301,7 @@ __device__ __forceinline__ void long_smem_init(LongSmem<kP>& S) {
     mbar_init(&S.ring_full[threadIdx.x / kRingStages][threadIdx.x % kRingStages], 1);
     mbar_init(&S.ring_empty[threadIdx.x / kRingStages][threadIdx.x % kRingStages], 1);
   }
+  if (threadIdx.x < kP * 2) mbar_init(&S.wfull[threadIdx.x / 2][threadIdx.x % 2], 1);
 }
 
 // Long runs (>= kLongRun records), one producer/consumer warp pair per run,
@@ -1304,7 +1309,7 @@ __device__ __forceinline__ void long_smem_init(LongSmem<kP>& S) {
 // 2 kP pair warps (named barriers 1..kP). kSep: consumers only on
 // sub-partitions 0 and 1 (warp & 3 < 2), producers on 2 and 3, so no consumer
 // shares its scheduler with a producer.
-template <int kP, bool kSep>
+template <int kP, bool kSep, int kProd = 1>
 __device__ __forceinline__ void fold_long_pairs(
     LongSmem<kP>& S, const int wid, const float* poses, const uint32_t nruns, const uint32_t n_long,
     const uint32_t* __restrict__ order, const uint32_t* __restrict__ ukeys, const uint32_t* __restrict__ ustart,
@@ -1324,14 +1329,20 @@ __device__ __forceinline__ void fold_long_pairs(
     // default (kP = 4): consumers are warps 4..7 (highest ids: the warp
     // arbiter favours them); pair p = consumer 4+p (sub-partition p) +
     // producer (p+1)&3 (another one)
-    const bool producer = kSep ? (wid & 3) >= 2 : wid < kP;
-    const int pair = kSep ? ((wid >> 2) * 2 + (wid & 1)) : (producer ? ((wid + kP - 1) % kP) : (wid - kP));
-    uint32_t kk = 0;  // chunk counter of this pair across its runs (ring position / phase)
+    // kProd = 2 (kP = 4, the merged grid): warps 0..7 are producers, 8..11 consumers; producer h of pair p
+    // is warp 4 h + ((p + 1 + h) & 3): never on its consumer's sub-partition
+    static_assert(kProd == 1 || (kProd == 2 && kP == 4 && !kSep), "two producers: the kP = 4 merged layout only");
+    const bool producer = kProd == 2 ? wid < 2 * kP : (kSep ? (wid & 3) >= 2 : wid < kP);
+    const int ph = kProd == 2 ? (wid >> 2) : 0;  // which of the run's producers this warp is
+    const int pair = kProd == 2 ? (producer ? (((wid & 3) + 3 - ph) & 3) : (wid - 2 * kP))
+                                : (kSep ? ((wid >> 2) * 2 + (wid & 1)) : (producer ? ((wid + kP - 1) % kP) : (wid - kP)));
+    constexpr int kPairThreads = 32 * (1 + kProd);
+    uint32_t kk0 = 0;  // chunks of this pair's earlier runs (ring position / phase of chunk k: kk0 + k)
     while (true) {
       if (!producer && lane == 0) pair_run[pair] = atomicAdd(&work[0], 1u);
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + pair), "n"(kPairThreads) : "memory");
       const uint32_t r = pair_run[pair];
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");  // pair_run is rewritten next run
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + pair), "n"(kPairThreads) : "memory");  // pair_run is rewritten next run
       if (r >= n_long) break;
       const RunCtx c = run_ctx(map, tp, ukeys, ustart, ulen, order[r]);
       if (c.key == kInvalidRecord) continue;
@@ -1360,22 +1371,24 @@ __device__ __forceinline__ void fold_long_pairs(
           }
           return x;
         };
-        FoldIn ry1 = ray_at(32 + lane, id_at(32 + lane));
-        FoldIn ry2 = ray_at(64 + lane, id_at(64 + lane));
-        uint32_t v3 = id_at(96 + lane), v4 = id_at(128 + lane);
+        // this producer's chunks: ph, ph + kProd, ...; pos(i) = its lane's record of own chunk i
+        auto pos = [&](uint32_t i) { return ((static_cast<uint32_t>(ph) + kProd * i) << 5) + lane; };
+        FoldIn ry1 = ray_at(pos(1), id_at(pos(1)));
+        FoldIn ry2 = ray_at(pos(2), id_at(pos(2)));
+        uint32_t v3 = id_at(pos(3)), v4 = id_at(pos(4));
         // records are weighed one chunk ahead of their hand-over
-        Upd u_next = weigh_at(lane, ray_at(lane, id_at(lane)));
-        for (uint32_t k = 0; k < nchunks; ++k, ++kk) {
+        Upd u_next = weigh_at(pos(0), ray_at(pos(0), id_at(pos(0))));
+        for (uint32_t i = 0, k = ph; k < nchunks; ++i, k += kProd) {
+          const uint32_t kk = kk0 + k;
           const long long tt0 = dbg != nullptr ? clock64() : 0;
-          const uint32_t j = k * 32 + lane;
-          const FoldIn ry3 = ray_at(j + 96, v3);
+          const FoldIn ry3 = ray_at(pos(i + 3), v3);
           v3 = v4;
-          v4 = id_at(j + 160);
+          v4 = id_at(pos(i + 5));
           const uint32_t cnt = min(32u, c.len - k * 32);
           const Upd u = u_next;
           const long long tp0 = dbg != nullptr ? clock64() : 0;
           pt_top += tp0 - tt0;
-          u_next = weigh_at(j + 32, ry1);
+          u_next = weigh_at(pos(i + 1), ry1);
           if (dbg != nullptr) {  // force the weighing to complete before the timestamp
             asm volatile("" ::"f"(u_next.d), "f"(u_next.w));
             pt_weigh += clock64() - tp0;
@@ -1388,6 +1401,11 @@ __device__ __forceinline__ void fold_long_pairs(
           // (w+ = w > 0 ? w : 0, and RN(S + 0) = S), W_i = min(S_i, Wmax) —
           // before saturation S_i = W_i, and once S_k >= Wmax every later
           // S >= Wmax while W stays Wmax. The serial part is one FADD per record.
+          if (kProd == 2 && k > 0) {  // the weight after chunk k - 1, from the run's other producer
+            const uint32_t cp = kk - 1u;
+            mbar_wait(&S.wfull[pair][cp & 1u], (cp >> 1) & 1u);
+            W = S.wbox[pair][cp & 1u];
+          }
           const float w = u.w;
           float Wmine = W;
           if (W != Wmax) {  // W is warp-uniform (replicated scan)
@@ -1421,6 +1439,11 @@ __device__ __forceinline__ void fold_long_pairs(
           }
           // else saturated: W_i = min(RN(Wmax + w), Wmax) = Wmax for w > 0 and
           // unchanged for w <= 0, so every record sees Wmax and W stays Wmax
+          if (kProd == 2) {  // hand the weight after this chunk on (every chunk arrives once: phase = kk / 2)
+            if (lane == 0) S.wbox[pair][kk & 1u] = W;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.wfull[pair][kk & 1u]);
+          }
           if (dbg != nullptr) {
             asm volatile("" ::"f"(W), "f"(Wmine));
             pt_scan += clock64() - tp1;
@@ -1495,7 +1518,8 @@ __device__ __forceinline__ void fold_long_pairs(
         long long cwait = 0, cbusy0 = dbg != nullptr ? clock64() : 0, ct_vote = 0, ct_chain = 0, ct_spec = 0, nc_spec = 0,
                   ct_serial = 0, nc_serial = 0;
         if (dbg != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-        for (uint32_t k = 0; k < nchunks; ++k, ++kk) {
+        for (uint32_t k = 0; k < nchunks; ++k) {
+          const uint32_t kk = kk0 + k;
           const int s = static_cast<int>(kk % kRingStages);
           const long long tw0 = dbg != nullptr ? clock64() : 0;
           mbar_wait(&ring_full[pair][s], (kk / kRingStages) & 1u);
@@ -1686,6 +1710,7 @@ __device__ __forceinline__ void fold_long_pairs(
           }
         }
       }
+      kk0 += nchunks;
     }
   }
 
@@ -1816,12 +1841,17 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_fold_short(
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
-// Long and short runs in ONE persistent grid, one 512-thread CTA per SM: warps
-// 8..15 are the four long-run producer/consumer pairs (consumers = warps
-// 12..15, one per sub-partition, the highest warp ids so the arbiter favours
-// the serial chains), warps 0..7 fold short runs from the start; every pair
-// warp joins the short runs once the long runs are handed out.
-template <bool kSmemOrg, int kC = 2>
+// Long and short runs in ONE persistent grid, one 512-thread CTA per SM.
+// kProd = 1: warps 8..15 are four long-run producer/consumer pairs, warps 0..7
+// fold short runs from the start. kProd = 2: warps 4..15 are four teams of
+// TWO producers and a consumer (a run's producers take alternate chunks and
+// hand the running weight to each other), warps 0..3 fold short runs — the
+// consumer, not the producer, then bounds a chain (faster chains, fewer
+// short-run warps beside them: the host picks it for small folds, where the
+// longest chain is the whole fold). Consumers are the highest warp ids, one per
+// sub-partition, so the arbiter favours the serial chains; every team warp
+// joins the short runs once the long runs are handed out.
+template <bool kSmemOrg, int kC = 2, int kProd = 1>
 __global__ void __launch_bounds__(512, 1) k_fold_all(
     const uint32_t* __restrict__ num_runs_p, const uint32_t* __restrict__ order,
     const uint32_t* __restrict__ sorted_len, const uint32_t* __restrict__ ukeys, const uint32_t* __restrict__ ustart,
@@ -1838,9 +1868,10 @@ __global__ void __launch_bounds__(512, 1) k_fold_all(
   if ((threadIdx.x & 31) == 0) n_long = count_long_runs(sorted_len, nruns, tp.long_code);
   n_long = __shfl_sync(0xffffffffu, n_long, 0);
   const int wid = static_cast<int>(threadIdx.x >> 5);
-  if (wid >= 8)
-    fold_long_pairs<4, false>(S, wid - 8, poses, nruns, n_long, order, ukeys, ustart, ulen, svals, rays, far, map,
-                              tp, touched, work, dbg);
+  constexpr int kShortWarps = 16 - 4 * (1 + kProd);  // 8 beside pairs, 4 beside two-producer teams
+  if (wid >= kShortWarps)
+    fold_long_pairs<4, false, kProd>(S, wid - kShortWarps, poses, nruns, n_long, order, ukeys, ustart, ulen, svals,
+                                     rays, far, map, tp, touched, work, dbg);
   fold_short_loop<kC>(poses, nruns, n_long, order, ukeys, ustart, ulen, svals, rays, far, map, tp, touched, work);
 }
 

@@ -1256,11 +1256,18 @@ void vxg_handle::sort_fold(uint64_t T, uint64_t nslots, uint32_t F) {
         const char* e = getenv("VXG_FOLD_KC");
         return e ? atoi(e) : 2;  // measured apply 2.74 / 2.34 / 2.38 / 2.57 ms for 1 / 2 / 3 / 4 (cfg1)
       }();
-      auto kern = !smem_org ? k_fold_all<false, 2>
-                            : (fold_kc == 2 ? k_fold_all<true, 2>
-                                : (fold_kc == 1 ? k_fold_all<true, 1>
-                                                : (fold_kc == 3 ? k_fold_all<true, 3>
-                                                                : (fold_kc == 4 ? k_fold_all<true, 4> : k_fold_all<true, 2>))));
+      // two producers per long run for small folds (their longest chain IS the fold: a single scan, the
+      // simple integrator's one-frame batches); pairs + 8 short-run warps for full batches (issue-bound)
+      static const int fold_prod = [] {  // dev A/B: VXG_FOLD_PROD = 1 | 2 forces a layout
+        const char* e = getenv("VXG_FOLD_PROD");
+        return e ? atoi(e) : 0;
+      }();
+      const bool teams = fold_prod ? fold_prod == 2 : T < 100000000ull;
+      auto kern = !smem_org ? (teams ? k_fold_all<false, 2, 2> : k_fold_all<false, 2, 1>)
+                            : (fold_kc == 1 ? k_fold_all<true, 1>
+                                : (fold_kc == 3 ? k_fold_all<true, 3>
+                                                : (fold_kc == 4 ? k_fold_all<true, 4>
+                                                                : (teams ? k_fold_all<true, 2, 2> : k_fold_all<true, 2, 1>))));
       kern<<<static_cast<unsigned>(dev_sms), 512, 0, fold_long_st>>>(num_runs.p, run_order.p, run_len2.p, run_keys.p,
                                                                      run_start.p, run_len.p, svals, fold_rays.p,
                                                                      far_rays.p, d_org.p, F, view(), tp, tch, work.p,

@@ -96,3 +96,13 @@ def test_host_input_subbatches(gpu, parts):
 
 def test_synchronous_fold(gpu):
     _run({"VXG_SYNC_FOLD": "1"})
+
+
+@pytest.mark.parametrize("prod", [1, 2])
+def test_long_run_layouts(gpu, prod):
+    """Both long-run layouts of the fold on the same batches: producer/consumer
+    pairs (full batches) and two-producer teams (small folds), which the host
+    otherwise picks by the fold's record count (VXG_FOLD_PROD forces one); the
+    fixed long-run threshold (full-batch behaviour) on small batches as well."""
+    _run({"VXG_FOLD_PROD": str(prod)})
+    _run({"VXG_FOLD_PROD": str(prod), "VXG_FIXED_LONG_RUN": "1"}, batches=1, count=4)
