@@ -281,6 +281,13 @@ int vxg_kernel_launches(vxg_handle* h, uint64_t* out, int reset);
  * update_tsdf_voxel restatement), all on the device. out[0], out[1] =
  * mismatch counts (both must be 0). */
 int vxg_selftest_fold(int device, uint64_t n, uint64_t n_seq, uint32_t len, uint64_t seed, uint64_t* out);
+/* Self-test of the in-house device primitives the pipeline is built on
+ * (csrc/vxg_sort.cuh; they replace the CUB calls of round 1): exclusive prefix
+ * sums (32- and 64-bit, the latter in place), the stable 64-bit-key pair sort
+ * (ascending or descending over the low `bits` key bits) and the 32-bit pair
+ * sort, on n random items against the host. out[0..3] = mismatch counts (all
+ * must be 0; out must hold 4 values). */
+int vxg_selftest_prims(vxg_handle* h, uint64_t n, int bits, int descending, uint64_t seed, uint64_t* out);
 /* Debug: lengths and voxel keys of the n longest fold chains of the last batch. */
 int vxg_debug_top_runs(vxg_handle* h, uint32_t* len, uint32_t* keys, uint32_t n);
 

@@ -109,6 +109,7 @@ SIGNATURES = [
      [c_void_p, c_void_p, c_void_p, POINTER(c_uint64), POINTER(c_float), c_uint64, c_int, POINTER(VxgStats)]),
     ("vxg_group_serialize_vxblx", c_int, [c_void_p, c_void_p, c_uint64, POINTER(c_uint64)]),
     ("vxg_selftest_fold", c_int, [c_int, c_uint64, c_uint64, c_uint32, c_uint64, POINTER(c_uint64)]),
+    ("vxg_selftest_prims", c_int, [c_void_p, c_uint64, c_int, c_int, c_uint64, POINTER(c_uint64)]),
     ("vxg_debug_top_runs", c_int, [c_void_p, POINTER(c_uint32), POINTER(c_uint32), c_uint32]),
     ("vxg_eval_projective_distance", c_int, [c_int, c_void_p, c_void_p, c_void_p, c_uint64, c_void_p]),
     ("vxg_eval_measurement_weight", c_int, [c_int, c_int, c_void_p, c_void_p, c_uint64, c_float, c_float, c_void_p]),

@@ -1851,8 +1851,15 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_fold_short(
 // longest chain is the whole fold). Consumers are the highest warp ids, one per
 // sub-partition, so the arbiter favours the serial chains; every team warp
 // joins the short runs once the long runs are handed out.
+// VXG_FOLD_MAXREG (dev A/B): cap the fold's registers so that the next batch's
+// bundling kernels find room beside the persistent fold CTAs.
+#ifdef VXG_FOLD_MAXREG
+#define VXG_FOLD_BOUNDS __maxnreg__(VXG_FOLD_MAXREG)
+#else
+#define VXG_FOLD_BOUNDS __launch_bounds__(512, 1)
+#endif
 template <bool kSmemOrg, int kC = 2, int kProd = 1>
-__global__ void __launch_bounds__(512, 1) k_fold_all(
+__global__ void VXG_FOLD_BOUNDS k_fold_all(
     const uint32_t* __restrict__ num_runs_p, const uint32_t* __restrict__ order,
     const uint32_t* __restrict__ sorted_len, const uint32_t* __restrict__ ukeys, const uint32_t* __restrict__ ustart,
     const uint32_t* __restrict__ ulen, const uint32_t* __restrict__ svals, const FoldRay* __restrict__ rays, const uint2* __restrict__ far,

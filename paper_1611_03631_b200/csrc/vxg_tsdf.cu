@@ -737,7 +737,8 @@ void vxg_handle::sort_pairs64(const unsigned long long* keys, const uint32_t* va
   if (hi_bits > 0) {
     uint32_t* kf = sk == s64_k0.p ? s64_k1.p : s64_k0.p;  // free key buffer
     uint32_t* vf = sv == s64_v0.p ? s64_v1.p : s64_v0.p;  // free value buffer
-    k_key_word<<<grid_for(n), 256, 0, st>>>(n, keys, sv, 32, (1u << hi_bits) - 1u, descending, kf, nullptr);
+    k_key_word<<<grid_for(n), 256, 0, st>>>(n, keys, sv, 32, hi_bits == 32 ? 0xFFFFFFFFu : (1u << hi_bits) - 1u, descending,
+                                            kf, nullptr);
     ++launches;
     uint32_t *sk2 = nullptr, *sv2 = nullptr;
     sort_pairs32(n, hi_bits, kf, sv, sk, vf, &sk2, &sv2);
@@ -2830,6 +2831,90 @@ extern "C" int vxg_selftest_fold(int device, uint64_t n, uint64_t n_seq, uint32_
     CU(cudaMemcpy(h, mm.p, sizeof(h), cudaMemcpyDeviceToHost));
     out[0] = h[0];
     out[1] = h[1];
+  });
+}
+
+// Self-test of the in-house device primitives behind the pipeline (vxg_sort.cuh:
+// prefix sums, the 32-bit pair sort in both tile shapes, 64-bit-key sorts)
+// against the host: n random items, keys of `bits` bits. out[0] / out[1] =
+// mismatches of the 32- / 64-bit exclusive prefix sums, out[2] = of
+// sort_pairs64 (keys or values, stable order), out[3] = of sort_pairs32.
+extern "C" int vxg_selftest_prims(vxg_handle* h, uint64_t n, int bits, int descending, uint64_t seed,
+                                  uint64_t* out) {
+  return guarded([&] {
+    if (h == nullptr || out == nullptr || bits < 1 || bits > 64) throw VxgError(VXG_EINVAL, "bad argument");
+    set_device(h);
+    h->settle();
+    auto rnd = [&seed]() {  // splitmix64
+      uint64_t z = (seed += 0x9E3779B97F4A7C15ull);
+      z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+      z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+      return z ^ (z >> 31);
+    };
+    out[0] = out[1] = out[2] = out[3] = 0;
+    if (n == 0) return;
+    // ---- prefix sums
+    std::vector<uint32_t> a32(n), r32(n);
+    std::vector<unsigned long long> a64(n), r64(n);
+    for (uint64_t i = 0; i < n; ++i) {
+      a32[i] = static_cast<uint32_t>(rnd() & 15u);
+      a64[i] = rnd() & 0xFFFFFFFFFFull;
+    }
+    DBuf<uint32_t> d32, o32;
+    DBuf<unsigned long long> d64, o64;
+    d32.ensure(n), o32.ensure(n), d64.ensure(n), o64.ensure(n);
+    CU(cudaMemcpyAsync(d32.p, a32.data(), n * 4, cudaMemcpyHostToDevice, h->st));
+    CU(cudaMemcpyAsync(d64.p, a64.data(), n * 8, cudaMemcpyHostToDevice, h->st));
+    h->scan_exclusive<uint32_t>(d32.p, o32.p, n);
+    h->scan_exclusive<unsigned long long>(d64.p, d64.p, n);  // in place
+    CU(cudaMemcpyAsync(r32.data(), o32.p, n * 4, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaMemcpyAsync(r64.data(), d64.p, n * 8, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaStreamSynchronize(h->st));
+    uint32_t s32 = 0;
+    unsigned long long s64 = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+      out[0] += r32[i] != s32;
+      out[1] += r64[i] != s64;
+      s32 += a32[i];
+      s64 += a64[i];
+    }
+    // ---- pair sorts
+    const unsigned long long mask = bits == 64 ? ~0ull : (1ull << bits) - 1ull;
+    std::vector<unsigned long long> k64(n), rk(n);
+    std::vector<uint32_t> v(n), rv(n), idx(n);
+    for (uint64_t i = 0; i < n; ++i) {
+      // few distinct values in the low byte: plenty of ties for the stability check
+      k64[i] = ((rnd() & ~0xFFull) | (rnd() & 3u)) & mask;
+      v[i] = static_cast<uint32_t>(rnd());
+      idx[i] = static_cast<uint32_t>(i);
+    }
+    std::stable_sort(idx.begin(), idx.end(), [&](uint32_t x, uint32_t y) {
+      return descending ? k64[x] > k64[y] : k64[x] < k64[y];
+    });
+    DBuf<unsigned long long> dk, dko;
+    DBuf<uint32_t> dv, dvo;
+    dk.ensure(n), dko.ensure(n), dv.ensure(n), dvo.ensure(n);
+    CU(cudaMemcpyAsync(dk.p, k64.data(), n * 8, cudaMemcpyHostToDevice, h->st));
+    CU(cudaMemcpyAsync(dv.p, v.data(), n * 4, cudaMemcpyHostToDevice, h->st));
+    h->sort_pairs64(dk.p, dv.p, n, bits, descending != 0, dko.p, dvo.p);
+    CU(cudaMemcpyAsync(rk.data(), dko.p, n * 8, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaMemcpyAsync(rv.data(), dvo.p, n * 4, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaStreamSynchronize(h->st));
+    for (uint64_t i = 0; i < n; ++i) out[2] += rk[i] != k64[idx[i]] || rv[i] != v[idx[i]];
+    if (bits <= 32 && !descending) {
+      std::vector<uint32_t> k32(n), rk32(n);
+      for (uint64_t i = 0; i < n; ++i) k32[i] = static_cast<uint32_t>(k64[i]);
+      DBuf<uint32_t> a, b, c;
+      a.ensure(n), b.ensure(n), c.ensure(n);
+      CU(cudaMemcpyAsync(a.p, k32.data(), n * 4, cudaMemcpyHostToDevice, h->st));
+      CU(cudaMemcpyAsync(dv.p, v.data(), n * 4, cudaMemcpyHostToDevice, h->st));
+      uint32_t *sk = nullptr, *sv = nullptr;
+      h->sort_pairs32(n, bits, a.p, dv.p, b.p, c.p, &sk, &sv);
+      CU(cudaMemcpyAsync(rk32.data(), sk, n * 4, cudaMemcpyDeviceToHost, h->st));
+      CU(cudaMemcpyAsync(rv.data(), sv, n * 4, cudaMemcpyDeviceToHost, h->st));
+      CU(cudaStreamSynchronize(h->st));
+      for (uint64_t i = 0; i < n; ++i) out[3] += rk32[i] != k32[idx[i]] || rv[i] != v[idx[i]];
+    }
   });
 }
 

@@ -105,3 +105,20 @@ def test_fast_fold_selftest(gpu):
     check(lib().vxg_selftest_fold(0, 1 << 28, 20000, 2000, 12345, out))
     assert out[0] == 0, f"{out[0]} division mismatches"
     assert out[1] == 0, f"{out[1]} fold-sequence mismatches"
+
+
+@pytest.mark.parametrize("n", [1, 31, 4095, 4096, 4097, 8193, 70_001, 1_000_003, 20_000_001])
+def test_device_primitives_selftest(gpu, n):
+    """The in-house prefix sums and pair sorts (vxg_sort.cuh) against the
+    host at tile-boundary sizes, for both sort tile shapes (inputs under / over
+    16 M items), 32- and 64-bit keys, ascending and descending, with ties (the
+    sorts must be stable)."""
+    from paper_1611_03631_b200 import TsdfLayer
+    from paper_1611_03631_b200._capi import check, lib
+    layer = TsdfLayer(0.05, 16)
+    for bits, desc in ((8, 0), (21, 0), (32, 0), (46, 0), (64, 1), (19, 1)):
+        if n > 2_000_000 and (bits, desc) not in ((32, 0), (46, 0)):
+            continue
+        out = (ctypes.c_uint64 * 4)()
+        check(lib().vxg_selftest_prims(layer.handle, n, bits, desc, 777 + n + bits, out))
+        assert list(out) == [0, 0, 0, 0], f"n={n} bits={bits} desc={desc}: mismatches {list(out)}"
