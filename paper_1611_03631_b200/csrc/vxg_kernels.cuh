@@ -1764,40 +1764,57 @@ __device__ __forceinline__ void fold_short_loop(
     base = __shfl_sync(0xffffffffu, base, 0);
     if (n_long + base >= nruns) break;
     const uint32_t r = n_long + base + lane;
-    if (r >= nruns) continue;
-    const RunCtx c = run_ctx(map, tp, ukeys, ustart, ulen, order[r]);
-    if (c.key == kInvalidRecord) continue;
-    vxg_voxel* vp = map.slab + c.key;
-    VoxState st = load_vox(vp);
+    // The warp's 32 runs walk in lockstep to the longest of them (runs of one
+    // length code, at most 12.5 % apart: the fold order), so the lanes can
+    // vote: runs are neighbouring voxels (key order inside a code), and in free
+    // space ALL their records are far — then nobody weighs (no projective
+    // distance, no square root: most of a record's instructions). A lane
+    // without a run (grid tail, skipped candidates) walks an empty one.
+    RunCtx c{kInvalidRecord, 0u, 0u, 0.0f, 0.0f, 0.0f};
+    if (r < nruns) c = run_ctx(map, tp, ukeys, ustart, ulen, order[r]);
+    const bool act = c.key != kInvalidRecord;
+    if (!act) c.start = c.len = 0u;
+    vxg_voxel* vp = map.slab + (act ? c.key : 0u);
+    VoxState st{};
+    if (act) st = load_vox(vp);
     // software pipeline over chunks of kC records: rays gathered two chunks
     // ahead, weighed one chunk ahead of their fold steps. Positions past the
-    // run re-read its last record and carry w = 0 (a no-op step), so the
-    // loop body has no per-record guards.
+    // run re-read its last record (an empty run: record 0 of the batch) and
+    // carry w = 0 (a no-op step), so the loop body has no per-record guards.
     const uint32_t* ids = svals + c.start;
-    const uint32_t last = c.len - 1;
+    const uint32_t last = c.len ? c.len - 1u : 0u;
+    const uint32_t wlen = __reduce_max_sync(0xffffffffu, c.len);
     FoldIn rn[kC];
     Upd xn[kC], xs[kC];
-    auto weigh_at = [&](uint32_t idx, const FoldIn& ry) {
-      Upd x = weigh_in(ry, poses, c.x0, c.x1, c.x2, tp);
-      x.w = idx <= last ? x.w : 0.0f;
-      return x;
+    auto weigh_chunk = [&](uint32_t idx0, const FoldIn* ry, Upd* x) {  // all 32 lanes call
+#pragma unroll
+      for (int u = 0; u < kC; ++u) {  // one vote per record position of the chunk
+        const bool in = idx0 + u < c.len;
+        if (__all_sync(0xffffffffu, ry[u].fr.x != 0xFFFFFFFFu || !in)) {
+          x[u].d = tp.truncation;
+          x[u].w = in ? __uint_as_float(ry[u].fr.x) : 0.0f;
+          x[u].c = ry[u].fr.y;
+          x[u].pad = 0u;
+        } else {
+          x[u] = weigh_in(ry[u], poses, c.x0, c.x1, c.x2, tp);
+          x[u].w = in ? x[u].w : 0.0f;
+        }
+      }
     };
     uint32_t idn[kC];  // ray ids one chunk ahead of the gathers: no id -> ray load chain in the loop
 #pragma unroll
     for (int u = 0; u < kC; ++u) rn[u] = load_fold_in(rays, far, ids[min(static_cast<uint32_t>(u), last)]);
-#pragma unroll
-    for (int u = 0; u < kC; ++u) xn[u] = weigh_at(u, rn[u]);
+    weigh_chunk(0u, rn, xn);
 #pragma unroll
     for (int u = 0; u < kC; ++u) rn[u] = load_fold_in(rays, far, ids[min(static_cast<uint32_t>(kC + u), last)]);
 #pragma unroll
     for (int u = 0; u < kC; ++u) idn[u] = ids[min(static_cast<uint32_t>(2 * kC + u), last)];
-    for (uint32_t j = 0; j < c.len; j += kC) {
+    for (uint32_t j = 0; j < wlen; j += kC) {
 #pragma unroll
       for (int u = 0; u < kC; ++u) xs[u] = xn[u];
       // weigh chunk j+kC (gathered last iteration), gather chunk j+2kC (ids
       // loaded last iteration), load the ids of chunk j+3kC
-#pragma unroll
-      for (int u = 0; u < kC; ++u) xn[u] = weigh_at(j + kC + u, rn[u]);
+      weigh_chunk(j + kC, rn, xn);
 #pragma unroll
       for (int u = 0; u < kC; ++u) rn[u] = load_fold_in(rays, far, idn[u]);
 #pragma unroll
@@ -1813,8 +1830,10 @@ __device__ __forceinline__ void fold_short_loop(
           step_exact(st.D, st.W, st.cr, st.cg, st.cb, xs[u].d, xs[u].w, xs[u].c, tp.truncation, tp.max_weight);
       }
     }
-    store_vox(vp, st);
-    if (touched != nullptr) touched[c.key / static_cast<uint32_t>(map.nvox)] = 1u;
+    if (act) {
+      store_vox(vp, st);
+      if (touched != nullptr) touched[c.key / static_cast<uint32_t>(map.nvox)] = 1u;
+    }
   }
 }
 
