@@ -830,110 +830,36 @@ __device__ __host__ __forceinline__ uint32_t block_owner(int b0, int b1, int b2,
   return static_cast<uint32_t>(mix64(pack_block(b0, b1, b2)) % world);
 }
 
-// k_emit for one rank's slice [R0, R1) of the global ray order: same walk and
-// weights, but records carry (global voxel key, ray) and the block's owner;
-// no block allocation here (the owner allocates on receipt).
-__global__ void __launch_bounds__(128) k_emit_sharded(uint32_t R0, uint32_t R1, const RayInfo* __restrict__ rays,
-                                                      const unsigned long long* __restrict__ roff, uint64_t base,
-                                                      const float* __restrict__ poses, TsdfParams tp, int vps,
-                                                      uint32_t world, TermView tv,
-                                                      unsigned long long* __restrict__ gkeys,
-                                                      uint32_t* __restrict__ gvals, uint32_t* __restrict__ owner,
-                                                      uint32_t* __restrict__ counters, int keep_owner) {
-  // keep_owner >= 0 (replicated traversal): records of other owners are dropped
-  const float v = tp.voxel_size;
-  const bool anti = tp.merge_mode == VXG_MERGE_GROUPED_ANTI_GRAZE;
-  for (uint32_t j = R0 + blockIdx.x * blockDim.x + threadIdx.x; j < R1; j += gridDim.x * blockDim.x) {
-    const RayInfo r = rays[j];
-    const float* Pm = poses + 12 * r.frame;
-    const float o0 = Pm[3], o1 = Pm[7], o2 = Pm[11];
-    const float depth = r.depth;
-    if (!(r.valid == 1u && !(depth <= 0.0f))) continue;
-    const float ray0 = fsub(r.p[0], o0), ray1 = fsub(r.p[1], o1), ray2 = fsub(r.p[2], o2);
-    const float s = fdiv(tp.truncation, depth);
-    const float w_front = fmul(mweight_base(tp.weight_mode, r.base, 0.0f, tp.truncation, tp.dropoff_epsilon), r.weight);
-    Walk wk;
-    uint32_t span = 0;
-    walk_axis_init(o0, fadd(r.p[0], fmul(ray0, s)), v, &wk.c0, &wk.e0, &wk.s0, &wk.m0, &wk.d0, &span);
-    walk_axis_init(o1, fadd(r.p[1], fmul(ray1, s)), v, &wk.c1, &wk.e1, &wk.s1, &wk.m1, &wk.d1, &span);
-    walk_axis_init(o2, fadd(r.p[2], fmul(ray2, s)), v, &wk.c2, &wk.e2, &wk.s2, &wk.m2, &wk.d2, &span);
-    const uint32_t count = span + 1u;
-    const uint64_t out0 = roff[j] - base;
-    int og0 = 0, og1 = 0, og2 = 0;
-    if (anti) {
-      og0 = gidx(o0, v);
-      og1 = gidx(o1, v);
-      og2 = gidx(o2, v);
-    }
-    float x0 = vcenter(wk.c0, v), x1 = vcenter(wk.c1, v), x2 = vcenter(wk.c2, v);
-    int b0 = floor_div(wk.c0, vps), b1 = floor_div(wk.c1, vps), b2 = floor_div(wk.c2, vps);
-    int l0 = wk.c0 - b0 * vps, l1 = wk.c1 - b1 * vps, l2 = wk.c2 - b2 * vps;
-    int cb0 = 0x7fffffff, cb1 = 0, cb2 = 0;
-    uint32_t cown = 0;
-    for (uint32_t k = 0; k < count; ++k) {
-      unsigned long long key = ~0ull;
-      uint32_t own = world;
-      bool skip = false;
-      if (anti) {
-        const int g[3] = {wk.c0, wk.c1, wk.c2};
-        const int og[3] = {og0, og1, og2};
-        skip = !(wk.c0 == r.term[0] && wk.c1 == r.term[1] && wk.c2 == r.term[2]) && is_terminal(tv, r.frame, og, g);
-      }
-      if (!skip) {
-        const float t0 = fsub(r.p[0], x0), t1 = fsub(r.p[1], x1), t2 = fsub(r.p[2], x2);
-        const float along = dot3(t0, t1, t2, ray0, ray1, ray2);
-        float w = w_front;  // as in k_emit: d >= 0 in front of the point
-        if (!(along >= 0.0f)) {
-          const float magnitude = norm3(t0, t1, t2);
-          const float d = along < 0.0f ? -magnitude : magnitude;
-          w = fmul(mweight_base(tp.weight_mode, r.base, d, tp.truncation, tp.dropoff_epsilon), r.weight);
-        }
-        if (!(w <= 0.0f)) {
-          if (b0 != cb0 || b1 != cb1 || b2 != cb2) {
-            cb0 = b0;
-            cb1 = b1;
-            cb2 = b2;
-            cown = block_owner(b0, b1, b2, world);
-          }
-          uint64_t gk;
-          if (gkey_encode(b0, b1, b2, static_cast<uint32_t>(l0 + vps * (l1 + vps * l2)), &gk)) {
-            key = gk;
-            own = cown;
-          } else {
-            atomicOr(&counters[1], static_cast<uint32_t>(kErrKeyRange));
-          }
-        }
-      }
-      const uint64_t o_idx = out0 + k;
-      if (keep_owner >= 0 && own != static_cast<uint32_t>(keep_owner)) own = world;
-      gkeys[o_idx] = key;
-      gvals[o_idx] = j;
-      owner[o_idx] = own;
-      if (k + 1 < count && !(wk.c0 == wk.e0 && wk.c1 == wk.e1 && wk.c2 == wk.e2)) {
-        const bool a1 = wk.m1 < wk.m0;
-        const float mlo = a1 ? wk.m1 : wk.m0;
-        const bool a2 = wk.m2 < mlo;
-        if (a2) {
-          wk.c2 += wk.s2;
-          wk.m2 = fadd(wk.m2, wk.d2);
-          x2 = vcenter(wk.c2, v);
-          l2 += wk.s2;
-          if (l2 == vps) { l2 = 0; ++b2; } else if (l2 < 0) { l2 = vps - 1; --b2; }
-        } else if (a1) {
-          wk.c1 += wk.s1;
-          wk.m1 = fadd(wk.m1, wk.d1);
-          x1 = vcenter(wk.c1, v);
-          l1 += wk.s1;
-          if (l1 == vps) { l1 = 0; ++b1; } else if (l1 < 0) { l1 = vps - 1; --b1; }
-        } else {
-          wk.c0 += wk.s0;
-          wk.m0 = fadd(wk.m0, wk.d0);
-          x0 = vcenter(wk.c0, v);
-          l0 += wk.s0;
-          if (l0 == vps) { l0 = 0; ++b0; } else if (l0 < 0) { l0 = vps - 1; --b0; }
-        }
+// Sharded emit, second half: the walk itself is the single-GPU k_emit run
+// against a DICTIONARY (a block hash without a slab: the blocks this rank's ray
+// slice touches, in first-touch order), so its records carry 32-bit keys
+// dict_slot * nvox + local. This pass turns them into what travels: the global
+// voxel key and the owner of its block (world = dropped: skipped candidates,
+// zero-weight updates, blocks outside the +-2^14 key range, and in the
+// replicated traversal the other owners' records). The values (ray id + far
+// flag) are used as they are.
+__global__ void k_globalize(uint64_t n, const uint32_t* __restrict__ keys, const int32_t* __restrict__ dict_bidx,
+                            uint32_t nvox, uint32_t world, int keep_owner, unsigned long long* __restrict__ gkeys,
+                            uint32_t* __restrict__ owner, uint32_t* __restrict__ counters) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t k = keys[i];
+    unsigned long long gk = ~0ull;
+    uint32_t own = world;
+    if (k != kInvalidRecord) {
+      const uint32_t slot = k / nvox, lin = k - slot * nvox;
+      const int b0 = dict_bidx[3 * slot], b1 = dict_bidx[3 * slot + 1], b2 = dict_bidx[3 * slot + 2];
+      uint64_t e;
+      if (gkey_encode(b0, b1, b2, lin, &e)) {
+        gk = e;
+        own = block_owner(b0, b1, b2, world);
+        if (keep_owner >= 0 && own != static_cast<uint32_t>(keep_owner)) own = world;
+      } else {
+        atomicOr(&counters[1], static_cast<uint32_t>(kErrKeyRange));
       }
     }
+    gkeys[i] = gk;
+    owner[i] = own;
   }
 }
 
@@ -980,20 +906,49 @@ __global__ void k_gather_send(uint64_t n, const uint32_t* __restrict__ perm, con
 __global__ void k_localize(uint64_t n, const uint4* __restrict__ recv, MapView map, const FoldRay* __restrict__ rays,
                            uint32_t* __restrict__ rkeys, uint32_t* __restrict__ rvals,
                            unsigned long long* __restrict__ updates) {
+  // Records arrive in ray order, so a warp's 32 consecutive records are a few
+  // segments of one ray inside one block each: the first lane of a block
+  // segment looks the block up (shared-memory cache, then the hash) and hands
+  // the slot to its segment, the first lane of a ray segment reads the ray's
+  // frame and adds the segment's length to the frame's update count.
   __shared__ unsigned long long bcache[kBlockCacheSize];
   for (int i = threadIdx.x; i < kBlockCacheSize; i += blockDim.x) bcache[i] = ~0ull;
   __syncthreads();
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint4 m = recv[i];
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + (threadIdx.x & ~31u); i0 < n; i0 += stride) {
+    const uint64_t i = i0 + lane;  // warp-uniform trip count (full-warp shuffles)
+    const bool in = i < n;
+    const uint4 m = in ? recv[i] : make_uint4(0u, 0u, 0u, 0u);
     const uint64_t k = static_cast<uint64_t>(m.x) | (static_cast<uint64_t>(m.y) << 32);
-    int b[3];
-    uint32_t lin;
-    gkey_decode(k, b, &lin);
-    const int32_t slot = cached_find_or_insert(bcache, map, b[0], b[1], b[2]);
-    rkeys[i] = slot >= 0 ? static_cast<uint32_t>(slot) * static_cast<uint32_t>(map.nvox) + lin : kInvalidRecord;
-    rvals[i] = m.z;
-    warp_add_by_key(updates, rays[m.z].frame, 1u);
+    const uint64_t blk = k >> 19;  // the block part of the global key
+    const uint32_t ray = m.z & kRayMask;
+    const uint64_t pblk = __shfl_up_sync(0xffffffffu, blk, 1);
+    const uint32_t pray = __shfl_up_sync(0xffffffffu, ray, 1);
+    const uint32_t inm = __ballot_sync(0xffffffffu, in);
+    const bool bhead = in && (lane == 0u || pblk != blk);
+    const bool rhead = in && (lane == 0u || pray != ray);
+    const uint32_t bheads = __ballot_sync(0xffffffffu, bhead), rheads = __ballot_sync(0xffffffffu, rhead);
+    int32_t slot = -1;
+    if (bhead) {
+      int b[3];
+      uint32_t l;
+      gkey_decode(k, b, &l);
+      slot = cached_find_or_insert(bcache, map, b[0], b[1], b[2]);
+    }
+    const uint32_t upto = (2u << lane) - 1u;  // lanes 0..lane
+    const int bsrc = 31 - __clz(bheads & upto);
+    slot = __shfl_sync(0xffffffffu, slot, bsrc < 0 ? 0 : bsrc);
+    if (in) {
+      const uint32_t lin = static_cast<uint32_t>(k & ((1ull << 19) - 1ull));
+      rkeys[i] = slot >= 0 ? static_cast<uint32_t>(slot) * static_cast<uint32_t>(map.nvox) + lin : kInvalidRecord;
+      rvals[i] = m.z;  // ray id + far flag
+    }
+    if (rhead) {  // this ray segment: [lane, next ray head or the end of the valid lanes)
+      const uint32_t after = rheads & ~upto;
+      const uint32_t end = after ? static_cast<uint32_t>(__ffs(after) - 1) : static_cast<uint32_t>(__popc(inm));
+      atomicAdd(&updates[rays[ray].frame], static_cast<unsigned long long>(end - lane));
+    }
   }
 }
 

@@ -711,8 +711,14 @@ struct vxg_handle {
   std::vector<uint64_t> send_counts, send_offsets, recv_counts;
   uint64_t recv_total = 0;
   DBuf<unsigned long long> gkeys, sbounds, obounds, dev_counts;
-  DBuf<uint32_t> gvals, gowner, gowner2, giota, gperm;
+  DBuf<uint32_t> gowner, gowner2, giota, gperm;
   DBuf<uint4> send_buf, recv_buf;
+  // sharded emit: dictionary of the blocks this rank's ray slice touches (hash + block index table, no
+  // slab) for the single-GPU k_emit to write 32-bit keys against; k_globalize turns them into global keys
+  DBuf<unsigned long long> dict_hkeys, sh_upd;
+  DBuf<int32_t> dict_hvals, dict_bidx;
+  DBuf<uint32_t> dict_counters, sh_keys, sh_vals;
+  uint64_t dict_cap = 0;
   void shard_front(uint32_t R, uint32_t F, const TermView& tv);
   void shard_back(const uint4* recv, uint64_t n, uint32_t F);
   void nccl_exchange();
@@ -1565,16 +1571,61 @@ void vxg_handle::shard_front(uint32_t R, uint32_t F, const TermView& tv) {
   }  // replicated traversal (SURVEY.md 8e fallback): every rank walks all rays, keeps its own blocks
   const uint64_t T = endrec - base;
   if (T == 0) return;
+  if (T >= 0xFFFFFFFFull) throw VxgError(VXG_EINVAL, "too many records in one sharded batch slice (32-bit offsets)");
   begin(ST_EMIT);
   gkeys.ensure(T);
-  gvals.ensure(T);
   gowner.ensure(T);
   gowner2.ensure(T);
   giota.ensure(T);
   gperm.ensure(T);
-  k_emit_sharded<<<grid_for(R1 - R0, 128), 128, 0, st>>>(R0, R1, rays.p, roff.p, base, d_poses.p, tp, vps,
-                                                          static_cast<uint32_t>(shard_world), tv, gkeys.p, gvals.p,
-                                                          gowner.p, counters.p, shard_replicated ? shard_rank : -1);
+  sh_keys.ensure(T);
+  sh_vals.ensure(T);
+  sh_upd.ensure(std::max<uint32_t>(F, 1));
+  ray_iota.ensure(R);
+  k_iota<<<grid_for(R), 256, 0, st>>>(R, ray_iota.p);  // the slice is walked in ray order
+  ++launches;
+  if (dict_cap == 0) dict_cap = std::max<uint64_t>(cap_blocks, 1024);
+  for (;;) {
+    if (dict_cap * static_cast<uint64_t>(nvox) >= 0xFFFFFFFFull)
+      throw VxgError(VXG_ENOMEM, "sharded emit: block dictionary would exceed the 32-bit voxel key range");
+    uint64_t hc = 1;
+    while (hc < 2 * dict_cap) hc <<= 1;
+    dict_hkeys.ensure(hc);
+    dict_hvals.ensure(hc);
+    dict_bidx.ensure(3 * dict_cap);
+    dict_counters.ensure(2);
+    CU(cudaMemsetAsync(dict_hkeys.p, 0xFF, hc * sizeof(unsigned long long), st));  // kEmptyKey
+    CU(cudaMemsetAsync(dict_hvals.p, 0xFF, hc * sizeof(int32_t), st));             // kEmptySlot
+    CU(cudaMemsetAsync(dict_counters.p, 0, 2 * sizeof(uint32_t), st));
+    CU(cudaMemsetAsync(sh_upd.p, 0, std::max<uint32_t>(F, 1) * sizeof(unsigned long long), st));
+    MapView dv = view();
+    dv.hkeys = dict_hkeys.p;
+    dv.hvals = dict_hvals.p;
+    dv.hmask = hc - 1;
+    dv.slab = nullptr;
+    dv.block_idx = dict_bidx.p;
+    dv.counters = dict_counters.p;
+    dv.cap_blocks = static_cast<uint32_t>(dict_cap);
+    const bool anti = tp.merge_mode == VXG_MERGE_GROUPED_ANTI_GRAZE;
+    const bool pow2 = (vps & (vps - 1)) == 0;
+    auto kern = anti ? (pow2 ? k_emit<true, true> : k_emit<true, false>)
+                     : (pow2 ? k_emit<false, true> : k_emit<false, false>);
+    kern<<<grid_for(R1 - R0, kEmitThreads), kEmitThreads, 0, st>>>(R0, R1, ray_iota.p, rays.p, roff.p, base, d_poses.p,
+                                                                   tp, dv, tv, sh_keys.p, sh_vals.p, sh_upd.p);
+    ++launches;
+    CU(cudaGetLastError());
+    uint32_t dc[2];
+    fetch({{dc, dict_counters.p, sizeof(dc)}});
+    if (dc[1] & kErrKeyRange) throw VxgError(VXG_ERANGE, "voxel block index outside the packed key range");
+    if (dc[1] & (kErrSlabFull | kErrHashFull)) {  // dictionary too small: grow and walk again
+      dict_cap = std::max<uint64_t>(2 * dict_cap, static_cast<uint64_t>(dc[0]) + dc[0] / 4);
+      continue;
+    }
+    break;
+  }
+  k_globalize<<<grid_for(T), 256, 0, st>>>(T, sh_keys.p, dict_bidx.p, static_cast<uint32_t>(nvox),
+                                           static_cast<uint32_t>(shard_world), shard_replicated ? shard_rank : -1,
+                                           gkeys.p, gowner.p, counters.p);
   k_iota<<<grid_for(T), 256, 0, st>>>(static_cast<uint32_t>(T), giota.p);
   launches += 2;
   CU(cudaGetLastError());
@@ -1594,7 +1645,7 @@ void vxg_handle::shard_front(uint32_t R, uint32_t F, const TermView& tv) {
   const uint64_t n_valid = bnd[shard_world];
   send_buf.ensure(std::max<uint64_t>(n_valid, 1));
   if (n_valid) {
-    k_gather_send<<<grid_for(n_valid), 256, 0, st>>>(n_valid, sp, gkeys.p, gvals.p, send_buf.p);
+    k_gather_send<<<grid_for(n_valid), 256, 0, st>>>(n_valid, sp, gkeys.p, sh_vals.p, send_buf.p);
     ++launches;
     CU(cudaGetLastError());
   }
