@@ -556,7 +556,10 @@ __device__ __forceinline__ bool is_terminal(const TermView& tv, uint32_t f, cons
 constexpr int kBlockCacheSize = 1024;
 
 __device__ __forceinline__ bool cache_key13(int bx, int by, int bz, uint64_t* k) {
-  if (bx < -4096 || bx >= 4096 || by < -4096 || by >= 4096 || bz < -4096 || bz >= 4096) return false;
+  // all three in [-4096, 4096): one unsigned compare on the biased values
+  const uint32_t ux = static_cast<uint32_t>(bx + 4096), uy = static_cast<uint32_t>(by + 4096),
+                 uz = static_cast<uint32_t>(bz + 4096);
+  if ((ux | uy | uz) >= 8192u) return false;
   *k = (static_cast<uint64_t>(bx & 0x1FFF) << 26) | (static_cast<uint64_t>(by & 0x1FFF) << 13) |
        static_cast<uint64_t>(bz & 0x1FFF);
   return true;
@@ -568,7 +571,11 @@ __device__ __forceinline__ int32_t cached_find_or_insert(unsigned long long* cac
   const bool cacheable = cache_key13(bx, by, bz, &k13);
   uint32_t idx = 0;
   if (cacheable) {
-    idx = static_cast<uint32_t>(mix64(k13)) & (kBlockCacheSize - 1);
+    // the cache index only has to spread neighbouring blocks (this path runs at a few
+    // active lanes per warp in the walk: every instruction counts): two 32-bit multiplies
+    const uint32_t h = static_cast<uint32_t>(bx) * 0x9E3779B1u ^ static_cast<uint32_t>(by) * 0x85EBCA6Bu ^
+                       static_cast<uint32_t>(bz) * 0xC2B2AE35u;
+    idx = (h >> 16) & (kBlockCacheSize - 1);
     const unsigned long long e = cache[idx];
     if (e != ~0ull && (e & ((1ull << 40) - 1)) == k13) return static_cast<int32_t>(e >> 40);
   }
