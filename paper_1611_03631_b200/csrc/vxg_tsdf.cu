@@ -285,18 +285,34 @@ struct vxg_handle {
     return t;
   }
   // Length code from which a run of a fold over T records goes to the warp
-  // pairs (21 ns per record, one run per pair) instead of one thread (~250 ns
-  // per record, 32 runs per warp). The thread path has ~3x the throughput, the
-  // pair path 12x less latency per run: a run should take the pair path when
-  // folding it in one thread would outlast the rest of the fold, i.e. when
-  // its length exceeds a fixed fraction of T (kLongRun / 2.4e8 on the cfg1
-  // batch the threshold was tuned on). Full batches keep kLongRun; a single
-  // 640x480 frame (2 M records) sends runs >= 64 to the pairs.
+  // pairs (~21 ns per record, one run per pair) instead of one thread (~250 ns
+  // per record, 32 runs per warp). The thread path has ~3x the throughput per
+  // issue slot, the pair path 12x less latency per run: a run should take the
+  // pair path when folding it in one thread would outlast the rest of the fold,
+  // i.e. when its length exceeds a fixed fraction of T. The fraction is
+  // 6144 / 2.4e8 (kLongFrac): on the cfg1 batch 4096 gives the shortest apply
+  // STAGE (2.09 ms) but 6144 the shortest STEP (9.67 vs 9.95 ms) — fewer runs on
+  // the instruction-hungry pair path, and the few threads still folding 4-6 k
+  // records leave the SMs to the next batch's bundling (apply 2.28 ms, mostly
+  // overlapped). Floor 64 (a single 640x480 frame, 2 M records: its longest
+  // chain is the whole fold), ceiling 8192 (larger folds are chunked at 5e8
+  // records and hidden behind the next chunk's emit and sort: a higher ceiling
+  // only stretches their thin tail — cfg3 apply 18 / 33 ms at 4096 / 13.7 k
+  // with the same step).
+  static constexpr double kLongFrac = 6144.0 / 2.4e8;
   static uint32_t long_code_for(uint64_t T) {
-    static const bool fixed = getenv("VXG_FIXED_LONG_RUN") != nullptr;  // dev A/B
+    static const bool fixed = getenv("VXG_FIXED_LONG_RUN") != nullptr;  // dev A/B: kLongRun whatever T
     if (fixed) return run_len_code(kLongRun);
-    const double want = static_cast<double>(T) * (static_cast<double>(kLongRun) / 2.4e8);
-    const uint32_t len = static_cast<uint32_t>(std::min<double>(kLongRun, std::max(64.0, want)));
+    static const double scale = [] {  // dev A/B: VXG_LONG_SCALE multiplies the fraction
+      const char* e = getenv("VXG_LONG_SCALE");
+      return e ? atof(e) : 1.0;
+    }();
+    static const double cap = [] {  // dev A/B: VXG_LONG_CAP
+      const char* e = getenv("VXG_LONG_CAP");
+      return e ? atof(e) : 8192.0;
+    }();
+    const double want = scale * static_cast<double>(T) * kLongFrac;
+    const uint32_t len = static_cast<uint32_t>(std::min<double>(cap, std::max(64.0, want)));
     return run_len_code(len);
   }
 
