@@ -1271,13 +1271,15 @@ __device__ __forceinline__ void long_smem_init(LongSmem<kP>& S) {
 // 2 kP pair warps (named barriers 1..kP). kSep: consumers only on
 // sub-partitions 0 and 1 (warp & 3 < 2), producers on 2 and 3, so no consumer
 // shares its scheduler with a producer.
-template <int kP, bool kSep, int kProd = 1>
+template <int kP, bool kSep, int kProd = 1, bool kDbg = true>
 __device__ __forceinline__ void fold_long_pairs(
     LongSmem<kP>& S, const int wid, const float* poses, const uint32_t nruns, const uint32_t n_long,
     const uint32_t* __restrict__ order, const uint32_t* __restrict__ ukeys, const uint32_t* __restrict__ ustart,
     const uint32_t* __restrict__ ulen, const uint32_t* __restrict__ svals, const FoldRay* __restrict__ rays, const uint2* __restrict__ far,
     const MapView& map, const TsdfParams& tp, uint8_t* __restrict__ touched, uint32_t* __restrict__ work,
-    unsigned long long* __restrict__ dbg) {
+    unsigned long long* __restrict__ dbg_arg) {
+  // kDbg = false: the trace hooks below (22 per chunk) compile away
+  unsigned long long* const dbg = kDbg ? dbg_arg : nullptr;
   auto& ring = S.ring;
   auto& ring_full = S.ring_full;
   auto& ring_empty = S.ring_empty;
@@ -1839,7 +1841,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_fold_short(
 #else
 #define VXG_FOLD_BOUNDS __launch_bounds__(512, 1)
 #endif
-template <bool kSmemOrg, int kC = 2, int kProd = 1>
+template <bool kSmemOrg, int kC = 2, int kProd = 1, bool kDbg = false>
 __global__ void VXG_FOLD_BOUNDS k_fold_all(
     const uint32_t* __restrict__ num_runs_p, const uint32_t* __restrict__ order,
     const uint32_t* __restrict__ sorted_len, const uint32_t* __restrict__ ukeys, const uint32_t* __restrict__ ustart,
@@ -1858,8 +1860,8 @@ __global__ void VXG_FOLD_BOUNDS k_fold_all(
   const int wid = static_cast<int>(threadIdx.x >> 5);
   constexpr int kShortWarps = 16 - 4 * (1 + kProd);  // 8 beside pairs, 4 beside two-producer teams
   if (wid >= kShortWarps)
-    fold_long_pairs<4, false, kProd>(S, wid - kShortWarps, poses, nruns, n_long, order, ukeys, ustart, ulen, svals,
-                                     rays, far, map, tp, touched, work, dbg);
+    fold_long_pairs<4, false, kProd, kDbg>(S, wid - kShortWarps, poses, nruns, n_long, order, ukeys, ustart, ulen,
+                                           svals, rays, far, map, tp, touched, work, dbg);
   fold_short_loop<kC>(poses, nruns, n_long, order, ukeys, ustart, ulen, svals, rays, far, map, tp, touched, work);
 }
 

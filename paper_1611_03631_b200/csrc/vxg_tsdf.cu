@@ -1286,7 +1286,9 @@ void vxg_handle::sort_fold(uint64_t T, uint64_t nslots, uint32_t F) {
         return e ? atoi(e) : 0;
       }();
       const bool teams = fold_prod ? fold_prod == 2 : T < 100000000ull;
-      auto kern = !smem_org ? (teams ? k_fold_all<false, 2, 2> : k_fold_all<false, 2, 1>)
+      if (!smem_org) dbg = nullptr;  // the trace build stages the origins in shared memory (F <= kOrgCache)
+      auto kern = dbg != nullptr ? (teams ? k_fold_all<true, 2, 2, true> : k_fold_all<true, 2, 1, true>)  // (trace: smem origins)
+                  : !smem_org ? (teams ? k_fold_all<false, 2, 2> : k_fold_all<false, 2, 1>)
                             : (fold_kc == 1 ? k_fold_all<true, 1>
                                 : (fold_kc == 3 ? k_fold_all<true, 3>
                                                 : (fold_kc == 4 ? k_fold_all<true, 4>
