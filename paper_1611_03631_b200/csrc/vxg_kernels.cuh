@@ -1205,6 +1205,21 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t pari
       : "memory");
 }
 
+// Non-blocking look at a phase (acquire, like try_wait): 1 when it has completed.
+// The result is an ordinary register, so the instruction's latency overlaps
+// whatever the warp does before it reads the flag.
+__device__ __forceinline__ uint32_t mbar_test(unsigned long long* bar, uint32_t parity) {
+  uint32_t r;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(r)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return r;
+}
+
 // Run marks of the sorted records: voxel k's records are [dense_start[k],
 // dense_end[k]) (dense_end[k] stays 0 for a voxel without records).
 __global__ void k_run_marks(uint64_t T, const uint32_t* __restrict__ skeys, uint32_t* __restrict__ dense_start,
@@ -1482,16 +1497,30 @@ __device__ __forceinline__ void fold_long_pairs(
         long long cwait = 0, cbusy0 = dbg != nullptr ? clock64() : 0, ct_vote = 0, ct_chain = 0, ct_spec = 0, nc_spec = 0,
                   ct_serial = 0, nc_serial = 0;
         if (dbg != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+        // The chain's critical path is D -> candidates -> table exchange -> walk -> D. What does not depend
+        // on D is taken off it: a chunk's header and this lane's record are loaded at the end of the previous
+        // iteration, and whether the NEXT chunk has arrived is asked (mbar_test) before this chunk's walk and
+        // read after it — the blocking wait (90 cycles even when complete) only runs when it has not.
+        ChunkHdr hd;
+        float4 xrec;
+        {
+          const int s0 = static_cast<int>(kk0 % kRingStages);
+          const long long tw0 = dbg != nullptr ? clock64() : 0;
+          mbar_wait(&ring_full[pair][s0], (kk0 / kRingStages) & 1u);
+          if (dbg != nullptr) cwait += clock64() - tw0;
+          hd = ring_hdr[pair][s0];
+          xrec = reinterpret_cast<const float4*>(ring[pair][s0] + lane)[0];
+        }
         for (uint32_t k = 0; k < nchunks; ++k) {
           const uint32_t kk = kk0 + k;
           const int s = static_cast<int>(kk % kRingStages);
-          const long long tw0 = dbg != nullptr ? clock64() : 0;
-          mbar_wait(&ring_full[pair][s], (kk / kRingStages) & 1u);
-          if (dbg != nullptr) cwait += clock64() - tw0;
+          const int sn = static_cast<int>((kk + 1u) % kRingStages);
+          const uint32_t pn = ((kk + 1u) / kRingStages) & 1u;
+          const bool more = k + 1 < nchunks;
+          const uint32_t next_ready = more ? mbar_test(&ring_full[pair][sn], pn) : 0u;
           const long long tc0 = dbg != nullptr ? clock64() : 0;
           const PreRec* rb = ring[pair][s];
           const uint32_t cnt = min(32u, c.len - k * 32);
-          const ChunkHdr hd = ring_hdr[pair][s];
           const float W_end = hd.W_end;
           // colours provably unchanged over the whole chunk? (intervals from the producer)
           const int o0 = static_cast<int>(st.cr), o1 = static_cast<int>(st.cg), o2 = static_cast<int>(st.cb);
@@ -1516,7 +1545,7 @@ __device__ __forceinline__ void fold_long_pairs(
               --spec_skip;
               ++n_skip;
             } else if (b0 - 0x00800004u < 0x7e000000u) {  // D0 and its neighbours positive, normal, finite
-              const float4 x = reinterpret_cast<const float4*>(rb + lane)[0];  // W, T, r1, wc
+              const float4 x = xrec;  // this lane's record: W, T, r1, wc
               const Recip rt{x.y, x.z, true};
               const uint32_t base = b0 - 3u;
               uint32_t tlo = 0u, thi = 0x07000000u;
@@ -1650,6 +1679,15 @@ __device__ __forceinline__ void fold_long_pairs(
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(&ring_empty[pair][s]);
+          if (more) {  // the next chunk's header and this lane's record of it
+            if (!next_ready) {
+              const long long tw0 = dbg != nullptr ? clock64() : 0;
+              mbar_wait(&ring_full[pair][sn], pn);
+              if (dbg != nullptr) cwait += clock64() - tw0;
+            }
+            hd = ring_hdr[pair][sn];
+            xrec = reinterpret_cast<const float4*>(ring[pair][sn] + lane)[0];
+          }
         }
         if (dbg != nullptr && lane == 0) {
           atomicAdd(&dbg[4 * n_all + 2], static_cast<unsigned long long>(cwait));
