@@ -1803,24 +1803,45 @@ __device__ __forceinline__ void fold_short_loop(
         }
       }
     };
-    uint32_t idn[kC];  // ray ids one chunk ahead of the gathers: no id -> ray load chain in the loop
+    // Gathers run ahead of their use: a far record's 8-byte FarRay two chunks
+    // ahead (most records, and the only gather of an all-far warp: an L2 / DRAM
+    // round trip is longer than one chunk's work), a near record's 32-byte ray
+    // one chunk ahead (it would cost 8 more registers per chunk position), the
+    // ids one chunk ahead of the first gather that needs them.
+    auto far_part = [&](uint32_t v) {
+      return (v & kFarRecord) ? far[v & kRayMask] : make_uint2(0xFFFFFFFFu, 0u);
+    };
+    auto near_part = [&](uint32_t v) { return (v & kFarRecord) ? FoldRay{} : rays[v & kRayMask]; };
+    uint32_t idq[kC], idn[kC];  // ids of chunk c+3 (far part in flight) and c+4
+    uint2 fq[kC];               // far parts of chunk c+3
 #pragma unroll
     for (int u = 0; u < kC; ++u) rn[u] = load_fold_in(rays, far, ids[min(static_cast<uint32_t>(u), last)]);
     weigh_chunk(0u, rn, xn);
 #pragma unroll
     for (int u = 0; u < kC; ++u) rn[u] = load_fold_in(rays, far, ids[min(static_cast<uint32_t>(kC + u), last)]);
 #pragma unroll
-    for (int u = 0; u < kC; ++u) idn[u] = ids[min(static_cast<uint32_t>(2 * kC + u), last)];
+    for (int u = 0; u < kC; ++u) {
+      idq[u] = ids[min(static_cast<uint32_t>(2 * kC + u), last)];
+      fq[u] = far_part(idq[u]);
+      idn[u] = ids[min(static_cast<uint32_t>(3 * kC + u), last)];
+    }
     for (uint32_t j = 0; j < wlen; j += kC) {
 #pragma unroll
       for (int u = 0; u < kC; ++u) xs[u] = xn[u];
-      // weigh chunk j+kC (gathered last iteration), gather chunk j+2kC (ids
-      // loaded last iteration), load the ids of chunk j+3kC
+      // weigh chunk j+kC; complete chunk j+2kC (its far parts were loaded last
+      // iteration, its near rays now); far parts of chunk j+3kC; ids of j+4kC
       weigh_chunk(j + kC, rn, xn);
 #pragma unroll
-      for (int u = 0; u < kC; ++u) rn[u] = load_fold_in(rays, far, idn[u]);
+      for (int u = 0; u < kC; ++u) {
+        rn[u].ry = near_part(idq[u]);
+        rn[u].fr = fq[u];
+      }
 #pragma unroll
-      for (int u = 0; u < kC; ++u) idn[u] = ids[min(j + 3 * kC + u, last)];
+      for (int u = 0; u < kC; ++u) {
+        idq[u] = idn[u];
+        fq[u] = far_part(idq[u]);
+        idn[u] = ids[min(j + 4 * kC + u, last)];
+      }
       const VoxState s0 = st;
       bool ok = true;
 #pragma unroll
