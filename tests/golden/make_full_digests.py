@@ -25,8 +25,9 @@ sys.path.insert(0, os.path.dirname(HERE))
 from oracle_bindings import OracleLayer, RefLayer, ref_available  # noqa: E402
 from paper_1611_03631_b200 import workload as W  # noqa: E402
 
-# (name, config id, first frame, frame count): two full 2048x2048 cfg4 frames
-CASES = [("cfg4_full_f1_f2", 4, 1, 2)]
+# (name, config id, first frame, frame count): two full 2048x2048 cfg4 frames, the
+# 100-frame cfg1 batch bench.py times, and 40-frame prefixes of cfg2 and cfg3
+CASES = [("cfg4_full_f1_f2", 4, 1, 2), ("cfg1_bench_x100", 1, 0, 100), ("cfg2_x40", 2, 0, 40), ("cfg3_x40", 3, 0, 40)]
 
 
 def input_digest(frames) -> str:
@@ -41,8 +42,11 @@ def input_digest(frames) -> str:
 
 def main():
     assert ref_available(), "oracle/_ref not built"
-    out = {}
+    path = os.path.join(HERE, "full_digests.json")
+    out = json.load(open(path)) if os.path.exists(path) and "--all" not in sys.argv else {}
     for name, cfg_id, start, count in CASES:
+        if name in out:  # kept (cfg4 alone is minutes of reference time); --all regenerates everything
+            continue
         wc = W.CONFIGS[cfg_id]
         cfg = W.tsdf_config(wc)
         frames = W.frames(cfg_id, count=count, start=start)
@@ -58,7 +62,7 @@ def main():
                      "stats": stats, "blocks": ref.block_count(), "vxblx_bytes": len(ref_bytes),
                      "vxblx_sha256": hashlib.sha256(ref_bytes).hexdigest(), "ref_seconds": round(t_ref, 1)}
         print(name, out[name], flush=True)
-    json.dump(out, open(os.path.join(HERE, "full_digests.json"), "w"), indent=1)
+    json.dump(out, open(path, "w"), indent=1)
 
 
 if __name__ == "__main__":

@@ -307,6 +307,30 @@ def test_cfg4_full_frames(gpu):
     assert len(b) == d["vxblx_bytes"] and hashlib.sha256(b).hexdigest() == d["vxblx_sha256"]
 
 
+@pytest.mark.parametrize("case", ["cfg1_bench_x100", "cfg2_x40", "cfg3_x40"])
+def test_full_batches_against_reference_digests(gpu, case):
+    """Full-size batches against the REFERENCE ITSELF (not the restatement):
+    the 100-frame cfg1 batch bench.py times, and 40-frame prefixes of cfg2 and
+    cfg3, each integrated in one call; the layer's VXBLX bytes and the per-frame
+    counters must equal oracle/_ref's (tests/golden/full_digests.json)."""
+    import hashlib
+    import json
+    import os
+    from golden_full import input_digest
+    d = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "full_digests.json")))[case]
+    wc = W.CONFIGS[d["config"]]
+    cfg = W.tsdf_config(wc)
+    frames = W.frames(d["config"], count=d["count"], start=d["start"])
+    assert input_digest(frames) == d["input_sha256"], "workload generator drift"
+    layer = TsdfLayer(wc.voxel_size, wc.vps, block_capacity=1024)
+    integ = TsdfIntegrator(cfg, layer)
+    stats = integ.integrate_batch([Scan(*f) for f in frames])
+    assert [[int(v) for v in row] for row in stats] == d["stats"]
+    assert layer.block_count() == d["blocks"]
+    b = layer.save_bytes()
+    assert len(b) == d["vxblx_bytes"] and hashlib.sha256(b).hexdigest() == d["vxblx_sha256"]
+
+
 def test_batch_split_invariance_full_size(gpu):
     """Property at full size (no oracle): the same 40 frames integrated as one
     batch, as 4 batches of 10 and as 40 single calls give identical bytes."""
