@@ -68,6 +68,8 @@ struct Mirror {
   float voxel_size = 0.f;
   int vps = 0;
   std::map<std::tuple<int, int, int>, const void*> fingerprint;  // block index -> Block* after last sync
+  std::vector<int32_t> wb_idx;     // writeback scratch, kept across scans (no 10-20 MB
+  std::vector<vxg_voxel> wb_vox;   // allocation + zero fill per scan)
   ~Mirror() {
     if (h) vxg_destroy(h);
   }
@@ -123,11 +125,13 @@ void upload(Mirror& m, TsdfLayer& layer, const TsdfConfig& cfg) {
 void download(Mirror& m, TsdfLayer& layer) {
   uint64_t n = 0;
   check(vxg_drain_updated(m.h, kConsumer, nullptr, 0, &n));
-  std::vector<int32_t> idx(3 * (n + 1));
+  std::vector<int32_t>& idx = m.wb_idx;
+  if (idx.size() < 3 * (n + 1)) idx.resize(3 * (n + 1));
   check(vxg_drain_updated(m.h, kConsumer, idx.data(), n, &n));
   if (n == 0) return;
   const size_t nv = static_cast<size_t>(m.vps) * m.vps * m.vps;
-  std::vector<vxg_voxel> out(nv * n);
+  std::vector<vxg_voxel>& out = m.wb_vox;
+  if (out.size() < nv * n) out.resize(nv * n);
   check(vxg_fetch_blocks(m.h, idx.data(), n, out.data(), nullptr));
   for (uint64_t b = 0; b < n; ++b) {
     const BlockIndex bidx(idx[3 * b], idx[3 * b + 1], idx[3 * b + 2]);
