@@ -6,7 +6,7 @@
 // _ref/bench_insert_vxg links the B200 drop-in
 // (paper_1611_03631_b200/dropin/vxf_tsdf_integrator_vxg.cpp + libvxg.so), which
 // also writes the updated blocks back into the caller's host TsdfLayer.
-// Input: a scan file written by tools/bench_dropin.py — u32 F, then per scan
+// Input: a scan file written by tests/dropin_insert_timing.py — u32 F, then per scan
 // u32 n, 12 floats (row-major 3x4 sensor-to-world), n x 3 floats, n x 3 bytes.
 // Args: <scan file> <voxel_size> <truncation> <epsilon> <max_ray> <merge 0|1|2> <weight 0|1|2> <min_ray> <max_weight>
 #include <algorithm>

@@ -38,3 +38,21 @@ def test_reference_mesh_doctests_on_gpu_dropin(gpu):
     vxg = subprocess.run([MESH_VXG], capture_output=True, text=True, timeout=600)
     assert "test cases: 5" in ref.stdout, ref.stdout[-2000:]
     assert vxg.stdout == ref.stdout, "drop-in:\n" + vxg.stdout[-3000:] + "\nreference:\n" + ref.stdout[-3000:]
+
+
+INS_REF = os.path.join(ROOT, "oracle", "_ref", "bench_insert_ref")
+INS_VXG = os.path.join(ROOT, "oracle", "_ref", "bench_insert_vxg")
+
+
+@pytest.mark.skipif(not (os.path.exists(INS_REF) and os.path.exists(INS_VXG)),
+                    reason="oracle/_ref/bench_insert_* not built (needs /root/reference)")
+def test_per_scan_insert_through_dropin(gpu):
+    """A caller of the reference's C++ API inserting 30 cfg1 scans one by one
+    (oracle/bench_insert.cpp, timed like cli.cpp:168-186), linked against the
+    reference's integrator and against the B200 drop-in: same update and block
+    counts, and the drop-in's median insert is well below the reference's
+    (the full 100-scan numbers are in profiles/r3_dropin_cfg1.json)."""
+    from dropin_insert_timing import run
+    out = run(1, 30)
+    assert out["vxg"]["updates"] == out["ref"]["updates"] and out["vxg"]["blocks"] == out["ref"]["blocks"]
+    assert out["vxg"]["median_ms"] < 0.5 * out["ref"]["median_ms"], out
