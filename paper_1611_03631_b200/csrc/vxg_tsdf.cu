@@ -163,6 +163,8 @@ struct vxg_handle {
   uint32_t* top_pinned = nullptr;  // longest run per chunk (read back at the batch end)
   uint32_t n_top = 0;
   static constexpr uint32_t kTopCap = 256;
+  uint64_t top_T[256] = {};      // records of the fold each top_pinned entry belongs to
+  double chain_ratio = -1.0;     // longest run / records of the most recent folds read back (-1: none yet)
   std::vector<cudaEvent_t> copy_events;
   // ---- streaming ingestion: two staging slots (vxg_stage_packed / vxg_integrate_staged)
   struct StageSlot {
@@ -626,7 +628,12 @@ struct vxg_handle {
   uint64_t reset_used = 0;  // blocks in use when vxg_reset was called (deferred)
   // After a host sync of st that followed join_folds(): longest runs of the batch.
   void drain_tops() {
-    for (uint32_t i = 0; i < n_top; ++i) info_max_run = std::max<uint64_t>(info_max_run, top_pinned[i]);
+    double ratio = -1.0;
+    for (uint32_t i = 0; i < n_top; ++i) {
+      info_max_run = std::max<uint64_t>(info_max_run, top_pinned[i]);
+      if (top_T[i]) ratio = std::max(ratio, static_cast<double>(top_pinned[i]) / static_cast<double>(top_T[i]));
+    }
+    if (n_top) chain_ratio = ratio;
     n_top = 0;
   }
 
@@ -1222,6 +1229,7 @@ void vxg_handle::sort_fold(uint64_t T, uint64_t nslots, uint32_t F) {
       CU(cudaStreamSynchronize(st));
       drain_tops();
     }
+    top_T[n_top] = T;
     CU(cudaMemcpyAsync(top_pinned + n_top++, run_max.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   }
   uint8_t* tch = consumers.empty() ? nullptr : touched.p;
@@ -1285,7 +1293,13 @@ void vxg_handle::sort_fold(uint64_t T, uint64_t nslots, uint32_t F) {
         const char* e = getenv("VXG_FOLD_PROD");
         return e ? atoi(e) : 0;
       }();
-      const bool teams = fold_prod ? fold_prod == 2 : T < 100000000ull;
+      // Teams when the fold is chain-bound: its longest run, at ~20 ns per record, outlasts the rest of
+      // the fold at ~1.1e11 records/s. Measured: cfg4 (longest run 9e-4 of the chunk's records) gains
+      // 11 % with teams, cfg2 (~5e-4) loses 2 %, cfg1 (3e-4) loses 0.3 ms of apply: threshold 7e-4. The
+      // longest run of THIS fold is only on the device; the ratio of the handle's most recent folds
+      // stands in for it, and a small fold is one scan (its longest chain is all its rays).
+      const bool teams = fold_prod ? fold_prod == 2
+                                   : (chain_ratio >= 0.0 ? chain_ratio > 7e-4 || T < 20000000ull : T < 100000000ull);
       if (!smem_org) dbg = nullptr;  // the trace build stages the origins in shared memory (F <= kOrgCache)
       auto kern = dbg != nullptr ? (teams ? k_fold_all<true, 2, 2, true> : k_fold_all<true, 2, 1, true>)  // (trace: smem origins)
                   : !smem_org ? (teams ? k_fold_all<false, 2, 2> : k_fold_all<false, 2, 1>)
